@@ -1,0 +1,163 @@
+/*
+ * heat_b200.h -- C-ABI of the B200-native FTCS hot path (arXiv 1510.08982).
+ *
+ * Drop-in boundary for the reference's solver API in namespace heat
+ * (/root/reference/proj/include/heat/{sync_solver,async_sim,async_exec}.hpp).
+ * Plain pointers and sizes only: no torch, no CUDA types in the signatures.
+ * Host buffers are caller-owned; device memory belongs to the library (a
+ * per-device workspace, or an explicit heat_plan for resident runs).
+ *
+ * Conventions shared by every entry point
+ *   - Fields are IEEE-754 binary64 arrays u[0..n-1] (TemperatureField,
+ *     core.hpp:42-64).  `r` is the exact bits of SolverParams::r()
+ *     (core.hpp:27); the caller derives it, the library never re-derives it.
+ *   - Boundary condition (core.hpp:68-81): bc_kind HEAT_BC_DIRICHLET with
+ *     ends (c1, c2), or HEAT_BC_PERIODIC (c1, c2 ignored).
+ *   - Return value: HEAT_OK or a status that maps 1:1 onto the reference's
+ *     exception types; heat_last_error() gives the message.
+ *   - Trajectory recording follows sync_run (sync_solver.cpp:52-77): step 0,
+ *     every `stride`-th step and the final step; stride 0 selects the
+ *     default (1 when n <= 1000, else 100; sync_solver.hpp:52-54).  Use
+ *     heat_trajectory_length() to size `snapshots` (rows of n doubles) and
+ *     `steps`.  Either may be NULL when only the final state is wanted
+ *     (then pass `final_out`).
+ *   - Thread safety: every entry point may be called from any host thread;
+ *     the per-device workspace is guarded by a mutex (the reference's
+ *     ensemble_run calls AsyncSimulator from many threads, analysis.cpp:68-85).
+ */
+#ifndef HEAT_B200_H
+#define HEAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define HEAT_OK        0
+#define HEAT_EDOMAIN   1  /* std::domain_error      (core.cpp:8-31, core.hpp:46-50, async_sim.cpp:8-22) */
+#define HEAT_EINVAL    2  /* std::invalid_argument  (sync_solver.cpp:31-32, async_exec.cpp:266-270)     */
+#define HEAT_ELOGIC    3  /* std::logic_error       (async_sim.cpp:35,44)                                 */
+#define HEAT_EDIVERGE  4  /* heat::DivergenceError  (sync_solver.hpp:81-83)                              */
+#define HEAT_ECUDA     5  /* CUDA runtime failure   -> std::runtime_error                                */
+#define HEAT_ETIMEOUT  6  /* async watchdog: a halo-ring wait exceeded its deadline                      */
+#define HEAT_ENOMEM    7  /* device or host allocation failure                                           */
+#define HEAT_ENODEV    8  /* no CUDA device / extension unusable: never falls back to the CPU            */
+
+#define HEAT_BC_DIRICHLET 0
+#define HEAT_BC_PERIODIC  1
+
+/* DelayModel::Distribution (async_sim.hpp:16-28) */
+#define HEAT_DELAY_UNIFORM   0
+#define HEAT_DELAY_FIXED     1
+#define HEAT_DELAY_GEOMETRIC 2
+
+/* ExecMode (async_exec.hpp:15) */
+#define HEAT_EXEC_BARRIERED   0
+#define HEAT_EXEC_BARRIER_FREE 1
+
+/* LagStats (async_exec.hpp:42-51); kLagHistogramSize = 64 (async_exec.cpp:42). */
+typedef struct heat_lag_stats {
+    uint64_t reads;
+    uint64_t min_lag;
+    uint64_t max_lag;
+    uint64_t overflow;
+    uint64_t histogram[64];
+} heat_lag_stats;
+
+/* Free-running async diagnostics (GPU-only, no reference counterpart):
+ * reader-relative delay k - k* of every cross-PE read (the paper's quantity),
+ * plus the writer lag the reference's LagStats measures. */
+typedef struct heat_async_stats {
+    uint64_t reads;
+    uint64_t max_delay;
+    uint64_t delay_histogram[64];
+    uint64_t waits;        /* reads that had to spin for the bound q          */
+    double   residual_sum; /* sum_k ||u(k+1) - A u(k)||_inf (a-posteriori bound), when logged */
+} heat_async_stats;
+
+/* ---- library state ---------------------------------------------------- */
+const char* heat_last_error(void);
+const char* heat_version(void);
+int heat_device_count(void);
+/* Number of kernels this library has launched in this process (all devices). */
+uint64_t heat_kernel_launches(void);
+
+/* set_strict_finite_checks / strict_finite_checks (sync_solver.hpp:77-78) */
+void heat_set_strict_finite_checks(int enabled);
+int heat_strict_finite_checks(void);
+
+/* Snapshot count sync_run / async_run record for (n, k_end, stride). */
+size_t heat_trajectory_length(size_t n, size_t k_end, size_t stride);
+
+/* ---- synchronous solver (sync_solver.hpp:60-73) ------------------------- */
+/* sync_step (sync_solver.hpp:60-62): one step of u (ends snapped per BC). */
+int heat_sync_step(const double* u, size_t n, double r, int bc_kind, double c1, double c2,
+                   double* out);
+
+/* sync_run (sync_solver.hpp:64-67). */
+int heat_sync_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                  size_t k_end, size_t stride, double* final_out, double* snapshots,
+                  size_t* steps, size_t max_snapshots, size_t* n_snapshots);
+
+/* sync_run_f32 (sync_solver.hpp:69-73): FP32 arithmetic, results widened. */
+int heat_sync_run_f32(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                      size_t k_end, size_t stride, double* final_out, double* snapshots,
+                      size_t* steps, size_t max_snapshots, size_t* n_snapshots);
+
+/* ---- deterministic asynchronous solver (async_sim.hpp:59-101) ----------- */
+/* async_run: Eq. (4) with the model's seeded delay stream replayed exactly.
+ * per_pe = PartitionSpec::per_pe (core.hpp:85-102). */
+int heat_async_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                   size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                   uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                   double* snapshots, size_t* steps, size_t max_snapshots,
+                   size_t* n_snapshots);
+
+/* sample_delay (async_sim.cpp:57-73) for draw index j of a stream (counter
+ * form): the delay the j-th draw yields at step k. */
+int heat_sample_delay(size_t q, int law, size_t fixed_delay, double geometric_p, uint64_t seed,
+                      uint64_t j, size_t k, size_t* delay);
+
+/* ---- executors (async_exec.hpp:53-70) ----------------------------------- */
+/* exec_run: Barriered = bit-identical to sync_run (one launch-chain on the
+ * GPU, no per-step barrier); BarrierFree = free-running PEs on the GPU with
+ * bounded staleness q_free (0 selects the default 8) through acquire/release
+ * halo rings.  duration_ns is device time of the run (CUDA events).  lag is
+ * filled when record_lag != 0 (writer lag, LagStats semantics); stats (may be
+ * NULL) receives the reader-relative delay log. */
+int heat_exec_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                  size_t per_pe, size_t workers, size_t k_end, int mode, int record_lag,
+                  size_t q_free, double* field_out, uint64_t* duration_ns, heat_lag_stats* lag,
+                  heat_async_stats* stats);
+
+/* ---- device-resident plans (bench, multi-GPU slabs) --------------------- */
+typedef struct heat_plan heat_plan;
+/* Allocates two device arrays of n doubles on `device` (ping-pong). */
+int heat_plan_create(heat_plan** plan, size_t n, int device);
+int heat_plan_destroy(heat_plan* plan);
+/* Stream the plan's work is issued on (a cudaStream_t owned by the caller,
+ * passed as an opaque handle; NULL = the plan's own stream). */
+int heat_plan_set_stream(heat_plan* plan, void* stream);
+int heat_plan_upload(heat_plan* plan, const double* host);
+int heat_plan_download(heat_plan* plan, double* host);
+/* Device IC u_i = sin(pi*i/(N-1)) with Dirichlet(0,0) ends snapped (bench only). */
+int heat_plan_fill_sine(heat_plan* plan);
+/* Advance the resident field by `steps` synchronous steps (no host sync). */
+int heat_plan_sync_advance(heat_plan* plan, double r, int bc_kind, double c1, double c2,
+                           size_t steps);
+/* Advance by `steps` with the free-running async kernel on P = n/per_pe PEs. */
+int heat_plan_async_advance(heat_plan* plan, double r, int bc_kind, double c1, double c2,
+                            size_t per_pe, size_t q, size_t steps, heat_async_stats* stats);
+/* Blocks until the plan's stream is idle; reports strict-check / watchdog status. */
+int heat_plan_synchronize(heat_plan* plan);
+/* Device pointer of the current field (for peer copies / NCCL in multi-GPU). */
+int heat_plan_device_ptr(heat_plan* plan, double** cur);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEAT_B200_H */

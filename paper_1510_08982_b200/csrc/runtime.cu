@@ -1,0 +1,139 @@
+// runtime.cu -- library state, per-device workspace, validation helpers and
+// the small C-ABI entry points (errors, strict checks, trajectory sizing).
+#include <cmath>
+#include <cstdio>
+#include <memory>
+
+#include "runtime.cuh"
+
+namespace hb {
+
+std::atomic<uint64_t> g_launches{0};
+std::atomic<bool> g_strict{false};
+
+namespace {
+thread_local std::string t_error;
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+}  // namespace
+
+void set_error(const std::string& msg) { t_error = msg; }
+
+int dev_ctx(int device, DevCtx** out) {
+    if (device < 0) {
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0)
+            return fail(HEAT_ENODEV, std::string("no CUDA device available: ") +
+                                         (e == cudaSuccess ? "count = 0" : cudaGetErrorString(e)));
+        HB_CUDA(cudaGetDevice(&device));
+    }
+    DevCtx* d = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(g_ctx_mu);
+        if (g_ctx.size() <= size_t(device)) g_ctx.resize(size_t(device) + 1);
+        if (!g_ctx[device]) g_ctx[device] = std::make_unique<DevCtx>();
+        d = g_ctx[device].get();
+    }
+    HB_CUDA(cudaSetDevice(device));
+    if (d->device < 0) {
+        std::lock_guard<std::mutex> lock(d->mu);
+        if (d->device < 0) {
+            cudaDeviceProp prop{};
+            HB_CUDA(cudaGetDeviceProperties(&prop, device));
+            if (prop.major < 10)
+                return fail(HEAT_ENODEV, std::string("device ") + prop.name +
+                                             " is not sm_100 (Blackwell); this build targets sm_100a only");
+            d->sms = prop.multiProcessorCount;
+            HB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+            HB_CUDA(cudaMalloc(&d->flag, 4 * sizeof(unsigned int)));
+            d->device = device;
+        }
+    }
+    *out = d;
+    return HEAT_OK;
+}
+
+int ensure_buffers(DevCtx& d, size_t bytes) {
+    if (d.bytes >= bytes) return HEAT_OK;
+    if (d.buf[0]) cudaFree(d.buf[0]);
+    d.buf[0] = nullptr;
+    d.bytes = 0;
+    cudaError_t e = cudaMalloc(&d.buf[0], bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HEAT_ENOMEM, std::string("cudaMalloc(") + std::to_string(bytes) +
+                                     "): " + cudaGetErrorString(e));
+    }
+    d.bytes = bytes;
+    return HEAT_OK;
+}
+
+int ensure_scratch(DevCtx& d, size_t bytes) {
+    if (d.scratch_bytes >= bytes) return HEAT_OK;
+    if (d.scratch) cudaFree(d.scratch);
+    d.scratch = nullptr;
+    d.scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&d.scratch, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(HEAT_ENOMEM, std::string("cudaMalloc(scratch ") + std::to_string(bytes) +
+                                     "): " + cudaGetErrorString(e));
+    }
+    d.scratch_bytes = bytes;
+    return HEAT_OK;
+}
+
+int check_field(const double* u, size_t n) {
+    if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u) return fail(HEAT_EINVAL, "null field pointer");
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(u[i])) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    return HEAT_OK;
+}
+
+int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
+                    std::vector<double>& out) {
+    out.assign(u0, u0 + n);
+    if (bc_kind == HEAT_BC_DIRICHLET) {
+        constexpr double kTol = 1e-9;  // kDirichletEndTol, sync_solver.hpp:44
+        if (std::abs(out.front() - c1) > kTol || std::abs(out.back() - c2) > kTol)
+            return fail(HEAT_EINVAL, "Dirichlet BC inconsistent with initial end values");
+        out.front() = c1;
+        out.back() = c2;
+    }
+    return HEAT_OK;
+}
+
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" {
+
+const char* heat_last_error(void) { return t_error.c_str(); }
+
+const char* heat_version(void) { return "heat_b200 0.1 (sm_100a)"; }
+
+int heat_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+uint64_t heat_kernel_launches(void) { return g_launches.load(); }
+
+void heat_set_strict_finite_checks(int enabled) { g_strict = enabled != 0; }
+int heat_strict_finite_checks(void) { return g_strict ? 1 : 0; }
+
+size_t heat_trajectory_length(size_t n, size_t k_end, size_t stride) {
+    if (stride == 0) stride = default_stride(n);
+    size_t count = 1 + k_end / stride;
+    if (k_end % stride != 0) ++count;
+    return count;
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// runtime.cuh -- host-side runtime shared by the C-ABI translation units:
+// error reporting, the per-device workspace, launch accounting.
+#pragma once
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/heat_b200.h"
+
+namespace hb {
+
+void set_error(const std::string& msg);
+inline int fail(int code, const std::string& msg) {
+    set_error(msg);
+    return code;
+}
+
+extern std::atomic<uint64_t> g_launches;
+extern std::atomic<bool> g_strict;
+
+#define HB_CUDA(x)                                                                         \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            return ::hb::fail(HEAT_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define HB_TRY(x)                 \
+    do {                          \
+        int s_ = (x);             \
+        if (s_ != HEAT_OK) return s_; \
+    } while (0)
+
+// Per-device state: a grow-only pair of field buffers for the one-shot
+// entry points, the non-finite flag word, and a private stream.
+struct DevCtx {
+    std::mutex mu;
+    int device = -1;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    void* buf[2] = {nullptr, nullptr};
+    size_t bytes = 0;
+    unsigned int* flag = nullptr;  // [0] non-finite, [1] watchdog timeout
+    void* scratch = nullptr;       // async rings / logs
+    size_t scratch_bytes = 0;
+};
+
+// Locks and initialises the context of the current (or given) device.
+int dev_ctx(int device, DevCtx** out);
+int ensure_buffers(DevCtx& d, size_t bytes);
+int ensure_scratch(DevCtx& d, size_t bytes);
+
+// Validation helpers mirroring the reference's constructors.
+int check_field(const double* u, size_t n);  // BasicField ctor, core.hpp:45-51
+int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
+                    std::vector<double>& out);  // sync_solver.cpp:25-37
+
+inline size_t default_stride(size_t n) { return n <= 1000 ? 1 : 100; }
+
+// Synchronous advance on device buffers (ping-pong).  `cur` selects the
+// buffer holding u(k) on entry and is updated.  Does not synchronise.
+template <typename Real>
+int sync_advance(int sms, Real* bufs[2], int& cur, long long n, double r, int periodic,
+                 double c1, double c2, size_t steps, unsigned int* flag, cudaStream_t st);
+
+}  // namespace hb

@@ -1,0 +1,510 @@
+"""Python mirror of the reference's solver API (namespace heat), running on the
+B200 through the C-ABI in include/heat_b200.h.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/heat/{core,sync_solver,async_sim,async_exec}.hpp;
+the exception classes in ``_lib`` stand in for the C++ exception types
+(``DomainError`` ~ std::domain_error, ``InvalidArgument`` ~
+std::invalid_argument, ``LogicError`` ~ std::logic_error, ``DivergenceError``).
+Every solver call executes the sm_100a kernels; nothing here steps the field
+on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (DivergenceError, DomainError, InvalidArgument, LogicError,  # noqa: F401
+                   NativeUnavailable, WatchdogTimeout)
+
+
+# ---- core.hpp:11-35 -------------------------------------------------------
+def derive_r(alpha: float, dt: float, dx: float) -> float:
+    """core.cpp:7-11"""
+    if not (alpha > 0.0) or not (dt > 0.0) or not (dx > 0.0):
+        raise DomainError("derive_r: alpha, dt, dx must all be positive")
+    return alpha * dt / (dx * dx)
+
+
+class SolverParams:
+    """core.hpp:13-35: r = alpha*dt/dx^2, always re-derived."""
+
+    __slots__ = ("_alpha", "_dt", "_dx")
+
+    def __init__(self, alpha: float, dt: float, dx: float, _token=None):
+        if _token is not SolverParams._TOKEN:
+            raise TypeError("use SolverParams.checked / unchecked / from_r")
+        self._alpha, self._dt, self._dx = float(alpha), float(dt), float(dx)
+
+    _TOKEN = object()
+
+    @staticmethod
+    def checked(alpha: float, dt: float, dx: float) -> "SolverParams":
+        r = derive_r(alpha, dt, dx)
+        if not (r > 0.0) or r > 0.5:
+            raise DomainError("SolverParams: r = alpha*dt/dx^2 must lie in (0, 0.5]")
+        return SolverParams(alpha, dt, dx, SolverParams._TOKEN)
+
+    @staticmethod
+    def unchecked(alpha: float, dt: float, dx: float) -> "SolverParams":
+        derive_r(alpha, dt, dx)
+        return SolverParams(alpha, dt, dx, SolverParams._TOKEN)
+
+    @staticmethod
+    def from_r(r: float, allow_unstable: bool = False) -> "SolverParams":
+        return (SolverParams.unchecked if allow_unstable else SolverParams.checked)(r, 1.0, 1.0)
+
+    def alpha(self) -> float:
+        return self._alpha
+
+    def dt(self) -> float:
+        return self._dt
+
+    def dx(self) -> float:
+        return self._dx
+
+    def r(self) -> float:
+        return self._alpha * self._dt / (self._dx * self._dx)
+
+
+class TemperatureField:
+    """core.hpp:40-64 BasicField<double>: N >= 3, all values finite."""
+
+    __slots__ = ("_v",)
+
+    def __init__(self, values: Sequence[float] | np.ndarray):
+        v = np.array(values, dtype=np.float64, copy=True).reshape(-1)
+        if v.size < 3:
+            raise DomainError("TemperatureField requires N >= 3")
+        if not np.all(np.isfinite(v)):
+            raise DomainError("TemperatureField values must be finite")
+        v.setflags(write=False)
+        self._v = v
+
+    def size(self) -> int:
+        return int(self._v.size)
+
+    def __len__(self) -> int:
+        return int(self._v.size)
+
+    def __getitem__(self, i):
+        return self._v[i]
+
+    def values(self) -> np.ndarray:
+        return self._v
+
+    def __eq__(self, other) -> bool:  # element-wise == like std::vector<double>
+        return isinstance(other, TemperatureField) and self._v.shape == other._v.shape and bool(
+            np.all(self._v == other._v))
+
+    def __repr__(self) -> str:
+        return f"TemperatureField(N={self._v.size})"
+
+
+@dataclass(frozen=True)
+class BoundaryCondition:
+    """core.hpp:66-81"""
+
+    kind: int = _lib.BC_DIRICHLET
+    c1: float = 0.0
+    c2: float = 0.0
+
+    @staticmethod
+    def dirichlet(c1: float, c2: float) -> "BoundaryCondition":
+        return BoundaryCondition(_lib.BC_DIRICHLET, float(c1), float(c2))
+
+    @staticmethod
+    def periodic() -> "BoundaryCondition":
+        return BoundaryCondition(_lib.BC_PERIODIC, 0.0, 0.0)
+
+    def is_dirichlet(self) -> bool:
+        return self.kind == _lib.BC_DIRICHLET
+
+
+class PartitionSpec:
+    """core.hpp:83-102, core.cpp:66-72"""
+
+    def __init__(self, total_points: int, points_per_pe: int):
+        if total_points < 3:
+            raise DomainError("PartitionSpec: N >= 3 required")
+        if points_per_pe == 0 or total_points % points_per_pe != 0:
+            raise DomainError("PartitionSpec: n must divide N")
+        self._total, self._per = int(total_points), int(points_per_pe)
+
+    def total(self) -> int:
+        return self._total
+
+    def per_pe(self) -> int:
+        return self._per
+
+    def pe_count(self) -> int:
+        return self._total // self._per
+
+    def pe_of(self, i: int) -> int:
+        return i // self._per
+
+    def crosses(self, i: int, j: int) -> bool:
+        return self.pe_of(i) != self.pe_of(j)
+
+
+# ---- harness helpers (core.hpp:111-123); CPU, not on the hot path ----------
+def cosine_init(n_points: int) -> TemperatureField:
+    """core.cpp:29-39 (math.cos is the platform libm cos, as std::cos)."""
+    if n_points < 3:
+        raise DomainError("cosine_init: N >= 3 required")
+    v = []
+    for i in range(n_points):
+        c = math.cos(3.0 * math.pi / 2.0 * float(i) / float(n_points - 1))
+        v.append(c * c)
+    return TemperatureField(v)
+
+
+def linear_steady_state(n_points: int, c1: float, c2: float) -> TemperatureField:
+    """core.cpp:41-48"""
+    if n_points < 3:
+        raise DomainError("linear_steady_state: N >= 3 required")
+    return TemperatureField([c1 + (c2 - c1) * float(i) / float(n_points - 1)
+                             for i in range(n_points)])
+
+
+def l2_norm(u) -> float:
+    """core.cpp:50-56 (sequential sum, same rounding order)."""
+    v = u.values() if isinstance(u, TemperatureField) else np.asarray(u, np.float64)
+    s = 0.0
+    for x in v.tolist():
+        s += x * x
+    return math.sqrt(s)
+
+
+def total_heat(u) -> float:
+    """core.cpp:58-64"""
+    v = u.values() if isinstance(u, TemperatureField) else np.asarray(u, np.float64)
+    s = 0.0
+    for x in v.tolist():
+        s += x
+    return s
+
+
+# ---- sync_solver.hpp -------------------------------------------------------
+@dataclass
+class Trajectory:
+    """sync_solver.hpp:12-20"""
+
+    snapshots: list
+    steps: list
+    params: SolverParams
+    bc: BoundaryCondition
+
+    def initial(self) -> TemperatureField:
+        return self.snapshots[0]
+
+    def final(self) -> TemperatureField:
+        return self.snapshots[-1]
+
+
+K_DIRICHLET_END_TOL = 1e-9  # sync_solver.hpp:44
+
+
+def default_stride(n_points: int) -> int:
+    """sync_solver.hpp:52-54"""
+    return 1 if n_points <= 1000 else 100
+
+
+def set_strict_finite_checks(enabled: bool) -> None:
+    _lib.lib().heat_set_strict_finite_checks(int(bool(enabled)))
+
+
+def strict_finite_checks() -> bool:
+    return bool(_lib.lib().heat_strict_finite_checks())
+
+
+def _field(u0) -> np.ndarray:
+    if isinstance(u0, TemperatureField):
+        return np.ascontiguousarray(u0.values())
+    return np.ascontiguousarray(TemperatureField(u0).values())
+
+
+def _trajectory(fn, what, u0, params, bc, k_end, stride, extra=()) -> Trajectory:
+    v = _field(u0)
+    n = v.size
+    L = _lib.lib()
+    count = L.heat_trajectory_length(n, k_end, stride)
+    snaps = np.empty((count, n), np.float64)
+    steps = np.empty(count, np.uintp)
+    ns = C.c_size_t(0)
+    _lib.check(fn(_lib.dptr(v), n, params.r(), bc.kind, bc.c1, bc.c2, *extra, k_end, stride,
+                  C.cast(None, _lib._pd), _lib.dptr(snaps), _lib.szptr(steps), count,
+                  C.byref(ns)), what)
+    m = ns.value
+    return Trajectory([TemperatureField(snaps[j]) for j in range(m)],
+                      [int(s) for s in steps[:m]], params, bc)
+
+
+def sync_step(u: TemperatureField, params: SolverParams, bc: BoundaryCondition) -> TemperatureField:
+    """sync_solver.hpp:60-62"""
+    v = _field(u)
+    out = np.empty_like(v)
+    _lib.check(_lib.lib().heat_sync_step(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1, bc.c2,
+                                         _lib.dptr(out)), "sync_step")
+    return TemperatureField(out)
+
+
+def sync_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition, k_end: int,
+             stride: int = 1) -> Trajectory:
+    """sync_solver.hpp:64-67"""
+    return _trajectory(_lib.lib().heat_sync_run, "sync_run", u0, params, bc, k_end, stride)
+
+
+def sync_run_f32(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition, k_end: int,
+                 stride: int = 1) -> Trajectory:
+    """sync_solver.hpp:69-73"""
+    return _trajectory(_lib.lib().heat_sync_run_f32, "sync_run_f32", u0, params, bc, k_end, stride)
+
+
+def sync_final(u0, params: SolverParams, bc: BoundaryCondition, k_end: int) -> np.ndarray:
+    """Final state only (no snapshot copies): sync_run(...).final() without the trajectory."""
+    v = _field(u0)
+    out = np.empty_like(v)
+    _lib.check(_lib.lib().heat_sync_run(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1, bc.c2,
+                                        k_end, k_end or 1, _lib.dptr(out), None, None, 0, None),
+               "sync_run")
+    return out
+
+
+# ---- async_sim.hpp -----------------------------------------------------------
+class Distribution(enum.IntEnum):
+    Uniform = _lib.DELAY_UNIFORM
+    Fixed = _lib.DELAY_FIXED
+    GeometricTruncated = _lib.DELAY_GEOMETRIC
+
+
+@dataclass
+class DelayModel:
+    """async_sim.hpp:16-28, factories async_sim.cpp:7-23"""
+
+    q: int = 1
+    distribution: Distribution = Distribution.Uniform
+    fixed_delay: int = 0
+    geometric_p: float = 0.5
+    seed: int = 0
+
+    @staticmethod
+    def uniform(q: int, seed: int) -> "DelayModel":
+        if q == 0:
+            raise DomainError("DelayModel: q >= 1 required")
+        return DelayModel(q, Distribution.Uniform, 0, 0.5, seed)
+
+    @staticmethod
+    def fixed(q: int, d: int, seed: int) -> "DelayModel":
+        if q == 0:
+            raise DomainError("DelayModel: q >= 1 required")
+        if d >= q:
+            raise DomainError("DelayModel: fixed delay must satisfy d < q")
+        return DelayModel(q, Distribution.Fixed, d, 0.5, seed)
+
+    @staticmethod
+    def geometric(q: int, p: float, seed: int) -> "DelayModel":
+        if q == 0:
+            raise DomainError("DelayModel: q >= 1 required")
+        if not (p > 0.0) or p > 1.0:
+            raise DomainError("DelayModel: geometric p must lie in (0, 1]")
+        return DelayModel(q, Distribution.GeometricTruncated, 0, p, seed)
+
+    def _args(self):
+        return (self.q, int(self.distribution), self.fixed_delay, self.geometric_p,
+                self.seed & 0xFFFFFFFFFFFFFFFF)
+
+
+def sample_delay_at(model: DelayModel, j: int, k: int) -> int:
+    """Counter form of sample_delay (async_sim.cpp:57-73): the j-th draw at step k."""
+    d = C.c_size_t(0)
+    _lib.check(_lib.lib().heat_sample_delay(*model._args(), j, k, C.byref(d)), "sample_delay")
+    return d.value
+
+
+def async_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
+              part: PartitionSpec, model: DelayModel, k_end: int, stride: int = 1) -> Trajectory:
+    """async_sim.hpp:97-101 -- the seeded delay stream replayed on the GPU."""
+    v = _field(u0)
+    if part.total() != v.size:
+        raise InvalidArgument("AsyncSimulator: partition inconsistent with grid")
+    return _trajectory(_lib.lib().heat_async_run, "async_run", v, params, bc, k_end, stride,
+                       extra=(part.per_pe(), *model._args()))
+
+
+def async_final(u0, params: SolverParams, bc: BoundaryCondition, part: PartitionSpec,
+                model: DelayModel, k_end: int) -> np.ndarray:
+    """Final state of async_run without the trajectory copies."""
+    v = _field(u0)
+    if part.total() != v.size:
+        raise InvalidArgument("AsyncSimulator: partition inconsistent with grid")
+    out = np.empty_like(v)
+    _lib.check(_lib.lib().heat_async_run(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1, bc.c2,
+                                         part.per_pe(), *model._args(), k_end, k_end or 1,
+                                         _lib.dptr(out), None, None, 0, None), "async_run")
+    return out
+
+
+# ---- async_exec.hpp ----------------------------------------------------------
+class ExecMode(enum.IntEnum):
+    Barriered = _lib.EXEC_BARRIERED
+    BarrierFree = _lib.EXEC_BARRIER_FREE
+
+
+def to_string(mode: ExecMode) -> str:
+    return "barriered" if mode == ExecMode.Barriered else "barrier-free"
+
+
+@dataclass
+class LagStats:
+    """async_exec.hpp:42-51"""
+
+    reads: int = 0
+    min_lag: int = 0
+    max_lag: int = 0
+    histogram: list = field(default_factory=list)
+    overflow: int = 0
+
+    def merge(self, other: "LagStats") -> None:
+        if other.reads == 0:
+            return
+        if self.reads == 0:
+            self.reads, self.min_lag, self.max_lag = other.reads, other.min_lag, other.max_lag
+            self.histogram, self.overflow = list(other.histogram), other.overflow
+            return
+        self.min_lag = min(self.min_lag, other.min_lag)
+        self.max_lag = max(self.max_lag, other.max_lag)
+        self.reads += other.reads
+        if len(self.histogram) < len(other.histogram):
+            self.histogram += [0] * (len(other.histogram) - len(self.histogram))
+        for i, c in enumerate(other.histogram):
+            self.histogram[i] += c
+        self.overflow += other.overflow
+
+    def mean(self) -> float:
+        if self.reads == 0:
+            return 0.0
+        return sum(float(d) * float(c) for d, c in enumerate(self.histogram)) / float(self.reads)
+
+
+@dataclass
+class AsyncStats:
+    """Reader-relative delay log of the GPU free-running executor."""
+
+    reads: int = 0
+    max_delay: int = 0
+    delay_histogram: list = field(default_factory=list)
+    waits: int = 0
+    residual_sum: float = 0.0
+
+
+@dataclass
+class ExecConfig:
+    """async_exec.hpp:53-58 (+ q_free: the GPU free-running staleness bound)."""
+
+    workers: int = 1
+    k_end: int = 1
+    mode: ExecMode = ExecMode.Barriered
+    record_lag: bool = False
+    q_free: int = 0
+
+
+@dataclass
+class ExecResult:
+    """async_exec.hpp:60-66 (duration is GPU device time, ns)."""
+
+    field: TemperatureField
+    steps_per_pe: list
+    duration_ns: int = 0
+    oversubscribed: bool = False
+    lag: Optional[LagStats] = None
+    stats: Optional[AsyncStats] = None
+
+
+def exec_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
+             part: PartitionSpec, cfg: ExecConfig) -> ExecResult:
+    """async_exec.hpp:68-70 / async_exec.cpp:263-279"""
+    v = _field(u0)
+    out = np.empty_like(v)
+    dur = C.c_uint64(0)
+    lag = _lib.LagStatsC()
+    st = _lib.AsyncStatsC()
+    _lib.check(_lib.lib().heat_exec_run(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1, bc.c2,
+                                        part.per_pe(), cfg.workers, cfg.k_end, int(cfg.mode),
+                                        int(cfg.record_lag), cfg.q_free, _lib.dptr(out),
+                                        C.byref(dur), C.byref(lag), C.byref(st)), "exec_run")
+    res = ExecResult(TemperatureField(out), [cfg.k_end] * cfg.workers, int(dur.value))
+    if cfg.record_lag:
+        res.lag = LagStats(int(lag.reads), int(lag.min_lag), int(lag.max_lag),
+                           [int(x) for x in lag.histogram], int(lag.overflow))
+    if cfg.mode == ExecMode.BarrierFree:
+        res.stats = AsyncStats(int(st.reads), int(st.max_delay),
+                               [int(x) for x in st.delay_histogram], int(st.waits),
+                               float(st.residual_sum))
+    return res
+
+
+# ---- device-resident plan ------------------------------------------------------
+class Plan:
+    """A field resident in HBM (heat_plan_*): bench and multi-GPU slabs."""
+
+    def __init__(self, n: int, device: int = 0):
+        self._h = C.c_void_p()
+        _lib.check(_lib.lib().heat_plan_create(C.byref(self._h), n, device), "heat_plan_create")
+        self.n = n
+        self.device = device
+
+    def close(self):
+        if self._h:
+            _lib.lib().heat_plan_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int | None):
+        _lib.check(_lib.lib().heat_plan_set_stream(self._h, stream_handle), "set_stream")
+
+    def upload(self, host: np.ndarray):
+        assert host.dtype == np.float64 and host.size == self.n and host.flags.c_contiguous
+        _lib.check(_lib.lib().heat_plan_upload(self._h, host.ctypes.data), "upload")
+
+    def download(self, host: Optional[np.ndarray] = None) -> np.ndarray:
+        if host is None:
+            host = np.empty(self.n, np.float64)
+        _lib.check(_lib.lib().heat_plan_download(self._h, host.ctypes.data), "download")
+        return host
+
+    def fill_sine(self):
+        _lib.check(_lib.lib().heat_plan_fill_sine(self._h), "fill_sine")
+
+    def sync_advance(self, r: float, bc: BoundaryCondition, steps: int):
+        _lib.check(_lib.lib().heat_plan_sync_advance(self._h, r, bc.kind, bc.c1, bc.c2, steps),
+                   "sync_advance")
+
+    def async_advance(self, r: float, bc: BoundaryCondition, per_pe: int, q: int, steps: int):
+        st = _lib.AsyncStatsC()
+        _lib.check(_lib.lib().heat_plan_async_advance(self._h, r, bc.kind, bc.c1, bc.c2, per_pe,
+                                                      q, steps, C.byref(st)), "async_advance")
+        return st
+
+    def synchronize(self):
+        _lib.check(_lib.lib().heat_plan_synchronize(self._h), "synchronize")
+
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        _lib.check(_lib.lib().heat_plan_device_ptr(self._h, C.byref(p)), "device_ptr")
+        return int(p.value or 0)
+
+
+def kernel_launches() -> int:
+    return int(_lib.lib().heat_kernel_launches())
