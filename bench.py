@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""Benchmark of the FTCS hot path (BASELINE.json metric: FP64 lattice updates/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[2], "cfg3"): N = 2^30 FP64 points per GPU,
+r = from_r(0.4), Dirichlet(0,0), sine initial profile, 10^4 FTCS time steps.
+One bench STEP = 1000 FTCS time steps over the whole field, so the default
+--steps 10 is exactly the cfg3 run.  For N > 1 GPUs (torchrun, one rank per
+GPU) each rank owns a 2^30-point slab of a G*2^30 domain (weak scaling) and
+exchanges 32-point ghosts with its neighbours every 32-step pass.
+
+Arms
+  b200       the sm_100a kernels (libheat_b200.so) -- value is device-timed
+             with inputs resident in HBM; e2e is timed through the C-ABI
+             (heat_sync_run with pinned host buffers, copies included).
+  reference  the reference's own CPU executor (exec_run Barriered, all host
+             threads) from oracle/_ref (compiled from /root/reference), or the
+             C port when that library is absent; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 lattice updates/s (GLUPS) at 1/2/4/8 B200, % HBM roofline, async vs sync"
+UNIT = "GLUPS"
+N_PER_GPU = 1 << 30
+R = 0.4
+STEPS_PER_BENCH_STEP = 1000
+STEPS_PER_PASS = 32
+BYTES_PER_UPDATE = 16  # one FP64 read + one FP64 write per point per step
+FP64_OPS_PER_UPDATE = 4  # 2 DMUL + 2 DADD with the shared r*u products
+CPU_SAMPLE_STEPS = 4
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic_per_launch():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("sync_tb_kernel", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons during the timed region (NVML)."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def cpu_baseline_run(n: int, steps: int, warm: bool = True):
+    """The reference's exec_run(Barriered) on all host threads (oracle/_ref),
+    or the C port's threaded executor when the reference library is absent.
+    Returns (GLUPS, cores, kind, sample description)."""
+    from oracle import oracle as O
+    port = O.port()
+    u0 = port.sine_init(n)
+    u0[0] = 0.0
+    u0[-1] = 0.0
+    kind = "reference" if O.Ref.available() else "port"
+    eng = O.ref() if kind == "reference" else port
+    hw = os.cpu_count() or 1
+    if kind == "reference":
+        hw = eng.hardware_concurrency() or hw
+    workers = 1
+    while workers * 2 <= hw and n % (workers * 2) == 0:
+        workers *= 2
+    if kind == "reference":
+        fin, dur, _ = eng.exec_run(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
+                                   O.BARRIERED)
+    else:
+        fin, dur = eng.exec_run(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
+                                O.BARRIERED)
+    glups = n * steps / (dur * 1e-9) / 1e9
+    sample = (f"N=2^{n.bit_length() - 1} FP64, {steps} FTCS steps, exec_run(Barriered) with P={workers} "
+              f"threads; time = exec_run's own duration (thread spawn..join, async_exec.cpp:101-106)")
+    return glups, workers, kind, sample
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    n = N_PER_GPU
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        g, cores, kind, sample = cpu_baseline_run(n, CPU_SAMPLE_STEPS)
+        if i >= args.warmup:
+            vals.append(g)
+        info = (cores, kind, sample)
+    v = statistics.median(vals)
+    ms = n * CPU_SAMPLE_STEPS / (v * 1e9) * 1e3 * (STEPS_PER_BENCH_STEP / CPU_SAMPLE_STEPS)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (sine IC)",
+        "config": config_dict(world),
+        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": info[0], "kind": info[1],
+                         "sample": info[2] + f"; median of {args.steps} samples"},
+        "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(world):
+    return {
+        "workload": "cfg3: N=2^30 FP64 per GPU, r=0.4, Dirichlet(0,0), sine IC, "
+                    "10^4 FTCS steps (= 10 bench steps of 1000)" +
+                    ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"),
+        "N_per_gpu": N_PER_GPU, "N_total": N_PER_GPU * world, "r": R,
+        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": STEPS_PER_PASS,
+        "kernel": "sync_tb_kernel<double,32> (temporal-blocked, 32 steps per HBM pass)",
+        "l2": "inputs larger than L2 (8 GiB per array vs 126 MB L2)",
+        "parallelism": "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)",
+    }
+
+
+def run_b200(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_1510_08982_b200 import heat as H
+    from paper_1510_08982_b200 import multigpu as MG
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream(local)
+    n = N_PER_GPU
+    bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
+    r = H.SolverParams.from_r(R).r()
+
+    if world == 1:
+        plan = H.Plan(n, local)
+        plan.set_stream(stream.cuda_stream)
+        plan.fill_sine()
+
+        def advance(k):
+            plan.sync_advance(r, bc, k)
+    else:
+        solver = MG.SlabSolver(n, r, bc, local, rank, world)
+        solver.plan.fill_sine()  # each slab gets a sine profile (data-independent cost)
+        plan = solver.plan
+
+        def advance(k):
+            solver.advance(k)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        advance(STEPS_PER_BENCH_STEP)
+    plan.synchronize()
+    barrier()
+
+    launches0 = H.kernel_launches()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            advance(STEPS_PER_BENCH_STEP)
+        e1.record(stream)
+        barrier()
+    plan.synchronize()
+    launches = H.kernel_launches() - launches0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_updates = float(n) * world * STEPS_PER_BENCH_STEP * args.steps
+    glups = total_updates / (ms * 1e-3) / 1e9
+
+    # Roofline of the dominant kernel: every launch is one 32-step pass.
+    passes_per_step = -(-STEPS_PER_BENCH_STEP // STEPS_PER_PASS)
+    sync_launches = passes_per_step * args.steps
+    per_launch_s = ms * 1e-3 / sync_launches
+    alg_bytes = BYTES_PER_UPDATE * n * STEPS_PER_PASS
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / per_launch_s / 1e9
+    fp64_peak = 148 * 64 * 1.965e9 / 1e12  # DP lanes x SMs x boost clock, T ops/s (nominal)
+    fp64_achieved = FP64_OPS_PER_UPDATE * n * STEPS_PER_PASS / per_launch_s / 1e12
+    roofline = {
+        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(achieved / peak, 4), "traffic": ncu_traffic_per_launch(),
+        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+        "algorithmic_bytes_per_launch": alg_bytes,
+        "note": "effective bandwidth with temporal blocking (16 B/update counted for every "
+                "step); the pass itself is FP64-pipe bound, see fp64",
+        "fp64": {"ops_per_update": FP64_OPS_PER_UPDATE, "achieved_tops": round(fp64_achieved, 3),
+                 "peak_tops_nominal": round(fp64_peak, 3),
+                 "frac": round(fp64_achieved / fp64_peak, 4)},
+    }
+
+    # End to end through the public API with host buffers (copies timed).
+    e2e = None
+    if not args.skip_e2e:
+        e2e = run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        g, cores, kind, sample = cpu_baseline_run(n, CPU_SAMPLE_STEPS)
+        cpu = {"value": round(g, 4), "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": round(glups, 3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (sine IC generated on device)", "config": config_dict(world),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance):
+    """Same metric through the public API with HOST buffers: per step the
+    pinned host field goes H2D, 1000 FTCS steps run, the result comes back D2H."""
+    k = max(1, min(args.steps, 3))
+    host_in = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    plan.download(host_in.numpy())  # a valid (prepared) field to start from
+    a_in, a_out = host_in.numpy(), host_out.numpy()
+    times = []
+    for i in range(k + 1):
+        if world == 1:
+            t0 = time.perf_counter()
+            H._lib.check(H._lib.lib().heat_sync_run(
+                H._lib.dptr(a_in), n, r, bc.kind, bc.c1, bc.c2, STEPS_PER_BENCH_STEP,
+                STEPS_PER_BENCH_STEP, H._lib.dptr(a_out), None, None, 0, None), "heat_sync_run")
+            t1 = time.perf_counter()
+        else:
+            import torch.distributed as dist
+            dist.barrier()
+            t0 = time.perf_counter()
+            plan.upload(a_in)
+            advance(STEPS_PER_BENCH_STEP)
+            plan.download(a_out)
+            dist.barrier()
+            t1 = time.perf_counter()
+        if i > 0:
+            times.append(t1 - t0)
+    t = statistics.median(times)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    v = float(n) * world * STEPS_PER_BENCH_STEP / t / 1e9
+    return {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+            "d2h_bytes_per_step": 8 * n, "steps": k,
+            "api": "heat_sync_run (C-ABI, pinned host buffers)" if world == 1 else
+                   "heat.Plan upload/advance/download per rank"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -156,6 +156,19 @@ int heat_plan_synchronize(heat_plan* plan);
 /* Device pointer of the current field (for peer copies / NCCL in multi-GPU). */
 int heat_plan_device_ptr(heat_plan* plan, double** cur);
 
+/* ---- multi-GPU slabs (1-D domain decomposition, no reference counterpart:
+ * the reference is single-process) -------------------------
+ * Rank `rank` of `world` owns n_local consecutive points of the global field.
+ * Every pass of <= heat_slab_halo() steps needs fresh ghosts: pack the slab's
+ * first/last H points into a 2H-double device buffer, exchange with the
+ * neighbours (NCCL / peer copy), unpack the neighbours' points as ghosts.
+ * Only the true global ends are pinned (rank 0 / rank world-1, Dirichlet);
+ * periodic slabs wrap through the exchange. */
+size_t heat_slab_halo(void);
+int heat_plan_create_slab(heat_plan** plan, size_t n_local, int device, int rank, int world);
+int heat_plan_halo_pack(heat_plan* plan, void* dst_device);
+int heat_plan_halo_unpack(heat_plan* plan, const void* src_device);
+
 #ifdef __cplusplus
 }
 #endif

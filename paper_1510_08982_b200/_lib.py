@@ -119,6 +119,10 @@ SIGNATURES = {
     "heat_plan_async_advance": (_i, [_vp, _d, _i, _d, _d, _sz, _sz, _sz, _P(AsyncStatsC)]),
     "heat_plan_synchronize": (_i, [_vp]),
     "heat_plan_device_ptr": (_i, [_vp, _P(_vp)]),
+    "heat_slab_halo": (_sz, []),
+    "heat_plan_create_slab": (_i, [_P(_vp), _sz, _i, _i, _i]),
+    "heat_plan_halo_pack": (_i, [_vp, _vp]),
+    "heat_plan_halo_unpack": (_i, [_vp, _vp]),
 }
 
 _lib = None

@@ -4,8 +4,15 @@
 
 #include "runtime.cuh"
 
+// Every plan is a slab with kSlabHalo ghost points on each side:
+// array = [ghost H | n owned points | ghost H].  A single-GPU plan
+// (world == 1) ignores the ghosts and advances the owned points as a whole
+// domain; a multi-GPU slab (world > 1) gets its ghosts refreshed by the caller
+// (heat_plan_halo_pack / _unpack around an NCCL or peer exchange) before each
+// pass of <= H steps, and only the true global ends are pinned.
 struct heat_plan {
     int device = 0;
+    int rank = 0, world = 1;
     size_t n = 0;
     size_t pitch = 0;
     double* base = nullptr;
@@ -14,7 +21,8 @@ struct heat_plan {
     cudaStream_t stream = nullptr;
     unsigned int* flag = nullptr;
     int sms = 0;
-    double* bufs[2] = {nullptr, nullptr};
+    double* bufs[2] = {nullptr, nullptr};  // owned points (base + H)
+    double* ext[2] = {nullptr, nullptr};   // ghosted arrays (base)
 };
 
 namespace hb {
@@ -45,7 +53,7 @@ int heat_plan_create(heat_plan** out, size_t n, int device) {
     auto* p = new heat_plan();
     p->device = d->device;
     p->n = n;
-    p->pitch = (n + 63) / 64 * 64;
+    p->pitch = (n + 2 * kSlabHalo + 63) / 64 * 64;
     p->sms = d->sms;
     cudaError_t e = cudaMalloc(&p->base, 2 * p->pitch * sizeof(double));
     if (e != cudaSuccess) {
@@ -53,8 +61,11 @@ int heat_plan_create(heat_plan** out, size_t n, int device) {
         delete p;
         return fail(HEAT_ENOMEM, std::string("plan cudaMalloc: ") + cudaGetErrorString(e));
     }
-    p->bufs[0] = p->base;
-    p->bufs[1] = p->base + p->pitch;
+    p->ext[0] = p->base;
+    p->ext[1] = p->base + p->pitch;
+    p->bufs[0] = p->ext[0] + kSlabHalo;
+    p->bufs[1] = p->ext[1] + kSlabHalo;
+    HB_CUDA(cudaMemset(p->base, 0, 2 * p->pitch * sizeof(double)));
     HB_CUDA(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
     p->stream = p->own;
     HB_CUDA(cudaMalloc(&p->flag, 4 * sizeof(unsigned int)));
@@ -112,8 +123,56 @@ int heat_plan_sync_advance(heat_plan* p, double r, int bc_kind, double c1, doubl
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     HB_CUDA(cudaSetDevice(p->device));
-    return sync_advance<double>(p->sms, p->bufs, p->cur, (long long)p->n, r,
-                                bc_kind == HEAT_BC_PERIODIC, c1, c2, steps, p->flag, p->stream);
+    if (p->world == 1)
+        return sync_advance<double>(p->sms, p->bufs, p->cur, (long long)p->n, r,
+                                    bc_kind == HEAT_BC_PERIODIC, c1, c2, steps, p->flag,
+                                    p->stream);
+    if (steps > size_t(kSlabHalo))
+        return fail(HEAT_EINVAL, "slab plans advance at most heat_slab_halo() steps per exchange");
+    const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+    SlabGeom g;
+    g.len = (long long)p->n + 2 * kSlabHalo;
+    g.out_lo = kSlabHalo;
+    g.out_hi = kSlabHalo + (long long)p->n;
+    g.pin_lo = (dir && p->rank == 0) ? kSlabHalo : -1;
+    g.pin_hi = (dir && p->rank == p->world - 1) ? kSlabHalo + (long long)p->n - 1 : -1;
+    g.wrap = 0;
+    return sync_advance_slab<double>(p->sms, p->ext, p->cur, g, r, c1, c2, steps, p->flag,
+                                     p->stream);
+}
+
+size_t heat_slab_halo(void) { return size_t(kSlabHalo); }
+
+int heat_plan_create_slab(heat_plan** out, size_t n_local, int device, int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) return fail(HEAT_EINVAL, "bad rank/world");
+    if (n_local < size_t(kSlabHalo))
+        return fail(HEAT_EDOMAIN, "slab smaller than the halo width");
+    HB_TRY(heat_plan_create(out, n_local, device));
+    (*out)->rank = rank;
+    (*out)->world = world;
+    return HEAT_OK;
+}
+
+int heat_plan_halo_pack(heat_plan* p, void* dst) {
+    if (!p || !dst) return fail(HEAT_EINVAL, "null plan or buffer");
+    HB_CUDA(cudaSetDevice(p->device));
+    const size_t H = kSlabHalo, b = H * sizeof(double);
+    double* cur = p->bufs[p->cur];
+    HB_CUDA(cudaMemcpyAsync(dst, cur, b, cudaMemcpyDeviceToDevice, p->stream));
+    HB_CUDA(cudaMemcpyAsync(static_cast<double*>(dst) + H, cur + p->n - H, b,
+                            cudaMemcpyDeviceToDevice, p->stream));
+    return HEAT_OK;
+}
+
+int heat_plan_halo_unpack(heat_plan* p, const void* src) {
+    if (!p || !src) return fail(HEAT_EINVAL, "null plan or buffer");
+    HB_CUDA(cudaSetDevice(p->device));
+    const size_t H = kSlabHalo, b = H * sizeof(double);
+    double* ext = p->ext[p->cur];
+    HB_CUDA(cudaMemcpyAsync(ext, src, b, cudaMemcpyDeviceToDevice, p->stream));
+    HB_CUDA(cudaMemcpyAsync(ext + H + p->n, static_cast<const double*>(src) + H, b,
+                            cudaMemcpyDeviceToDevice, p->stream));
+    return HEAT_OK;
 }
 
 int heat_plan_synchronize(heat_plan* p) {

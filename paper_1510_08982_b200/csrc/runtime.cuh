@@ -63,6 +63,18 @@ int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c
 
 inline size_t default_stride(size_t n) { return n <= 1000 ? 1 : 100; }
 
+// Geometry of one synchronous pass (see SyncPassArgs in sync_tb.cuh).
+struct SlabGeom {
+    long long len = 0, out_lo = 0, out_hi = 0, pin_lo = -1, pin_hi = -1;
+    int wrap = 0;
+};
+constexpr int kSlabHalo = 32;  // ghost points per side of a multi-GPU slab (= V)
+
+template <typename Real>
+int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,
+                      double c2, size_t steps, unsigned int* flag, cudaStream_t st,
+                      int max_steps_per_pass = 0);
+
 // Synchronous advance on device buffers (ping-pong).  `cur` selects the
 // buffer holding u(k) on entry and is updated.  Does not synchronise.
 template <typename Real>

@@ -32,16 +32,35 @@ int occupancy_blocks(int sms) {
 template <typename Real>
 int sync_advance(int sms, Real* bufs[2], int& cur, long long n, double r, int periodic,
                  double c1, double c2, size_t steps, unsigned int* flag, cudaStream_t st) {
+    SlabGeom g;
+    g.len = n;
+    g.out_lo = 0;
+    g.out_hi = n;
+    g.pin_lo = periodic ? -1 : 0;
+    g.pin_hi = periodic ? -1 : n - 1;
+    g.wrap = periodic;
+    return sync_advance_slab<Real>(sms, bufs, cur, g, r, c1, c2, steps, flag, st);
+}
+
+template <typename Real>
+int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,
+                      double c2, size_t steps, unsigned int* flag, cudaStream_t st,
+                      int max_steps_per_pass) {
     using T = SyncTB<Real, kV>;
     if (steps == 0) return HEAT_OK;
     int occ = occupancy_blocks<Real>(sms);
     if (occ > 0) return occ;
     occ = -occ;
-    const long long tiles = (n + T::kOut - 1) / T::kOut;
+    const long long tiles = (g.out_hi - g.out_lo + T::kOut - 1) / T::kOut;
     const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
     const int grid = int(std::min<long long>(want, (long long)sms * occ));
     SyncPassArgs a{};
-    a.n = n;
+    a.len = g.len;
+    a.out_lo = g.out_lo;
+    a.out_hi = g.out_hi;
+    a.pin_lo = g.pin_lo;
+    a.pin_hi = g.pin_hi;
+    a.wrap = g.wrap;
     a.tiles = tiles;
     a.r = r;
     if (sizeof(Real) == 8) {
@@ -52,10 +71,11 @@ int sync_advance(int sms, Real* bufs[2], int& cur, long long n, double r, int pe
     }
     a.c1 = c1;
     a.c2 = c2;
-    a.periodic = periodic;
     a.nonfinite = flag;
+    const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, T::kMaxSteps)
+                                           : T::kMaxSteps;
     while (steps > 0) {
-        const int s = int(std::min<size_t>(steps, T::kMaxSteps));
+        const int s = int(std::min<size_t>(steps, size_t(cap)));
         a.src = bufs[cur];
         a.dst = bufs[cur ^ 1];
         a.nsteps = s;
@@ -72,46 +92,110 @@ template int sync_advance<double>(int, double* [2], int&, long long, double, int
                                   size_t, unsigned int*, cudaStream_t);
 template int sync_advance<float>(int, float* [2], int&, long long, double, int, double, double,
                                  size_t, unsigned int*, cudaStream_t);
+template int sync_advance_slab<double>(int, double* [2], int&, const SlabGeom&, double, double,
+                                       double, size_t, unsigned int*, cudaStream_t, int);
 
 namespace {
 
-// Shared body of sync_run / sync_run_f32 (sync_solver.cpp:52-91).
+// Device-side TemperatureField validation (core.hpp:45-51): flag[2] |= 1 on a
+// non-finite value.  Runs right after the upload so the host never walks the
+// field (an O(N) host pass would dominate end-to-end time at N = 2^30).
+__global__ void validate_kernel(const double* __restrict__ u, long long n, unsigned int* flag) {
+    bool bad = false;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        bad |= !isfinite(u[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag + 2, 1u);
+}
+
+__global__ void narrow_kernel(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = float(in[i]);
+}
+
+// Upload u0 (caller's host buffer, pinned or pageable) into `dst` (double),
+// validate it on the device and snap the Dirichlet ends
+// (prepare_initial, sync_solver.cpp:25-37).  Leaves the stream synchronised.
+int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
+                    double* dst) {
+    cudaStream_t st = d.stream;
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
+    HB_CUDA(cudaMemcpyAsync(dst, u0, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    validate_kernel<<<d.sms * 4, 256, 0, st>>>(dst, (long long)n, d.flag);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    unsigned int flags[4] = {0, 0, 0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    if (bc_kind == HEAT_BC_DIRICHLET) {
+        constexpr double kTol = 1e-9;  // kDirichletEndTol, sync_solver.hpp:44
+        if (std::abs(u0[0] - c1) > kTol || std::abs(u0[n - 1] - c2) > kTol)
+            return fail(HEAT_EINVAL, "Dirichlet BC inconsistent with initial end values");
+        const double ends[2] = {c1, c2};
+        HB_CUDA(cudaMemcpy(dst, &ends[0], sizeof(double), cudaMemcpyHostToDevice));
+        HB_CUDA(cudaMemcpy(dst + n - 1, &ends[1], sizeof(double), cudaMemcpyHostToDevice));
+    }
+    return HEAT_OK;
+}
+
+// Shared body of sync_run / sync_run_f32 (sync_solver.cpp:52-91).  Snapshots
+// and the final state are copied straight into the caller's buffers.
 template <typename Real>
 int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                   size_t k_end, size_t stride, double* final_out, double* snapshots,
                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots) {
-    HB_TRY(check_field(u0, n));
+    if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u0) return fail(HEAT_EINVAL, "null field pointer");
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     if (stride == 0) stride = default_stride(n);
-    std::vector<double> start;
-    HB_TRY(prepare_initial(u0, n, bc_kind, c1, c2, start));
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
     const size_t pitch = (n + 63) / 64 * 64;  // keep the second array 256-B aligned
-    HB_TRY(ensure_buffers(*d, 2 * pitch * sizeof(Real)));
+    const bool f32 = sizeof(Real) == 4;
+    const size_t need = 2 * pitch * sizeof(Real) + (f32 ? pitch * sizeof(double) : 0);
+    HB_TRY(ensure_buffers(*d, need));
     Real* bufs[2] = {static_cast<Real*>(d->buf[0]), static_cast<Real*>(d->buf[0]) + pitch};
+    double* staging = f32 ? reinterpret_cast<double*>(bufs[1] + pitch)
+                          : reinterpret_cast<double*>(bufs[0]);
     cudaStream_t st = d->stream;
+    HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, staging));
+    if (f32) {
+        narrow_kernel<<<d->sms * 4, 256, 0, st>>>(staging, reinterpret_cast<float*>(bufs[0]),
+                                                  (long long)n);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
 
-    std::vector<Real> host(n);
-    for (size_t i = 0; i < n; ++i) host[i] = Real(start[i]);
-    HB_CUDA(cudaMemcpyAsync(bufs[0], host.data(), n * sizeof(Real), cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemsetAsync(d->flag, 0, 2 * sizeof(unsigned int), st));
-
+    std::vector<Real> host;  // f32 staging for snapshots only
     size_t ns = 0;
-    auto record = [&](const Real* v, size_t k) {
+    // Copies the device field into snapshot row `ns` (or `final_out`).
+    auto fetch = [&](const Real* dev, double* out_row) -> int {
+        if (!f32) {
+            HB_CUDA(cudaMemcpyAsync(out_row, dev, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            return HEAT_OK;
+        }
+        host.resize(n);
+        HB_CUDA(cudaMemcpyAsync(host.data(), dev, n * sizeof(Real), cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        for (size_t i = 0; i < n; ++i) out_row[i] = double(host[i]);
+        return HEAT_OK;
+    };
+    auto record = [&](const Real* dev, size_t k) -> int {
         if (ns < max_snapshots) {
-            if (snapshots)
-                for (size_t i = 0; i < n; ++i) snapshots[ns * n + i] = double(v[i]);
+            if (snapshots) HB_TRY(fetch(dev, snapshots + ns * n));
             if (steps_out) steps_out[ns] = k;
         }
         ++ns;
+        return HEAT_OK;
     };
-    record(host.data(), 0);
-
     const bool want_snaps = snapshots != nullptr || steps_out != nullptr;
+    if (want_snaps) HB_TRY(record(bufs[0], 0));
+
     int cur = 0;
     size_t k = 0;
     const int periodic = bc_kind == HEAT_BC_PERIODIC;
@@ -123,19 +207,16 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
         k = next;
         unsigned int flags[2] = {0, 0};
         HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
-        if (want_snaps || k == k_end)
-            HB_CUDA(cudaMemcpyAsync(host.data(), bufs[cur], n * sizeof(Real),
-                                    cudaMemcpyDeviceToHost, st));
         HB_CUDA(cudaStreamSynchronize(st));
         if (flags[0]) {
             if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
             return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
         }
-        if (want_snaps) record(host.data(), k);
+        if (want_snaps) HB_TRY(record(bufs[cur], k));
     }
-    if (final_out)
-        for (size_t i = 0; i < n; ++i) final_out[i] = double(host[i]);
-    if (n_snapshots) *n_snapshots = ns;
+    if (final_out) HB_TRY(fetch(bufs[cur], final_out));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (n_snapshots) *n_snapshots = ns;  // 0 when no trajectory was requested
     return HEAT_OK;
 }
 

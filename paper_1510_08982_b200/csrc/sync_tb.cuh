@@ -116,23 +116,32 @@ __device__ __forceinline__ void warp_step(Real (&u)[V], Real r, Real c) {
 }
 
 template <typename Real, int V>
-__device__ __forceinline__ void pin_dirichlet(Real (&u)[V], long long g0, long long n, Real c1,
-                                              Real c2) {
+__device__ __forceinline__ void pin_ends(Real (&u)[V], long long g0, long long pin_lo,
+                                         long long pin_hi, Real c1, Real c2) {
 #pragma unroll
     for (int i = 0; i < V; ++i) {
         const long long g = g0 + i;
-        if (g == 0) u[i] = c1;
-        if (g == n - 1) u[i] = c2;
+        if (g == pin_lo) u[i] = c1;
+        if (g == pin_hi) u[i] = c2;
     }
 }
 
+// One pass over an array of `len` points.  Outputs [out_lo, out_hi) are
+// advanced by `nsteps`; reads outside [0, len) wrap (single-domain periodic)
+// or read as zero (their influence cannot reach the outputs in <= V steps, or
+// is cut off by a pinned Dirichlet end).  pin_lo / pin_hi (or -1) are pinned
+// to c1 / c2 after every step.  A whole Dirichlet domain is
+// {len=N, out=[0,N), pin_lo=0, pin_hi=N-1}; a multi-GPU slab with H ghost
+// points per side is {len=n+2H, out=[H,H+n), pins only at true global ends}.
 struct SyncPassArgs {
     const void* src;
     void* dst;
-    long long n;
+    long long len;
+    long long out_lo, out_hi;
+    long long pin_lo, pin_hi;
     long long tiles;
     double r, c, c1, c2;  // converted to Real inside
-    int periodic;
+    int wrap;
     int nsteps;
     unsigned int* nonfinite;  // set to 1 when an exact output value is not finite
 };
@@ -144,9 +153,9 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
     extern __shared__ __align__(128) unsigned char smem[];
     const Real* __restrict__ src = static_cast<const Real*>(a.src);
     Real* __restrict__ dst = static_cast<Real*>(a.dst);
-    const long long n = a.n;
+    const long long len = a.len;
     const Real r = Real(a.r), c = Real(a.c), c1 = Real(a.c1), c2 = Real(a.c2);
-    const bool periodic = a.periodic != 0;
+    const bool wrap = a.wrap != 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* wbase = smem + warp * 2 * T::kBufBytes;
@@ -159,10 +168,13 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
     __syncwarp();
 
     const long long nwarps = (long long)gridDim.x * T::kWarpsPerCta;
-    auto window = [&](long long t) { return t * T::kOut - V; };
+    auto window = [&](long long t) { return a.out_lo + t * T::kOut - V; };
+    auto in_window = [&](long long g, long long w0) { return g >= w0 && g < w0 + kWarp * V; };
+    // Bulk-copy fast path: window in bounds, 16-B aligned, no pinned point inside.
     auto interior = [&](long long t) {
         const long long w0 = window(t);
-        return periodic ? (w0 >= 0 && w0 + kWarp * V <= n) : (w0 >= 1 && w0 + kWarp * V <= n - 1);
+        return w0 >= 0 && w0 + kWarp * V <= len && ((w0 * (long long)sizeof(Real)) & 15) == 0 &&
+               !in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0);
     };
     auto bufp = [&](int b) { return reinterpret_cast<Real*>(wbase + b * T::kBufBytes); };
     auto issue = [&](int b, long long t) {
@@ -195,12 +207,12 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
             for (int j = lane; j < kWarp * V; j += kWarp) {
                 long long g = w0 + j;
                 Real v;
-                if (periodic) {
-                    g %= n;
-                    if (g < 0) g += n;
+                if (wrap) {
+                    g %= len;
+                    if (g < 0) g += len;
                     v = src[g];
                 } else {
-                    v = (g >= 0 && g < n) ? src[g] : Real(0);
+                    v = (g >= 0 && g < len) ? src[g] : Real(0);
                 }
                 buf[(j / V) * T::kStrideElems + (j % V)] = v;
             }
@@ -210,13 +222,13 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
         const long long tn = t + nwarps;
         if (tn < a.tiles && interior(tn)) issue(b ^ 1, tn);
 
-        if (inter || periodic) {
+        if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
             for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
         } else {
             const long long g0 = w0 + (long long)lane * V;
             for (int s = 0; s < a.nsteps; ++s) {
                 warp_step<Real, V>(u, r, c);
-                pin_dirichlet<Real, V>(u, g0, n, c1, c2);
+                pin_ends<Real, V>(u, g0, a.pin_lo, a.pin_hi, c1, c2);
             }
         }
 
@@ -224,11 +236,11 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
             const long long g0 = w0 + (long long)lane * V;
 #pragma unroll
             for (int i = 0; i < V; ++i)
-                if (g0 + i < n && !isfinite(u[i])) bad = true;
+                if (g0 + i < a.out_hi && !isfinite(u[i])) bad = true;
         }
         __syncwarp();
         chunk_to_smem<Real, V>(buf + lane * T::kStrideElems, u);
-        if (inter) {
+        if (inter && w0 + (kWarp - 1) * V <= a.out_hi) {
             fence_proxy_async_smem();
             if (lane >= 1 && lane <= kWarp - 2) {
                 bulk_s2g(dst + w0 + (long long)lane * V, buf + lane * T::kStrideElems,
@@ -239,7 +251,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
             __syncwarp();
             for (int j = V + lane; j < (kWarp - 1) * V; j += kWarp) {
                 const long long g = w0 + j;
-                if (g < n) dst[g] = buf[(j / V) * T::kStrideElems + (j % V)];
+                if (g < a.out_hi) dst[g] = buf[(j / V) * T::kStrideElems + (j % V)];
             }
             __syncwarp();
         }

@@ -454,11 +454,28 @@ def exec_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
 class Plan:
     """A field resident in HBM (heat_plan_*): bench and multi-GPU slabs."""
 
-    def __init__(self, n: int, device: int = 0):
+    def __init__(self, n: int, device: int = 0, rank: int = 0, world: int = 1):
         self._h = C.c_void_p()
-        _lib.check(_lib.lib().heat_plan_create(C.byref(self._h), n, device), "heat_plan_create")
+        if world == 1:
+            _lib.check(_lib.lib().heat_plan_create(C.byref(self._h), n, device),
+                       "heat_plan_create")
+        else:
+            _lib.check(_lib.lib().heat_plan_create_slab(C.byref(self._h), n, device, rank, world),
+                       "heat_plan_create_slab")
         self.n = n
         self.device = device
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def halo() -> int:
+        """Ghost points per side of a slab = max steps per exchange."""
+        return int(_lib.lib().heat_slab_halo())
+
+    def halo_pack(self, dst_device_ptr: int):
+        _lib.check(_lib.lib().heat_plan_halo_pack(self._h, dst_device_ptr), "halo_pack")
+
+    def halo_unpack(self, src_device_ptr: int):
+        _lib.check(_lib.lib().heat_plan_halo_unpack(self._h, src_device_ptr), "halo_unpack")
 
     def close(self):
         if self._h:

@@ -1,0 +1,130 @@
+"""Multi-GPU 1-D slab decomposition of the FTCS field.
+
+One process per GPU (torchrun).  Rank g owns points [g*n, (g+1)*n) of a global
+field of G*n points.  Every pass of s <= H steps (H = heat_slab_halo() = 32)
+each rank needs the H points beyond each of its ends at the pass's start
+step: a nearest-neighbour halo exchange of 2 x H doubles (256 B each way),
+not a collective.  Only the true global ends are pinned (Dirichlet on rank 0
+and rank G-1); periodic domains wrap rank G-1 <-> rank 0 through the same
+exchange.  The result is bit-identical to the single-domain sync_run: inside a
+pass the slab's points never depend on anything further than H away.
+
+The exchange uses torch.distributed point-to-point ops (NCCL over NVLink on the
+GPU box, gloo in the CPU tests) on the plan's stream.  This module holds the
+host logic only; the stepping is the sm_100a kernel behind heat.Plan.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+# tags: which ghost of the RECEIVER the message fills
+_TAG_LEFT_GHOST = 0
+_TAG_RIGHT_GHOST = 1
+
+
+def neighbours(rank: int, world: int, periodic: bool):
+    """(left, right) neighbour ranks, None at a Dirichlet global end."""
+    left = rank - 1 if rank > 0 else (world - 1 if periodic and world > 1 else None)
+    right = rank + 1 if rank < world - 1 else (0 if periodic and world > 1 else None)
+    return left, right
+
+
+def halo_exchange(send: torch.Tensor, recv: torch.Tensor, rank: int, world: int, periodic: bool,
+                  group=None) -> None:
+    """send = [my first H | my last H]; recv <- [left ghost H | right ghost H].
+
+    Posting order is fixed (to-right before to-left; from-left before
+    from-right) and tags name the receiver's ghost, so a 2-rank periodic ring
+    -- where left and right are the same peer -- pairs correctly under both
+    NCCL's in-order matching and gloo's tag matching."""
+    H = send.numel() // 2
+    left, right = neighbours(rank, world, periodic)
+    ops = []
+    if right is not None:
+        ops.append(dist.P2POp(dist.isend, send[H:], right, group, _TAG_LEFT_GHOST))
+    if left is not None:
+        ops.append(dist.P2POp(dist.isend, send[:H], left, group, _TAG_RIGHT_GHOST))
+    if left is not None:
+        ops.append(dist.P2POp(dist.irecv, recv[:H], left, group, _TAG_LEFT_GHOST))
+    if right is not None:
+        ops.append(dist.P2POp(dist.irecv, recv[H:], right, group, _TAG_RIGHT_GHOST))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+def pass_schedule(steps: int, halo: int):
+    """Pass lengths: full passes of `halo` steps and one remainder."""
+    out = []
+    while steps > 0:
+        s = min(steps, halo)
+        out.append(s)
+        steps -= s
+    return out
+
+
+class SlabEngine:
+    """What a slab runner needs from its stepper (heat.Plan on the GPU)."""
+
+    halo: int
+
+    def halo_pack(self, dst: torch.Tensor) -> None: ...
+
+    def halo_unpack(self, src: torch.Tensor) -> None: ...
+
+    def advance(self, steps: int) -> None: ...
+
+
+def run_passes(engine: SlabEngine, steps: int, rank: int, world: int, periodic: bool,
+               send: torch.Tensor, recv: torch.Tensor, group=None,
+               on_pass: Optional[Callable[[int], None]] = None) -> None:
+    """Advance a slab by `steps`, exchanging ghosts before every pass."""
+    for s in pass_schedule(steps, engine.halo):
+        if world > 1:
+            engine.halo_pack(send)
+            halo_exchange(send, recv, rank, world, periodic, group)
+            engine.halo_unpack(recv)
+        engine.advance(s)
+        if on_pass is not None:
+            on_pass(s)
+
+
+class PlanEngine(SlabEngine):
+    """heat.Plan slab bound to torch device tensors for the exchange."""
+
+    def __init__(self, plan, r: float, bc):
+        self.plan, self.r, self.bc = plan, r, bc
+        self.halo = plan.halo()
+
+    def halo_pack(self, dst: torch.Tensor) -> None:
+        self.plan.halo_pack(dst.data_ptr())
+
+    def halo_unpack(self, src: torch.Tensor) -> None:
+        self.plan.halo_unpack(src.data_ptr())
+
+    def advance(self, steps: int) -> None:
+        self.plan.sync_advance(self.r, self.bc, steps)
+
+
+class SlabSolver:
+    """Sync FTCS on a G-way slab decomposition, one rank per GPU."""
+
+    def __init__(self, n_local: int, r: float, bc, device: int, rank: int, world: int,
+                 group=None):
+        from .heat import Plan
+        torch.cuda.set_device(device)
+        self.rank, self.world, self.group = rank, world, group
+        self.periodic = not bc.is_dirichlet()
+        self.plan = Plan(n_local, device, rank, world)
+        self.plan.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        self.engine = PlanEngine(self.plan, r, bc)
+        H = self.engine.halo
+        self.send = torch.empty(2 * H, dtype=torch.float64, device=f"cuda:{device}")
+        self.recv = torch.zeros(2 * H, dtype=torch.float64, device=f"cuda:{device}")
+
+    def advance(self, steps: int) -> None:
+        run_passes(self.engine, steps, self.rank, self.world, self.periodic, self.send,
+                   self.recv, self.group)
