@@ -201,7 +201,10 @@ def run_b200(args, rank, world, local):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream(local)
+    # a dedicated (non-legacy) stream: the kernels, the halo NCCL ops and the
+    # timing events all live on it
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)
     n = N_PER_GPU
     bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
     r = H.SolverParams.from_r(R).r()

@@ -1,8 +1,294 @@
-// async_host.cu -- asynchronous entry points (placeholder until K3/K4 land).
+// async_host.cu -- host side of the asynchronous kernels: draw-order tables,
+// launch selection, recording, executors.  C-ABI: heat_async_run,
+// heat_sample_delay, heat_exec_run.
+#include <algorithm>
 #include <cmath>
+#include <functional>
 
-#include "common.cuh"
+#include "async_pe.cuh"
 #include "runtime.cuh"
+
+namespace hb {
+
+// In-step rank of every cross-PE read (async_sim.cpp:86-101: points in
+// ascending i, pinned Dirichlet ends skipped, left before right, a draw only
+// when the neighbour lies in another PE).  With P >= 2 only a PE's first
+// point reads left across and only its last point reads right across.
+int draw_offsets(size_t N, size_t n, int dirichlet, std::vector<int>& offL, std::vector<int>& offR) {
+    const size_t P = N / n;
+    offL.assign(P, -1);
+    offR.assign(P, -1);
+    int cnt = 0;
+    for (size_t p = 0; p < P; ++p) {
+        const size_t first = p * n, last = p * n + n - 1;
+        const bool pin_first = dirichlet && (first == 0 || first == N - 1);
+        const bool pin_last = dirichlet && (last == 0 || last == N - 1);
+        if (P >= 2 && !pin_first) offL[p] = cnt++;  // left neighbour is always another PE
+        if (P >= 2 && !pin_last) offR[p] = cnt++;   // (n == 1: same point, left then right)
+    }
+    return cnt;
+}
+
+namespace {
+
+struct AsyncWork {
+    // device allocations inside DevCtx::scratch
+    double* field;
+    double* ring;
+    unsigned long long* prog;
+    int* offL;
+    int* offR;
+    unsigned char* dtable;
+    unsigned long long* stats;
+    unsigned int* abort_word;
+    double* edge_log;
+    int* used_log;
+};
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+int pick_ring(int q) {
+    int R = 64;
+    while (R < 4 * q) R *= 2;
+    return R;
+}
+
+template <int V, bool S>
+int launch_v(const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
+    if (S) {
+        if (smem > 48 * 1024)
+            HB_CUDA(cudaFuncSetAttribute(async_pe_kernel<V, S>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        async_pe_kernel<V, S><<<1, 32 * P, smem, st>>>(a);
+        HB_CUDA(cudaGetLastError());
+    } else {
+        // every PE warp must be co-resident: cooperative launch or refuse
+        const int threads = 256;
+        const int blocks = (P * 32 + threads - 1) / threads;
+        int dev = 0, per_sm = 0, sms = 0;
+        HB_CUDA(cudaGetDevice(&dev));
+        HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_pe_kernel<V, S>,
+                                                              threads, 0));
+        if ((long long)per_sm * sms < blocks)
+            return fail(HEAT_EINVAL, "async: " + std::to_string(P) +
+                                         " PE warps cannot be co-resident on this device");
+        AsyncPeArgs copy = a;
+        void* params[] = {&copy};
+        HB_CUDA(cudaLaunchCooperativeKernel((const void*)async_pe_kernel<V, S>, dim3(blocks),
+                                            dim3(threads), params, 0, st));
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return HEAT_OK;
+}
+
+template <bool S>
+int launch_s(int V, const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
+    switch (V) {
+        case 1: return launch_v<1, S>(a, P, st, smem);
+        case 2: return launch_v<2, S>(a, P, st, smem);
+        case 4: return launch_v<4, S>(a, P, st, smem);
+        case 8: return launch_v<8, S>(a, P, st, smem);
+        case 16: return launch_v<16, S>(a, P, st, smem);
+        default: return launch_v<32, S>(a, P, st, smem);
+    }
+}
+
+}  // namespace
+
+// Shared driver of async_run (deterministic) and exec_run(BarrierFree) (free).
+// Advances `field` (device, prepared) from step 0 to k_end, calling
+// on_record(k) after every `stride` steps when stride > 0.
+struct AsyncRunSpec {
+    size_t N, n;
+    double r;
+    int bc_kind;
+    double c1, c2;
+    int mode;  // 0 deterministic, 1 free
+    size_t q;
+    int law;
+    size_t fixed_d;
+    double geometric_p;
+    uint64_t seed;
+    size_t k_end;
+    bool want_logs;
+};
+
+int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride,
+                 const std::function<int(size_t)>& on_record, unsigned long long* host_stats,
+                 std::vector<double>* edge_log, std::vector<int>* used_log, float* device_ms) {
+    const size_t P = s.N / s.n;
+    if (s.n > 32 * 32)
+        return fail(HEAT_ENODEV, "async: PEs wider than 1024 points need the streaming kernel "
+                                 "(heat_plan_async_advance)");
+    if (P > 65536) return fail(HEAT_EINVAL, "async: too many PEs");
+    int V = 1;
+    while (V * 32 < int(s.n)) V *= 2;
+    const int q = int(s.q);
+    const int R = pick_ring(q);
+    const int dir = s.bc_kind == HEAT_BC_DIRICHLET;
+    std::vector<int> offL, offR;
+    const int D = draw_offsets(s.N, s.n, dir, offL, offR);
+
+    // host-drawn geometric delays (glibc log1p, bit-identical to the reference)
+    std::vector<unsigned char> dtab;
+    if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {
+        if (q > 256) return fail(HEAT_EINVAL, "async: geometric law on the GPU needs q <= 256");
+        dtab.resize(std::max<size_t>(1, s.k_end * size_t(D)));
+        const double lp = std::log1p(-s.geometric_p);
+        for (size_t k = 0; k < s.k_end; ++k) {
+            const size_t bound = std::min<size_t>(size_t(q - 1), k);
+            for (int o = 0; o < D; ++o) {
+                const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * D + o);
+                const double u = double(x >> 11) * 0x1.0p-53;
+                double g = std::floor(std::log1p(-u) / lp);
+                if (!std::isfinite(g) || g < 0.0) g = 0.0;
+                dtab[k * D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
+            }
+        }
+    }
+
+    // scratch layout
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += align256(bytes); return o; };
+    const size_t o_ring = take(P * 2 * R * sizeof(double));
+    const size_t o_prog = take(P * sizeof(unsigned long long));
+    const size_t o_offL = take(P * sizeof(int));
+    const size_t o_offR = take(P * sizeof(int));
+    const size_t o_dtab = take(std::max<size_t>(1, dtab.size()));
+    const size_t o_stats = take(kStatWords * sizeof(unsigned long long));
+    const size_t o_abort = take(sizeof(unsigned int));
+    const size_t o_elog = take(s.want_logs ? (s.k_end + 1) * P * 2 * sizeof(double) : 0);
+    const size_t o_ulog = take(s.want_logs ? std::max<size_t>(1, s.k_end) * P * 2 * sizeof(int) : 0);
+    HB_TRY(ensure_scratch(d, off));
+    char* base = static_cast<char*>(d.scratch);
+    cudaStream_t st = d.stream;
+
+    // initial ring: slot 0 = step-0 edge values, prog = 0
+    std::vector<double> edges0(P * 2);
+    for (size_t p = 0; p < P; ++p) {
+        HB_CUDA(cudaMemcpyAsync(&edges0[p * 2 + 0], dfield + p * s.n, sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(&edges0[p * 2 + 1], dfield + p * s.n + s.n - 1, sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+    }
+    HB_CUDA(cudaStreamSynchronize(st));
+    std::vector<double> ring0(P * 2 * R, 0.0);
+    for (size_t p = 0; p < P; ++p) {
+        ring0[(p * 2 + 0) * R] = edges0[p * 2 + 0];
+        ring0[(p * 2 + 1) * R] = edges0[p * 2 + 1];
+    }
+    std::vector<unsigned long long> stats0(kStatWords, 0);
+    stats0[kStatLagMin] = ~0ull;
+    HB_CUDA(cudaMemcpyAsync(base + o_ring, ring0.data(), ring0.size() * sizeof(double),
+                            cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemsetAsync(base + o_prog, 0, P * sizeof(unsigned long long), st));
+    HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!dtab.empty())
+        HB_CUDA(cudaMemcpyAsync(base + o_dtab, dtab.data(), dtab.size(), cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(base + o_stats, stats0.data(), kStatWords * sizeof(unsigned long long),
+                            cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemsetAsync(base + o_abort, 0, sizeof(unsigned int), st));
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
+    if (s.want_logs) {
+        HB_CUDA(cudaMemcpyAsync(base + o_elog, edges0.data(), P * 2 * sizeof(double),
+                                cudaMemcpyHostToDevice, st));
+    }
+
+    AsyncPeArgs a{};
+    a.field = dfield;
+    a.N = (long long)s.N;
+    a.n = int(s.n);
+    a.P = int(P);
+    a.r = s.r;
+    a.c = 1.0 - 2.0 * s.r;  // core.hpp:108
+    a.c1 = s.c1;
+    a.c2 = s.c2;
+    a.dirichlet = dir;
+    a.mode = s.mode;
+    a.q = q;
+    a.R = R;
+    a.law = s.law;
+    a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
+    a.seed = s.seed;
+    a.D = D;
+    a.off_left = reinterpret_cast<const int*>(base + o_offL);
+    a.off_right = reinterpret_cast<const int*>(base + o_offR);
+    a.dtable = reinterpret_cast<const unsigned char*>(base + o_dtab);
+    a.ring = reinterpret_cast<double*>(base + o_ring);
+    a.prog = reinterpret_cast<unsigned long long*>(base + o_prog);
+    a.stats = reinterpret_cast<unsigned long long*>(base + o_stats);
+    a.edge_log = s.want_logs ? reinterpret_cast<double*>(base + o_elog) : nullptr;
+    a.used_log = s.want_logs ? reinterpret_cast<int*>(base + o_ulog) : nullptr;
+    a.flag = d.flag;
+    a.abort_word = reinterpret_cast<unsigned int*>(base + o_abort);
+    a.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s watchdog per wait
+
+    const size_t smem = P * 2 * R * sizeof(double) + P * sizeof(unsigned long long);
+    const bool shared = P <= 16 && smem <= 160 * 1024;  // one CTA of <= 512 threads
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (device_ms) {
+        HB_CUDA(cudaEventCreate(&ev0));
+        HB_CUDA(cudaEventCreate(&ev1));
+        HB_CUDA(cudaEventRecord(ev0, st));
+    }
+    size_t k = 0;
+    while (k < s.k_end) {
+        const size_t next = stride ? std::min(s.k_end, (k / stride + 1) * stride) : s.k_end;
+        a.k0 = (long long)k;
+        a.k1 = (long long)next;
+        HB_TRY(shared ? launch_s<true>(V, a, int(P), st, smem)
+                      : launch_s<false>(V, a, int(P), st, 0));
+        k = next;
+        if (stride && on_record) {
+            unsigned int flags[2] = {0, 0};
+            HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+            if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
+            if (flags[0]) {
+                if (g_strict.load())
+                    return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+                return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+            }
+            HB_TRY(on_record(k));
+        }
+    }
+    if (device_ms) {
+        HB_CUDA(cudaEventRecord(ev1, st));
+        HB_CUDA(cudaEventSynchronize(ev1));
+        HB_CUDA(cudaEventElapsedTime(device_ms, ev0, ev1));
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
+    unsigned int flags[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    if (host_stats)
+        HB_CUDA(cudaMemcpyAsync(host_stats, base + o_stats, kStatWords * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st));
+    if (s.want_logs && edge_log && used_log) {
+        edge_log->resize((s.k_end + 1) * P * 2);
+        used_log->resize(s.k_end * P * 2);
+        HB_CUDA(cudaMemcpyAsync(edge_log->data(), base + o_elog, edge_log->size() * sizeof(double),
+                                cudaMemcpyDeviceToHost, st));
+        if (!used_log->empty())
+            HB_CUDA(cudaMemcpyAsync(used_log->data(), base + o_ulog, used_log->size() * sizeof(int),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    return HEAT_OK;
+}
+
+int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
+                    double* dst);
+
+}  // namespace hb
 
 using namespace hb;
 
@@ -32,41 +318,138 @@ int heat_sample_delay(size_t q, int law, size_t fixed_delay, double geometric_p,
     return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
 }
 
-int heat_async_run(const double*, size_t, double, int, double, double, size_t, size_t, int,
-                   size_t, double, uint64_t, size_t, size_t, double*, double*, size_t*, size_t,
-                   size_t*) {
-    return fail(HEAT_ENODEV, "heat_async_run: not built yet");
+int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                   size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                   uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                   double* snapshots, size_t* steps_out, size_t max_snapshots,
+                   size_t* n_snapshots) {
+    if (N < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u0) return fail(HEAT_EINVAL, "null field pointer");
+    if (per_pe == 0 || N % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
+    if (law == HEAT_DELAY_FIXED && fixed_delay >= q)
+        return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
+    if (law == HEAT_DELAY_GEOMETRIC && (!(geometric_p > 0.0) || geometric_p > 1.0))
+        return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
+    if (law < 0 || law > 2) return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+    // A single PE never reads across: no draws, bit-identical to sync_run
+    // (test_async_sim.cpp:131-150).
+    if (per_pe == N)
+        return heat_sync_run(u0, N, r, bc_kind, c1, c2, k_end, stride, final_out, snapshots,
+                             steps_out, max_snapshots, n_snapshots);
+    if (stride == 0) stride = default_stride(N);
+
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    std::lock_guard<std::mutex> lock(d->mu);
+    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
+    double* field = static_cast<double*>(d->buf[0]);
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+
+    const bool want_snaps = snapshots != nullptr || steps_out != nullptr;
+    size_t ns = 0;
+    cudaStream_t st = d->stream;
+    auto record = [&](size_t k) -> int {
+        if (ns < max_snapshots) {
+            if (snapshots)
+                HB_CUDA(cudaMemcpyAsync(snapshots + ns * N, field, N * sizeof(double),
+                                        cudaMemcpyDeviceToHost, st));
+            if (steps_out) steps_out[ns] = k;
+        }
+        ++ns;
+        HB_CUDA(cudaStreamSynchronize(st));
+        return HEAT_OK;
+    };
+    if (want_snaps) HB_TRY(record(0));
+    AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 0, q, law, fixed_delay, geometric_p, seed,
+                   k_end, false};
+    HB_TRY(async_pe_run(*d, s, field, want_snaps ? stride : 0, record, nullptr, nullptr, nullptr,
+                        nullptr));
+    if (final_out) {
+        HB_CUDA(cudaMemcpyAsync(final_out, field, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+    }
+    if (n_snapshots) *n_snapshots = ns;
+    return HEAT_OK;
 }
 
-int heat_exec_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
                   size_t per_pe, size_t workers, size_t k_end, int mode, int record_lag,
                   size_t q_free, double* field_out, uint64_t* duration_ns, heat_lag_stats* lag,
                   heat_async_stats* stats) {
-    (void)record_lag;
-    (void)q_free;
-    (void)lag;
-    (void)stats;
-    // exec_run validation order (async_exec.cpp:263-272)
-    HB_TRY(check_field(u0, n));
-    if (per_pe == 0 || n % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
-    if (workers == 0 || workers != n / per_pe)
+    // exec_run validation order (async_exec.cpp:263-272); the PartitionSpec
+    // ctor (core.cpp:66-72) runs first at the caller.
+    if (N < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (per_pe == 0 || N % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (workers == 0 || workers != N / per_pe)
         return fail(HEAT_EINVAL, "exec_run: cfg.workers must equal part.P");
     if (k_end == 0) return fail(HEAT_EINVAL, "exec_run: k_end >= 1 required");
-    if (mode != HEAT_EXEC_BARRIERED) return fail(HEAT_ENODEV, "heat_exec_run: barrier-free not built yet");
-    cudaEvent_t e0, e1;
-    HB_CUDA(cudaEventCreate(&e0));
-    HB_CUDA(cudaEventCreate(&e1));
-    int st = heat_sync_run(u0, n, r, bc_kind, c1, c2, k_end, k_end, field_out, nullptr, nullptr, 0,
-                           nullptr);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (duration_ns) *duration_ns = 0;
-    return st;
+    if (mode != HEAT_EXEC_BARRIERED && mode != HEAT_EXEC_BARRIER_FREE)
+        return fail(HEAT_EINVAL, "exec_run: unknown mode");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    const bool sync_path = mode == HEAT_EXEC_BARRIERED || workers == 1;
+    if (sync_path) {
+        // Barriered is bit-identical to sync_run (acceptance.cpp:225-229); so is
+        // BarrierFree with one PE (test_exec.cpp:69-87).
+        cudaEvent_t e0, e1;
+        HB_CUDA(cudaEventCreate(&e0));
+        HB_CUDA(cudaEventCreate(&e1));
+        HB_CUDA(cudaEventRecord(e0, d->stream));
+        int st = heat_sync_run(u0, N, r, bc_kind, c1, c2, k_end, k_end, field_out, nullptr,
+                               nullptr, 0, nullptr);
+        HB_CUDA(cudaEventRecord(e1, d->stream));
+        HB_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
+        if (lag) std::memset(lag, 0, sizeof *lag);
+        if (stats) std::memset(stats, 0, sizeof *stats);
+        return st;
+    }
+
+    std::lock_guard<std::mutex> lock(d->mu);
+    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
+    double* field = static_cast<double*>(d->buf[0]);
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+    const size_t q = q_free ? q_free : 8;
+    AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, k_end,
+                   false};
+    std::vector<unsigned long long> hs(kStatWords, 0);
+    float ms = 0.f;
+    HB_TRY(async_pe_run(*d, s, field, 0, nullptr, hs.data(), nullptr, nullptr, &ms));
+    HB_CUDA(cudaMemcpy(field_out, field, N * sizeof(double), cudaMemcpyDeviceToHost));
+    if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
+    if (lag) {
+        std::memset(lag, 0, sizeof *lag);
+        if (record_lag && hs[kStatReads]) {
+            lag->reads = hs[kStatReads];
+            lag->min_lag = hs[kStatLagMin];
+            lag->max_lag = hs[kStatLagMax];
+            lag->overflow = hs[kStatLagOverflow];
+            for (int i = 0; i < 64; ++i) lag->histogram[i] = hs[kStatLagHist + i];
+        }
+    }
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->reads = hs[kStatReads];
+        stats->waits = hs[kStatWaits];
+        stats->max_delay = hs[kStatMaxDelay];
+        for (int i = 0; i < 64; ++i) stats->delay_histogram[i] = hs[kStatDelayHist + i];
+    }
+    return HEAT_OK;
 }
 
 int heat_plan_async_advance(heat_plan*, double, int, double, double, size_t, size_t, size_t,
                             heat_async_stats*) {
-    return fail(HEAT_ENODEV, "heat_plan_async_advance: not built yet");
+    return fail(HEAT_ENODEV, "heat_plan_async_advance: streaming async kernel not built yet");
 }
 
 }  // extern "C"

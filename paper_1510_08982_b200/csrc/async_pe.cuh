@@ -1,0 +1,312 @@
+// async_pe.cuh -- K3/K4: asynchronous FTCS with one WARP per processing
+// element (PE), PEs exchanging their boundary values through halo rings
+// under acquire/release flags -- no grid-wide or block-wide barrier.
+//
+// Replaces (GPU-side):
+//   * async_step_into / AsyncSimulator / async_run (async_sim.cpp:77-160)
+//     in DETERMINISTIC mode: every cross-PE read u_j(k - d) uses exactly the
+//     delay d the reference draws for it.  The reference's single sequential
+//     SplitMix64 stream is replayed per PE in counter form: the draw for the
+//     read with in-step rank `off` at step k is draw number k*D + off of the
+//     stream (D = cross-PE reads per step), i.e. mix(seed + (k*D+off+1)*gamma)
+//     (rng.hpp:20-26, async_sim.cpp:57-73, draw order async_sim.cpp:86-101).
+//   * run_barrier_free (async_exec.cpp:156-259) in FREE mode: a PE reads the
+//     newest published neighbour value u_j(k*) with k - k* <= q - 1 (bounded
+//     staleness, the paper's Eq. (4) with k* in {k, ..., k-q+1}); it only
+//     waits when the neighbour is more than q-1 steps behind.  Observed
+//     delays k - k* are logged.
+//
+// Mapping: PE p = warp p (global warp index).  Its n <= 32*V points live in
+// registers for the whole launch: lane l holds local points [lV, lV+V).
+// Per step a PE needs the LEFT neighbour's last point and the RIGHT
+// neighbour's first point; it publishes its own first and last point for
+// step k+1 into ring slot (k+1) mod R and then releases prog[p] = k+1.
+// Rings live in shared memory (CTA scope) when all PEs fit in one CTA, else
+// in global memory (GPU scope).  The ring/progress state persists in global
+// memory between launches, so runs can be split at recorded steps.
+//
+// Flow control: a producer may overwrite the slot of step k+1-R only when
+// every consumer has reached step >= k+1+q-R (it never reads older than
+// k_c-q+1).  Deadlock freedom requires all P warps to be co-resident
+// (single CTA, or a cooperative launch).  Spins carry a %globaltimer
+// watchdog that aborts the whole grid with HEAT_ETIMEOUT.
+#pragma once
+
+#include "common.cuh"
+
+namespace hb {
+
+struct AsyncPeArgs {
+    double* field;  // N doubles; PE p reads/writes only [p*n, (p+1)*n)
+    long long N;
+    int n;
+    int P;
+    double r, c, c1, c2;
+    int dirichlet;
+    long long k0, k1;  // steps [k0, k1) of this launch
+    int mode;          // 0 deterministic replay, 1 free-running (bounded)
+    int q;             // delays in {0, ..., q-1}
+    int R;             // ring slots per PE side (power of two, > q)
+    int law;           // HEAT_DELAY_*
+    int fixed_d;
+    unsigned long long seed;
+    long long D;            // cross-PE reads (draws) per step
+    const int* off_left;    // [P] in-step draw rank of the first point's left read, -1 none
+    const int* off_right;   // [P] ... of the last point's right read, -1 none
+    const unsigned char* dtable;  // GEOMETRIC: host-drawn delays [k*D + off], k < k_total
+    double* ring;                 // [P][2][R]: side 0 = first point, 1 = last point
+    unsigned long long* prog;     // [P] published step count
+    unsigned long long* stats;    // see kStat* offsets
+    double* edge_log;             // optional [(k_total+1)][P][2] published edge values
+    int* used_log;                // optional [k_total][P][2] step k* actually read
+    unsigned int* flag;           // [0] non-finite, [1] watchdog timeout
+    unsigned int* abort_word;     // set on timeout: every spin bails out
+    unsigned long long timeout_ns;
+};
+
+// stats layout (u64 words)
+constexpr int kStatReads = 0, kStatWaits = 1, kStatMaxDelay = 2, kStatDelayHist = 3,
+              kStatLagMin = 67, kStatLagMax = 68, kStatLagHist = 69, kStatLagOverflow = 133,
+              kStatWords = 134;
+
+template <bool kShared>
+struct RingOps;
+
+template <>
+struct RingOps<false> {
+    static __device__ __forceinline__ uint64_t load_prog(const uint64_t* p) { return ld_acquire_gpu(p); }
+    static __device__ __forceinline__ void store_prog(uint64_t* p, uint64_t v) { st_release_gpu(p, v); }
+    static __device__ __forceinline__ double load_val(const double* p) { return ld_relaxed_gpu_f64(p); }
+    static __device__ __forceinline__ void store_val(double* p, double v) { st_relaxed_gpu_f64(p, v); }
+};
+
+template <>
+struct RingOps<true> {
+    static __device__ __forceinline__ uint64_t load_prog(const uint64_t* p) {
+        return ld_acquire_cta_shared(p);
+    }
+    static __device__ __forceinline__ void store_prog(uint64_t* p, uint64_t v) {
+        st_release_cta_shared(p, v);
+    }
+    static __device__ __forceinline__ double load_val(const double* p) {
+        return *reinterpret_cast<const volatile double*>(p);
+    }
+    static __device__ __forceinline__ void store_val(double* p, double v) {
+        *reinterpret_cast<volatile double*>(p) = v;
+    }
+};
+
+// Delay of the draw with in-step rank `off` at step k (async_sim.cpp:57-73).
+__device__ __forceinline__ int det_delay(const AsyncPeArgs& a, long long k, int off) {
+    const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
+    if (a.law == 2) return a.dtable[k * a.D + off];  // host-drawn, already bounded
+    const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
+    if (a.law == 0) return int(x % uint64_t(bound + 1));
+    return a.fixed_d < bound ? a.fixed_d : int(bound);
+}
+
+// Spin until prog[pe] >= need (acquire).  Returns the observed progress, or
+// ~0ull when the watchdog fired.
+template <bool kShared>
+__device__ __forceinline__ uint64_t wait_prog(const AsyncPeArgs& a, const uint64_t* prog,
+                                              long long need, bool* waited) {
+    uint64_t v = RingOps<kShared>::load_prog(prog);
+    if ((long long)v >= need) return v;
+    *waited = true;
+    const uint64_t t0 = globaltimer_ns();
+    unsigned spins = 0;
+    while ((long long)(v = RingOps<kShared>::load_prog(prog)) < need) {
+        if ((++spins & 255u) == 0) {
+            if (*reinterpret_cast<volatile unsigned int*>(a.abort_word)) return ~0ull;
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+                atomicOr(a.flag + 1, 1u);
+                atomicExch(a.abort_word, 1u);
+                return ~0ull;
+            }
+        }
+    }
+    return v;
+}
+
+template <int V, bool kShared>
+__global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const AsyncPeArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int p = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    const int R = a.R;
+    double* ring = a.ring;
+    uint64_t* prog = reinterpret_cast<uint64_t*>(a.prog);
+    if constexpr (kShared) {
+        // stage the persistent ring state into shared memory (one CTA holds every PE)
+        double* sring = reinterpret_cast<double*>(smem);
+        uint64_t* sprog = reinterpret_cast<uint64_t*>(sring + (size_t)a.P * 2 * R);
+        for (int i = threadIdx.x; i < a.P * 2 * R; i += blockDim.x) sring[i] = a.ring[i];
+        for (int i = threadIdx.x; i < a.P; i += blockDim.x) sprog[i] = a.prog[i];
+        __syncthreads();
+        ring = sring;
+        prog = sprog;
+    }
+    const bool active = p < a.P;
+    if constexpr (!kShared) {
+        if (!active) return;  // warp-uniform; no block barrier in the global-ring variant
+    }
+    const int n = a.n;
+    const long long lo = (long long)p * n;
+    const double r = a.r, c = a.c;
+    using A = Arith<double>;
+
+    // neighbours (periodic wraps, Dirichlet ends have none); P >= 2 here
+    const int lpe = p > 0 ? p - 1 : (a.dirichlet ? -1 : a.P - 1);
+    const int rpe = p + 1 < a.P ? p + 1 : (a.dirichlet ? -1 : 0);
+    const bool pin_first = a.dirichlet && p == 0;
+    const bool pin_last = a.dirichlet && p == a.P - 1;
+    const bool needL = active && lpe >= 0 && !pin_first;
+    const bool needR = active && rpe >= 0 && !pin_last;
+    const int offL = active ? a.off_left[p] : -1;
+    const int offR = active ? a.off_right[p] : -1;
+    const int lastLane = (n - 1) / V, lastElem = (n - 1) % V;
+
+    double u[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const int li = lane * V + i;
+        u[i] = (active && li < n) ? a.field[lo + li] : 0.0;
+    }
+
+    unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
+    bool abort = false;
+    for (long long k = a.k0; k < a.k1 && !abort; ++k) {
+        // ---- 1. ghosts: lane 0 fetches the left one, lane 31 the right one
+        double ghost = 0.0;
+        int used = -1;
+        if ((lane == 0 && needL) || (lane == 31 && needR)) {
+            const bool left = lane == 0;
+            const int nb = left ? lpe : rpe;
+            const int side = left ? 1 : 0;  // left ghost = neighbour's last point
+            bool waited = false;
+            long long m;
+            uint64_t v;
+            if (a.mode == 0) {
+                const int d = det_delay(a, k, left ? offL : offR);
+                m = k - d;
+                v = wait_prog<kShared>(a, prog + nb, m, &waited);
+            } else {
+                v = wait_prog<kShared>(a, prog + nb, k - (a.q - 1), &waited);
+                m = (long long)v < k ? (long long)v : k;
+            }
+            if (v == ~0ull) abort = true;
+            if (!abort) {
+                ghost = RingOps<kShared>::load_val(ring + ((size_t)nb * 2 + side) * R + (m & (R - 1)));
+                used = int(k - m);
+                // writer lag as LagStats measures it: producer progress - step consumed
+                const unsigned long long lag = v - (unsigned long long)m;
+                reads++;
+                waits += waited;
+                if ((unsigned long long)used > maxd) maxd = used;
+                lag_min = lag < lag_min ? lag : lag_min;
+                lag_max = lag > lag_max ? lag : lag_max;
+                if (a.stats) {
+                    atomicAdd(a.stats + kStatDelayHist + (used < 64 ? used : 63), 1ull);
+                    if (lag < 64)
+                        atomicAdd(a.stats + kStatLagHist + lag, 1ull);
+                    else
+                        atomicAdd(a.stats + kStatLagOverflow, 1ull);
+                }
+                if (a.used_log) a.used_log[(k * a.P + p) * 2 + (left ? 0 : 1)] = int(m);
+            }
+        }
+        abort = __any_sync(0xffffffffu, abort);
+        if (abort) break;
+        const double gL = __shfl_sync(0xffffffffu, ghost, 0);
+        const double gR = __shfl_sync(0xffffffffu, ghost, 31);
+
+        // ---- 2. one step of the PE's points
+        if (lane == lastLane && lastElem + 1 < V) {
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+                if (i == lastElem + 1) u[i] = gR;  // ghost slot right of the last point
+        }
+        const double pFirst = A::mul(r, u[0]);
+        const double pLast = A::mul(r, u[V - 1]);
+        double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
+        double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
+        if (lane == 0) pL = A::mul(r, gL);
+        if (lane == lastLane && lastElem == V - 1) pR = A::mul(r, gR);
+        {
+            double pm1 = pL, p0 = pFirst;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                double p1;
+                if (i + 1 == V)
+                    p1 = pR;
+                else if (i + 1 == V - 1)
+                    p1 = pLast;
+                else
+                    p1 = A::mul(r, u[i + 1]);
+                const double cs = A::mul(c, u[i]);
+                u[i] = stencil_p(p1, cs, pm1);
+                pm1 = p0;
+                p0 = p1;
+            }
+        }
+        if (pin_first && lane == 0) u[0] = a.c1;
+        if (pin_last && lane == lastLane) {
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+                if (i == lastElem) u[i] = a.c2;
+        }
+
+        // ---- 3. publish u_first(k+1), u_last(k+1) then release prog = k+1
+        double last = 0.0;
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+            if (i == lastElem) last = u[i];
+        last = __shfl_sync(0xffffffffu, last, lastLane);
+        if (lane == 0 && active) {
+            const long long slot = (k + 1) & (R - 1);
+            // flow control: consumers must be past the step this slot held
+            const long long need = k + 1 + a.q - R;
+            bool w = false;
+            if (need > 0) {
+                if (lpe >= 0 && wait_prog<kShared>(a, prog + lpe, need, &w) == ~0ull) abort = true;
+                if (rpe >= 0 && wait_prog<kShared>(a, prog + rpe, need, &w) == ~0ull) abort = true;
+            }
+            RingOps<kShared>::store_val(ring + ((size_t)p * 2 + 0) * R + slot, u[0]);
+            RingOps<kShared>::store_val(ring + ((size_t)p * 2 + 1) * R + slot, last);
+            if (a.edge_log) {
+                a.edge_log[((k + 1) * a.P + p) * 2 + 0] = u[0];
+                a.edge_log[((k + 1) * a.P + p) * 2 + 1] = last;
+            }
+            RingOps<kShared>::store_prog(prog + p, (uint64_t)(k + 1));
+        }
+        abort = __any_sync(0xffffffffu, abort);
+    }
+
+    // ---- results, finite check, statistics, ring state back to global
+    bool bad = false;
+    if (active && !abort) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            const int li = lane * V + i;
+            if (li < n) {
+                a.field[lo + li] = u[i];
+                bad |= !isfinite(u[i]);
+            }
+        }
+    }
+    if (bad) atomicOr(a.flag, 1u);
+    if (a.stats && reads) {
+        atomicAdd(a.stats + kStatReads, reads);
+        atomicAdd(a.stats + kStatWaits, waits);
+        atomicMax(a.stats + kStatMaxDelay, maxd);
+        atomicMin(a.stats + kStatLagMin, lag_min);
+        atomicMax(a.stats + kStatLagMax, lag_max);
+    }
+    if constexpr (kShared) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.P * 2 * R; i += blockDim.x) a.ring[i] = ring[i];
+        for (int i = threadIdx.x; i < a.P; i += blockDim.x) a.prog[i] = prog[i];
+    }
+}
+
+}  // namespace hb

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
 
     const long long nwarps = (long long)gridDim.x * T::kWarpsPerCta;
     auto window = [&](long long t) { return a.out_lo + t * T::kOut - V; };
-    auto in_window = [&](long long g, long long w0) { return g >= w0 && g < w0 + kWarp * V; };
+    auto in_window = [&](long long g, long long w0) { return g >= 0 && g >= w0 && g < w0 + kWarp * V; };
     // Bulk-copy fast path: window in bounds, 16-B aligned, no pinned point inside.
     auto interior = [&](long long t) {
         const long long w0 = window(t);

@@ -119,7 +119,10 @@ class SlabSolver:
         self.rank, self.world, self.group = rank, world, group
         self.periodic = not bc.is_dirichlet()
         self.plan = Plan(n_local, device, rank, world)
-        self.plan.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        stream = torch.cuda.current_stream(device)
+        if stream.cuda_stream == 0:
+            raise ValueError("SlabSolver needs a non-default current stream (torch.cuda.set_stream)")
+        self.plan.set_stream(stream.cuda_stream)
         self.engine = PlanEngine(self.plan, r, bc)
         H = self.engine.halo
         self.send = torch.empty(2 * H, dtype=torch.float64, device=f"cuda:{device}")

@@ -1,0 +1,202 @@
+"""GPU parity of the asynchronous paths against the oracle.
+
+Deterministic mode (async_run): bit-exact with the reference's seeded stream
+(proj/tests/test_async_sim.cpp, acceptance.cpp criterion 1, BASELINE cfg2).
+Executors (exec_run): Barriered bit-exact with sync_run; BarrierFree (free-
+running, bounded staleness) checked for the reference's stability properties
+(test_exec.cpp:89-136) and its logged delays against the bound."""
+import numpy as np
+import pytest
+
+from helpers import SplitMix64, bits_equal, fnv1a64, random_divisor, random_field
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H(gpu):
+    from paper_1510_08982_b200 import heat
+    return heat
+
+
+def _sine(port, n):
+    return port.prepare_initial(port.sine_init(n), 0, 0.0, 0.0)
+
+
+@pytest.mark.parametrize("seed,expect", [(1, 0x50008031848D280C), (42, 0x1E3D733CB51BD50B)])
+def test_cfg2_golden(H, port, seed, expect):
+    # BASELINE configs[1]: N=1024, 8 PEs, q=2 uniform, r=0.25, 1000 steps, sine IC.
+    u0 = _sine(port, 1024)
+    got = H.async_final(u0, H.SolverParams.from_r(0.25), H.BoundaryCondition.dirichlet(0, 0),
+                        H.PartitionSpec(1024, 128), H.DelayModel.uniform(2, seed), 1000)
+    assert fnv1a64(got) == expect
+
+
+def test_cfg2_trajectory_bit_exact(H, port):
+    u0 = _sine(port, 1024)
+    p = H.SolverParams.from_r(0.25)
+    t = H.async_run(H.TemperatureField(u0), p, H.BoundaryCondition.dirichlet(0, 0),
+                    H.PartitionSpec(1024, 128), H.DelayModel.uniform(3, 7), 300, 25)
+    steps, snaps = port.async_run(u0, p.r(), 0, 0.0, 0.0, 128, 0, 3, seed=7, k_end=300,
+                                  stride=25, record=True)
+    assert t.steps == steps
+    for j, s in enumerate(t.snapshots):
+        assert bits_equal(s.values(), snaps[j]), j
+
+
+def _law(gen, q):
+    k = gen.next_bounded(2)
+    if k == 0:
+        return 0, 0, 0.5
+    if k == 1:
+        return 1, gen.next_bounded(q - 1), 0.5
+    return 2, 0, 0.05 + 0.9 * gen.next_double()
+
+
+@pytest.mark.parametrize("seed", [20260824, 4048, 2024])
+def test_random_partitions_bit_exact(H, port, seed):
+    # acceptance.cpp:67-99 style, with random divisor partitions (n = 1 included),
+    # q in 1..10, all three delay laws, both BCs, every step recorded.
+    gen = SplitMix64(seed)
+    for _ in range(20):
+        n = 3 + gen.next_bounded(60)
+        r = 0.5 * (gen.next_double() * 0.999 + 0.001)
+        periodic = gen.next() & 1
+        u0 = random_field(gen, n)
+        k_end = 1 + gen.next_bounded(150)
+        per_pe = random_divisor(gen, n)
+        q = 1 + gen.next_bounded(9)
+        law, fd, gp = _law(gen, q)
+        mseed = gen.next()
+        bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(
+            u0[0], u0[-1])
+        model = H.DelayModel(q, H.Distribution(law), fd, gp, mseed)
+        params = H.SolverParams.from_r(r)
+        t = H.async_run(H.TemperatureField(u0), params, bc, H.PartitionSpec(n, per_pe), model,
+                        k_end, 1)
+        steps, snaps = port.async_run(u0, params.r(), bc.kind, bc.c1, bc.c2, per_pe, law, q, fd,
+                                      gp, mseed, k_end, 1, record=True)
+        assert t.steps == steps
+        for j, s in enumerate(t.snapshots):
+            assert bits_equal(s.values(), snaps[j]), (n, per_pe, q, law, periodic, j)
+
+
+@pytest.mark.parametrize("n_total,per_pe,q,bc", [
+    (1024, 512, 2, 0), (1024, 32, 3, 1), (1024, 8, 9, 0), (4096, 1024, 4, 1),
+    (1 << 16, 1024, 5, 0), (3 * 1000, 1000, 2, 1)])
+def test_larger_grids_bit_exact(H, port, n_total, per_pe, q, bc):
+    gen = SplitMix64(n_total + per_pe + q)
+    u0 = random_field(gen, n_total)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.4)
+    k = 200
+    got = H.async_final(u0, p, b, H.PartitionSpec(n_total, per_pe), H.DelayModel.uniform(q, 99),
+                        k)
+    exp = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, 0, q, seed=99, k_end=k)
+    assert bits_equal(got, exp)
+
+
+def test_reductions_to_sync(H, port):
+    # q = 1 and single-PE runs are bit-identical to sync (test_async_sim.cpp:110-150)
+    gen = SplitMix64(11)
+    u0 = random_field(gen, 200)
+    bc = H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.3)
+    sync = port.sync_run(u0, p.r(), 0, bc.c1, bc.c2, 150)
+    a = H.async_final(u0, p, bc, H.PartitionSpec(200, 20), H.DelayModel.uniform(1, 5), 150)
+    b = H.async_final(u0, p, bc, H.PartitionSpec(200, 200), H.DelayModel.uniform(7, 5), 150)
+    assert bits_equal(a, sync) and bits_equal(b, sync)
+
+
+def test_async_model_validation(H):
+    u0 = H.cosine_init(12)
+    p = H.SolverParams.from_r(0.5)
+    bc = H.BoundaryCondition.dirichlet(1.0, 0.0)
+    with pytest.raises(H.DomainError):
+        H.DelayModel.uniform(0, 1)
+    with pytest.raises(H.DomainError):
+        H.DelayModel.fixed(3, 3, 1)
+    with pytest.raises(H.DomainError):
+        H.PartitionSpec(12, 5)
+    with pytest.raises(H.InvalidArgument):
+        H.async_run(u0, p, bc, H.PartitionSpec(24, 4), H.DelayModel.uniform(2, 1), 5)
+
+
+def test_counter_form_matches_stream(H, port):
+    # the per-draw counter form equals the sequential SplitMix64 stream
+    # (golden vector test_async_sim.cpp:64-71)
+    assert [H.sample_delay_at(H.DelayModel.uniform(4, 42), j, 100) for j in range(8)] == \
+        [1, 3, 2, 0, 2, 2, 1, 0]
+    m = H.DelayModel.geometric(6, 0.7, 99)
+    assert [H.sample_delay_at(m, j, 1000) for j in range(200)] == \
+        port.delay_stream(2, 6, 0, 0.7, 99, 1000, 200)
+
+
+# ---- executors ------------------------------------------------------------
+def test_exec_barriered_bit_exact(H, port):
+    # test_exec.cpp:45-67 / acceptance.cpp:208-237
+    gen = SplitMix64(555)
+    for _ in range(10):
+        pe = 1 << gen.next_bounded(2)
+        per = 1 + gen.next_bounded(7)
+        n = max(3 * pe, pe * per)
+        per = n // pe
+        r = 0.5 * (gen.next_double() * 0.999 + 0.001)
+        periodic = gen.next() & 1
+        u0 = random_field(gen, n)
+        bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(
+            u0[0], u0[-1])
+        k = 1 + gen.next_bounded(99)
+        res = H.exec_run(H.TemperatureField(u0), H.SolverParams.from_r(r), bc,
+                         H.PartitionSpec(n, per), H.ExecConfig(pe, k, H.ExecMode.Barriered))
+        assert bits_equal(res.field.values(), port.sync_run(u0, r, bc.kind, bc.c1, bc.c2, k))
+        assert res.steps_per_pe == [k] * pe
+        # barrier-free with one PE is also exact
+        res1 = H.exec_run(H.TemperatureField(u0), H.SolverParams.from_r(r), bc,
+                          H.PartitionSpec(n, n), H.ExecConfig(1, k, H.ExecMode.BarrierFree))
+        assert bits_equal(res1.field.values(), port.sync_run(u0, r, bc.kind, bc.c1, bc.c2, k))
+
+
+def test_exec_validation(H):
+    u0 = H.cosine_init(12)
+    p = H.SolverParams.from_r(0.5)
+    bc = H.BoundaryCondition.dirichlet(1.0, 0.0)
+    part = H.PartitionSpec(12, 3)
+    with pytest.raises(H.InvalidArgument):
+        H.exec_run(u0, p, bc, part, H.ExecConfig(3, 10, H.ExecMode.Barriered))
+    with pytest.raises(H.InvalidArgument):
+        H.exec_run(u0, p, bc, part, H.ExecConfig(4, 0, H.ExecMode.Barriered))
+
+
+def test_barrier_free_steady_state_and_lag(H):
+    # test_exec.cpp:89-97 and 121-136
+    u0 = H.cosine_init(100)
+    res = H.exec_run(u0, H.SolverParams.from_r(0.5), H.BoundaryCondition.dirichlet(1.0, 0.0),
+                     H.PartitionSpec(100, 25),
+                     H.ExecConfig(4, 200000, H.ExecMode.BarrierFree, True))
+    steady = H.linear_steady_state(100, 1.0, 0.0)
+    assert np.max(np.abs(res.field.values() - steady.values())) <= 1e-3
+    lag = res.lag
+    assert lag.reads > 0 and lag.max_lag >= lag.min_lag
+    assert sum(lag.histogram) + lag.overflow == lag.reads
+    st = res.stats
+    assert st.reads == lag.reads
+    assert st.max_delay <= 7  # default bound q_free = 8: delays in {0..7}
+    assert sum(st.delay_histogram) == st.reads
+
+
+def test_barrier_free_envelope(H):
+    # free-running iterates stay inside the initial envelope (SPEC maximum principle,
+    # test_async_sim.cpp:175-198)
+    gen = SplitMix64(31)
+    for _ in range(5):
+        n = 64
+        u0 = random_field(gen, n)
+        lo, hi = u0.min(), u0.max()
+        r = 0.5 * (gen.next_double() * 0.999 + 0.001)
+        res = H.exec_run(H.TemperatureField(u0), H.SolverParams.from_r(r),
+                         H.BoundaryCondition.dirichlet(u0[0], u0[-1]), H.PartitionSpec(n, 8),
+                         H.ExecConfig(8, 2000, H.ExecMode.BarrierFree, False, 4))
+        v = res.field.values()
+        assert v.min() >= lo - 1e-12 and v.max() <= hi + 1e-12
+        assert res.stats.max_delay <= 3
