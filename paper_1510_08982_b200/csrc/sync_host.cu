@@ -114,6 +114,8 @@ __global__ void narrow_kernel(const double* __restrict__ in, float* __restrict__
         out[i] = float(in[i]);
 }
 
+}  // namespace
+
 // Upload u0 (caller's host buffer, pinned or pageable) into `dst` (double),
 // validate it on the device and snap the Dirichlet ends
 // (prepare_initial, sync_solver.cpp:25-37).  Leaves the stream synchronised.
@@ -139,6 +141,8 @@ int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c
     }
     return HEAT_OK;
 }
+
+namespace {
 
 // Shared body of sync_run / sync_run_f32 (sync_solver.cpp:52-91).  Snapshots
 // and the final state are copied straight into the caller's buffers.
