@@ -254,15 +254,20 @@ def run_b200(args, rank, world, local):
     total_updates = float(n) * world * STEPS_PER_BENCH_STEP * args.steps
     glups = total_updates / (ms * 1e-3) / 1e9
 
-    # Roofline of the dominant kernel: every launch is one 32-step pass.
+    # Roofline of the dominant kernel (sync_tb_kernel, one launch per pass of
+    # <= 32 steps; each 1000-step chunk is 31 passes of 32 + one of 8).
+    # achieved = algorithmic bytes of all its launches / their device time;
+    # the timed region is nothing but those back-to-back launches.
     passes_per_step = -(-STEPS_PER_BENCH_STEP // STEPS_PER_PASS)
     sync_launches = passes_per_step * args.steps
     per_launch_s = ms * 1e-3 / sync_launches
-    alg_bytes = BYTES_PER_UPDATE * n * STEPS_PER_PASS
+    alg_bytes_total = BYTES_PER_UPDATE * float(n) * STEPS_PER_BENCH_STEP * args.steps
+    alg_bytes = alg_bytes_total / sync_launches  # per launch (average)
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / per_launch_s / 1e9
     fp64_peak = 148 * 64 * 1.965e9 / 1e12  # DP lanes x SMs x boost clock, T ops/s (nominal)
-    fp64_achieved = FP64_OPS_PER_UPDATE * n * STEPS_PER_PASS / per_launch_s / 1e12
+    fp64_achieved = FP64_OPS_PER_UPDATE * float(n) * STEPS_PER_BENCH_STEP * args.steps / (
+        ms * 1e-3) / 1e12
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
         "frac": round(achieved / peak, 4), "traffic": ncu_traffic_per_launch(),

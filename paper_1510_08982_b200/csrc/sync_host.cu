@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cudaTypedefs.h>
+
 #include "runtime.cuh"
 #include "sync_tb.cuh"
 
@@ -10,6 +12,44 @@ namespace hb {
 
 namespace {
 constexpr int kV = 32;  // points per lane; also the maximum steps per pass
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 3-D view of a field as [chunk][128-B row][row elements] with 128B swizzle;
+// the box is `box_chunks` whole V-point chunks.
+template <typename Real, int V>
+int make_chunk_map(CUtensorMap* m, const void* base, long long nchunks, int box_chunks) {
+    using T = SyncTB<Real, V>;
+    auto enc = tensor_map_encoder();
+    if (!enc) return fail(HEAT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {cuuint64_t(T::kRowElems), cuuint64_t(T::kRowsPerChunk),
+                                cuuint64_t(nchunks > 0 ? nchunks : 1)};
+    const cuuint64_t strides[2] = {128, cuuint64_t(T::kChunkBytes)};
+    const cuuint32_t box[3] = {cuuint32_t(T::kRowElems), cuuint32_t(T::kRowsPerChunk),
+                               cuuint32_t(box_chunks)};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, sizeof(Real) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(HEAT_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return HEAT_OK;
+}
 
 template <typename Real>
 int occupancy_blocks(int sms) {
@@ -72,6 +112,15 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
     a.c1 = c1;
     a.c2 = c2;
     a.nonfinite = flag;
+    if (g.out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
+    a.nchunks = g.len / kV;
+    // tensor maps: [chunk][row][16 doubles] views of both ping-pong arrays,
+    // 32-chunk boxes for window loads, 30-chunk boxes for output stores
+    CUtensorMap load_map[2], store_map[2];
+    for (int b = 0; b < 2; ++b) {
+        HB_TRY((make_chunk_map<Real, kV>(&load_map[b], bufs[b], a.nchunks, kWarp)));
+        HB_TRY((make_chunk_map<Real, kV>(&store_map[b], bufs[b], a.nchunks, kWarp - 2)));
+    }
     const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, T::kMaxSteps)
                                            : T::kMaxSteps;
     while (steps > 0) {
@@ -79,7 +128,8 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
         a.src = bufs[cur];
         a.dst = bufs[cur ^ 1];
         a.nsteps = s;
-        sync_tb_kernel<Real, kV><<<grid, T::kThreads, T::kSmemBytes, st>>>(a);
+        sync_tb_kernel<Real, kV><<<grid, T::kThreads, T::kSmemBytes, st>>>(load_map[cur],
+                                                                            store_map[cur ^ 1], a);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cur ^= 1;

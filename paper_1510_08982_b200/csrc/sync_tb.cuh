@@ -11,22 +11,26 @@
 //     __shfl_up / __shfl_down of the boundary PRODUCT r*u per step.
 //   * Lanes 0 and 31 are halo (redundant recompute).  After s <= V steps
 //     lanes 1..30 are exact, so a tile emits 30V points: tile t covers
-//     outputs [30Vt, 30V(t+1)), window start w0 = 30Vt - V.
+//     outputs [out_lo + 30Vt, out_lo + 30V(t+1)), window w0 = that - V.
 //   * No block barrier anywhere: warps are independent.  Each warp
-//     double-buffers its window in shared memory: a 1-D TMA bulk copy
-//     (cp.async.bulk, one V-point chunk per lane, padded by 16 B so the
-//     per-lane 16-B shared loads are bank-conflict free) lands the NEXT tile
-//     while the current one is being stepped; results go back through the
-//     same padded buffer with cp.async.bulk shared->global.
-//   * Tiles whose window touches a domain end (or is not 16-B aligned / in
-//     bounds) take the generic path: coalesced element loads with zero fill
-//     (Dirichlet) or modular wrap (periodic), Dirichlet ends re-pinned after
-//     every step, bounds-checked stores.
+//     double-buffers its window in shared memory.  One elected lane moves a
+//     whole window with ONE TMA tensor copy (cp.async.bulk.tensor.3d, SASS
+//     UTMALDG) into a 128B-swizzled buffer -- the tensor map views the array
+//     as [chunk][row][16 doubles] so each lane's chunk is two 128-B rows and
+//     the swizzle makes the per-lane 16-B shared loads conflict-light -- while
+//     the previous tile is being stepped; results return through the same
+//     buffer with one TMA tensor store (UTMASTG) of the 30 exact chunks.
+//   * Tiles whose window touches a pinned end, leaves [0, len) or whose
+//     outputs overrun out_hi take the generic path: per-lane element loads
+//     (zero fill or modular wrap), Dirichlet ends re-pinned after every
+//     step, bounds-checked stores.
 //
 // HBM traffic per pass: read 32V + write 30V points per 30V*s updates, i.e.
 // ~16.5/s bytes per lattice update (0.52 B at s = 32) -- the pass is bound by
 // the FP64 pipe (4 DP instructions per update), not by HBM.
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 
@@ -35,31 +39,39 @@ namespace hb {
 template <typename Real, int V>
 struct SyncTB {
     static constexpr int kChunkBytes = V * int(sizeof(Real));
-    static constexpr int kStrideBytes = kChunkBytes + 16;
-    static constexpr int kStrideElems = kStrideBytes / int(sizeof(Real));
-    static constexpr int kBufBytes = kWarp * kStrideBytes;
-    static constexpr int kOut = (kWarp - 2) * V;  // exact points per tile
+    static constexpr int kRowsPerChunk = kChunkBytes / 128;       // 128-B swizzle rows
+    static constexpr int kRowElems = 128 / int(sizeof(Real));
+    static constexpr int kPer16 = 16 / int(sizeof(Real));         // elements per 16-B unit
+    static constexpr int kBufBytes = kWarp * kChunkBytes;         // dense window
+    static constexpr int kOut = (kWarp - 2) * V;                  // exact points per tile
     static constexpr int kWarpsPerCta = 4;
     static constexpr int kThreads = kWarpsPerCta * kWarp;
-    static constexpr int kSmemBytes = kWarpsPerCta * 2 * kBufBytes + kWarpsPerCta * 2 * 8;
+    static constexpr int kSmemBytes = kWarpsPerCta * 2 * kBufBytes + kWarpsPerCta * 2 * 8 + 1024;
     static constexpr int kMaxSteps = V;  // halo of one lane per side
-    static_assert((V * sizeof(Real)) % 16 == 0, "chunk must be a multiple of 16 B");
+    static_assert(kChunkBytes % 128 == 0, "chunk must be whole 128-B swizzle rows");
 };
 
-// Padded shared chunk <-> registers, 16-byte vector accesses.
+// Byte offset of 16-B unit `m` of lane-slot `slot`'s chunk in a 128B-swizzled
+// buffer (row = slot*rows_per_chunk + m/8, unit ^= row & 7).
 template <typename Real, int V>
-__device__ __forceinline__ void chunk_from_smem(const Real* p, Real (&u)[V]) {
-    if constexpr (sizeof(Real) == 8) {
+__device__ __forceinline__ uint32_t swz_off(int slot, int m) {
+    using T = SyncTB<Real, V>;
+    const int row = slot * T::kRowsPerChunk + (m >> 3);
+    return uint32_t(row * 128 + (((m & 7) ^ (row & 7)) << 4));
+}
+
+template <typename Real, int V>
+__device__ __forceinline__ void chunk_from_smem(const unsigned char* buf, int slot, Real (&u)[V]) {
+    using T = SyncTB<Real, V>;
 #pragma unroll
-        for (int m = 0; m < V / 2; ++m) {
-            double2 v = reinterpret_cast<const double2*>(p)[m];
+    for (int m = 0; m < V / T::kPer16; ++m) {
+        const unsigned char* p = buf + swz_off<Real, V>(slot, m);
+        if constexpr (sizeof(Real) == 8) {
+            const double2 v = *reinterpret_cast<const double2*>(p);
             u[2 * m] = v.x;
             u[2 * m + 1] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int m = 0; m < V / 4; ++m) {
-            float4 v = reinterpret_cast<const float4*>(p)[m];
+        } else {
+            const float4 v = *reinterpret_cast<const float4*>(p);
             u[4 * m] = v.x;
             u[4 * m + 1] = v.y;
             u[4 * m + 2] = v.z;
@@ -68,16 +80,15 @@ __device__ __forceinline__ void chunk_from_smem(const Real* p, Real (&u)[V]) {
     }
 }
 template <typename Real, int V>
-__device__ __forceinline__ void chunk_to_smem(Real* p, const Real (&u)[V]) {
-    if constexpr (sizeof(Real) == 8) {
+__device__ __forceinline__ void chunk_to_smem(unsigned char* buf, int slot, const Real (&u)[V]) {
+    using T = SyncTB<Real, V>;
 #pragma unroll
-        for (int m = 0; m < V / 2; ++m)
-            reinterpret_cast<double2*>(p)[m] = make_double2(u[2 * m], u[2 * m + 1]);
-    } else {
-#pragma unroll
-        for (int m = 0; m < V / 4; ++m)
-            reinterpret_cast<float4*>(p)[m] =
-                make_float4(u[4 * m], u[4 * m + 1], u[4 * m + 2], u[4 * m + 3]);
+    for (int m = 0; m < V / T::kPer16; ++m) {
+        unsigned char* p = buf + swz_off<Real, V>(slot, m);
+        if constexpr (sizeof(Real) == 8)
+            *reinterpret_cast<double2*>(p) = make_double2(u[2 * m], u[2 * m + 1]);
+        else
+            *reinterpret_cast<float4*>(p) = make_float4(u[4 * m], u[4 * m + 1], u[4 * m + 2], u[4 * m + 3]);
     }
 }
 
@@ -126,6 +137,26 @@ __device__ __forceinline__ void pin_ends(Real (&u)[V], long long g0, long long p
     }
 }
 
+// ---- TMA tensor copies (3-D tile mode, 128B swizzle) ----------------------
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2,
+                                             const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::
+                     "l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
 // One pass over an array of `len` points.  Outputs [out_lo, out_hi) are
 // advanced by `nsteps`; reads outside [0, len) wrap (single-domain periodic)
 // or read as zero (their influence cannot reach the outputs in <= V steps, or
@@ -133,10 +164,12 @@ __device__ __forceinline__ void pin_ends(Real (&u)[V], long long g0, long long p
 // to c1 / c2 after every step.  A whole Dirichlet domain is
 // {len=N, out=[0,N), pin_lo=0, pin_hi=N-1}; a multi-GPU slab with H ghost
 // points per side is {len=n+2H, out=[H,H+n), pins only at true global ends}.
+// out_lo must be a multiple of V (tensor-map chunk coordinates).
 struct SyncPassArgs {
     const void* src;
     void* dst;
     long long len;
+    long long nchunks;  // whole V-point chunks of the array the tensor maps cover
     long long out_lo, out_hi;
     long long pin_lo, pin_hi;
     long long tiles;
@@ -148,9 +181,13 @@ struct SyncPassArgs {
 
 template <typename Real, int V>
 __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
-    sync_tb_kernel(const SyncPassArgs a) {
+    sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
+                   const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
     using T = SyncTB<Real, V>;
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 128B swizzle needs 1024-B aligned buffers
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const Real* __restrict__ src = static_cast<const Real*>(a.src);
     Real* __restrict__ dst = static_cast<Real*>(a.dst);
     const long long len = a.len;
@@ -164,27 +201,34 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
+        if (warp == 0) {
+            tma_prefetch_desc(&tm_src);
+            tma_prefetch_desc(&tm_dst);
+        }
     }
     __syncwarp();
 
     const long long nwarps = (long long)gridDim.x * T::kWarpsPerCta;
+    const long long tma_len = a.nchunks * V;
     auto window = [&](long long t) { return a.out_lo + t * T::kOut - V; };
-    auto in_window = [&](long long g, long long w0) { return g >= 0 && g >= w0 && g < w0 + kWarp * V; };
-    // Bulk-copy fast path: window in bounds, 16-B aligned, no pinned point inside.
+    auto in_window = [&](long long g, long long w0) {
+        return g >= 0 && g >= w0 && g < w0 + kWarp * V;
+    };
+    // TMA fast path: whole window inside the tensor, no pinned point inside.
     auto interior = [&](long long t) {
         const long long w0 = window(t);
-        return w0 >= 0 && w0 + kWarp * V <= len && ((w0 * (long long)sizeof(Real)) & 15) == 0 &&
-               !in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0);
+        return w0 >= 0 && w0 + kWarp * V <= tma_len && !in_window(a.pin_lo, w0) &&
+               !in_window(a.pin_hi, w0);
     };
-    auto bufp = [&](int b) { return reinterpret_cast<Real*>(wbase + b * T::kBufBytes); };
+    auto bufp = [&](int b) { return wbase + b * T::kBufBytes; };
     auto issue = [&](int b, long long t) {
-        bulk_wait_read_all();      // this lane's earlier bulk stores have left the buffer
-        fence_proxy_async_smem();  // and its generic accesses are ordered before the copy
+        fence_proxy_async_smem();  // this lane's generic accesses to the buffer come first
         __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&bars[b], kWarp * T::kChunkBytes);
-        __syncwarp();
-        bulk_g2s(bufp(b) + lane * T::kStrideElems, src + window(t) + (long long)lane * V,
-                 T::kChunkBytes, &bars[b]);
+        if (lane == 0) {
+            bulk_wait_read_all();  // the TMA store that last used this buffer has read it
+            mbar_arrive_expect_tx(&bars[b], T::kBufBytes);
+            tma_load_3d(bufp(b), &tm_src, 0, 0, int(window(t) / V), &bars[b]);
+        }
     };
 
     uint32_t phase = 0;
@@ -193,31 +237,27 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
     if (t < a.tiles && interior(t)) issue(0, t);
     for (int it = 0; t < a.tiles; ++it, t += nwarps) {
         const int b = it & 1;
-        Real* buf = bufp(b);
+        unsigned char* buf = bufp(b);
         const long long w0 = window(t);
         const bool inter = interior(t);
+        const long long g0 = w0 + (long long)lane * V;
         Real u[V];
         if (inter) {
             mbar_wait(&bars[b], (phase >> b) & 1u);
             phase ^= 1u << b;
-            chunk_from_smem<Real, V>(buf + lane * T::kStrideElems, u);
+            chunk_from_smem<Real, V>(buf, lane, u);
         } else {
-            bulk_wait_read_all();
-            __syncwarp();
-            for (int j = lane; j < kWarp * V; j += kWarp) {
-                long long g = w0 + j;
-                Real v;
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                long long g = g0 + i;
                 if (wrap) {
                     g %= len;
                     if (g < 0) g += len;
-                    v = src[g];
+                    u[i] = src[g];
                 } else {
-                    v = (g >= 0 && g < len) ? src[g] : Real(0);
+                    u[i] = (g >= 0 && g < len) ? src[g] : Real(0);
                 }
-                buf[(j / V) * T::kStrideElems + (j % V)] = v;
             }
-            __syncwarp();
-            chunk_from_smem<Real, V>(buf + lane * T::kStrideElems, u);
         }
         const long long tn = t + nwarps;
         if (tn < a.tiles && interior(tn)) issue(b ^ 1, tn);
@@ -225,38 +265,34 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
             for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
         } else {
-            const long long g0 = w0 + (long long)lane * V;
             for (int s = 0; s < a.nsteps; ++s) {
                 warp_step<Real, V>(u, r, c);
                 pin_ends<Real, V>(u, g0, a.pin_lo, a.pin_hi, c1, c2);
             }
         }
 
-        if (lane >= 1 && lane <= kWarp - 2) {
-            const long long g0 = w0 + (long long)lane * V;
+        const bool out_lane = lane >= 1 && lane <= kWarp - 2;
+        if (out_lane) {
 #pragma unroll
             for (int i = 0; i < V; ++i)
                 if (g0 + i < a.out_hi && !isfinite(u[i])) bad = true;
         }
-        __syncwarp();
-        chunk_to_smem<Real, V>(buf + lane * T::kStrideElems, u);
         if (inter && w0 + (kWarp - 1) * V <= a.out_hi) {
+            // stage the 30 exact chunks as a [30 x rows] box at the buffer start
+            if (out_lane) chunk_to_smem<Real, V>(buf, lane - 1, u);
             fence_proxy_async_smem();
-            if (lane >= 1 && lane <= kWarp - 2) {
-                bulk_s2g(dst + w0 + (long long)lane * V, buf + lane * T::kStrideElems,
-                         T::kChunkBytes);
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d(&tm_dst, 0, 0, int((w0 + V) / V), buf);
                 bulk_commit();
             }
-        } else {
-            __syncwarp();
-            for (int j = V + lane; j < (kWarp - 1) * V; j += kWarp) {
-                const long long g = w0 + j;
-                if (g < a.out_hi) dst[g] = buf[(j / V) * T::kStrideElems + (j % V)];
-            }
-            __syncwarp();
+        } else if (out_lane) {
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+                if (g0 + i < a.out_hi) dst[g0 + i] = u[i];
         }
     }
-    bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
     if (bad) atomicOr(a.nonfinite, 1u);
 }
 
