@@ -2,6 +2,7 @@
 // C-ABI entry points: heat_sync_step / heat_sync_run / heat_sync_run_f32.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include <cudaTypedefs.h>
 
@@ -51,21 +52,44 @@ int make_chunk_map(CUtensorMap* m, const void* base, long long nchunks, int box_
     return HEAT_OK;
 }
 
+// Compile-time variants of K1 (window buffers per warp x step-loop unroll);
+// HEAT_SYNC_VARIANT selects one for A/B measurements, the default is the
+// fastest measured on B200 (profiles/).
+using SyncKernelFn = void (*)(CUtensorMap, CUtensorMap, SyncPassArgs);
+struct SyncVariant {
+    SyncKernelFn fn;
+    int nbuf;
+    int blocks_per_sm;  // filled by the occupancy query
+};
+constexpr int kDefaultSyncVariant = 0;
+
 template <typename Real>
-int occupancy_blocks(int sms) {
-    static int cached[2] = {0, 0};
-    int& slot = cached[sizeof(Real) == 8 ? 0 : 1];
-    if (slot == 0) {
+int sync_variant(SyncVariant** out) {
+    static SyncVariant table[] = {
+        {sync_tb_kernel<Real, kV, 2, 1>, 2, 0},
+        {sync_tb_kernel<Real, kV, 2, 2>, 2, 0},
+        {sync_tb_kernel<Real, kV, 1, 1>, 1, 0},
+        {sync_tb_kernel<Real, kV, 1, 2>, 1, 0},
+    };
+    static const int idx = [] {
+        const char* e = std::getenv("HEAT_SYNC_VARIANT");
+        const int v = e ? std::atoi(e) : kDefaultSyncVariant;
+        return (v >= 0 && v < 4) ? v : kDefaultSyncVariant;
+    }();
+    SyncVariant& v = table[idx];
+    if (v.blocks_per_sm == 0) {
         using T = SyncTB<Real, kV>;
-        HB_CUDA(cudaFuncSetAttribute(sync_tb_kernel<Real, kV>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmemBytes));
+        const int smem = T::smem_bytes(v.nbuf);
+        HB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int per_sm = 0;
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sync_tb_kernel<Real, kV>,
-                                                              T::kThreads, T::kSmemBytes));
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, reinterpret_cast<const void*>(v.fn), T::kThreads, smem));
         if (per_sm < 1) return fail(HEAT_ECUDA, "sync_tb_kernel does not fit on an SM");
-        slot = per_sm;
+        v.blocks_per_sm = per_sm;
     }
-    return -slot;  // negative = ok, value = blocks per SM
+    *out = &v;
+    return HEAT_OK;
 }
 }  // namespace
 
@@ -88,9 +112,9 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
                       int max_steps_per_pass) {
     using T = SyncTB<Real, kV>;
     if (steps == 0) return HEAT_OK;
-    int occ = occupancy_blocks<Real>(sms);
-    if (occ > 0) return occ;
-    occ = -occ;
+    SyncVariant* var = nullptr;
+    HB_TRY(sync_variant<Real>(&var));
+    const int occ = var->blocks_per_sm;
     const long long tiles = (g.out_hi - g.out_lo + T::kOut - 1) / T::kOut;
     const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
     const int grid = int(std::min<long long>(want, (long long)sms * occ));
@@ -128,8 +152,8 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
         a.src = bufs[cur];
         a.dst = bufs[cur ^ 1];
         a.nsteps = s;
-        sync_tb_kernel<Real, kV><<<grid, T::kThreads, T::kSmemBytes, st>>>(load_map[cur],
-                                                                            store_map[cur ^ 1], a);
+        var->fn<<<grid, T::kThreads, T::smem_bytes(var->nbuf), st>>>(load_map[cur],
+                                                                      store_map[cur ^ 1], a);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cur ^= 1;

@@ -46,7 +46,10 @@ struct SyncTB {
     static constexpr int kOut = (kWarp - 2) * V;                  // exact points per tile
     static constexpr int kWarpsPerCta = 4;
     static constexpr int kThreads = kWarpsPerCta * kWarp;
-    static constexpr int kSmemBytes = kWarpsPerCta * 2 * kBufBytes + kWarpsPerCta * 2 * 8 + 1024;
+    // shared memory for NBUF window buffers per warp (+ mbarriers, + 1 KB alignment slack)
+    static constexpr int smem_bytes(int nbuf) {
+        return kWarpsPerCta * nbuf * kBufBytes + kWarpsPerCta * 2 * 8 + 1024;
+    }
     static constexpr int kMaxSteps = V;  // halo of one lane per side
     static_assert(kChunkBytes % 128 == 0, "chunk must be whole 128-B swizzle rows");
 };
@@ -179,11 +182,19 @@ struct SyncPassArgs {
     unsigned int* nonfinite;  // set to 1 when an exact output value is not finite
 };
 
-template <typename Real, int V>
-__global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
+// NBUF = 2: the window of the next tile lands in the second buffer while this
+//           tile is stepped; outputs are staged in the swizzled buffer and
+//           leave with one TMA tensor store.
+// NBUF = 1: the next tile's window lands in the (only) buffer as soon as this
+//           tile is in registers; outputs leave with 16-B vector stores
+//           straight from registers (half the shared memory -> more warps).
+// UNR:      unroll factor of the step loop.
+template <typename Real, int V, int NBUF, int UNR>
+__global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
     using T = SyncTB<Real, V>;
+    static_assert(NBUF == 1 || NBUF == 2, "one or two window buffers per warp");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 128B swizzle needs 1024-B aligned buffers
     unsigned char* smem = reinterpret_cast<unsigned char*>(
@@ -195,15 +206,16 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
     const bool wrap = a.wrap != 0;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* wbase = smem + warp * 2 * T::kBufBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kWarpsPerCta * 2 * T::kBufBytes) + 2 * warp;
+    unsigned char* wbase = smem + warp * NBUF * T::kBufBytes;
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(smem + T::kWarpsPerCta * NBUF * T::kBufBytes) + 2 * warp;
     if (lane == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
         if (warp == 0) {
             tma_prefetch_desc(&tm_src);
-            tma_prefetch_desc(&tm_dst);
+            if (NBUF == 2) tma_prefetch_desc(&tm_dst);
         }
     }
     __syncwarp();
@@ -225,7 +237,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
         fence_proxy_async_smem();  // this lane's generic accesses to the buffer come first
         __syncwarp();
         if (lane == 0) {
-            bulk_wait_read_all();  // the TMA store that last used this buffer has read it
+            if (NBUF == 2) bulk_wait_read_all();  // the TMA store that last used it has read it
             mbar_arrive_expect_tx(&bars[b], T::kBufBytes);
             tma_load_3d(bufp(b), &tm_src, 0, 0, int(window(t) / V), &bars[b]);
         }
@@ -236,7 +248,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
     long long t = (long long)blockIdx.x * T::kWarpsPerCta + warp;
     if (t < a.tiles && interior(t)) issue(0, t);
     for (int it = 0; t < a.tiles; ++it, t += nwarps) {
-        const int b = it & 1;
+        const int b = NBUF == 2 ? (it & 1) : 0;
         unsigned char* buf = bufp(b);
         const long long w0 = window(t);
         const bool inter = interior(t);
@@ -260,9 +272,10 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
             }
         }
         const long long tn = t + nwarps;
-        if (tn < a.tiles && interior(tn)) issue(b ^ 1, tn);
+        if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
+#pragma unroll UNR
             for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
         } else {
             for (int s = 0; s < a.nsteps; ++s) {
@@ -277,7 +290,8 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
             for (int i = 0; i < V; ++i)
                 if (g0 + i < a.out_hi && !isfinite(u[i])) bad = true;
         }
-        if (inter && w0 + (kWarp - 1) * V <= a.out_hi) {
+        const bool full = w0 + (kWarp - 1) * V <= a.out_hi;
+        if (NBUF == 2 && inter && full) {
             // stage the 30 exact chunks as a [30 x rows] box at the buffer start
             if (out_lane) chunk_to_smem<Real, V>(buf, lane - 1, u);
             fence_proxy_async_smem();
@@ -286,13 +300,23 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads)
                 tma_store_3d(&tm_dst, 0, 0, int((w0 + V) / V), buf);
                 bulk_commit();
             }
+        } else if (out_lane && full && g0 >= 0) {
+            // whole chunk in range: 16-B vector stores from registers
+#pragma unroll
+            for (int m = 0; m < V / T::kPer16; ++m) {
+                if constexpr (sizeof(Real) == 8)
+                    reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[2 * m], u[2 * m + 1]);
+                else
+                    reinterpret_cast<float4*>(dst + g0)[m] =
+                        make_float4(u[4 * m], u[4 * m + 1], u[4 * m + 2], u[4 * m + 3]);
+            }
         } else if (out_lane) {
 #pragma unroll
             for (int i = 0; i < V; ++i)
                 if (g0 + i < a.out_hi) dst[g0 + i] = u[i];
         }
     }
-    if (lane == 0) bulk_wait_all();
+    if (NBUF == 2 && lane == 0) bulk_wait_all();
     if (bad) atomicOr(a.nonfinite, 1u);
 }
 
