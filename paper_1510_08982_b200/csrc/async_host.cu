@@ -164,25 +164,15 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     char* base = static_cast<char*>(d.scratch);
     cudaStream_t st = d.stream;
 
-    // initial ring: slot 0 = step-0 edge values, prog = 0
-    std::vector<double> edges0(P * 2);
-    for (size_t p = 0; p < P; ++p) {
-        HB_CUDA(cudaMemcpyAsync(&edges0[p * 2 + 0], dfield + p * s.n, sizeof(double),
-                                cudaMemcpyDeviceToHost, st));
-        HB_CUDA(cudaMemcpyAsync(&edges0[p * 2 + 1], dfield + p * s.n + s.n - 1, sizeof(double),
-                                cudaMemcpyDeviceToHost, st));
-    }
-    HB_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> ring0(P * 2 * R, 0.0);
-    for (size_t p = 0; p < P; ++p) {
-        ring0[(p * 2 + 0) * R] = edges0[p * 2 + 0];
-        ring0[(p * 2 + 1) * R] = edges0[p * 2 + 1];
-    }
+    // initial ring: slot 0 = step-0 edge values, prog = 0 (one small kernel)
+    async_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (P * 2 * R + 255) / 256)), 256,
+                        0, st>>>(dfield, int(s.n), int(P), R, reinterpret_cast<double*>(base + o_ring),
+                                 reinterpret_cast<unsigned long long*>(base + o_prog),
+                                 s.want_logs ? reinterpret_cast<double*>(base + o_elog) : nullptr);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     std::vector<unsigned long long> stats0(kStatWords, 0);
     stats0[kStatLagMin] = ~0ull;
-    HB_CUDA(cudaMemcpyAsync(base + o_ring, ring0.data(), ring0.size() * sizeof(double),
-                            cudaMemcpyHostToDevice, st));
-    HB_CUDA(cudaMemsetAsync(base + o_prog, 0, P * sizeof(unsigned long long), st));
     HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
     if (!dtab.empty())
@@ -191,10 +181,6 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
                             cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemsetAsync(base + o_abort, 0, sizeof(unsigned int), st));
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
-    if (s.want_logs) {
-        HB_CUDA(cudaMemcpyAsync(base + o_elog, edges0.data(), P * 2 * sizeof(double),
-                                cudaMemcpyHostToDevice, st));
-    }
 
     AsyncPeArgs a{};
     a.field = dfield;

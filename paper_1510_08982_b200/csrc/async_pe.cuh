@@ -128,6 +128,23 @@ __device__ __forceinline__ uint64_t wait_prog(const AsyncPeArgs& a, const uint64
     return v;
 }
 
+// Ring state at step 0: slot 0 of every PE's two rings holds its step-0 edge
+// values, prog = 0 (everything else zero); the edge log gets step 0 too.
+__global__ void async_init_kernel(const double* __restrict__ field, int n, int P, int R,
+                                  double* ring, unsigned long long* prog, double* edge_log) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)P * 2 * R;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long ps = i / R;  // p*2 + side
+        const int slot = int(i % R);
+        const long long p = ps >> 1;
+        double v = 0.0;
+        if (slot == 0) v = field[p * n + ((ps & 1) ? n - 1 : 0)];
+        ring[i] = v;
+        if (slot == 0 && edge_log) edge_log[ps] = v;
+        if (slot == 0 && (ps & 1) == 0) prog[p] = 0;
+    }
+}
+
 template <int V, bool kShared>
 __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const AsyncPeArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -150,6 +167,11 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     if constexpr (!kShared) {
         if (!active) return;  // warp-uniform; no block barrier in the global-ring variant
     }
+    // [0,64) delay histogram, [64,128) writer-lag histogram, [128] lag overflow
+    __shared__ unsigned int s_hist[16][129];
+    unsigned int* whist = s_hist[(threadIdx.x >> 5) & 15];
+    for (int i = lane; i < 129; i += 32) whist[i] = 0;
+    __syncwarp();
     const int n = a.n;
     const long long lo = (long long)p * n;
     const double r = a.r, c = a.c;
@@ -205,13 +227,10 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 if ((unsigned long long)used > maxd) maxd = used;
                 lag_min = lag < lag_min ? lag : lag_min;
                 lag_max = lag > lag_max ? lag : lag_max;
-                if (a.stats) {
-                    atomicAdd(a.stats + kStatDelayHist + (used < 64 ? used : 63), 1ull);
-                    if (lag < 64)
-                        atomicAdd(a.stats + kStatLagHist + lag, 1ull);
-                    else
-                        atomicAdd(a.stats + kStatLagOverflow, 1ull);
-                }
+                // per-warp shared histograms: a global atomic here would sit in
+                // front of every st.release of the publish step below
+                atomicAdd(&whist[used < 64 ? used : 63], 1u);
+                atomicAdd(&whist[64 + (lag < 64 ? lag : 64)], 1u);
                 if (a.used_log) a.used_log[(k * a.P + p) * 2 + (left ? 0 : 1)] = int(m);
             }
         }
@@ -295,6 +314,14 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
         }
     }
     if (bad) atomicOr(a.flag, 1u);
+    __syncwarp();
+    if (a.stats) {
+        for (int i = lane; i < 129; i += 32) {
+            const unsigned int cnt = whist[i];
+            if (cnt) atomicAdd(a.stats + (i < 64 ? kStatDelayHist + i : kStatLagHist + (i - 64)),
+                               (unsigned long long)cnt);
+        }
+    }
     if (a.stats && reads) {
         atomicAdd(a.stats + kStatReads, reads);
         atomicAdd(a.stats + kStatWaits, waits);
