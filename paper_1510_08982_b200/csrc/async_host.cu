@@ -6,6 +6,7 @@
 #include <functional>
 
 #include "async_pe.cuh"
+#include "async_stream.cuh"
 #include "runtime.cuh"
 
 namespace hb {
@@ -271,8 +272,219 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     return HEAT_OK;
 }
 
-int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
-                    double* dst);
+// ---- K5: streaming async (PEs wider than a warp) ---------------------------
+namespace {
+constexpr int kSV = 32;  // points per lane of the stream kernel (= K1's V)
+
+__global__ void stream_init_kernel(const double* __restrict__ field, long long n, int P, int R,
+                                   double* ringL, double* ringR, unsigned long long* progL,
+                                   unsigned long long* progR) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)P * R;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long p = i / R;
+        const bool s0 = (i % R) == 0;
+        ringL[i] = s0 ? field[p * n] : 0.0;
+        ringR[i] = s0 ? field[p * n + n - 1] : 0.0;
+        if (s0) {
+            progL[p] = 0;
+            progR[p] = 0;
+        }
+    }
+}
+}  // namespace
+
+// Device scratch of one streaming run (rings persist across its launches).
+struct StreamLayout {
+    size_t P = 0, Tp = 0;
+    int R = 0, D = 0;
+    size_t o_ringL, o_ringR, o_progL, o_progR, o_done, o_counter, o_offL, o_offR, o_dtab, o_stats,
+        o_abort, bytes;
+};
+
+int stream_layout(const AsyncRunSpec& s, StreamLayout& L, std::vector<int>& offL,
+                  std::vector<int>& offR) {
+    if (s.n % kSV != 0)
+        return fail(HEAT_EINVAL, "async: PEs wider than 1024 points must be a multiple of 32 points");
+    L.P = s.N / s.n;
+    L.Tp = (s.n + SyncTB<double, kSV>::kOut - 1) / SyncTB<double, kSV>::kOut;
+    if (L.Tp < 2) return fail(HEAT_ELOGIC, "async stream: a PE needs >= 2 tiles");
+    L.R = 64;
+    while (L.R < 2 * int(s.q) + 2) L.R *= 2;
+    L.D = draw_offsets(s.N, s.n, s.bc_kind == HEAT_BC_DIRICHLET, offL, offR);
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += (b + 255) / 256 * 256; return o; };
+    L.o_ringL = take(L.P * L.R * sizeof(double));
+    L.o_ringR = take(L.P * L.R * sizeof(double));
+    L.o_progL = take(L.P * 8);
+    L.o_progR = take(L.P * 8);
+    L.o_done = take(L.P * L.Tp * 4);
+    L.o_counter = take(8);
+    L.o_offL = take(L.P * 4);
+    L.o_offR = take(L.P * 4);
+    L.o_dtab = take(s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC ? s.k_end * size_t(L.D) : 1);
+    L.o_stats = take(kStatWords * 8);
+    L.o_abort = take(4);
+    L.bytes = off;
+    return HEAT_OK;
+}
+
+// Advances bufs[cur] (device, prepared, N points) by `steps` from absolute
+// step k0 with the streaming kernel; init=true seeds the rings from the field.
+int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, const AsyncRunSpec& s,
+                         const StreamLayout& L, char* base, const std::vector<int>& offL,
+                         const std::vector<int>& offR, size_t k0, size_t steps, bool init,
+                         unsigned int* flag, float* device_ms) {
+    using T = SyncTB<double, kSV>;
+    if (init) {
+        std::vector<unsigned long long> stats0(kStatWords, 0);
+        stats0[kStatLagMin] = ~0ull;
+        stream_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (L.P * L.R + 255) / 256)),
+                             256, 0, st>>>(bufs[cur], (long long)s.n, int(L.P), L.R,
+                                           reinterpret_cast<double*>(base + L.o_ringL),
+                                           reinterpret_cast<double*>(base + L.o_ringR),
+                                           reinterpret_cast<unsigned long long*>(base + L.o_progL),
+                                           reinterpret_cast<unsigned long long*>(base + L.o_progR));
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        HB_CUDA(cudaMemcpyAsync(base + L.o_offL, offL.data(), L.P * 4, cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemcpyAsync(base + L.o_offR, offR.data(), L.P * 4, cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemcpyAsync(base + L.o_stats, stats0.data(), kStatWords * 8,
+                                cudaMemcpyHostToDevice, st));
+        if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {
+            std::vector<unsigned char> dtab(s.k_end * size_t(L.D));
+            const double lp = std::log1p(-s.geometric_p);
+            for (size_t k = 0; k < s.k_end; ++k) {
+                const size_t bound = std::min<size_t>(s.q - 1, k);
+                for (int o = 0; o < L.D; ++o) {
+                    const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * L.D + o);
+                    const double u = double(x >> 11) * 0x1.0p-53;
+                    double g = std::floor(std::log1p(-u) / lp);
+                    if (!std::isfinite(g) || g < 0.0) g = 0.0;
+                    dtab[k * L.D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
+                }
+            }
+            HB_CUDA(cudaMemcpy(base + L.o_dtab, dtab.data(), dtab.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    if (steps == 0) return HEAT_OK;
+    HB_CUDA(cudaMemsetAsync(base + L.o_done, 0, L.P * L.Tp * 4, st));
+    HB_CUDA(cudaMemsetAsync(base + L.o_counter, 0, 8, st));
+    HB_CUDA(cudaMemsetAsync(base + L.o_abort, 0, 4, st));
+
+    static int per_sm = 0;
+    const int smem = T::smem_bytes(2);
+    if (per_sm == 0) {
+        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<kSV>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<kSV>,
+                                                              T::kThreads, smem));
+        if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
+    }
+    const long long nchunks = (long long)(s.N / kSV);
+    CUtensorMap ld[2], stm[2];
+    for (int b = 0; b < 2; ++b) {
+        HB_TRY(make_chunk_map_f64(&ld[b], bufs[b], nchunks, kWarp));
+        HB_TRY(make_chunk_map_f64(&stm[b], bufs[b], nchunks, kWarp - 2));
+    }
+    AsyncStreamArgs a{};
+    a.buf[0] = bufs[cur];
+    a.buf[1] = bufs[cur ^ 1];
+    a.N = (long long)s.N;
+    a.n = (long long)s.n;
+    a.P = int(L.P);
+    a.Tp = int(L.Tp);
+    a.r = s.r;
+    a.c = 1.0 - 2.0 * s.r;
+    a.c1 = s.c1;
+    a.c2 = s.c2;
+    a.dirichlet = s.bc_kind == HEAT_BC_DIRICHLET;
+    a.k0 = (long long)k0;
+    a.steps = (long long)steps;
+    a.s = T::kMaxSteps;
+    a.npass = (a.steps + a.s - 1) / a.s;
+    a.mode = s.mode;
+    a.q = int(s.q);
+    a.R = L.R;
+    a.law = s.law;
+    a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
+    a.seed = s.seed;
+    a.D = L.D;
+    a.off_left = reinterpret_cast<const int*>(base + L.o_offL);
+    a.off_right = reinterpret_cast<const int*>(base + L.o_offR);
+    a.dtable = reinterpret_cast<const unsigned char*>(base + L.o_dtab);
+    a.ringL = reinterpret_cast<double*>(base + L.o_ringL);
+    a.ringR = reinterpret_cast<double*>(base + L.o_ringR);
+    a.progL = reinterpret_cast<unsigned long long*>(base + L.o_progL);
+    a.progR = reinterpret_cast<unsigned long long*>(base + L.o_progR);
+    a.done = reinterpret_cast<unsigned int*>(base + L.o_done);
+    a.counter = reinterpret_cast<unsigned long long*>(base + L.o_counter);
+    a.stats = reinterpret_cast<unsigned long long*>(base + L.o_stats);
+    a.flag = flag;
+    a.abort_word = reinterpret_cast<unsigned int*>(base + L.o_abort);
+    a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+    // maps follow the pass parity: pass pi reads a.buf[pi & 1]
+    const CUtensorMap& l0 = ld[cur];
+    const CUtensorMap& l1 = ld[cur ^ 1];
+    const CUtensorMap& s0 = stm[cur];
+    const CUtensorMap& s1 = stm[cur ^ 1];
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (device_ms) {
+        HB_CUDA(cudaEventCreate(&e0));
+        HB_CUDA(cudaEventCreate(&e1));
+        HB_CUDA(cudaEventRecord(e0, st));
+    }
+    async_stream_kernel<kSV><<<sms * per_sm, T::kThreads, smem, st>>>(l0, l1, s0, s1, a);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (device_ms) {
+        HB_CUDA(cudaEventRecord(e1, st));
+        HB_CUDA(cudaEventSynchronize(e1));
+        HB_CUDA(cudaEventElapsedTime(device_ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    if (a.npass & 1) cur ^= 1;
+    return HEAT_OK;
+}
+
+// Whole-run driver used by heat_async_run / heat_exec_run for wide PEs.
+int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur, size_t stride,
+                     const std::function<int(size_t, const double*)>& on_record,
+                     unsigned long long* host_stats, float* device_ms) {
+    StreamLayout L;
+    std::vector<int> offL, offR;
+    HB_TRY(stream_layout(s, L, offL, offR));
+    if (d.sms * 12 < 2) return fail(HEAT_ELOGIC, "async stream: too few warps");
+    HB_TRY(ensure_scratch(d, L.bytes));
+    char* base = static_cast<char*>(d.scratch);
+    cudaStream_t st = d.stream;
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
+    HB_TRY(async_stream_advance(d.sms, st, bufs, cur, s, L, base, offL, offR, 0, 0, true, d.flag,
+                                nullptr));
+    float total_ms = 0.f;
+    size_t k = 0;
+    while (k < s.k_end) {
+        const size_t next = stride ? std::min(s.k_end, (k / stride + 1) * stride) : s.k_end;
+        float ms = 0.f;
+        HB_TRY(async_stream_advance(d.sms, st, bufs, cur, s, L, base, offL, offR, k, next - k,
+                                    false, d.flag, device_ms ? &ms : nullptr));
+        total_ms += ms;
+        k = next;
+        unsigned int flags[2] = {0, 0};
+        HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
+        if (flags[0]) {
+            if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+            return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+        }
+        if (stride && on_record) HB_TRY(on_record(k, bufs[cur]));
+    }
+    if (device_ms) *device_ms = total_ms;
+    if (host_stats)
+        HB_CUDA(cudaMemcpy(host_stats, base + L.o_stats, kStatWords * 8, cudaMemcpyDeviceToHost));
+    return HEAT_OK;
+}
 
 }  // namespace hb
 
@@ -330,14 +542,17 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
-    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
-    double* field = static_cast<double*>(d->buf[0]);
-    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+    const bool wide = per_pe > 32 * 32;  // K5 streaming kernel, else K3 warp-per-PE
+    const size_t pitch = (N + 63) / 64 * 64;
+    HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
+    double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
+    int cur = 0;
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, bufs[0]));
 
     const bool want_snaps = snapshots != nullptr || steps_out != nullptr;
     size_t ns = 0;
     cudaStream_t st = d->stream;
-    auto record = [&](size_t k) -> int {
+    auto record_from = [&](size_t k, const double* field) -> int {
         if (ns < max_snapshots) {
             if (snapshots)
                 HB_CUDA(cudaMemcpyAsync(snapshots + ns * N, field, N * sizeof(double),
@@ -348,13 +563,20 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
         HB_CUDA(cudaStreamSynchronize(st));
         return HEAT_OK;
     };
-    if (want_snaps) HB_TRY(record(0));
+    if (want_snaps) HB_TRY(record_from(0, bufs[0]));
     AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 0, q, law, fixed_delay, geometric_p, seed,
                    k_end, false};
-    HB_TRY(async_pe_run(*d, s, field, want_snaps ? stride : 0, record, nullptr, nullptr, nullptr,
-                        nullptr));
+    if (wide) {
+        HB_TRY(async_stream_run(*d, s, bufs, cur, want_snaps ? stride : 0, record_from, nullptr,
+                                nullptr));
+    } else {
+        HB_TRY(async_pe_run(*d, s, bufs[0], want_snaps ? stride : 0,
+                            [&](size_t k) { return record_from(k, bufs[0]); }, nullptr, nullptr,
+                            nullptr, nullptr));
+    }
     if (final_out) {
-        HB_CUDA(cudaMemcpyAsync(final_out, field, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(final_out, bufs[cur], N * sizeof(double), cudaMemcpyDeviceToHost,
+                                st));
         HB_CUDA(cudaStreamSynchronize(st));
     }
     if (n_snapshots) *n_snapshots = ns;
@@ -402,16 +624,22 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     }
 
     std::lock_guard<std::mutex> lock(d->mu);
-    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
-    double* field = static_cast<double*>(d->buf[0]);
-    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+    const bool wide = per_pe > 32 * 32;
+    const size_t pitch = (N + 63) / 64 * 64;
+    HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
+    double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
+    int cur = 0;
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, bufs[0]));
     const size_t q = q_free ? q_free : 8;
     AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, k_end,
                    false};
     std::vector<unsigned long long> hs(kStatWords, 0);
     float ms = 0.f;
-    HB_TRY(async_pe_run(*d, s, field, 0, nullptr, hs.data(), nullptr, nullptr, &ms));
-    HB_CUDA(cudaMemcpy(field_out, field, N * sizeof(double), cudaMemcpyDeviceToHost));
+    if (wide)
+        HB_TRY(async_stream_run(*d, s, bufs, cur, 0, nullptr, hs.data(), &ms));
+    else
+        HB_TRY(async_pe_run(*d, s, bufs[0], 0, nullptr, hs.data(), nullptr, nullptr, &ms));
+    HB_CUDA(cudaMemcpy(field_out, bufs[cur], N * sizeof(double), cudaMemcpyDeviceToHost));
     if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
     if (lag) {
         std::memset(lag, 0, sizeof *lag);
@@ -433,9 +661,48 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     return HEAT_OK;
 }
 
-int heat_plan_async_advance(heat_plan*, double, int, double, double, size_t, size_t, size_t,
-                            heat_async_stats*) {
-    return fail(HEAT_ENODEV, "heat_plan_async_advance: streaming async kernel not built yet");
+int heat_plan_async_advance(heat_plan* p, double r, int bc_kind, double c1, double c2,
+                            size_t per_pe, size_t q, size_t steps, heat_async_stats* stats) {
+    // Free-running bounded-staleness async on a resident field: every call is
+    // a fresh run (rings seeded from the current field, k counted from 0).
+    if (!p) return fail(HEAT_EINVAL, "null plan");
+    if (p->world != 1) return fail(HEAT_EINVAL, "async advance of multi-GPU slabs is not supported");
+    if (per_pe == 0 || p->n % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+    if (per_pe <= 32 * 32 || per_pe == p->n)
+        return fail(HEAT_EINVAL, "plan async advance needs >= 2 PEs wider than 1024 points");
+    HB_CUDA(cudaSetDevice(p->device));
+    AsyncRunSpec s{p->n, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, steps,
+                   false};
+    StreamLayout L;
+    std::vector<int> offL, offR;
+    HB_TRY(stream_layout(s, L, offL, offR));
+    if (p->async_bytes < L.bytes) {
+        if (p->async_scratch) cudaFree(p->async_scratch);
+        p->async_scratch = nullptr;
+        p->async_bytes = 0;
+        HB_CUDA(cudaMalloc(&p->async_scratch, L.bytes));
+        p->async_bytes = L.bytes;
+    }
+    char* base = static_cast<char*>(p->async_scratch);
+    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, offL, offR, 0, 0,
+                                true, p->flag, nullptr));
+    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, offL, offR, 0,
+                                steps, false, p->flag, nullptr));
+    if (stats) {
+        std::vector<unsigned long long> hs(kStatWords, 0);
+        HB_CUDA(cudaMemcpyAsync(hs.data(), base + L.o_stats, kStatWords * 8, cudaMemcpyDeviceToHost,
+                                p->stream));
+        HB_CUDA(cudaStreamSynchronize(p->stream));
+        std::memset(stats, 0, sizeof *stats);
+        stats->reads = hs[kStatReads];
+        stats->waits = hs[kStatWaits];
+        stats->max_delay = hs[kStatMaxDelay];
+        for (int i = 0; i < 64; ++i) stats->delay_histogram[i] = hs[kStatDelayHist + i];
+    }
+    return HEAT_OK;
 }
 
 }  // extern "C"

@@ -1,0 +1,406 @@
+// async_stream.cuh -- K5: asynchronous FTCS at scale (PEs far wider than a
+// warp), one persistent launch for the whole run, no grid-wide barrier.
+//
+// Semantics (async_sim.cpp:77-106 / Eq. (4) of the paper): the field is split
+// into P contiguous PEs of n points.  Inside a PE every read is synchronous
+// (Jacobi); the first point of PE p reads the LAST point of PE p-1 at step
+// k - d, the last point reads the FIRST point of PE p+1 at step k - d, with d
+// replayed from the reference's SplitMix64 stream (deterministic mode, bit-
+// exact with async_run) or the newest value within the bound q (free mode).
+//
+// Execution: each PE's slab is cut into K1 tiles (30V exact points, V = 32)
+// advanced s <= V steps per HBM pass with redundant halo recompute (the same
+// warp_step, TMA tensor loads/stores and 128B-swizzled buffers as K1).  Work
+// items (pass, tile) are handed out in pass-major order by one atomic counter;
+// a tile may start pass pi once its same-PE neighbours finished pass pi-1
+// (per-tile pass counters, acquire/release) -- a local dependency, never a
+// barrier.  The two tiles at a PE boundary inject the neighbour's value into
+// the stencil every step: lane 1 (the PE's first point) and lane lR (its
+// last point) spin on the neighbour's progress counter, read the edge ring
+// slot, and publish their own new edge value + progress (release).  Within a
+// pass the boundary tiles are handed out first, in (right edge of PE b, left
+// edge of PE b+1) pairs, so every pair that handshakes is co-resident and the
+// kernel cannot deadlock with >= 2 warps.
+//
+// Rings: ringL[p][R] = history of PE p's first point, ringR[p][R] of its last
+// point, progL/progR = published step counts.  The two sides of a boundary
+// read each other, so neither runs more than q-1 steps ahead of the other and
+// R >= 2q + 2 slots can never be overwritten while still readable.
+#pragma once
+
+#include "async_pe.cuh"
+#include "sync_tb.cuh"
+
+namespace hb {
+
+struct AsyncStreamArgs {
+    double* buf[2];  // ping-pong fields (pass pi reads buf[pi & 1])
+    long long N;
+    long long n;   // points per PE (multiple of V)
+    int P;
+    int Tp;        // tiles per PE (>= 2)
+    double r, c, c1, c2;
+    int dirichlet;
+    long long k0;  // absolute step of the first pass
+    long long steps;
+    int s;         // steps per pass (<= V)
+    long long npass;
+    int mode;      // 0 deterministic, 1 free
+    int q, R;
+    int law, fixed_d;
+    unsigned long long seed;
+    long long D;
+    const int* off_left;
+    const int* off_right;
+    const unsigned char* dtable;  // GEOMETRIC delays [k*D + off] (absolute k)
+    double* ringL;                // [P][R]
+    double* ringR;                // [P][R]
+    unsigned long long* progL;    // [P]
+    unsigned long long* progR;    // [P]
+    unsigned int* done;           // [P*Tp] passes completed in this launch
+    unsigned long long* counter;  // work-item counter
+    unsigned long long* stats;
+    unsigned int* flag;
+    unsigned int* abort_word;
+    unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k, int off) {
+    const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
+    if (a.law == 2) return a.dtable[k * a.D + off];
+    const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
+    if (a.law == 0) return int(x % uint64_t(bound + 1));
+    return a.fixed_d < bound ? a.fixed_d : int(bound);
+}
+
+__device__ __forceinline__ bool spin_until(const AsyncStreamArgs& a, const unsigned long long* w,
+                                           long long need, unsigned long long* seen, bool* waited) {
+    uint64_t v = ld_acquire_gpu(reinterpret_cast<const uint64_t*>(w));
+    if ((long long)v >= need) {
+        *seen = v;
+        return true;
+    }
+    *waited = true;
+    const uint64_t t0 = globaltimer_ns();
+    unsigned spins = 0;
+    while ((long long)(v = ld_acquire_gpu(reinterpret_cast<const uint64_t*>(w))) < need) {
+        if ((++spins & 127u) == 0) {
+            if (*reinterpret_cast<volatile unsigned int*>(a.abort_word)) return false;
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+                atomicOr(a.flag + 1, 1u);
+                atomicExch(a.abort_word, 1u);
+                return false;
+            }
+        }
+    }
+    *seen = v;
+    return true;
+}
+
+__device__ __forceinline__ bool wait_done(const AsyncStreamArgs& a, const unsigned int* w,
+                                          unsigned int need) {
+    if (ld_acquire_gpu_u32(w) >= need) return true;
+    const uint64_t t0 = globaltimer_ns();
+    unsigned spins = 0;
+    while (ld_acquire_gpu_u32(w) < need) {
+        __nanosleep(64);
+        if ((++spins & 127u) == 0) {
+            if (*reinterpret_cast<volatile unsigned int*>(a.abort_word)) return false;
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+                atomicOr(a.flag + 1, 1u);
+                atomicExch(a.abort_word, 1u);
+                return false;
+            }
+        }
+    }
+    return true;
+}
+
+// Decoded work item.
+struct StreamItem {
+    long long pass;
+    int p;   // PE
+    int m;   // tile within the PE
+};
+
+__device__ __forceinline__ StreamItem decode_item(const AsyncStreamArgs& a, long long i) {
+    const long long T = (long long)a.P * a.Tp;
+    StreamItem it;
+    it.pass = i / T;
+    long long idx = i % T;
+    if (idx < 2LL * a.P) {  // boundary pairs first: (right edge of b, left edge of b+1)
+        const int b = int(idx >> 1);
+        if ((idx & 1) == 0) {
+            it.p = b;
+            it.m = a.Tp - 1;
+        } else {
+            it.p = (b + 1) % a.P;
+            it.m = 0;
+        }
+    } else {
+        idx -= 2LL * a.P;
+        const int inner = a.Tp - 2;
+        it.p = int(idx / inner);
+        it.m = 1 + int(idx % inner);
+    }
+    return it;
+}
+
+template <int V>
+__global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
+    async_stream_kernel(const __grid_constant__ CUtensorMap tm_load0,
+                        const __grid_constant__ CUtensorMap tm_load1,
+                        const __grid_constant__ CUtensorMap tm_store0,
+                        const __grid_constant__ CUtensorMap tm_store1, const AsyncStreamArgs a) {
+    using T = SyncTB<double, V>;
+    using A = Arith<double>;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* wbase = smem + warp * 2 * T::kBufBytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kWarpsPerCta * 2 * T::kBufBytes) + 2 * warp;
+    __shared__ unsigned int s_hist[T::kWarpsPerCta][129];
+    unsigned int* whist = s_hist[warp];
+    for (int i = lane; i < 129; i += 32) whist[i] = 0;
+    if (lane == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+
+    const double r = a.r, c = a.c;
+    const long long T_all = (long long)a.P * a.Tp;
+    const long long total = a.npass * T_all;
+    const long long tma_len = (a.N / V) * V;
+    uint32_t phase = 0;
+    bool bad = false, abort = false;
+    unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
+    int b = 0;
+
+    auto grab = [&]() -> long long {
+        unsigned long long i = 0;
+        if (lane == 0) i = atomicAdd(a.counter, 1ull);
+        return (long long)__shfl_sync(0xffffffffu, i, 0);
+    };
+    auto geometry = [&](const StreamItem& it, long long& lo, long long& w0, long long& out_hi) {
+        lo = (long long)it.p * a.n;
+        w0 = lo + (long long)it.m * T::kOut - V;
+        out_hi = lo + a.n;
+    };
+    auto deps_ready = [&](const StreamItem& it, bool block) -> bool {
+        if (it.pass == 0) return true;
+        const unsigned int need = unsigned(it.pass);
+        const int base = it.p * a.Tp;
+        bool ok = true;
+        if (lane < 3) {
+            const int mm = it.m + lane - 1;
+            if (mm >= 0 && mm < a.Tp) {
+                const unsigned int* w = a.done + base + mm;
+                ok = block ? wait_done(a, w, need) : (ld_acquire_gpu_u32(w) >= need);
+            }
+        }
+        return __all_sync(0xffffffffu, ok);
+    };
+    auto tma_ok = [&](long long w0) { return w0 >= 0 && w0 + kWarp * V <= tma_len; };
+    auto issue = [&](int bb, const StreamItem& it, long long w0) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            bulk_wait_read_all();
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> async proxy
+            mbar_arrive_expect_tx(&bars[bb], T::kBufBytes);
+            tma_load_3d(wbase + bb * T::kBufBytes, (it.pass & 1) ? &tm_load1 : &tm_load0, 0, 0,
+                        int(w0 / V), &bars[bb]);
+        }
+    };
+
+    long long pend_tile = -1;
+    unsigned int pend_pass = 0;
+    // Publish done[pend_tile] = pend_pass once its stores have landed
+    // (keep_groups = 1: the newest bulk store group may still be in flight).
+    auto signal_pending = [&](int keep_groups) {
+        __threadfence();  // every lane's generic stores of the pending tile, then...
+        __syncwarp();
+        if (lane == 0) {  // ...its TMA store group, then the release
+            if (keep_groups)
+                asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+            else
+                bulk_wait_all();
+            if (pend_tile >= 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                st_release_gpu_u32(a.done + pend_tile, pend_pass);
+            }
+        }
+        __syncwarp();
+        pend_tile = -1;
+    };
+
+    long long cur = grab();
+    bool cur_pref = false;  // window of `cur` already in flight into buffer b
+    while (cur < total && !abort) {
+        const StreamItem it = decode_item(a, cur);
+        long long lo, w0, out_hi;
+        geometry(it, lo, w0, out_hi);
+        const bool left_edge = it.m == 0, right_edge = it.m == a.Tp - 1;
+        const double* src = a.buf[it.pass & 1];
+        double* dst = a.buf[(it.pass & 1) ^ 1];
+        const long long kbeg = a.k0 + it.pass * a.s;
+        const int nst = int(min((long long)a.s, a.k0 + a.steps - kbeg));
+
+        // ---- window in
+        if (!cur_pref) {
+            if (!deps_ready(it, false)) signal_pending(0);  // never block holding a signal
+            if (!deps_ready(it, true)) { abort = true; break; }
+            if (tma_ok(w0)) issue(b, it, w0);
+        }
+        double u[V];
+        const long long g0 = w0 + (long long)lane * V;
+        if (tma_ok(w0)) {
+            mbar_wait(&bars[b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+            chunk_from_smem<double, V>(wbase + b * T::kBufBytes, lane, u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                const long long g = g0 + i;
+                u[i] = (g >= 0 && g < a.N) ? ld_relaxed_gpu_f64(src + g) : 0.0;
+            }
+        }
+        // ---- next item: grab now, prefetch if its dependencies are already met
+        const long long nxt = grab();
+        bool nxt_pref = false;
+        if (nxt < total) {
+            const StreamItem ni = decode_item(a, nxt);
+            long long nlo, nw0, nhi;
+            geometry(ni, nlo, nw0, nhi);
+            if (tma_ok(nw0) && deps_ready(ni, false)) {
+                issue(b ^ 1, ni, nw0);
+                nxt_pref = true;
+            }
+        }
+
+        // ---- step the tile; boundary tiles exchange edge values every step
+        const int lR = int((out_hi - 1 - w0) / V);  // lane holding the PE's last point
+        const bool pin_first = a.dirichlet && it.p == 0;
+        const bool pin_last = a.dirichlet && it.p == a.P - 1;
+        const int lpe = it.p > 0 ? it.p - 1 : (a.dirichlet ? -1 : a.P - 1);
+        const int rpe = it.p + 1 < a.P ? it.p + 1 : (a.dirichlet ? -1 : 0);
+        const bool needL = left_edge && lpe >= 0 && !pin_first;
+        const bool needR = right_edge && rpe >= 0 && !pin_last;
+        if (!left_edge && !right_edge) {
+            for (int s = 0; s < nst; ++s) warp_step<double, V>(u, r, c);
+        } else {
+            signal_pending(0);  // boundary tiles spin on other PEs: flush first
+            for (int s = 0; s < nst && !abort; ++s) {
+                const long long k = kbeg + s;
+                double ghost = 0.0;
+                const bool mine = (lane == 1 && needL) || (lane == lR && needR && !(lane == 1 && needL));
+                // a lane may own both sides only if lR == 1 (never: Tp >= 2 puts them in different tiles)
+                if (mine) {
+                    const bool left = lane == 1 && needL;
+                    const unsigned long long* pw = left ? a.progR + lpe : a.progL + rpe;
+                    const double* ring = left ? a.ringR + (size_t)lpe * a.R : a.ringL + (size_t)rpe * a.R;
+                    unsigned long long seen = 0;
+                    bool waited = false;
+                    long long mstep;
+                    if (a.mode == 0) {
+                        mstep = k - det_delay_s(a, k, left ? a.off_left[it.p] : a.off_right[it.p]);
+                        if (!spin_until(a, pw, mstep, &seen, &waited)) abort = true;
+                    } else {
+                        if (!spin_until(a, pw, k - (a.q - 1), &seen, &waited)) abort = true;
+                        mstep = (long long)seen < k ? (long long)seen : k;
+                    }
+                    if (!abort) {
+                        ghost = ld_relaxed_gpu_f64(ring + (mstep & (a.R - 1)));
+                        const unsigned long long used = (unsigned long long)(k - mstep);
+                        const unsigned long long lag = seen - (unsigned long long)mstep;
+                        reads++;
+                        waits += waited;
+                        maxd = used > maxd ? used : maxd;
+                        lag_min = lag < lag_min ? lag : lag_min;
+                        lag_max = lag > lag_max ? lag : lag_max;
+                        atomicAdd(&whist[used < 64 ? used : 63], 1u);
+                        atomicAdd(&whist[64 + (lag < 64 ? lag : 64)], 1u);
+                    }
+                }
+                if (__any_sync(0xffffffffu, abort)) {
+                    abort = true;
+                    break;
+                }
+                const double pFirst = A::mul(r, u[0]);
+                const double pLast = A::mul(r, u[V - 1]);
+                double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
+                double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
+                if (lane == 1 && needL) pL = A::mul(r, ghost);
+                if (lane == lR && needR) pR = A::mul(r, ghost);
+                chunk_step<double, V>(u, r, c, pL, pR, pFirst, pLast);
+                if (left_edge && pin_first && lane == 1) u[0] = a.c1;
+                if (right_edge && pin_last && lane == lR) u[V - 1] = a.c2;
+                // publish u_first(k+1) / u_last(k+1), then the progress (release)
+                const long long slot = (k + 1) & (a.R - 1);
+                if (left_edge && lane == 1) {
+                    st_relaxed_gpu_f64(a.ringL + (size_t)it.p * a.R + slot, u[0]);
+                    st_release_gpu(reinterpret_cast<uint64_t*>(a.progL + it.p), uint64_t(k + 1));
+                }
+                if (right_edge && lane == lR) {
+                    st_relaxed_gpu_f64(a.ringR + (size_t)it.p * a.R + slot, u[V - 1]);
+                    st_release_gpu(reinterpret_cast<uint64_t*>(a.progR + it.p), uint64_t(k + 1));
+                }
+            }
+            if (abort) break;
+        }
+
+        // ---- window out: lanes 1..30 that lie inside this PE
+        const bool out_lane = lane >= 1 && lane <= kWarp - 2 && g0 >= lo && g0 < out_hi;
+        if (out_lane) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) bad |= !isfinite(u[i]);
+        }
+        const bool full = w0 + (kWarp - 1) * V <= out_hi && w0 + V >= lo;
+        unsigned char* bufb = wbase + b * T::kBufBytes;
+        if (tma_ok(w0) && full) {
+            if (out_lane) chunk_to_smem<double, V>(bufb, lane - 1, u);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_3d((it.pass & 1) ? &tm_store0 : &tm_store1, 0, 0, int((w0 + V) / V), bufb);
+                bulk_commit();
+            }
+        } else if (out_lane) {
+#pragma unroll
+            for (int m = 0; m < V / 2; ++m)
+                reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[2 * m], u[2 * m + 1]);
+        }
+        // Declare the PREVIOUS item done (its store has had a whole compute
+        // phase to land: wait until at most this item's store group is in
+        // flight), and keep this one pending.  Blocking waits flush first.
+        signal_pending(1);
+        pend_tile = (long long)it.p * a.Tp + it.m;
+        pend_pass = unsigned(it.pass + 1);
+        cur = nxt;
+        cur_pref = nxt_pref;
+        if (nxt_pref) b ^= 1;
+    }
+    signal_pending(0);
+    if (bad) atomicOr(a.flag, 1u);
+    __syncwarp();
+    if (a.stats) {
+        for (int i = lane; i < 129; i += 32) {
+            const unsigned int cnt = whist[i];
+            if (cnt) atomicAdd(a.stats + (i < 64 ? kStatDelayHist + i : kStatLagHist + (i - 64)),
+                               (unsigned long long)cnt);
+        }
+        if (reads) {
+            atomicAdd(a.stats + kStatReads, reads);
+            atomicAdd(a.stats + kStatWaits, waits);
+            atomicMax(a.stats + kStatMaxDelay, maxd);
+            atomicMin(a.stats + kStatLagMin, lag_min);
+            atomicMax(a.stats + kStatLagMax, lag_max);
+        }
+    }
+}
+
+}  // namespace hb

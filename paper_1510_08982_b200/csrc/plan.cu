@@ -4,26 +4,6 @@
 
 #include "runtime.cuh"
 
-// Every plan is a slab with kSlabHalo ghost points on each side:
-// array = [ghost H | n owned points | ghost H].  A single-GPU plan
-// (world == 1) ignores the ghosts and advances the owned points as a whole
-// domain; a multi-GPU slab (world > 1) gets its ghosts refreshed by the caller
-// (heat_plan_halo_pack / _unpack around an NCCL or peer exchange) before each
-// pass of <= H steps, and only the true global ends are pinned.
-struct heat_plan {
-    int device = 0;
-    int rank = 0, world = 1;
-    size_t n = 0;
-    size_t pitch = 0;
-    double* base = nullptr;
-    int cur = 0;
-    cudaStream_t own = nullptr;
-    cudaStream_t stream = nullptr;
-    unsigned int* flag = nullptr;
-    int sms = 0;
-    double* bufs[2] = {nullptr, nullptr};  // owned points (base + H)
-    double* ext[2] = {nullptr, nullptr};   // ghosted arrays (base)
-};
 
 namespace hb {
 namespace {
@@ -80,6 +60,7 @@ int heat_plan_destroy(heat_plan* p) {
     cudaStreamSynchronize(p->stream);
     cudaFree(p->base);
     cudaFree(p->flag);
+    if (p->async_scratch) cudaFree(p->async_scratch);
     cudaStreamDestroy(p->own);
     delete p;
     return HEAT_OK;

@@ -13,6 +13,29 @@
 
 #include "../../include/heat_b200.h"
 
+// Every plan is a slab with kSlabHalo ghost points on each side:
+// array = [ghost H | n owned points | ghost H].  A single-GPU plan
+// (world == 1) ignores the ghosts and advances the owned points as a whole
+// domain; a multi-GPU slab (world > 1) gets its ghosts refreshed by the caller
+// (heat_plan_halo_pack / _unpack around an NCCL or peer exchange) before each
+// pass of <= H steps, and only the true global ends are pinned.
+struct heat_plan {
+    int device = 0;
+    int rank = 0, world = 1;
+    size_t n = 0;
+    size_t pitch = 0;
+    double* base = nullptr;
+    int cur = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    unsigned int* flag = nullptr;
+    int sms = 0;
+    double* bufs[2] = {nullptr, nullptr};  // owned points (base + H)
+    double* ext[2] = {nullptr, nullptr};   // ghosted arrays (base)
+    void* async_scratch = nullptr;         // rings / counters of heat_plan_async_advance
+    size_t async_bytes = 0;
+};
+
 namespace hb {
 
 void set_error(const std::string& msg);
@@ -74,6 +97,18 @@ template <typename Real>
 int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,
                       double c2, size_t steps, unsigned int* flag, cudaStream_t st,
                       int max_steps_per_pass = 0);
+
+// Tensor map over an f64 array viewed as [chunk of 32][128-B row][16]
+// (128B swizzle), `box_chunks` chunks per box (sync_host.cu).
+int make_chunk_map_f64(struct CUtensorMap_st* m, const void* base, long long nchunks,
+                       int box_chunks);
+
+// Upload + validate + snap a host field into `dst` (sync_host.cu).
+int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
+                    double* dst);
+
+// In-step draw ranks of the cross-PE reads (async_host.cu), returns D.
+int draw_offsets(size_t N, size_t n, int dirichlet, std::vector<int>& offL, std::vector<int>& offR);
 
 // Synchronous advance on device buffers (ping-pong).  `cur` selects the
 // buffer holding u(k) on entry and is updated.  Does not synchronise.

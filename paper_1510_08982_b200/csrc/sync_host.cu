@@ -162,6 +162,10 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
     return HEAT_OK;
 }
 
+int make_chunk_map_f64(CUtensorMap* m, const void* base, long long nchunks, int box_chunks) {
+    return make_chunk_map<double, kV>(m, base, nchunks, box_chunks);
+}
+
 template int sync_advance<double>(int, double* [2], int&, long long, double, int, double, double,
                                   size_t, unsigned int*, cudaStream_t);
 template int sync_advance<float>(int, float* [2], int&, long long, double, int, double, double,

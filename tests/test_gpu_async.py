@@ -200,3 +200,62 @@ def test_barrier_free_envelope(H):
         v = res.field.values()
         assert v.min() >= lo - 1e-12 and v.max() <= hi + 1e-12
         assert res.stats.max_delay <= 3
+
+
+# ---- K5: streaming async (PEs wider than a warp) ---------------------------
+@pytest.mark.parametrize("n_total,per_pe,q,bc,law", [
+    (16384, 2048, 3, 0, 0), (16384, 4096, 2, 1, 0), (12288, 3072, 4, 0, 1),
+    (8192, 2048, 5, 1, 2), (1 << 20, 1 << 15, 5, 0, 0)])
+def test_stream_deterministic_bit_exact(H, port, n_total, per_pe, q, bc, law):
+    gen = SplitMix64(n_total + per_pe + q + bc)
+    u0 = random_field(gen, n_total)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.4)
+    k = 100 if n_total >= (1 << 20) else 150
+    fd = 1 if law == 1 else 0
+    model = H.DelayModel(q, H.Distribution(law), fd, 0.6, 1234 + q)
+    got = H.async_final(u0, p, b, H.PartitionSpec(n_total, per_pe), model, k)
+    exp = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, law, q, fd, 0.6, 1234 + q, k)
+    assert bits_equal(got, exp)
+
+
+def test_stream_trajectory_bit_exact(H, port):
+    gen = SplitMix64(77)
+    u0 = random_field(gen, 8192)
+    p = H.SolverParams.from_r(0.3)
+    b = H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    t = H.async_run(H.TemperatureField(u0), p, b, H.PartitionSpec(8192, 2048),
+                    H.DelayModel.uniform(3, 5), 90, 40)
+    steps, snaps = port.async_run(u0, p.r(), 0, b.c1, b.c2, 2048, 0, 3, seed=5, k_end=90,
+                                  stride=40, record=True)
+    assert t.steps == steps == [0, 40, 80, 90]
+    for j, s in enumerate(t.snapshots):
+        assert bits_equal(s.values(), snaps[j])
+
+
+def test_stream_free_q1_is_sync(H, port):
+    # free-running with q = 1 must read exactly u_j(k): bit-identical to sync
+    n = 1 << 18
+    gen = SplitMix64(3)
+    u0 = random_field(gen, n)
+    u0[0] = u0[-1] = 0.0
+    plan = H.Plan(n)
+    plan.upload(u0)
+    st = plan.async_advance(0.4, H.BoundaryCondition.dirichlet(0, 0), 1 << 13, 1, 200)
+    got = plan.download()
+    exp = port.sync_run(u0, 0.4, 0, 0.0, 0.0, 200)
+    assert bits_equal(got, exp)
+    assert st.max_delay == 0 and st.reads > 0
+
+
+def test_stream_free_bounded(H, port):
+    n = 1 << 18
+    u0 = port.prepare_initial(port.sine_init(n), 0, 0.0, 0.0)
+    plan = H.Plan(n)
+    plan.upload(u0)
+    st = plan.async_advance(0.4, H.BoundaryCondition.dirichlet(0, 0), 1 << 12, 4, 500)
+    got = plan.download()
+    assert st.max_delay <= 3 and sum(st.delay_histogram) == st.reads > 0
+    assert got.min() >= -1e-12 and got.max() <= 1.0 + 1e-12  # envelope of the sine IC
+    exp = port.sync_run(u0, 0.4, 0, 0.0, 0.0, 500)
+    assert np.max(np.abs(got - exp)) < 1e-3
