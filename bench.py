@@ -280,6 +280,13 @@ def run_b200(args, rank, world, local):
                  "frac": round(fp64_achieved / fp64_peak, 4)},
     }
 
+    # Asynchronous scheme on the same workload (single GPU): K5 streaming
+    # kernel, PEs of 2^21 points, free-running with delays <= 7 and the
+    # deterministic replay of a seeded q=2 stream.
+    async_info = None
+    if world == 1 and not args.skip_async:
+        async_info = run_async(args, H, torch, plan, stream, n, r, bc, glups)
+
     # End to end through the public API with host buffers (copies timed).
     e2e = None
     if not args.skip_e2e:
@@ -297,7 +304,7 @@ def run_b200(args, rank, world, local):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (sine IC generated on device)", "config": config_dict(world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clk.summary(), "async": async_info,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -305,6 +312,45 @@ def run_b200(args, rank, world, local):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+ASYNC_PES = 512  # 2^21 points per PE at N = 2^30
+
+
+def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
+    """Async vs sync on the cfg3 workload: same steps, device-timed."""
+    per_pe = n // ASYNC_PES
+    out = {"pes": ASYNC_PES, "points_per_pe": per_pe,
+           "kernel": "async_stream_kernel<32> (persistent, PE-boundary acquire/release rings)"}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for name, call in (
+            ("free", lambda: plan.async_advance(r, bc, per_pe, 8, STEPS_PER_BENCH_STEP)),
+            ("deterministic", lambda: plan.async_replay(r, bc, per_pe, H.DelayModel.uniform(2, 1),
+                                                        STEPS_PER_BENCH_STEP))):
+        plan.fill_sine()
+        for _ in range(max(1, args.warmup)):
+            call()
+        plan.synchronize()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        stats = [call() for _ in range(args.steps)]
+        e1.record(stream)
+        plan.synchronize()
+        ms = e0.elapsed_time(e1)
+        v = float(n) * STEPS_PER_BENCH_STEP * args.steps / (ms * 1e-3) / 1e9
+        st = stats[-1]
+        out[name] = {
+            "value": round(v, 3), "unit": UNIT, "ms_per_step": round(ms / args.steps, 3),
+            "q": 8 if name == "free" else 2,
+            "delay_law": "newest value with k-k* <= 7" if name == "free"
+            else "DelayModel::uniform(q=2, seed=1) replayed bit-exactly",
+            "reads_per_run": int(st.reads), "waits_per_run": int(st.waits),
+            "max_delay": int(st.max_delay),
+            "delay_histogram": [int(x) for x in st.delay_histogram[:8]],
+            "vs_sync": round(v / sync_glups, 4),
+        }
+    return out
 
 
 def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance):
@@ -355,6 +401,7 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-async", action="store_true")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":

@@ -148,9 +148,17 @@ int heat_plan_fill_sine(heat_plan* plan);
 /* Advance the resident field by `steps` synchronous steps (no host sync). */
 int heat_plan_sync_advance(heat_plan* plan, double r, int bc_kind, double c1, double c2,
                            size_t steps);
-/* Advance by `steps` with the free-running async kernel on P = n/per_pe PEs. */
+/* Advance by `steps` with the free-running async kernel on P = n/per_pe PEs
+ * (delays bounded by q-1, observed delays logged in `stats`).  Each call is a
+ * fresh run from the current field. */
 int heat_plan_async_advance(heat_plan* plan, double r, int bc_kind, double c1, double c2,
                             size_t per_pe, size_t q, size_t steps, heat_async_stats* stats);
+/* Same, deterministic: replays the DelayModel's seeded stream exactly as
+ * async_run would (async_sim.cpp:77-160) for `steps` steps from step 0. */
+int heat_plan_async_replay(heat_plan* plan, double r, int bc_kind, double c1, double c2,
+                           size_t per_pe, size_t q, int law, size_t fixed_delay,
+                           double geometric_p, uint64_t seed, size_t steps,
+                           heat_async_stats* stats);
 /* Blocks until the plan's stream is idle; reports strict-check / watchdog status. */
 int heat_plan_synchronize(heat_plan* plan);
 /* Device pointer of the current field (for peer copies / NCCL in multi-GPU). */

@@ -117,6 +117,8 @@ SIGNATURES = {
     "heat_plan_fill_sine": (_i, [_vp]),
     "heat_plan_sync_advance": (_i, [_vp, _d, _i, _d, _d, _sz]),
     "heat_plan_async_advance": (_i, [_vp, _d, _i, _d, _d, _sz, _sz, _sz, _P(AsyncStatsC)]),
+    "heat_plan_async_replay": (_i, [_vp, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _u64, _sz,
+                                    _P(AsyncStatsC)]),
     "heat_plan_synchronize": (_i, [_vp]),
     "heat_plan_device_ptr": (_i, [_vp, _P(_vp)]),
     "heat_slab_halo": (_sz, []),

@@ -661,11 +661,36 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     return HEAT_OK;
 }
 
+static int plan_async(heat_plan* p, const AsyncRunSpec& s, heat_async_stats* stats);
+
 int heat_plan_async_advance(heat_plan* p, double r, int bc_kind, double c1, double c2,
                             size_t per_pe, size_t q, size_t steps, heat_async_stats* stats) {
-    // Free-running bounded-staleness async on a resident field: every call is
-    // a fresh run (rings seeded from the current field, k counted from 0).
     if (!p) return fail(HEAT_EINVAL, "null plan");
+    AsyncRunSpec s{p->n, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, steps,
+                   false};
+    return plan_async(p, s, stats);
+}
+
+int heat_plan_async_replay(heat_plan* p, double r, int bc_kind, double c1, double c2,
+                           size_t per_pe, size_t q, int law, size_t fixed_delay,
+                           double geometric_p, uint64_t seed, size_t steps,
+                           heat_async_stats* stats) {
+    if (!p) return fail(HEAT_EINVAL, "null plan");
+    if (law < 0 || law > 2) return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
+    if (q > 0 && law == HEAT_DELAY_FIXED && fixed_delay >= q)
+        return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
+    if (law == HEAT_DELAY_GEOMETRIC && (!(geometric_p > 0.0) || geometric_p > 1.0))
+        return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
+    AsyncRunSpec s{p->n, per_pe, r, bc_kind, c1, c2, 0, q, law, fixed_delay, geometric_p, seed,
+                   steps, false};
+    return plan_async(p, s, stats);
+}
+
+// Bounded-staleness async on a resident field: every call is a fresh run
+// (rings seeded from the current field, k counted from 0).
+static int plan_async(heat_plan* p, const AsyncRunSpec& s, heat_async_stats* stats) {
+    const size_t per_pe = s.n, q = s.q, steps = s.k_end;
+    const int bc_kind = s.bc_kind;
     if (p->world != 1) return fail(HEAT_EINVAL, "async advance of multi-GPU slabs is not supported");
     if (per_pe == 0 || p->n % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
     if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
@@ -674,8 +699,6 @@ int heat_plan_async_advance(heat_plan* p, double r, int bc_kind, double c1, doub
     if (per_pe <= 32 * 32 || per_pe == p->n)
         return fail(HEAT_EINVAL, "plan async advance needs >= 2 PEs wider than 1024 points");
     HB_CUDA(cudaSetDevice(p->device));
-    AsyncRunSpec s{p->n, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, steps,
-                   false};
     StreamLayout L;
     std::vector<int> offL, offR;
     HB_TRY(stream_layout(s, L, offL, offR));

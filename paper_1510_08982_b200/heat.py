@@ -509,9 +509,19 @@ class Plan:
                    "sync_advance")
 
     def async_advance(self, r: float, bc: BoundaryCondition, per_pe: int, q: int, steps: int):
+        """Free-running bounded-staleness async (delays <= q-1), a fresh run."""
         st = _lib.AsyncStatsC()
         _lib.check(_lib.lib().heat_plan_async_advance(self._h, r, bc.kind, bc.c1, bc.c2, per_pe,
                                                       q, steps, C.byref(st)), "async_advance")
+        return st
+
+    def async_replay(self, r: float, bc: BoundaryCondition, per_pe: int, model: "DelayModel",
+                     steps: int):
+        """Deterministic async: replays `model`'s seeded delays (async_run semantics)."""
+        st = _lib.AsyncStatsC()
+        _lib.check(_lib.lib().heat_plan_async_replay(self._h, r, bc.kind, bc.c1, bc.c2, per_pe,
+                                                     *model._args(), steps, C.byref(st)),
+                   "async_replay")
         return st
 
     def synchronize(self):

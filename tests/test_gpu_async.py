@@ -259,3 +259,17 @@ def test_stream_free_bounded(H, port):
     assert got.min() >= -1e-12 and got.max() <= 1.0 + 1e-12  # envelope of the sine IC
     exp = port.sync_run(u0, 0.4, 0, 0.0, 0.0, 500)
     assert np.max(np.abs(got - exp)) < 1e-3
+
+
+def test_plan_async_replay_bit_exact(H, port):
+    # the resident-plan deterministic replay (bench's async_det leg) == async_run
+    n = 1 << 16
+    gen = SplitMix64(123)
+    u0 = random_field(gen, n)
+    u0[0] = u0[-1] = 0.0
+    plan = H.Plan(n)
+    plan.upload(u0)
+    plan.async_replay(0.4, H.BoundaryCondition.dirichlet(0, 0), 1 << 13,
+                      H.DelayModel.uniform(2, 1), 300)
+    exp = port.async_run(u0, 0.4, 0, 0.0, 0.0, 1 << 13, 0, 2, seed=1, k_end=300)
+    assert bits_equal(plan.download(), exp)
