@@ -121,6 +121,17 @@ int heat_async_run(const double* u0, size_t n, double r, int bc_kind, double c1,
 int heat_sample_delay(size_t q, int law, size_t fixed_delay, double geometric_p, uint64_t seed,
                       uint64_t j, size_t k, size_t* delay);
 
+/* Free-running asynchronous run (bounded staleness: every neighbour value a PE
+ * consumes at step k is u_j(k*) with 0 <= k - k* <= q-1) with full edge logs,
+ * for PEs of <= 1024 points.  On return `stats` holds the reader-relative
+ * delay histogram and stats->residual_sum = sum_k ||u(k+1) - A u(k)||_inf, the
+ * a-posteriori bound on ||u_async(K) - u_sync(K)||_inf (A = one synchronous
+ * step; valid for 0 < r <= 1/2 where A is inf-norm non-expansive, plus a
+ * K*8*eps*max|u| rounding allowance).  SURVEY.md §8a row 12. */
+int heat_async_free_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                        size_t per_pe, size_t q, size_t k_end, double* final_out,
+                        heat_async_stats* stats);
+
 /* ---- executors (async_exec.hpp:53-70) ----------------------------------- */
 /* exec_run: Barriered = bit-identical to sync_run (one launch-chain on the
  * GPU, no per-step barrier); BarrierFree = free-running PEs on the GPU with

@@ -107,6 +107,7 @@ SIGNATURES = {
     "heat_async_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _u64, _sz, _sz,
                             _pd, _pd, _psz, _sz, _psz]),
     "heat_sample_delay": (_i, [_sz, _i, _sz, _d, _u64, _u64, _sz, _psz]),
+    "heat_async_free_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _pd, _P(AsyncStatsC)]),
     "heat_exec_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _i, _sz, _pd, _pu64,
                            _P(LagStatsC), _P(AsyncStatsC)]),
     "heat_plan_create": (_i, [_P(_vp), _sz, _i]),

@@ -583,6 +583,73 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
     return HEAT_OK;
 }
 
+int heat_async_free_run(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                        size_t per_pe, size_t q, size_t k_end, double* final_out,
+                        heat_async_stats* stats) {
+    if (N < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u0 || !final_out) return fail(HEAT_EINVAL, "null field pointer");
+    if (per_pe == 0 || N % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
+    if (per_pe > 32 * 32) return fail(HEAT_EINVAL, "logged free run: PEs of <= 1024 points");
+    if (per_pe == N) return fail(HEAT_EINVAL, "logged free run: needs >= 2 PEs");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    std::lock_guard<std::mutex> lock(d->mu);
+    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
+    double* field = static_cast<double*>(d->buf[0]);
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+    AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, k_end, true};
+    std::vector<unsigned long long> hs(kStatWords, 0);
+    std::vector<double> elog;
+    std::vector<int> ulog;
+    HB_TRY(async_pe_run(*d, s, field, 0, nullptr, hs.data(), &elog, &ulog, nullptr));
+    HB_CUDA(cudaMemcpy(final_out, field, N * sizeof(double), cudaMemcpyDeviceToHost));
+
+    // a-posteriori residual: only PE-boundary points read a neighbour; the
+    // async step differs from A u(k) there by r*(u_j(k*) - u_j(k)).
+    const size_t P = N / per_pe;
+    const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+    double umax = 0.0, sum = 0.0;
+    for (size_t i = 0; i < N; ++i) umax = std::max(umax, std::abs(u0[i]));
+    for (double v : elog) umax = std::max(umax, std::abs(v));
+    for (size_t k = 0; k < k_end; ++k) {
+        double res = 0.0;
+        for (size_t p = 0; p < P; ++p) {
+            const size_t first = p * per_pe, last = first + per_pe - 1;
+            const long long lpe = p > 0 ? (long long)p - 1 : (dir ? -1 : (long long)P - 1);
+            const long long rpe = p + 1 < P ? (long long)p + 1 : (dir ? -1 : 0);
+            double rp = 0.0;
+            const bool pin_first = dir && (first == 0 || first == N - 1);
+            const bool pin_last = dir && (last == 0 || last == N - 1);
+            if (lpe >= 0 && !pin_first) {  // first point read PE lpe's last point at k*
+                const int ks = ulog[(k * P + p) * 2 + 0];
+                rp += r * std::abs(elog[(size_t(ks) * P + lpe) * 2 + 1] - elog[(k * P + lpe) * 2 + 1]);
+            }
+            double rq = 0.0;
+            if (rpe >= 0 && !pin_last) {  // last point read PE rpe's first point at k*
+                const int ks = ulog[(k * P + p) * 2 + 1];
+                rq = r * std::abs(elog[(size_t(ks) * P + rpe) * 2 + 0] - elog[(k * P + rpe) * 2 + 0]);
+            }
+            // with one point per PE both reads hit the same point
+            res = std::max(res, per_pe == 1 ? rp + rq : std::max(rp, rq));
+        }
+        sum += res;
+    }
+    const double eps = 0x1.0p-52;
+    sum += double(k_end) * 8.0 * eps * std::max(1.0, umax);  // rounding of both sequences
+    if (stats) {
+        std::memset(stats, 0, sizeof *stats);
+        stats->reads = hs[kStatReads];
+        stats->waits = hs[kStatWaits];
+        stats->max_delay = hs[kStatMaxDelay];
+        for (int i = 0; i < 64; ++i) stats->delay_histogram[i] = hs[kStatDelayHist + i];
+        stats->residual_sum = sum;
+    }
+    return HEAT_OK;
+}
+
 int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
                   size_t per_pe, size_t workers, size_t k_end, int mode, int record_lag,
                   size_t q_free, double* field_out, uint64_t* duration_ns, heat_lag_stats* lag,

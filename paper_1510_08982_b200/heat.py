@@ -351,6 +351,24 @@ def async_final(u0, params: SolverParams, bc: BoundaryCondition, part: Partition
     return out
 
 
+def async_free_run(u0, params: SolverParams, bc: BoundaryCondition, part: PartitionSpec,
+                   q: int, k_end: int):
+    """Free-running async with bounded staleness q and full edge logs (GPU only).
+
+    Returns (final field as ndarray, AsyncStats); stats.residual_sum is the
+    a-posteriori bound on ||u_async(K) - u_sync(K)||_inf."""
+    v = _field(u0)
+    if part.total() != v.size:
+        raise InvalidArgument("async_free_run: partition inconsistent with grid")
+    out = np.empty_like(v)
+    st = _lib.AsyncStatsC()
+    _lib.check(_lib.lib().heat_async_free_run(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1,
+                                              bc.c2, part.per_pe(), q, k_end, _lib.dptr(out),
+                                              C.byref(st)), "async_free_run")
+    return out, AsyncStats(int(st.reads), int(st.max_delay), [int(x) for x in st.delay_histogram],
+                           int(st.waits), float(st.residual_sum))
+
+
 # ---- async_exec.hpp ----------------------------------------------------------
 class ExecMode(enum.IntEnum):
     Barriered = _lib.EXEC_BARRIERED

@@ -273,3 +273,26 @@ def test_plan_async_replay_bit_exact(H, port):
                       H.DelayModel.uniform(2, 1), 300)
     exp = port.async_run(u0, 0.4, 0, 0.0, 0.0, 1 << 13, 0, 2, seed=1, k_end=300)
     assert bits_equal(plan.download(), exp)
+
+
+@pytest.mark.parametrize("r,q,periodic,per_pe", [
+    (0.25, 3, False, 128), (0.49, 9, False, 128), (0.1, 5, True, 64), (0.4, 2, False, 1)])
+def test_free_run_within_aposteriori_bound(H, port, r, q, periodic, per_pe):
+    # ||u_async(K) - u_sync(K)||_inf <= sum_k ||u(k+1) - A u(k)||_inf
+    n = 1024 if per_pe > 1 else 16
+    u0 = port.prepare_initial(port.sine_init(n), 0, 0.0, 0.0)
+    bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(0, 0)
+    p = H.SolverParams.from_r(r)
+    fin, st = H.async_free_run(u0, p, bc, H.PartitionSpec(n, per_pe), q, 1000)
+    sync = port.sync_run(u0, r, bc.kind, 0.0, 0.0, 1000)
+    err = np.max(np.abs(fin - sync))
+    assert err <= st.residual_sum
+    assert st.max_delay <= q - 1 and sum(st.delay_histogram) == st.reads > 0
+
+
+def test_free_run_q1_exact(H, port):
+    u0 = port.prepare_initial(port.sine_init(1024), 0, 0.0, 0.0)
+    fin, st = H.async_free_run(u0, H.SolverParams.from_r(0.3), H.BoundaryCondition.dirichlet(0, 0),
+                               H.PartitionSpec(1024, 128), 1, 700)
+    assert bits_equal(fin, port.sync_run(u0, 0.3, 0, 0.0, 0.0, 700))
+    assert st.max_delay == 0 and st.residual_sum < 1e-9
