@@ -116,7 +116,8 @@ struct AsyncRunSpec {
 };
 
 int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride,
-                 const std::function<int(size_t)>& on_record, unsigned long long* host_stats,
+                 const std::function<int(size_t, const double*)>& on_record,
+                 unsigned long long* host_stats,
                  std::vector<double>* edge_log, std::vector<int>* used_log, float* device_ms) {
     const size_t P = s.N / s.n;
     if (s.n > 32 * 32)
@@ -221,15 +222,32 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
         HB_CUDA(cudaEventCreate(&ev1));
         HB_CUDA(cudaEventRecord(ev0, st));
     }
+    // Recording: small trajectories are written by the kernel itself (one
+    // launch for the whole run); large ones split the run at recorded steps.
+    const size_t nsnap = stride ? 2 + s.k_end / stride : 0;
+    const bool in_kernel = stride && on_record && nsnap * s.N * sizeof(double) <= (512ull << 20);
+    if (in_kernel) {
+        if (d.snaps_bytes < nsnap * s.N * sizeof(double)) {
+            if (d.snaps) cudaFree(d.snaps);
+            d.snaps = nullptr;
+            d.snaps_bytes = 0;
+            HB_CUDA(cudaMalloc(&d.snaps, nsnap * s.N * sizeof(double)));
+            d.snaps_bytes = nsnap * s.N * sizeof(double);
+        }
+        a.snaps = static_cast<double*>(d.snaps);
+        a.snap_stride = (long long)stride;
+        a.k_final = (long long)s.k_end;
+    }
     size_t k = 0;
     while (k < s.k_end) {
-        const size_t next = stride ? std::min(s.k_end, (k / stride + 1) * stride) : s.k_end;
+        const size_t next = (stride && !in_kernel) ? std::min(s.k_end, (k / stride + 1) * stride)
+                                                   : s.k_end;
         a.k0 = (long long)k;
         a.k1 = (long long)next;
         HB_TRY(shared ? launch_s<true>(V, a, int(P), st, smem)
                       : launch_s<false>(V, a, int(P), st, 0));
         k = next;
-        if (stride && on_record) {
+        if (in_kernel) {
             unsigned int flags[2] = {0, 0};
             HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
             HB_CUDA(cudaStreamSynchronize(st));
@@ -239,7 +257,21 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
                     return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
                 return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
             }
-            HB_TRY(on_record(k));
+            for (size_t kk = stride; kk <= s.k_end; kk += stride)
+                HB_TRY(on_record(kk, a.snaps + (kk / stride) * s.N));
+            if (s.k_end % stride)
+                HB_TRY(on_record(s.k_end, a.snaps + (s.k_end / stride + 1) * s.N));
+        } else if (stride && on_record) {
+            unsigned int flags[2] = {0, 0};
+            HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaStreamSynchronize(st));
+            if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
+            if (flags[0]) {
+                if (g_strict.load())
+                    return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+                return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+            }
+            HB_TRY(on_record(k, dfield));
         }
     }
     if (device_ms) {
@@ -537,6 +569,22 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
     if (per_pe == N)
         return heat_sync_run(u0, N, r, bc_kind, c1, c2, k_end, stride, final_out, snapshots,
                              steps_out, max_snapshots, n_snapshots);
+    return async_run_core(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay, geometric_p,
+                          seed, k_end, stride, final_out, snapshots, steps_out, max_snapshots,
+                          n_snapshots);
+}
+
+}  // extern "C"
+
+namespace hb {
+
+// Body of async_run after validation; also the small-N exact sync path
+// (q = 1 replays d = 0 for every read: bit-identical to sync_run).
+int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                   size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                   uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                   double* snapshots, size_t* steps_out, size_t max_snapshots,
+                   size_t* n_snapshots) {
     if (stride == 0) stride = default_stride(N);
 
     DevCtx* d = nullptr;
@@ -571,7 +619,7 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
                                 nullptr));
     } else {
         HB_TRY(async_pe_run(*d, s, bufs[0], want_snaps ? stride : 0,
-                            [&](size_t k) { return record_from(k, bufs[0]); }, nullptr, nullptr,
+                            record_from, nullptr, nullptr,
                             nullptr, nullptr));
     }
     if (final_out) {
@@ -582,6 +630,10 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
     if (n_snapshots) *n_snapshots = ns;
     return HEAT_OK;
 }
+
+}  // namespace hb
+
+extern "C" {
 
 int heat_async_free_run(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
                         size_t per_pe, size_t q, size_t k_end, double* final_out,

@@ -62,6 +62,11 @@ struct AsyncPeArgs {
     unsigned int* flag;           // [0] non-finite, [1] watchdog timeout
     unsigned int* abort_word;     // set on timeout: every spin bails out
     unsigned long long timeout_ns;
+    // optional in-kernel trajectory: snapshot j (j >= 1) of the run lands at
+    // snaps[j*N ...]; recorded steps are multiples of snap_stride plus k_final
+    double* snaps;
+    long long snap_stride;
+    long long k_final;
 };
 
 // stats layout (u64 words)
@@ -297,6 +302,21 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 a.edge_log[((k + 1) * a.P + p) * 2 + 1] = last;
             }
             RingOps<kShared>::store_prog(prog + p, (uint64_t)(k + 1));
+        }
+        if (a.snaps && active) {
+            const long long kk = k + 1;
+            long long j = -1;
+            if (kk % a.snap_stride == 0)
+                j = kk / a.snap_stride;
+            else if (kk == a.k_final)
+                j = a.k_final / a.snap_stride + 1;
+            if (j >= 0) {
+#pragma unroll
+                for (int i = 0; i < V; ++i) {
+                    const int li = lane * V + i;
+                    if (li < n) a.snaps[j * a.N + lo + li] = u[i];
+                }
+            }
         }
         abort = __any_sync(0xffffffffu, abort);
     }

@@ -72,6 +72,8 @@ struct DevCtx {
     unsigned int* flag = nullptr;  // [0] non-finite, [1] watchdog timeout
     void* scratch = nullptr;       // async rings / logs
     size_t scratch_bytes = 0;
+    void* snaps = nullptr;         // in-kernel trajectories of small runs
+    size_t snaps_bytes = 0;
 };
 
 // Locks and initialises the context of the current (or given) device.
@@ -106,6 +108,13 @@ int make_chunk_map_f64(struct CUtensorMap_st* m, const void* base, long long nch
 // Upload + validate + snap a host field into `dst` (sync_host.cu).
 int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
                     double* dst);
+
+// async_run after validation (async_host.cu).
+int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                   size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                   uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                   double* snapshots, size_t* steps_out, size_t max_snapshots,
+                   size_t* n_snapshots);
 
 // In-step draw ranks of the cross-PE reads (async_host.cu), returns D.
 int draw_offsets(size_t N, size_t n, int dirichlet, std::vector<int>& offL, std::vector<int>& offR);
