@@ -1,0 +1,152 @@
+// heat_core_b200.cpp -- the reference-side binding: namespace heat's hot-path
+// entry points implemented on the B200 library through its C-ABI
+// (include/heat_b200.h).  Compiled against the reference's own headers
+// (proj/include/heat/*.hpp, unmodified), it replaces these definitions of
+// the reference library when linked in front of it:
+//
+//   heat::sync_step     sync_solver.hpp:60-62   -> heat_sync_step
+//   heat::sync_run      sync_solver.hpp:64-67   -> heat_sync_run
+//   heat::sync_run_f32  sync_solver.hpp:69-73   -> heat_sync_run_f32
+//   heat::async_run     async_sim.hpp:97-101    -> heat_async_run
+//   heat::exec_run      async_exec.hpp:68-70    -> heat_exec_run
+//
+// Everything else (AsyncSimulator, ensembles, CSV, the CLI) keeps running on
+// the reference's CPU code.  oracle/Makefile target `acceptance-b200` links
+// the reference's acceptance suite (proj/tests/acceptance.cpp) this way.
+#include <chrono>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "heat/async_exec.hpp"
+#include "heat/async_sim.hpp"
+#include "heat/core.hpp"
+#include "heat/sync_solver.hpp"
+#include "heat_b200.h"
+
+namespace heat {
+
+namespace {
+
+void throw_on(int st) {
+    if (st == HEAT_OK) return;
+    const char* m = heat_last_error();
+    switch (st) {
+        case HEAT_EDOMAIN: throw std::domain_error(m);
+        case HEAT_EINVAL: throw std::invalid_argument(m);
+        case HEAT_ELOGIC: throw std::logic_error(m);
+        case HEAT_EDIVERGE: throw DivergenceError(m);
+        default: throw std::runtime_error(m);
+    }
+}
+
+int bc_kind(const BoundaryCondition& bc) {
+    return bc.is_dirichlet() ? HEAT_BC_DIRICHLET : HEAT_BC_PERIODIC;
+}
+
+// The strict-check switch lives in the reference (sync_solver.cpp:9-20);
+// mirror it into the library before every call.
+void sync_strict() { heat_set_strict_finite_checks(strict_finite_checks() ? 1 : 0); }
+
+using RunFn = int (*)(const double*, size_t, double, int, double, double, size_t, size_t, double*,
+                      double*, size_t*, size_t, size_t*);
+
+Trajectory run_traj(RunFn fn, const TemperatureField& u0, const SolverParams& params,
+                    const BoundaryCondition& bc, std::size_t k_end, std::size_t stride) {
+    sync_strict();
+    const std::size_t n = u0.size();
+    const std::size_t cap = heat_trajectory_length(n, k_end, stride);
+    std::vector<double> snaps(cap * n);
+    std::vector<std::size_t> steps(cap);
+    std::size_t count = 0;
+    throw_on(fn(u0.values().data(), n, params.r(), bc_kind(bc), bc.c1, bc.c2, k_end, stride,
+                nullptr, snaps.data(), steps.data(), cap, &count));
+    Trajectory t{{}, {}, params, bc};
+    t.snapshots.reserve(count);
+    for (std::size_t j = 0; j < count; ++j) {
+        t.snapshots.emplace_back(
+            std::vector<double>(snaps.begin() + j * n, snaps.begin() + (j + 1) * n));
+        t.steps.push_back(steps[j]);
+    }
+    return t;
+}
+
+}  // namespace
+
+TemperatureField sync_step(const TemperatureField& u, const SolverParams& params,
+                           const BoundaryCondition& bc) {
+    sync_strict();
+    std::vector<double> out(u.size());
+    throw_on(heat_sync_step(u.values().data(), u.size(), params.r(), bc_kind(bc), bc.c1, bc.c2,
+                            out.data()));
+    return TemperatureField(std::move(out));
+}
+
+Trajectory sync_run(const TemperatureField& u0, const SolverParams& params,
+                    const BoundaryCondition& bc, std::size_t k_end, std::size_t stride) {
+    return run_traj(heat_sync_run, u0, params, bc, k_end, stride);
+}
+
+Trajectory sync_run_f32(const TemperatureField& u0, const SolverParams& params,
+                        const BoundaryCondition& bc, std::size_t k_end, std::size_t stride) {
+    return run_traj(heat_sync_run_f32, u0, params, bc, k_end, stride);
+}
+
+Trajectory async_run(const TemperatureField& u0, const SolverParams& params,
+                     const BoundaryCondition& bc, const PartitionSpec& part,
+                     const DelayModel& model, std::size_t k_end, std::size_t stride) {
+    sync_strict();
+    if (part.total() != u0.size())  // AsyncSimulator ctor, async_sim.cpp:131-132
+        throw std::invalid_argument("AsyncSimulator: partition inconsistent with grid");
+    const std::size_t n = u0.size();
+    const std::size_t cap = heat_trajectory_length(n, k_end, stride);
+    std::vector<double> snaps(cap * n);
+    std::vector<std::size_t> steps(cap);
+    std::size_t count = 0;
+    const int law = model.distribution == DelayModel::Distribution::Uniform ? HEAT_DELAY_UNIFORM
+                    : model.distribution == DelayModel::Distribution::Fixed ? HEAT_DELAY_FIXED
+                                                                            : HEAT_DELAY_GEOMETRIC;
+    throw_on(heat_async_run(u0.values().data(), n, params.r(), bc_kind(bc), bc.c1, bc.c2,
+                            part.per_pe(), model.q, law, model.fixed_delay, model.geometric_p,
+                            model.seed, k_end, stride, nullptr, snaps.data(), steps.data(), cap,
+                            &count));
+    Trajectory t{{}, {}, params, bc};
+    for (std::size_t j = 0; j < count; ++j) {
+        t.snapshots.emplace_back(
+            std::vector<double>(snaps.begin() + j * n, snaps.begin() + (j + 1) * n));
+        t.steps.push_back(steps[j]);
+    }
+    return t;
+}
+
+ExecResult exec_run(const TemperatureField& u0, const SolverParams& params,
+                    const BoundaryCondition& bc, const PartitionSpec& part,
+                    const ExecConfig& cfg) {
+    sync_strict();
+    std::vector<double> out(u0.size());
+    std::uint64_t ns = 0;
+    heat_lag_stats lag{};
+    throw_on(heat_exec_run(u0.values().data(), u0.size(), params.r(), bc_kind(bc), bc.c1, bc.c2,
+                           part.per_pe(), cfg.workers, cfg.k_end,
+                           cfg.mode == ExecMode::Barriered ? HEAT_EXEC_BARRIERED
+                                                           : HEAT_EXEC_BARRIER_FREE,
+                           cfg.record_lag ? 1 : 0, 0, out.data(), &ns, &lag, nullptr));
+    ExecResult res{TemperatureField(std::move(out)), std::vector<std::size_t>(cfg.workers, cfg.k_end),
+                   std::chrono::nanoseconds(ns), false, std::nullopt};
+    // run_barriered never reports lag; run_barrier_free reports the merged
+    // (possibly empty, P = 1) statistics when asked (async_exec.cpp:250-256).
+    if (cfg.record_lag && cfg.mode == ExecMode::BarrierFree) {
+        LagStats l;
+        if (lag.reads) {
+            l.reads = lag.reads;
+            l.min_lag = lag.min_lag;
+            l.max_lag = lag.max_lag;
+            l.overflow = lag.overflow;
+            l.histogram.assign(lag.histogram, lag.histogram + 64);
+        }
+        res.lag = l;
+    }
+    return res;
+}
+
+}  // namespace heat

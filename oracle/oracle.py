@@ -56,6 +56,9 @@ def build(ref: bool | None = None) -> None:
             ref = os.path.isdir(REF_SRC)
         if ref:
             subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+            lib = os.path.join(os.path.dirname(HERE), "paper_1510_08982_b200", "libheat_b200.so")
+            if os.path.exists(lib):  # reference acceptance suite vs. the GPU library
+                subprocess.run(["make", "-s", "-C", HERE, "acceptance"], check=True)
 
 
 def _ptr(a: np.ndarray | None, ty=_pd):

@@ -75,7 +75,9 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
             if (verbose or ptxas_info) and (p.stdout or p.stderr):
                 sys.stderr.write(p.stdout + p.stderr)
     if force or jobs or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+        # static CUDA runtime: the .so depends on the driver only, so it loads the
+        # same way from Python (next to torch's own runtime) and from C++ hosts
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -1,0 +1,31 @@
+"""The reference's OWN acceptance suite (proj/tests/acceptance.cpp, unmodified)
+linked with its hot path (sync_step, sync_run, sync_run_f32, async_run,
+exec_run) replaced by the B200 library through integration/heat_core_b200.cpp
+-- the drop-in proof.  Built by `make -C oracle acceptance` (needs
+/root/reference at build time; the binary ships to the GPU box prebuilt).
+
+Expected: criteria 1-8 pass exactly as they do for the reference itself;
+criterion 9 needs the reference CLI (CLI11 is not vendored) and fails for both."""
+import os
+import re
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+def test_reference_acceptance_suite_on_b200(gpu):
+    if not os.path.exists(BIN):
+        pytest.skip("oracle/_ref/acceptance_b200 not built (needs /root/reference at build time)")
+    p = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
+    out = p.stdout
+    print(out)
+    status = dict(re.findall(r"\[(PASS|FAIL)\] (\d+):", out)[i][::-1]
+                  for i in range(len(re.findall(r"\[(PASS|FAIL)\] (\d+):", out))))
+    for c in "12345678":
+        assert status.get(c) == "PASS", f"criterion {c}: {status.get(c)}\n{out}"
+    assert status.get("9") == "FAIL"  # CLI determinism: no CLI binary (same as the reference)
