@@ -54,13 +54,13 @@ int pick_ring(int q) {
     return R;
 }
 
-template <int V, bool S>
+template <int V, bool S, bool B>
 int launch_v(const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
     if (S) {
         if (smem > 48 * 1024)
-            HB_CUDA(cudaFuncSetAttribute(async_pe_kernel<V, S>,
+            HB_CUDA(cudaFuncSetAttribute(async_pe_kernel<V, S, B>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        async_pe_kernel<V, S><<<1, 32 * P, smem, st>>>(a);
+        async_pe_kernel<V, S, B><<<1, 32 * P, smem, st>>>(a);
         HB_CUDA(cudaGetLastError());
     } else {
         // every PE warp must be co-resident: cooperative launch or refuse
@@ -69,30 +69,39 @@ int launch_v(const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
         int dev = 0, per_sm = 0, sms = 0;
         HB_CUDA(cudaGetDevice(&dev));
         HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_pe_kernel<V, S>,
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_pe_kernel<V, S, B>,
                                                               threads, 0));
         if ((long long)per_sm * sms < blocks)
             return fail(HEAT_EINVAL, "async: " + std::to_string(P) +
                                          " PE warps cannot be co-resident on this device");
         AsyncPeArgs copy = a;
         void* params[] = {&copy};
-        HB_CUDA(cudaLaunchCooperativeKernel((const void*)async_pe_kernel<V, S>, dim3(blocks),
+        HB_CUDA(cudaLaunchCooperativeKernel((const void*)async_pe_kernel<V, S, B>, dim3(blocks),
                                             dim3(threads), params, 0, st));
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return HEAT_OK;
 }
 
-template <bool S>
-int launch_s(int V, const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
+template <bool S, bool B>
+int launch_sb(int V, const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
     switch (V) {
-        case 1: return launch_v<1, S>(a, P, st, smem);
-        case 2: return launch_v<2, S>(a, P, st, smem);
-        case 4: return launch_v<4, S>(a, P, st, smem);
-        case 8: return launch_v<8, S>(a, P, st, smem);
-        case 16: return launch_v<16, S>(a, P, st, smem);
-        default: return launch_v<32, S>(a, P, st, smem);
+        case 1: return launch_v<1, S, B>(a, P, st, smem);
+        case 2: return launch_v<2, S, B>(a, P, st, smem);
+        case 4: return launch_v<4, S, B>(a, P, st, smem);
+        case 8: return launch_v<8, S, B>(a, P, st, smem);
+        case 16: return launch_v<16, S, B>(a, P, st, smem);
+        default: return launch_v<32, S, B>(a, P, st, smem);
     }
+}
+
+// One CTA with shared rings (barrier mode for deterministic runs, flags for
+// free-running ones) or a cooperative multi-CTA launch with global rings.
+int launch_pe(int V, bool shared, bool barrier, const AsyncPeArgs& a, int P, cudaStream_t st,
+              size_t smem) {
+    if (!shared) return launch_sb<false, false>(V, a, P, st, 0);
+    return barrier ? launch_sb<true, true>(V, a, P, st, smem)
+                   : launch_sb<true, false>(V, a, P, st, smem);
 }
 
 }  // namespace
@@ -244,8 +253,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
                                                    : s.k_end;
         a.k0 = (long long)k;
         a.k1 = (long long)next;
-        HB_TRY(shared ? launch_s<true>(V, a, int(P), st, smem)
-                      : launch_s<false>(V, a, int(P), st, 0));
+        HB_TRY(launch_pe(V, shared, s.mode == 0, a, int(P), st, smem));
         k = next;
         if (in_kernel) {
             unsigned int flags[2] = {0, 0};

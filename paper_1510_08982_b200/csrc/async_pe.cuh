@@ -102,11 +102,26 @@ struct RingOps<true> {
 };
 
 // Delay of the draw with in-step rank `off` at step k (async_sim.cpp:57-73).
+// x mod m for a 64-bit x and m <= 65536 with 32-bit divisions only (exact:
+// x = hi*2^32 + lo, and every intermediate stays below 2^32).  The generic
+// 64-bit remainder is a long software routine on the latency-critical path.
+__device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t m) {
+    if (m == 1) return 0;
+    const uint32_t hi = uint32_t(x >> 32), lo = uint32_t(x);
+    const uint32_t two32 = (0xFFFFFFFFu % m + 1u) % m;      // 2^32 mod m
+    const uint32_t a = (hi % m) * two32;                    // < m^2 <= 2^32
+    return ((a % m) + (lo % m)) % m;
+}
+
 __device__ __forceinline__ int det_delay(const AsyncPeArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
+    if (bound == 0) return 0;  // every law yields 0 (the draw is still "consumed" by index)
     if (a.law == 2) return a.dtable[k * a.D + off];  // host-drawn, already bounded
     const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
-    if (a.law == 0) return int(x % uint64_t(bound + 1));
+    if (a.law == 0) {
+        if (bound < 65536) return int(mod64_small(x, uint32_t(bound + 1)));
+        return int(x % uint64_t(bound + 1));
+    }
     return a.fixed_d < bound ? a.fixed_d : int(bound);
 }
 
@@ -150,8 +165,14 @@ __global__ void async_init_kernel(const double* __restrict__ field, int n, int P
     }
 }
 
-template <int V, bool kShared>
+// kBarrier (single CTA, deterministic mode only): the PEs advance in
+// lockstep with one block barrier per step -- the GPU analogue of
+// run_barriered (async_exec.cpp:57-114).  Every value a deterministic read
+// can ask for (step k-d <= k) was published before the previous barrier, so
+// no progress flags are needed; results are identical to the flag protocol.
+template <int V, bool kShared, bool kBarrier>
 __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const AsyncPeArgs a) {
+    static_assert(kShared || !kBarrier, "barrier mode needs every PE in one CTA");
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int p = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
@@ -201,6 +222,12 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     }
 
     unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
+    // next recorded step and its snapshot index (no per-step 64-bit division)
+    long long next_snap = 0, next_snap_idx = 0;
+    if (a.snaps) {
+        next_snap_idx = a.k0 / a.snap_stride + 1;
+        next_snap = next_snap_idx * a.snap_stride;
+    }
     bool abort = false;
     for (long long k = a.k0; k < a.k1 && !abort; ++k) {
         // ---- 1. ghosts: lane 0 fetches the left one, lane 31 the right one
@@ -213,7 +240,10 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
             bool waited = false;
             long long m;
             uint64_t v;
-            if (a.mode == 0) {
+            if (kBarrier) {
+                m = k - det_delay(a, k, left ? offL : offR);
+                v = uint64_t(k);  // lockstep: the neighbour has published step k
+            } else if (a.mode == 0) {
                 const int d = det_delay(a, k, left ? offL : offR);
                 m = k - d;
                 v = wait_prog<kShared>(a, prog + nb, m, &waited);
@@ -291,7 +321,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
             // flow control: consumers must be past the step this slot held
             const long long need = k + 1 + a.q - R;
             bool w = false;
-            if (need > 0) {
+            if (!kBarrier && need > 0) {
                 if (lpe >= 0 && wait_prog<kShared>(a, prog + lpe, need, &w) == ~0ull) abort = true;
                 if (rpe >= 0 && wait_prog<kShared>(a, prog + rpe, need, &w) == ~0ull) abort = true;
             }
@@ -306,10 +336,12 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
         if (a.snaps && active) {
             const long long kk = k + 1;
             long long j = -1;
-            if (kk % a.snap_stride == 0)
-                j = kk / a.snap_stride;
-            else if (kk == a.k_final)
+            if (kk == next_snap) {
+                j = next_snap_idx++;
+                next_snap += a.snap_stride;
+            } else if (kk == a.k_final) {
                 j = a.k_final / a.snap_stride + 1;
+            }
             if (j >= 0) {
 #pragma unroll
                 for (int i = 0; i < V; ++i) {
@@ -318,6 +350,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 }
             }
         }
+        if constexpr (kBarrier) __syncthreads();  // step k+1 published by every PE
         abort = __any_sync(0xffffffffu, abort);
     }
 
