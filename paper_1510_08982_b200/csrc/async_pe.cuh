@@ -228,49 +228,65 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
         next_snap_idx = a.k0 / a.snap_stride + 1;
         next_snap = next_snap_idx * a.snap_stride;
     }
+    // Lane 0 fetches the left ghost (left PE's LAST point), lane 31 the right
+    // ghost (right PE's FIRST point); lane 0 publishes.  Everything a step
+    // touches is precomputed here so the loop body stays short: the paper's
+    // regime is latency-bound (one neighbour handshake per step).
+    const bool fetch = (lane == 0 && needL) || (lane == 31 && needR);
+    const int nb = lane == 0 ? lpe : rpe;
+    const double* gring = ring + ((size_t)(nb < 0 ? 0 : nb) * 2 + (lane == 0 ? 1 : 0)) * R;
+    const uint64_t* gprog = prog + (nb < 0 ? 0 : nb);
+    const int my_off = lane == 0 ? offL : offR;
+    double* my0 = ring + (size_t)(active ? p : 0) * 2 * R;
+    double* my1 = my0 + R;
+    const bool stats = a.stats != nullptr;
+    const int rmask = R - 1;
     bool abort = false;
-    for (long long k = a.k0; k < a.k1 && !abort; ++k) {
-        // ---- 1. ghosts: lane 0 fetches the left one, lane 31 the right one
+    const int k1 = int(a.k1);
+    for (int k = int(a.k0); k < k1; ++k) {
+        // ---- 1. ghosts
         double ghost = 0.0;
-        int used = -1;
-        if ((lane == 0 && needL) || (lane == 31 && needR)) {
-            const bool left = lane == 0;
-            const int nb = left ? lpe : rpe;
-            const int side = left ? 1 : 0;  // left ghost = neighbour's last point
+        if (fetch) {
             bool waited = false;
-            long long m;
+            int m;
             uint64_t v;
             if (kBarrier) {
-                m = k - det_delay(a, k, left ? offL : offR);
+                m = k - det_delay(a, k, my_off);
                 v = uint64_t(k);  // lockstep: the neighbour has published step k
             } else if (a.mode == 0) {
-                const int d = det_delay(a, k, left ? offL : offR);
-                m = k - d;
-                v = wait_prog<kShared>(a, prog + nb, m, &waited);
+                m = k - det_delay(a, k, my_off);
+                v = wait_prog<kShared>(a, gprog, m, &waited);
             } else {
-                v = wait_prog<kShared>(a, prog + nb, k - (a.q - 1), &waited);
-                m = (long long)v < k ? (long long)v : k;
+                v = wait_prog<kShared>(a, gprog, k - (a.q - 1), &waited);
+                m = (long long)v < k ? int(v) : k;
             }
-            if (v == ~0ull) abort = true;
-            if (!abort) {
-                ghost = RingOps<kShared>::load_val(ring + ((size_t)nb * 2 + side) * R + (m & (R - 1)));
-                used = int(k - m);
-                // writer lag as LagStats measures it: producer progress - step consumed
-                const unsigned long long lag = v - (unsigned long long)m;
-                reads++;
-                waits += waited;
-                if ((unsigned long long)used > maxd) maxd = used;
-                lag_min = lag < lag_min ? lag : lag_min;
-                lag_max = lag > lag_max ? lag : lag_max;
-                // per-warp shared histograms: a global atomic here would sit in
-                // front of every st.release of the publish step below
-                atomicAdd(&whist[used < 64 ? used : 63], 1u);
-                atomicAdd(&whist[64 + (lag < 64 ? lag : 64)], 1u);
-                if (a.used_log) a.used_log[(k * a.P + p) * 2 + (left ? 0 : 1)] = int(m);
+            if (v == ~0ull) {
+                abort = true;
+            } else {
+                ghost = RingOps<kShared>::load_val(gring + (m & rmask));
+                if (stats) {
+                    const unsigned used = unsigned(k - m);
+                    // writer lag as LagStats measures it: producer progress - step consumed
+                    const unsigned long long lag = v - (unsigned long long)m;
+                    reads++;
+                    waits += waited;
+                    maxd = used > maxd ? used : maxd;
+                    lag_min = lag < lag_min ? lag : lag_min;
+                    lag_max = lag > lag_max ? lag : lag_max;
+                    // per-warp shared histograms (a global atomic here would sit
+                    // in front of every release of the publish step below)
+                    atomicAdd(&whist[used < 64 ? used : 63], 1u);
+                    atomicAdd(&whist[64 + (lag < 64 ? lag : 64)], 1u);
+                }
+                if (a.used_log) a.used_log[((size_t)k * a.P + p) * 2 + (lane == 0 ? 0 : 1)] = m;
             }
         }
-        abort = __any_sync(0xffffffffu, abort);
-        if (abort) break;
+        if constexpr (!kBarrier) {
+            if (__any_sync(0xffffffffu, abort)) {
+                abort = true;
+                break;
+            }
+        }
         const double gL = __shfl_sync(0xffffffffu, ghost, 0);
         const double gR = __shfl_sync(0xffffffffu, ghost, 31);
 
@@ -310,28 +326,24 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 if (i == lastElem) u[i] = a.c2;
         }
 
-        // ---- 3. publish u_first(k+1), u_last(k+1) then release prog = k+1
+        // ---- 3. publish u_first(k+1), u_last(k+1), then release prog = k+1.
+        // No flow control: the two sides of a boundary read each other, so
+        // neither gets more than q-1 steps ahead, and R >= 4q slots cannot be
+        // overwritten while still readable.
         double last = 0.0;
 #pragma unroll
         for (int i = 0; i < V; ++i)
             if (i == lastElem) last = u[i];
         last = __shfl_sync(0xffffffffu, last, lastLane);
         if (lane == 0 && active) {
-            const long long slot = (k + 1) & (R - 1);
-            // flow control: consumers must be past the step this slot held
-            const long long need = k + 1 + a.q - R;
-            bool w = false;
-            if (!kBarrier && need > 0) {
-                if (lpe >= 0 && wait_prog<kShared>(a, prog + lpe, need, &w) == ~0ull) abort = true;
-                if (rpe >= 0 && wait_prog<kShared>(a, prog + rpe, need, &w) == ~0ull) abort = true;
-            }
-            RingOps<kShared>::store_val(ring + ((size_t)p * 2 + 0) * R + slot, u[0]);
-            RingOps<kShared>::store_val(ring + ((size_t)p * 2 + 1) * R + slot, last);
+            const int slot = (k + 1) & rmask;
+            RingOps<kShared>::store_val(my0 + slot, u[0]);
+            RingOps<kShared>::store_val(my1 + slot, last);
             if (a.edge_log) {
-                a.edge_log[((k + 1) * a.P + p) * 2 + 0] = u[0];
-                a.edge_log[((k + 1) * a.P + p) * 2 + 1] = last;
+                a.edge_log[((size_t)(k + 1) * a.P + p) * 2 + 0] = u[0];
+                a.edge_log[((size_t)(k + 1) * a.P + p) * 2 + 1] = last;
             }
-            RingOps<kShared>::store_prog(prog + p, (uint64_t)(k + 1));
+            if (!kBarrier) RingOps<kShared>::store_prog(prog + p, (uint64_t)(k + 1));
         }
         if (a.snaps && active) {
             const long long kk = k + 1;
@@ -351,8 +363,8 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
             }
         }
         if constexpr (kBarrier) __syncthreads();  // step k+1 published by every PE
-        abort = __any_sync(0xffffffffu, abort);
     }
+    if (kBarrier && lane == 0 && active) prog[p] = uint64_t(a.k1);
 
     // ---- results, finite check, statistics, ring state back to global
     bool bad = false;
