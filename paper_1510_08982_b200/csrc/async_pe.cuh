@@ -290,18 +290,17 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
         const double gL = __shfl_sync(0xffffffffu, ghost, 0);
         const double gR = __shfl_sync(0xffffffffu, ghost, 31);
 
-        // ---- 2. one step of the PE's points
-        if (lane == lastLane && lastElem + 1 < V) {
-#pragma unroll
-            for (int i = 0; i < V; ++i)
-                if (i == lastElem + 1) u[i] = gR;  // ghost slot right of the last point
-        }
+        // ---- 2. one step of the PE's points.  The PE's last point (lane
+        // lastLane, element lastElem) takes r*gR as its right product; a
+        // per-element select keeps u[] in registers (a dynamic index would
+        // push it to local memory on the critical path).
+        const double pG = A::mul(r, gR);
+        const bool last_lane = lane == lastLane;
         const double pFirst = A::mul(r, u[0]);
         const double pLast = A::mul(r, u[V - 1]);
         double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
         double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
         if (lane == 0) pL = A::mul(r, gL);
-        if (lane == lastLane && lastElem == V - 1) pR = A::mul(r, gR);
         {
             double pm1 = pL, p0 = pFirst;
 #pragma unroll
@@ -313,18 +312,15 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                     p1 = pLast;
                 else
                     p1 = A::mul(r, u[i + 1]);
+                if (last_lane && i == lastElem) p1 = pG;
                 const double cs = A::mul(c, u[i]);
                 u[i] = stencil_p(p1, cs, pm1);
+                if (pin_last && last_lane && i == lastElem) u[i] = a.c2;
                 pm1 = p0;
                 p0 = p1;
             }
         }
         if (pin_first && lane == 0) u[0] = a.c1;
-        if (pin_last && lane == lastLane) {
-#pragma unroll
-            for (int i = 0; i < V; ++i)
-                if (i == lastElem) u[i] = a.c2;
-        }
 
         // ---- 3. publish u_first(k+1), u_last(k+1), then release prog = k+1.
         // No flow control: the two sides of a boundary read each other, so
