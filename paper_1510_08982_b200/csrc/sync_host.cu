@@ -70,11 +70,13 @@ int sync_variant(SyncVariant** out) {
         {sync_tb_kernel<Real, kV, 2, 2>, 2, 0},
         {sync_tb_kernel<Real, kV, 1, 1>, 1, 0},
         {sync_tb_kernel<Real, kV, 1, 2>, 1, 0},
+        {sync_tb_kernel<Real, kV, 2, 0>, 2, 0},  // 4: pipelined steps, 2 buffers
+        {sync_tb_kernel<Real, kV, 1, 0>, 1, 0},  // 5: pipelined steps, 1 buffer
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
         const int v = e ? std::atoi(e) : kDefaultSyncVariant;
-        return (v >= 0 && v < 4) ? v : kDefaultSyncVariant;
+        return (v >= 0 && v < 6) ? v : kDefaultSyncVariant;
     }();
     SyncVariant& v = table[idx];
     if (v.blocks_per_sm == 0) {

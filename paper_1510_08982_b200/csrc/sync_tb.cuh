@@ -129,6 +129,50 @@ __device__ __forceinline__ void warp_step(Real (&u)[V], Real r, Real c) {
     chunk_step<Real, V>(u, r, c, pL, pR, pFirst, pLast);
 }
 
+// `nsteps` warp steps, software-pipelined across the step boundary: each step
+// first computes the lane's two boundary points, multiplies them by r and
+// issues the shuffles the NEXT step needs, and only then computes the V-2
+// interior points -- the shuffle latency hides behind them instead of
+// stalling the start of every step.  Same products, same rounding sequence
+// as warp_step (4 DP instructions per point).  No pinned ends allowed.
+template <typename Real, int V>
+__device__ __forceinline__ void warp_steps_pipelined(Real (&u)[V], Real r, Real c, int nsteps) {
+    static_assert(V >= 4, "pipelined step needs >= 4 points per lane");
+    using A = Arith<Real>;
+    Real pF = A::mul(r, u[0]);
+    Real pLs = A::mul(r, u[V - 1]);
+    Real pL = __shfl_up_sync(0xffffffffu, pLs, 1);
+    Real pR = __shfl_down_sync(0xffffffffu, pF, 1);
+    for (int s = 0; s < nsteps; ++s) {
+        const Real p1 = A::mul(r, u[1]);        // r*u[1]   (old)
+        const Real pVm2 = A::mul(r, u[V - 2]);  // r*u[V-2] (old)
+        const Real nF = stencil_p(p1, A::mul(c, u[0]), pL);
+        const Real nL = stencil_p(pR, A::mul(c, u[V - 1]), pVm2);
+        const Real pF2 = A::mul(r, nF);
+        const Real pLs2 = A::mul(r, nL);
+        pL = __shfl_up_sync(0xffffffffu, pLs2, 1);  // for step s+1
+        pR = __shfl_down_sync(0xffffffffu, pF2, 1);
+        Real pm1 = pF, p0 = p1;
+#pragma unroll
+        for (int i = 1; i <= V - 2; ++i) {
+            Real pn;
+            if (i + 1 == V - 1)
+                pn = pLs;
+            else if (i + 1 == V - 2)
+                pn = pVm2;
+            else
+                pn = A::mul(r, u[i + 1]);
+            u[i] = stencil_p(pn, A::mul(c, u[i]), pm1);
+            pm1 = p0;
+            p0 = pn;
+        }
+        u[0] = nF;
+        u[V - 1] = nL;
+        pF = pF2;
+        pLs = pLs2;
+    }
+}
+
 template <typename Real, int V>
 __device__ __forceinline__ void pin_ends(Real (&u)[V], long long g0, long long pin_lo,
                                          long long pin_hi, Real c1, Real c2) {
@@ -188,7 +232,8 @@ struct SyncPassArgs {
 // NBUF = 1: the next tile's window lands in the (only) buffer as soon as this
 //           tile is in registers; outputs leave with 16-B vector stores
 //           straight from registers (half the shared memory -> more warps).
-// UNR:      unroll factor of the step loop.
+// UNR:      unroll factor of the step loop; 0 = software-pipelined steps
+//           (warp_steps_pipelined) for tiles without pinned ends.
 template <typename Real, int V, int NBUF, int UNR>
 __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
@@ -275,8 +320,12 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
         if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
+            if constexpr (UNR == 0) {
+                warp_steps_pipelined<Real, V>(u, r, c, a.nsteps);
+            } else {
 #pragma unroll UNR
-            for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
+                for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
+            }
         } else {
             for (int s = 0; s < a.nsteps; ++s) {
                 warp_step<Real, V>(u, r, c);
