@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
         const bool needL = left_edge && lpe >= 0 && !pin_first;
         const bool needR = right_edge && rpe >= 0 && !pin_last;
         if (!left_edge && !right_edge) {
-            for (int s = 0; s < nst; ++s) warp_step<double, V>(u, r, c);
+            warp_steps_pipelined<double, V>(u, r, c, nst);
         } else {
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
             for (int s = 0; s < nst && !abort; ++s) {
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
 
         // ---- window out: lanes 1..30 that lie inside this PE
         const bool out_lane = lane >= 1 && lane <= kWarp - 2 && g0 >= lo && g0 < out_hi;
-        if (out_lane) {
+        if (out_lane && it.pass == a.npass - 1) {  // non-finite values are absorbing
 #pragma unroll
             for (int i = 0; i < V; ++i) bad |= !isfinite(u[i]);
         }

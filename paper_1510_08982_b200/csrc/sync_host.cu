@@ -154,6 +154,7 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
         a.src = bufs[cur];
         a.dst = bufs[cur ^ 1];
         a.nsteps = s;
+        a.check_finite = size_t(s) == steps;  // last pass of this advance
         var->fn<<<grid, T::kThreads, T::smem_bytes(var->nbuf), st>>>(load_map[cur],
                                                                       store_map[cur ^ 1], a);
         HB_CUDA(cudaGetLastError());
