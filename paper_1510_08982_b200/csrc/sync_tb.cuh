@@ -143,6 +143,7 @@ __device__ __forceinline__ void warp_steps_pipelined(Real (&u)[V], Real r, Real 
     Real pLs = A::mul(r, u[V - 1]);
     Real pL = __shfl_up_sync(0xffffffffu, pLs, 1);
     Real pR = __shfl_down_sync(0xffffffffu, pF, 1);
+#pragma unroll 2
     for (int s = 0; s < nsteps; ++s) {
         const Real p1 = A::mul(r, u[1]);        // r*u[1]   (old)
         const Real pVm2 = A::mul(r, u[V - 2]);  // r*u[V-2] (old)
