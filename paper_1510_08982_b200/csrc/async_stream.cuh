@@ -179,11 +179,13 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
     unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
     int b = 0;
 
-    auto grab = [&]() -> long long {
-        unsigned long long i = 0;
-        if (lane == 0) i = atomicAdd(a.counter, 1ull);
-        return (long long)__shfl_sync(0xffffffffu, i, 0);
-    };
+    // Items are dealt out statically in pass-major order (warp w takes w,
+    // w+W, w+2W, ...): every warp walks its items in increasing order, which
+    // is all the deadlock argument needs (handshaking boundary pairs are
+    // consecutive items, dependencies point to earlier items), and the next
+    // item is known without an atomic round trip.
+    const long long nwarps_all = (long long)gridDim.x * T::kWarpsPerCta;
+    const long long my_first = (long long)blockIdx.x * T::kWarpsPerCta + warp;
     auto geometry = [&](const StreamItem& it, long long& lo, long long& w0, long long& out_hi) {
         lo = (long long)it.p * a.n;
         w0 = lo + (long long)it.m * T::kOut - V;
@@ -218,27 +220,28 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
 
     long long pend_tile = -1;
     unsigned int pend_pass = 0;
+    bool pend_generic = false;  // the pending tile left through per-lane stores
     // Publish done[pend_tile] = pend_pass once its stores have landed
     // (keep_groups = 1: the newest bulk store group may still be in flight).
     auto signal_pending = [&](int keep_groups) {
-        __threadfence();  // every lane's generic stores of the pending tile, then...
+        if (pend_generic) __threadfence();  // every lane's generic stores first
         __syncwarp();
-        if (lane == 0) {  // ...its TMA store group, then the release
+        if (lane == 0) {  // TMA store group done, async-proxy writes ordered, release
             if (keep_groups)
                 asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
             else
                 bulk_wait_all();
             if (pend_tile >= 0) {
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                __threadfence();
                 st_release_gpu_u32(a.done + pend_tile, pend_pass);
             }
         }
         __syncwarp();
         pend_tile = -1;
+        pend_generic = false;
     };
 
-    long long cur = grab();
+    long long cur = my_first;
     bool cur_pref = false;  // window of `cur` already in flight into buffer b
     while (cur < total && !abort) {
         const StreamItem it = decode_item(a, cur);
@@ -269,18 +272,33 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
                 u[i] = (g >= 0 && g < a.N) ? ld_relaxed_gpu_f64(src + g) : 0.0;
             }
         }
-        // ---- next item: grab now, prefetch if its dependencies are already met
-        const long long nxt = grab();
+        // ---- next item (static): its dependency flags are loaded now and
+        // tested half-way through this tile's steps, so the acquire latency
+        // hides behind compute; the window prefetch then still has half a
+        // tile of compute to land.
+        const long long nxt = cur + nwarps_all;
         bool nxt_pref = false;
+        StreamItem ni{};
+        long long nlo = 0, nw0 = 0, nhi = 0;
+        bool nxt_cand = false;
+        unsigned int dep_seen = 0xffffffffu;
         if (nxt < total) {
-            const StreamItem ni = decode_item(a, nxt);
-            long long nlo, nw0, nhi;
+            ni = decode_item(a, nxt);
             geometry(ni, nlo, nw0, nhi);
-            if (tma_ok(nw0) && deps_ready(ni, false)) {
+            nxt_cand = tma_ok(nw0);
+            if (nxt_cand && ni.pass > 0 && lane < 3) {
+                const int mm = ni.m + lane - 1;
+                if (mm >= 0 && mm < a.Tp) dep_seen = ld_acquire_gpu_u32(a.done + ni.p * a.Tp + mm);
+            }
+        }
+        auto try_prefetch = [&]() {
+            if (!nxt_cand) return;
+            const bool ok = ni.pass == 0 || dep_seen >= unsigned(ni.pass);
+            if (__all_sync(0xffffffffu, ok)) {
                 issue(b ^ 1, ni, nw0);
                 nxt_pref = true;
             }
-        }
+        };
 
         // ---- step the tile; boundary tiles exchange edge values every step
         const int lR = int((out_hi - 1 - w0) / V);  // lane holding the PE's last point
@@ -291,8 +309,12 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
         const bool needL = left_edge && lpe >= 0 && !pin_first;
         const bool needR = right_edge && rpe >= 0 && !pin_last;
         if (!left_edge && !right_edge) {
-            warp_steps_pipelined<double, V>(u, r, c, nst);
+            const int half = nst / 2;
+            warp_steps_pipelined<double, V>(u, r, c, half);
+            try_prefetch();
+            warp_steps_pipelined<double, V>(u, r, c, nst - half);
         } else {
+            try_prefetch();
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
             for (int s = 0; s < nst && !abort; ++s) {
                 const long long k = kbeg + s;
@@ -380,6 +402,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
         signal_pending(1);
         pend_tile = (long long)it.p * a.Tp + it.m;
         pend_pass = unsigned(it.pass + 1);
+        pend_generic = !(tma_ok(w0) && full);
         cur = nxt;
         cur_pref = nxt_pref;
         if (nxt_pref) b ^= 1;
