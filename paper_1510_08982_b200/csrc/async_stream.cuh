@@ -179,13 +179,15 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
     unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
     int b = 0;
 
-    // Items are dealt out statically in pass-major order (warp w takes w,
-    // w+W, w+2W, ...): every warp walks its items in increasing order, which
-    // is all the deadlock argument needs (handshaking boundary pairs are
-    // consecutive items, dependencies point to earlier items), and the next
-    // item is known without an atomic round trip.
-    const long long nwarps_all = (long long)gridDim.x * T::kWarpsPerCta;
-    const long long my_first = (long long)blockIdx.x * T::kWarpsPerCta + warp;
+    // Items are handed out dynamically in pass-major order (one atomic
+    // counter): boundary tiles take ~5x longer than interior ones, and a
+    // static deal lets the warps that drew them hold back their neighbours'
+    // next pass (measured: -20%).
+    auto grab = [&]() -> long long {
+        unsigned long long i = 0;
+        if (lane == 0) i = atomicAdd(a.counter, 1ull);
+        return (long long)__shfl_sync(0xffffffffu, i, 0);
+    };
     auto geometry = [&](const StreamItem& it, long long& lo, long long& w0, long long& out_hi) {
         lo = (long long)it.p * a.n;
         w0 = lo + (long long)it.m * T::kOut - V;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
         pend_generic = false;
     };
 
-    long long cur = my_first;
+    long long cur = grab();
     bool cur_pref = false;  // window of `cur` already in flight into buffer b
     while (cur < total && !abort) {
         const StreamItem it = decode_item(a, cur);
@@ -272,11 +274,11 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
                 u[i] = (g >= 0 && g < a.N) ? ld_relaxed_gpu_f64(src + g) : 0.0;
             }
         }
-        // ---- next item (static): its dependency flags are loaded now and
+        // ---- next item: grabbed now; its dependency flags are loaded now and
         // tested half-way through this tile's steps, so the acquire latency
         // hides behind compute; the window prefetch then still has half a
         // tile of compute to land.
-        const long long nxt = cur + nwarps_all;
+        const long long nxt = grab();
         bool nxt_pref = false;
         StreamItem ni{};
         long long nlo = 0, nw0 = 0, nhi = 0;
