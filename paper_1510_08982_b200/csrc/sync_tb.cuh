@@ -319,33 +319,16 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
             }
         }
         const long long tn = t + nwarps;
-        const bool pref = tn < a.tiles && interior(tn);
-        auto run_steps = [&](int n) {
-            if constexpr (UNR == 0) {
-                warp_steps_pipelined<Real, V>(u, r, c, n);
-            } else {
-#pragma unroll UNR
-                for (int s = 0; s < n; ++s) warp_step<Real, V>(u, r, c);
-            }
-        };
+        if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
-            if (NBUF == 1) {
-                // one buffer: refill it as soon as this window is in registers
-                if (pref) issue(0, tn);
-                run_steps(a.nsteps);
+            if constexpr (UNR == 0) {
+                warp_steps_pipelined<Real, V>(u, r, c, a.nsteps);
             } else {
-                // two buffers: the other buffer was the source of the TMA store
-                // issued at the end of the previous tile -- prefetching into it
-                // half-way through this tile's steps means that store has long
-                // been read out and lane 0 does not stall on it.
-                const int half = a.nsteps / 2;
-                run_steps(half);
-                if (pref) issue(b ^ 1, tn);
-                run_steps(a.nsteps - half);
+#pragma unroll UNR
+                for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
             }
         } else {
-            if (pref) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
             for (int s = 0; s < a.nsteps; ++s) {
                 warp_step<Real, V>(u, r, c);
                 pin_ends<Real, V>(u, g0, a.pin_lo, a.pin_hi, c1, c2);
