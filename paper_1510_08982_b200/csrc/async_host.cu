@@ -8,6 +8,7 @@
 #include "async_pe.cuh"
 #include "async_stream.cuh"
 #include "runtime.cuh"
+#include "stream_host.cuh"
 
 namespace hb {
 
@@ -106,23 +107,6 @@ int launch_pe(int V, bool shared, bool barrier, const AsyncPeArgs& a, int P, cud
 
 }  // namespace
 
-// Shared driver of async_run (deterministic) and exec_run(BarrierFree) (free).
-// Advances `field` (device, prepared) from step 0 to k_end, calling
-// on_record(k) after every `stride` steps when stride > 0.
-struct AsyncRunSpec {
-    size_t N, n;
-    double r;
-    int bc_kind;
-    double c1, c2;
-    int mode;  // 0 deterministic, 1 free
-    size_t q;
-    int law;
-    size_t fixed_d;
-    double geometric_p;
-    uint64_t seed;
-    size_t k_end;
-    bool want_logs;
-};
 
 int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride,
                  const std::function<int(size_t, const double*)>& on_record,
@@ -312,219 +296,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     return HEAT_OK;
 }
 
-// ---- K5: streaming async (PEs wider than a warp) ---------------------------
-namespace {
-constexpr int kSV = 32;  // points per lane of the stream kernel (= K1's V)
-
-__global__ void stream_init_kernel(const double* __restrict__ field, long long n, int P, int R,
-                                   double* ringL, double* ringR, unsigned long long* progL,
-                                   unsigned long long* progR) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)P * R;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long p = i / R;
-        const bool s0 = (i % R) == 0;
-        ringL[i] = s0 ? field[p * n] : 0.0;
-        ringR[i] = s0 ? field[p * n + n - 1] : 0.0;
-        if (s0) {
-            progL[p] = 0;
-            progR[p] = 0;
-        }
-    }
-}
-}  // namespace
-
-// Device scratch of one streaming run (rings persist across its launches).
-struct StreamLayout {
-    size_t P = 0, Tp = 0;
-    int R = 0, D = 0;
-    size_t o_ringL, o_ringR, o_progL, o_progR, o_done, o_counter, o_offL, o_offR, o_dtab, o_stats,
-        o_abort, bytes;
-};
-
-int stream_layout(const AsyncRunSpec& s, StreamLayout& L, std::vector<int>& offL,
-                  std::vector<int>& offR) {
-    if (s.n % kSV != 0)
-        return fail(HEAT_EINVAL, "async: PEs wider than 1024 points must be a multiple of 32 points");
-    L.P = s.N / s.n;
-    L.Tp = (s.n + SyncTB<double, kSV>::kOut - 1) / SyncTB<double, kSV>::kOut;
-    if (L.Tp < 2) return fail(HEAT_ELOGIC, "async stream: a PE needs >= 2 tiles");
-    L.R = 64;
-    while (L.R < 2 * int(s.q) + 2) L.R *= 2;
-    L.D = draw_offsets(s.N, s.n, s.bc_kind == HEAT_BC_DIRICHLET, offL, offR);
-    size_t off = 0;
-    auto take = [&](size_t b) { size_t o = off; off += (b + 255) / 256 * 256; return o; };
-    L.o_ringL = take(L.P * L.R * sizeof(double));
-    L.o_ringR = take(L.P * L.R * sizeof(double));
-    L.o_progL = take(L.P * 8);
-    L.o_progR = take(L.P * 8);
-    L.o_done = take(L.P * L.Tp * 4);
-    L.o_counter = take(8);
-    L.o_offL = take(L.P * 4);
-    L.o_offR = take(L.P * 4);
-    L.o_dtab = take(s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC ? s.k_end * size_t(L.D) : 1);
-    L.o_stats = take(kStatWords * 8);
-    L.o_abort = take(4);
-    L.bytes = off;
-    return HEAT_OK;
-}
-
-// Advances bufs[cur] (device, prepared, N points) by `steps` from absolute
-// step k0 with the streaming kernel; init=true seeds the rings from the field.
-int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, const AsyncRunSpec& s,
-                         const StreamLayout& L, char* base, const std::vector<int>& offL,
-                         const std::vector<int>& offR, size_t k0, size_t steps, bool init,
-                         unsigned int* flag, float* device_ms) {
-    using T = SyncTB<double, kSV>;
-    if (init) {
-        std::vector<unsigned long long> stats0(kStatWords, 0);
-        stats0[kStatLagMin] = ~0ull;
-        stream_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (L.P * L.R + 255) / 256)),
-                             256, 0, st>>>(bufs[cur], (long long)s.n, int(L.P), L.R,
-                                           reinterpret_cast<double*>(base + L.o_ringL),
-                                           reinterpret_cast<double*>(base + L.o_ringR),
-                                           reinterpret_cast<unsigned long long*>(base + L.o_progL),
-                                           reinterpret_cast<unsigned long long*>(base + L.o_progR));
-        HB_CUDA(cudaGetLastError());
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        HB_CUDA(cudaMemcpyAsync(base + L.o_offL, offL.data(), L.P * 4, cudaMemcpyHostToDevice, st));
-        HB_CUDA(cudaMemcpyAsync(base + L.o_offR, offR.data(), L.P * 4, cudaMemcpyHostToDevice, st));
-        HB_CUDA(cudaMemcpyAsync(base + L.o_stats, stats0.data(), kStatWords * 8,
-                                cudaMemcpyHostToDevice, st));
-        if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {
-            std::vector<unsigned char> dtab(s.k_end * size_t(L.D));
-            const double lp = std::log1p(-s.geometric_p);
-            for (size_t k = 0; k < s.k_end; ++k) {
-                const size_t bound = std::min<size_t>(s.q - 1, k);
-                for (int o = 0; o < L.D; ++o) {
-                    const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * L.D + o);
-                    const double u = double(x >> 11) * 0x1.0p-53;
-                    double g = std::floor(std::log1p(-u) / lp);
-                    if (!std::isfinite(g) || g < 0.0) g = 0.0;
-                    dtab[k * L.D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
-                }
-            }
-            HB_CUDA(cudaMemcpy(base + L.o_dtab, dtab.data(), dtab.size(), cudaMemcpyHostToDevice));
-        }
-    }
-    if (steps == 0) return HEAT_OK;
-    HB_CUDA(cudaMemsetAsync(base + L.o_done, 0, L.P * L.Tp * 4, st));
-    HB_CUDA(cudaMemsetAsync(base + L.o_counter, 0, 8, st));
-    HB_CUDA(cudaMemsetAsync(base + L.o_abort, 0, 4, st));
-
-    static int per_sm = 0;
-    const int smem = T::smem_bytes(2);
-    if (per_sm == 0) {
-        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<kSV>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<kSV>,
-                                                              T::kThreads, smem));
-        if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
-    }
-    const long long nchunks = (long long)(s.N / kSV);
-    CUtensorMap ld[2], stm[2];
-    for (int b = 0; b < 2; ++b) {
-        HB_TRY(make_chunk_map_f64(&ld[b], bufs[b], nchunks, kWarp));
-        HB_TRY(make_chunk_map_f64(&stm[b], bufs[b], nchunks, kWarp - 2));
-    }
-    AsyncStreamArgs a{};
-    a.buf[0] = bufs[cur];
-    a.buf[1] = bufs[cur ^ 1];
-    a.N = (long long)s.N;
-    a.n = (long long)s.n;
-    a.P = int(L.P);
-    a.Tp = int(L.Tp);
-    a.r = s.r;
-    a.c = 1.0 - 2.0 * s.r;
-    a.c1 = s.c1;
-    a.c2 = s.c2;
-    a.dirichlet = s.bc_kind == HEAT_BC_DIRICHLET;
-    a.k0 = (long long)k0;
-    a.steps = (long long)steps;
-    a.s = T::kMaxSteps;
-    a.npass = (a.steps + a.s - 1) / a.s;
-    a.mode = s.mode;
-    a.q = int(s.q);
-    a.R = L.R;
-    a.law = s.law;
-    a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
-    a.seed = s.seed;
-    a.D = L.D;
-    a.off_left = reinterpret_cast<const int*>(base + L.o_offL);
-    a.off_right = reinterpret_cast<const int*>(base + L.o_offR);
-    a.dtable = reinterpret_cast<const unsigned char*>(base + L.o_dtab);
-    a.ringL = reinterpret_cast<double*>(base + L.o_ringL);
-    a.ringR = reinterpret_cast<double*>(base + L.o_ringR);
-    a.progL = reinterpret_cast<unsigned long long*>(base + L.o_progL);
-    a.progR = reinterpret_cast<unsigned long long*>(base + L.o_progR);
-    a.done = reinterpret_cast<unsigned int*>(base + L.o_done);
-    a.counter = reinterpret_cast<unsigned long long*>(base + L.o_counter);
-    a.stats = reinterpret_cast<unsigned long long*>(base + L.o_stats);
-    a.flag = flag;
-    a.abort_word = reinterpret_cast<unsigned int*>(base + L.o_abort);
-    a.timeout_ns = 20ull * 1000 * 1000 * 1000;
-    // maps follow the pass parity: pass pi reads a.buf[pi & 1]
-    const CUtensorMap& l0 = ld[cur];
-    const CUtensorMap& l1 = ld[cur ^ 1];
-    const CUtensorMap& s0 = stm[cur];
-    const CUtensorMap& s1 = stm[cur ^ 1];
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (device_ms) {
-        HB_CUDA(cudaEventCreate(&e0));
-        HB_CUDA(cudaEventCreate(&e1));
-        HB_CUDA(cudaEventRecord(e0, st));
-    }
-    async_stream_kernel<kSV><<<sms * per_sm, T::kThreads, smem, st>>>(l0, l1, s0, s1, a);
-    HB_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (device_ms) {
-        HB_CUDA(cudaEventRecord(e1, st));
-        HB_CUDA(cudaEventSynchronize(e1));
-        HB_CUDA(cudaEventElapsedTime(device_ms, e0, e1));
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
-    if (a.npass & 1) cur ^= 1;
-    return HEAT_OK;
-}
-
-// Whole-run driver used by heat_async_run / heat_exec_run for wide PEs.
-int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur, size_t stride,
-                     const std::function<int(size_t, const double*)>& on_record,
-                     unsigned long long* host_stats, float* device_ms) {
-    StreamLayout L;
-    std::vector<int> offL, offR;
-    HB_TRY(stream_layout(s, L, offL, offR));
-    if (d.sms * 12 < 2) return fail(HEAT_ELOGIC, "async stream: too few warps");
-    HB_TRY(ensure_scratch(d, L.bytes));
-    char* base = static_cast<char*>(d.scratch);
-    cudaStream_t st = d.stream;
-    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
-    HB_TRY(async_stream_advance(d.sms, st, bufs, cur, s, L, base, offL, offR, 0, 0, true, d.flag,
-                                nullptr));
-    float total_ms = 0.f;
-    size_t k = 0;
-    while (k < s.k_end) {
-        const size_t next = stride ? std::min(s.k_end, (k / stride + 1) * stride) : s.k_end;
-        float ms = 0.f;
-        HB_TRY(async_stream_advance(d.sms, st, bufs, cur, s, L, base, offL, offR, k, next - k,
-                                    false, d.flag, device_ms ? &ms : nullptr));
-        total_ms += ms;
-        k = next;
-        unsigned int flags[2] = {0, 0};
-        HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
-        HB_CUDA(cudaStreamSynchronize(st));
-        if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
-        if (flags[0]) {
-            if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
-            return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
-        }
-        if (stride && on_record) HB_TRY(on_record(k, bufs[cur]));
-    }
-    if (device_ms) *device_ms = total_ms;
-    if (host_stats)
-        HB_CUDA(cudaMemcpy(host_stats, base + L.o_stats, kStatWords * 8, cudaMemcpyDeviceToHost));
-    return HEAT_OK;
-}
+// K5 (streaming async) host code lives in stream_host.cu.
 
 }  // namespace hb
 
@@ -828,7 +600,8 @@ static int plan_async(heat_plan* p, const AsyncRunSpec& s, heat_async_stats* sta
     HB_CUDA(cudaSetDevice(p->device));
     StreamLayout L;
     std::vector<int> offL, offR;
-    HB_TRY(stream_layout(s, L, offL, offR));
+    const StreamExternal ext{};
+    HB_TRY(stream_layout(s, virtual_device_groups(p->n / per_pe), ext, L, offL, offR));
     if (p->async_bytes < L.bytes) {
         if (p->async_scratch) cudaFree(p->async_scratch);
         p->async_scratch = nullptr;
@@ -837,9 +610,9 @@ static int plan_async(heat_plan* p, const AsyncRunSpec& s, heat_async_stats* sta
         p->async_bytes = L.bytes;
     }
     char* base = static_cast<char*>(p->async_scratch);
-    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, offL, offR, 0, 0,
-                                true, p->flag, nullptr));
-    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, offL, offR, 0,
+    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, ext, offL, offR, 0,
+                                0, true, p->flag, nullptr));
+    HB_TRY(async_stream_advance(p->sms, p->stream, p->bufs, p->cur, s, L, base, ext, offL, offR, 0,
                                 steps, false, p->flag, nullptr));
     if (stats) {
         std::vector<unsigned long long> hs(kStatWords, 0);

@@ -150,7 +150,7 @@ __device__ __forceinline__ uint64_t wait_prog(const AsyncPeArgs& a, const uint64
 
 // Ring state at step 0: slot 0 of every PE's two rings holds its step-0 edge
 // values, prog = 0 (everything else zero); the edge log gets step 0 too.
-__global__ void async_init_kernel(const double* __restrict__ field, int n, int P, int R,
+static __global__ void async_init_kernel(const double* __restrict__ field, int n, int P, int R,
                                   double* ring, unsigned long long* prog, double* edge_log) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)P * 2 * R;
          i += (long long)gridDim.x * blockDim.x) {

@@ -33,6 +33,29 @@
 
 namespace hb {
 
+// Where a PE's boundary tiles read their neighbours' edge histories and where
+// they publish their own (built on the host).  Within one device every link
+// points into the local rings (GPU scope).  At a device boundary the reader
+// owns a receive ring that the neighbour device fills with P2P stores over
+// NVLink (system scope), so every load stays local and NCCL only sets up.
+enum : int {
+    kLinkSrcLSys = 1,   // srcL/progL_src are written by another device
+    kLinkSrcRSys = 2,
+    kLinkPubF1Sys = 4,  // pubF[1] lives on another device
+    kLinkPubL1Sys = 8,
+};
+struct PeLink {
+    const double* srcL;                 // left neighbour's LAST-point history (null: none)
+    const unsigned long long* progL_src;
+    const double* srcR;                 // right neighbour's FIRST-point history
+    const unsigned long long* progR_src;
+    double* pubF[2];                    // rings mirroring this PE's first point
+    unsigned long long* pubF_prog[2];
+    double* pubL[2];                    // rings mirroring this PE's last point
+    unsigned long long* pubL_prog[2];
+    int flags;
+};
+
 struct AsyncStreamArgs {
     double* buf[2];  // ping-pong fields (pass pi reads buf[pi & 1])
     long long N;
@@ -53,10 +76,9 @@ struct AsyncStreamArgs {
     const int* off_left;
     const int* off_right;
     const unsigned char* dtable;  // GEOMETRIC delays [k*D + off] (absolute k)
-    double* ringL;                // [P][R]
-    double* ringR;                // [P][R]
-    unsigned long long* progL;    // [P]
-    unsigned long long* progR;    // [P]
+    const struct PeLink* links;   // [P] neighbour sources / publish targets
+    int pin_first_pe;             // PE whose first point is the pinned global end 0 (or -1)
+    int pin_last_pe;              // PE whose last point is the pinned global end N-1 (or -1)
     unsigned int* done;           // [P*Tp] passes completed in this launch
     unsigned long long* counter;  // work-item counter
     unsigned long long* stats;
@@ -73,9 +95,15 @@ __device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k
     return a.fixed_d < bound ? a.fixed_d : int(bound);
 }
 
+__device__ __forceinline__ uint64_t ld_acq(const unsigned long long* w, bool sys) {
+    return sys ? ld_acquire_sys(reinterpret_cast<const uint64_t*>(w))
+               : ld_acquire_gpu(reinterpret_cast<const uint64_t*>(w));
+}
+
 __device__ __forceinline__ bool spin_until(const AsyncStreamArgs& a, const unsigned long long* w,
-                                           long long need, unsigned long long* seen, bool* waited) {
-    uint64_t v = ld_acquire_gpu(reinterpret_cast<const uint64_t*>(w));
+                                           long long need, unsigned long long* seen, bool* waited,
+                                           bool sys) {
+    uint64_t v = ld_acq(w, sys);
     if ((long long)v >= need) {
         *seen = v;
         return true;
@@ -83,7 +111,7 @@ __device__ __forceinline__ bool spin_until(const AsyncStreamArgs& a, const unsig
     *waited = true;
     const uint64_t t0 = globaltimer_ns();
     unsigned spins = 0;
-    while ((long long)(v = ld_acquire_gpu(reinterpret_cast<const uint64_t*>(w))) < need) {
+    while ((long long)(v = ld_acq(w, sys)) < need) {
         if ((++spins & 127u) == 0) {
             if (*reinterpret_cast<volatile unsigned int*>(a.abort_word)) return false;
             if (globaltimer_ns() - t0 > a.timeout_ns) {
@@ -304,12 +332,6 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
 
         // ---- step the tile; boundary tiles exchange edge values every step
         const int lR = int((out_hi - 1 - w0) / V);  // lane holding the PE's last point
-        const bool pin_first = a.dirichlet && it.p == 0;
-        const bool pin_last = a.dirichlet && it.p == a.P - 1;
-        const int lpe = it.p > 0 ? it.p - 1 : (a.dirichlet ? -1 : a.P - 1);
-        const int rpe = it.p + 1 < a.P ? it.p + 1 : (a.dirichlet ? -1 : 0);
-        const bool needL = left_edge && lpe >= 0 && !pin_first;
-        const bool needR = right_edge && rpe >= 0 && !pin_last;
         if (!left_edge && !right_edge) {
             const int half = nst / 2;
             warp_steps_pipelined<double, V>(u, r, c, half);
@@ -318,27 +340,35 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
         } else {
             try_prefetch();
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
+            // where this PE's neighbour values come from / its edge values go
+            const PeLink& lk = a.links[it.p];
+            const bool pin_first = it.p == a.pin_first_pe;
+            const bool pin_last = it.p == a.pin_last_pe;
+            const bool needL = left_edge && lk.srcL != nullptr && !pin_first;
+            const bool needR = right_edge && lk.srcR != nullptr && !pin_last;
+            // lane 1 holds the PE's first point, lane lR its last one
+            const bool mine = (lane == 1 && needL) || (lane == lR && needR && !(lane == 1 && needL));
+            const bool left = lane == 1 && needL;
+            const unsigned long long* pw = left ? lk.progL_src : lk.progR_src;
+            const double* gring = left ? lk.srcL : lk.srcR;
+            const bool gsys = (lk.flags & (left ? kLinkSrcLSys : kLinkSrcRSys)) != 0;
             for (int s = 0; s < nst && !abort; ++s) {
                 const long long k = kbeg + s;
                 double ghost = 0.0;
-                const bool mine = (lane == 1 && needL) || (lane == lR && needR && !(lane == 1 && needL));
-                // a lane may own both sides only if lR == 1 (never: Tp >= 2 puts them in different tiles)
                 if (mine) {
-                    const bool left = lane == 1 && needL;
-                    const unsigned long long* pw = left ? a.progR + lpe : a.progL + rpe;
-                    const double* ring = left ? a.ringR + (size_t)lpe * a.R : a.ringL + (size_t)rpe * a.R;
                     unsigned long long seen = 0;
                     bool waited = false;
                     long long mstep;
                     if (a.mode == 0) {
                         mstep = k - det_delay_s(a, k, left ? a.off_left[it.p] : a.off_right[it.p]);
-                        if (!spin_until(a, pw, mstep, &seen, &waited)) abort = true;
+                        if (!spin_until(a, pw, mstep, &seen, &waited, gsys)) abort = true;
                     } else {
-                        if (!spin_until(a, pw, k - (a.q - 1), &seen, &waited)) abort = true;
+                        if (!spin_until(a, pw, k - (a.q - 1), &seen, &waited, gsys)) abort = true;
                         mstep = (long long)seen < k ? (long long)seen : k;
                     }
                     if (!abort) {
-                        ghost = ld_relaxed_gpu_f64(ring + (mstep & (a.R - 1)));
+                        const double* slotp = gring + (mstep & (a.R - 1));
+                        ghost = gsys ? ld_relaxed_sys_f64(slotp) : ld_relaxed_gpu_f64(slotp);
                         const unsigned long long used = (unsigned long long)(k - mstep);
                         const unsigned long long lag = seen - (unsigned long long)mstep;
                         reads++;
@@ -363,15 +393,36 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
                 chunk_step<double, V>(u, r, c, pL, pR, pFirst, pLast);
                 if (left_edge && pin_first && lane == 1) u[0] = a.c1;
                 if (right_edge && pin_last && lane == lR) u[V - 1] = a.c2;
-                // publish u_first(k+1) / u_last(k+1), then the progress (release)
+                // publish u_first(k+1) / u_last(k+1) to every ring that mirrors
+                // it (local, plus the neighbour device's receive ring for a
+                // device boundary -- a P2P store over NVLink), then release
+                // the progress word with the matching scope
                 const long long slot = (k + 1) & (a.R - 1);
                 if (left_edge && lane == 1) {
-                    st_relaxed_gpu_f64(a.ringL + (size_t)it.p * a.R + slot, u[0]);
-                    st_release_gpu(reinterpret_cast<uint64_t*>(a.progL + it.p), uint64_t(k + 1));
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (!lk.pubF[t]) continue;
+                        if (lk.flags & (t ? kLinkPubF1Sys : 0)) {
+                            st_relaxed_sys_f64(lk.pubF[t] + slot, u[0]);
+                            st_release_sys(reinterpret_cast<uint64_t*>(lk.pubF_prog[t]), uint64_t(k + 1));
+                        } else {
+                            st_relaxed_gpu_f64(lk.pubF[t] + slot, u[0]);
+                            st_release_gpu(reinterpret_cast<uint64_t*>(lk.pubF_prog[t]), uint64_t(k + 1));
+                        }
+                    }
                 }
                 if (right_edge && lane == lR) {
-                    st_relaxed_gpu_f64(a.ringR + (size_t)it.p * a.R + slot, u[V - 1]);
-                    st_release_gpu(reinterpret_cast<uint64_t*>(a.progR + it.p), uint64_t(k + 1));
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        if (!lk.pubL[t]) continue;
+                        if (lk.flags & (t ? kLinkPubL1Sys : 0)) {
+                            st_relaxed_sys_f64(lk.pubL[t] + slot, u[V - 1]);
+                            st_release_sys(reinterpret_cast<uint64_t*>(lk.pubL_prog[t]), uint64_t(k + 1));
+                        } else {
+                            st_relaxed_gpu_f64(lk.pubL[t] + slot, u[V - 1]);
+                            st_release_gpu(reinterpret_cast<uint64_t*>(lk.pubL_prog[t]), uint64_t(k + 1));
+                        }
+                    }
                 }
             }
             if (abort) break;

@@ -109,6 +109,24 @@ int make_chunk_map_f64(struct CUtensorMap_st* m, const void* base, long long nch
 int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
                     double* dst);
 
+// Shared driver of async_run (deterministic) and exec_run(BarrierFree) (free).
+// Advances `field` (device, prepared) from step 0 to k_end, calling
+// on_record(k) after every `stride` steps when stride > 0.
+struct AsyncRunSpec {
+    size_t N, n;
+    double r;
+    int bc_kind;
+    double c1, c2;
+    int mode;  // 0 deterministic, 1 free
+    size_t q;
+    int law;
+    size_t fixed_d;
+    double geometric_p;
+    uint64_t seed;
+    size_t k_end;
+    bool want_logs;
+};
+
 // async_run after validation (async_host.cu).
 int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
                    size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
