@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
             try_prefetch();
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
             // where this PE's neighbour values come from / its edge values go
-            const PeLink& lk = a.links[it.p];
+            const PeLink lk = a.links[it.p];  // into registers once per boundary tile
             const bool pin_first = it.p == a.pin_first_pe;
             const bool pin_last = it.p == a.pin_last_pe;
             const bool needL = left_edge && lk.srcL != nullptr && !pin_first;
