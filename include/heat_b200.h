@@ -184,6 +184,27 @@ int heat_plan_device_ptr(heat_plan* plan, double** cur);
  * Only the true global ends are pinned (rank 0 / rank world-1, Dirichlet);
  * periodic slabs wrap through the exchange. */
 size_t heat_slab_halo(void);
+
+/* ---- multi-GPU asynchronous slabs over NVLink P2P (north star (3)) ------
+ * Rank r of `world` (a slab plan) runs the K5 asynchronous kernel on its
+ * n_local points split into PEs of per_pe points; the PE boundaries between
+ * ranks exchange edge values by P2P STORES into the neighbour's receive rings
+ * (system-scope release/acquire).  With mode 1 and q = 1 every read is exact
+ * and the run is the synchronous scheme; mode 0 replays a DelayModel's
+ * stream (uniform/fixed) over the global PE enumeration, bit-identical to
+ * async_run on the whole field.  Setup order on every rank:
+ *   xlink_setup -> exchange handles (heat_xlink_handle_size() bytes; any
+ *   transport) -> xlink_connect(left, right; NULL at Dirichlet ends);
+ * then per run: xlink_seed -> barrier across ranks -> xlink_advance. */
+size_t heat_xlink_handle_size(void);
+int heat_plan_xlink_setup(heat_plan* plan, size_t per_pe, size_t q, int bc_kind, void* handle_out);
+int heat_plan_xlink_connect(heat_plan* plan, const void* left_handle, const void* right_handle);
+int heat_plan_xlink_seed(heat_plan* plan);
+int heat_plan_xlink_advance(heat_plan* plan, double r, double c1, double c2, int mode, int law,
+                            size_t fixed_delay, double geometric_p, uint64_t seed, size_t steps,
+                            heat_async_stats* stats);
+/* Test hook: slot 0 of the two receive rings (the neighbours' seeded values). */
+int heat_plan_xlink_debug_recv(heat_plan* plan, double* out2);
 int heat_plan_create_slab(heat_plan** plan, size_t n_local, int device, int rank, int world);
 int heat_plan_halo_pack(heat_plan* plan, void* dst_device);
 int heat_plan_halo_unpack(heat_plan* plan, const void* src_device);

@@ -126,6 +126,13 @@ SIGNATURES = {
     "heat_plan_create_slab": (_i, [_P(_vp), _sz, _i, _i, _i]),
     "heat_plan_halo_pack": (_i, [_vp, _vp]),
     "heat_plan_halo_unpack": (_i, [_vp, _vp]),
+    "heat_xlink_handle_size": (_sz, []),
+    "heat_plan_xlink_setup": (_i, [_vp, _sz, _sz, _i, _vp]),
+    "heat_plan_xlink_connect": (_i, [_vp, _vp, _vp]),
+    "heat_plan_xlink_seed": (_i, [_vp]),
+    "heat_plan_xlink_advance": (_i, [_vp, _d, _d, _d, _i, _i, _sz, _d, _u64, _sz,
+                                     _P(AsyncStatsC)]),
+    "heat_plan_xlink_debug_recv": (_i, [_vp, _pd]),
 }
 
 _lib = None

@@ -58,6 +58,7 @@ int heat_plan_destroy(heat_plan* p) {
     if (!p) return HEAT_OK;
     cudaSetDevice(p->device);
     cudaStreamSynchronize(p->stream);
+    xlink_release(p);
     cudaFree(p->base);
     cudaFree(p->flag);
     if (p->async_scratch) cudaFree(p->async_scratch);

@@ -34,6 +34,7 @@ struct heat_plan {
     double* ext[2] = {nullptr, nullptr};   // ghosted arrays (base)
     void* async_scratch = nullptr;         // rings / counters of heat_plan_async_advance
     size_t async_bytes = 0;
+    void* xlink = nullptr;                 // multi-GPU P2P state (xlink.cu)
 };
 
 namespace hb {
@@ -75,6 +76,9 @@ struct DevCtx {
     void* snaps = nullptr;         // in-kernel trajectories of small runs
     size_t snaps_bytes = 0;
 };
+
+// Closes a plan's IPC mappings and frees its xlink state (xlink.cu).
+void xlink_release(heat_plan* p);
 
 // Locks and initialises the context of the current (or given) device.
 int dev_ctx(int device, DevCtx** out);

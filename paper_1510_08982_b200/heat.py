@@ -489,6 +489,41 @@ class Plan:
         """Ghost points per side of a slab = max steps per exchange."""
         return int(_lib.lib().heat_slab_halo())
 
+    # ---- multi-GPU asynchronous slabs over NVLink P2P (heat_plan_xlink_*) ----
+    def xlink_setup(self, per_pe: int, q: int, bc: BoundaryCondition) -> bytes:
+        """Allocate the receive rings; returns this rank's IPC handle to share."""
+        size = int(_lib.lib().heat_xlink_handle_size())
+        buf = C.create_string_buffer(size)
+        _lib.check(_lib.lib().heat_plan_xlink_setup(self._h, per_pe, q, bc.kind, buf),
+                   "xlink_setup")
+        return buf.raw
+
+    def xlink_connect(self, left: Optional[bytes], right: Optional[bytes]):
+        lb = C.create_string_buffer(left, len(left)) if left is not None else None
+        rb = C.create_string_buffer(right, len(right)) if right is not None else None
+        _lib.check(_lib.lib().heat_plan_xlink_connect(self._h, lb, rb), "xlink_connect")
+
+    def xlink_seed(self):
+        _lib.check(_lib.lib().heat_plan_xlink_seed(self._h), "xlink_seed")
+
+    def xlink_advance(self, r: float, bc: BoundaryCondition, steps: int,
+                      model: Optional["DelayModel"] = None):
+        """mode free (model None, bound = the q of xlink_setup) or replay of `model`."""
+        st = _lib.AsyncStatsC()
+        if model is None:
+            args = (1, int(Distribution.Uniform), 0, 0.5, 0)
+        else:
+            args = (0, int(model.distribution), model.fixed_delay, model.geometric_p,
+                    model.seed & 0xFFFFFFFFFFFFFFFF)
+        _lib.check(_lib.lib().heat_plan_xlink_advance(self._h, r, bc.c1, bc.c2, *args, steps,
+                                                      C.byref(st)), "xlink_advance")
+        return st
+
+    def xlink_debug_recv(self):
+        out = np.zeros(2, np.float64)
+        _lib.check(_lib.lib().heat_plan_xlink_debug_recv(self._h, _lib.dptr(out)), "debug")
+        return out
+
     def halo_pack(self, dst_device_ptr: int):
         _lib.check(_lib.lib().heat_plan_halo_pack(self._h, dst_device_ptr), "halo_pack")
 

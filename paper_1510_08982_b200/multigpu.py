@@ -109,6 +109,46 @@ class PlanEngine(SlabEngine):
         self.plan.sync_advance(self.r, self.bc, steps)
 
 
+def exchange_handles(handle: bytes, rank: int, world: int, periodic: bool, group=None):
+    """All-gather the 64-byte IPC handles (setup only) and pick the neighbours'."""
+    handles = [None] * world
+    dist.all_gather_object(handles, handle, group=group)
+    left, right = neighbours(rank, world, periodic)
+    return (handles[left] if left is not None else None,
+            handles[right] if right is not None else None)
+
+
+class AsyncSlabSolver:
+    """Asynchronous FTCS over G GPUs: each rank runs K5 on its slab; the PE
+    boundaries between ranks exchange edge values by P2P stores over NVLink
+    into the neighbour's receive rings (heat_plan_xlink_*).  NCCL/gloo only
+    ships the IPC handles and the per-run barrier after seeding; GPUs never
+    barrier per step.  q = 1 free mode is the exact synchronous scheme."""
+
+    def __init__(self, n_local: int, per_pe: int, q: int, bc, device: int, rank: int,
+                 world: int, group=None):
+        from .heat import Plan
+        torch.cuda.set_device(device)
+        self.rank, self.world, self.group, self.bc = rank, world, group, bc
+        self.periodic = not bc.is_dirichlet()
+        self.plan = Plan(n_local, device, rank, world)
+        stream = torch.cuda.current_stream(device)
+        if stream.cuda_stream == 0:
+            raise ValueError("AsyncSlabSolver needs a non-default current stream")
+        self.plan.set_stream(stream.cuda_stream)
+        handle = self.plan.xlink_setup(per_pe, q, bc)
+        left, right = exchange_handles(handle, rank, world, self.periodic, group)
+        self.plan.xlink_connect(left, right)
+        dist.barrier(group=group)
+
+    def advance(self, r: float, steps: int, model=None):
+        """One fresh run of `steps` steps from the current field."""
+        self.plan.xlink_seed()  # push my step-0 edges into the neighbours' rings
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        return self.plan.xlink_advance(r, self.bc, steps, model)
+
+
 class SlabSolver:
     """Sync FTCS on a G-way slab decomposition, one rank per GPU."""
 
