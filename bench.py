@@ -286,6 +286,12 @@ def run_b200(args, rank, world, local):
     async_info = None
     if world == 1 and not args.skip_async:
         async_info = run_async(args, H, torch, plan, stream, n, r, bc, glups)
+    elif world > 1 and not args.skip_async:
+        try:
+            async_info = run_async_multi(args, H, MG, torch, stream, n, r, bc, glups, rank, world,
+                                         local)
+        except Exception as exc:  # report, do not lose the sync line
+            async_info = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     # End to end through the public API with host buffers (copies timed).
     e2e = None
@@ -350,6 +356,42 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
             "delay_histogram": [int(x) for x in st.delay_histogram[:8]],
             "vs_sync": round(v / sync_glups, 4),
         }
+    return out
+
+
+def run_async_multi(args, H, MG, torch, stream, n, r, bc, sync_glups, rank, world, local):
+    """G-GPU legs over NVLink P2P (heat_plan_xlink_*): each rank runs K5 on its
+    2^30-point slab; PE boundaries between GPUs exchange edge values by P2P
+    stores into the neighbour's receive rings.  q=1 free mode is the exact
+    synchronous scheme with no collective in the loop; q=8 free-running."""
+    import torch.distributed as dist
+    per_pe = n // ASYNC_PES
+    out = {"pes_per_gpu": ASYNC_PES, "points_per_pe": per_pe,
+           "transport": "P2P stores into IPC-mapped neighbour receive rings (NVLink)"}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for name, q in (("sync_p2p", 1), ("free", 8)):
+        solver = MG.AsyncSlabSolver(n, per_pe, q, bc, local, rank, world)
+        solver.plan.fill_sine()
+        for _ in range(max(1, args.warmup)):
+            solver.advance(r, STEPS_PER_BENCH_STEP)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        st = None
+        for _ in range(args.steps):
+            st = solver.advance(r, STEPS_PER_BENCH_STEP)
+        e1.record(stream)
+        solver.plan.synchronize()
+        ms = e0.elapsed_time(e1)
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        v = float(n) * world * STEPS_PER_BENCH_STEP * args.steps / (ms * 1e-3) / 1e9
+        out[name] = {"value": round(v, 3), "unit": UNIT, "q": q,
+                     "max_delay": int(st.max_delay), "reads_per_run": int(st.reads),
+                     "vs_sync_nccl_halo": round(v / sync_glups, 4)}
+        solver.plan.close()
     return out
 
 
