@@ -132,6 +132,19 @@ int heat_async_free_run(const double* u0, size_t n, double r, int bc_kind, doubl
                         size_t per_pe, size_t q, size_t k_end, double* final_out,
                         heat_async_stats* stats);
 
+/* ---- ensembles (analysis.hpp:36-52) -------------------------------------- */
+/* ensemble_run: `runs` members of the deterministic asynchronous scheme with
+ * seeds base_seed + j (analysis.cpp:51-104), each recording l2_norm at steps
+ * 0, stride, 2*stride, ... and k_end.  Fills steps_out[S] (S via n_steps),
+ * norms[runs][S], terminals[runs][n] (may be NULL), mean_series[S] and
+ * std_series[S] (population std), bit-identical to the reference.  Uniform
+ * and fixed delay laws; N <= 4096 and (q+1)*N*8 bytes of shared memory. */
+int heat_ensemble_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                      size_t per_pe, size_t q, int law, size_t fixed_delay, size_t k_end,
+                      size_t stride, size_t runs, uint64_t base_seed, size_t* steps_out,
+                      size_t max_steps, size_t* n_steps, double* norms, double* terminals,
+                      double* mean_series, double* std_series);
+
 /* ---- executors (async_exec.hpp:53-70) ----------------------------------- */
 /* exec_run: Barriered = bit-identical to sync_run (one launch-chain on the
  * GPU, no per-step barrier); BarrierFree = free-running PEs on the GPU with

@@ -9,15 +9,17 @@
 //   heat::sync_run_f32  sync_solver.hpp:69-73   -> heat_sync_run_f32
 //   heat::async_run     async_sim.hpp:97-101    -> heat_async_run
 //   heat::exec_run      async_exec.hpp:68-70    -> heat_exec_run
+//   heat::ensemble_run  analysis.hpp:36-52      -> heat_ensemble_run
 //
-// Everything else (AsyncSimulator, ensembles, CSV, the CLI) keeps running on
-// the reference's CPU code.  oracle/Makefile target `acceptance-b200` links
+// Everything else (AsyncSimulator stepping, CSV, the CLI) keeps running on the
+// reference's CPU code.  oracle/Makefile target `acceptance-b200` links
 // the reference's acceptance suite (proj/tests/acceptance.cpp) this way.
 #include <chrono>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
 
+#include "heat/analysis.hpp"
 #include "heat/async_exec.hpp"
 #include "heat/async_sim.hpp"
 #include "heat/core.hpp"
@@ -117,6 +119,40 @@ Trajectory async_run(const TemperatureField& u0, const SolverParams& params,
         t.steps.push_back(steps[j]);
     }
     return t;
+}
+
+EnsembleResult ensemble_run(const EnsembleConfig& cfg, std::size_t runs,
+                            std::uint64_t base_seed) {
+    sync_strict();
+    if (cfg.part.total() != cfg.u0.size())  // AsyncSimulator ctor, async_sim.cpp:131-132
+        throw std::invalid_argument("AsyncSimulator: partition inconsistent with grid");
+    const std::size_t n = cfg.u0.size();
+    const std::size_t stride = cfg.stride == 0 ? detail::default_stride(n) : cfg.stride;
+    const std::size_t cap = 2 + cfg.k_end / stride;
+    std::vector<std::size_t> steps(cap);
+    std::size_t S = 0;
+    std::vector<double> norms(std::max<std::size_t>(1, runs) * cap), terms(runs * n), mean(cap),
+        stdv(cap);
+    const DelayModel& m = cfg.model;
+    const int law = m.distribution == DelayModel::Distribution::Uniform ? HEAT_DELAY_UNIFORM
+                    : m.distribution == DelayModel::Distribution::Fixed ? HEAT_DELAY_FIXED
+                                                                        : HEAT_DELAY_GEOMETRIC;
+    throw_on(heat_ensemble_run(cfg.u0.values().data(), n, cfg.params.r(), bc_kind(cfg.bc),
+                               cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(), m.q, law, m.fixed_delay,
+                               cfg.k_end, stride, runs, base_seed, steps.data(), cap, &S,
+                               norms.data(), terms.data(), mean.data(), stdv.data()));
+    EnsembleResult res;
+    res.steps.assign(steps.begin(), steps.begin() + S);
+    res.norm_series.resize(runs);
+    for (std::size_t j = 0; j < runs; ++j) {
+        res.norm_series[j].assign(norms.begin() + j * S, norms.begin() + (j + 1) * S);
+        res.terminal_fields.emplace_back(
+            std::vector<double>(terms.begin() + j * n, terms.begin() + (j + 1) * n));
+        res.seeds.push_back(base_seed + j);
+    }
+    res.mean_series.assign(mean.begin(), mean.begin() + S);
+    res.std_series.assign(stdv.begin(), stdv.begin() + S);
+    return res;
 }
 
 ExecResult exec_run(const TemperatureField& u0, const SolverParams& params,

@@ -267,6 +267,33 @@ class Ref(_Lib):
     def set_strict(self, on: bool):
         self.lib.ref_set_strict(int(on))
 
+    def ensemble_run(self, u0, r, bc, c1, c2, per_pe, law, q, fixed_d, k_end, stride, runs,
+                     base_seed):
+        """heat::ensemble_run -> (steps, norms[runs][S], terminals[runs][n], mean, std, spread2)."""
+        L = self.lib
+        if not getattr(L.ref_ensemble_run, "argtypes", None):
+            L.ref_ensemble_run.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _i, _sz, _sz, _sz, _sz,
+                                           _sz, _u64, _psz, _psz, _pd, _pd, _pd, _pd, _pd]
+        u0 = _f64(u0)
+        n = u0.size
+        s_ = stride if stride else (1 if n <= 1000 else 100)
+        cap = 2 + k_end // s_
+        steps = np.zeros(cap, np.uintp)
+        ns = C.c_size_t(0)
+        norms = np.zeros(runs * cap)
+        terms = np.zeros((runs, n))
+        mean = np.zeros(cap)
+        std = np.zeros(cap)
+        spread = np.zeros(2)
+        st = L.ref_ensemble_run(_ptr(u0), n, r, bc, c1, c2, per_pe, law, q, fixed_d, k_end, stride,
+                                runs, base_seed, _ptr(steps, _psz), C.byref(ns), _ptr(norms),
+                                _ptr(terms), _ptr(mean), _ptr(std), _ptr(spread))
+        if st:
+            raise OracleError(st, "ensemble_run")
+        S = ns.value
+        return ([int(x) for x in steps[:S]], norms[:runs * S].reshape(runs, S), terms,
+                mean[:S], std[:S], spread)
+
     def checked_r(self, alpha, dt, dx) -> float:
         r = C.c_double(0)
         st = self.lib.ref_params_checked_r(alpha, dt, dx, C.byref(r))

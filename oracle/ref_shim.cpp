@@ -17,6 +17,7 @@
 #include <thread>
 #include <vector>
 
+#include "heat/analysis.hpp"
 #include "heat/async_exec.hpp"
 #include "heat/async_sim.hpp"
 #include "heat/core.hpp"
@@ -225,5 +226,46 @@ int ref_cosine_init(std::size_t n, double* out) {
 }
 
 unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency(); }
+
+// ensemble_run (analysis.cpp:51-104): norms[runs][S], terminals[runs][n],
+// mean/std[S]; steps_out[S]; returns S through n_steps.
+int ref_ensemble_run(const double* u0, std::size_t n, double r, int bc, double c1, double c2,
+                     std::size_t per_pe, int law, std::size_t q, std::size_t fixed_d,
+                     std::size_t k_end, std::size_t stride, std::size_t runs,
+                     std::uint64_t base_seed, std::size_t* steps_out, std::size_t* n_steps,
+                     double* norms, double* terminals, double* mean, double* stdv,
+                     double* spread2) {
+    try {
+        heat::EnsembleConfig cfg{heat::TemperatureField(std::vector<double>(u0, u0 + n)),
+                                 heat::SolverParams::from_r(r, true),
+                                 make_bc(bc, c1, c2),
+                                 heat::PartitionSpec(n, per_pe),
+                                 make_model(law, q, fixed_d, 0.5, 0),
+                                 k_end,
+                                 stride};
+        heat::EnsembleResult res = heat::ensemble_run(cfg, runs, base_seed);
+        const std::size_t S = res.steps.size();
+        *n_steps = S;
+        for (std::size_t s = 0; s < S; ++s) {
+            steps_out[s] = res.steps[s];
+            mean[s] = res.mean_series[s];
+            stdv[s] = res.std_series[s];
+        }
+        for (std::size_t j = 0; j < runs; ++j) {
+            for (std::size_t s = 0; s < S; ++s) norms[j * S + s] = res.norm_series[j][s];
+            if (terminals)
+                std::memcpy(terminals + j * n, res.terminal_fields[j].values().data(),
+                            n * sizeof(double));
+        }
+        if (spread2 && runs >= 2) {
+            heat::SpreadStats sp = heat::terminal_spread(res);
+            spread2[0] = sp.std_terminal_mean_temp;
+            spread2[1] = sp.std_terminal_norm;
+        }
+        return 0;
+    } catch (...) {
+        return classify();
+    }
+}
 
 }  // extern "C"

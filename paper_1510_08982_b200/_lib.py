@@ -108,6 +108,8 @@ SIGNATURES = {
                             _pd, _pd, _psz, _sz, _psz]),
     "heat_sample_delay": (_i, [_sz, _i, _sz, _d, _u64, _u64, _sz, _psz]),
     "heat_async_free_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _pd, _P(AsyncStatsC)]),
+    "heat_ensemble_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _sz, _sz, _sz, _u64,
+                               _psz, _sz, _psz, _pd, _pd, _pd, _pd]),
     "heat_exec_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _i, _sz, _pd, _pu64,
                            _P(LagStatsC), _P(AsyncStatsC)]),
     "heat_plan_create": (_i, [_P(_vp), _sz, _i]),

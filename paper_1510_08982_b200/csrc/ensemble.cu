@@ -1,0 +1,260 @@
+// ensemble.cu -- K6: GPU ensemble driver (SURVEY.md §8f "next" #1).
+//
+// Replaces ensemble_run / run_member (analysis.cpp:16-104): M seeded members
+// of the deterministic asynchronous scheme (AsyncSimulator, async_sim.cpp:
+// 77-140) with seeds base_seed + j, each recording l2_norm (core.cpp:50-56)
+// at the recorded steps; the host then forms the mean / population-std
+// series in the reference's order (analysis.cpp:88-103).
+//
+// Mapping: one CTA per member; thread t owns points t, t+T, ...; the member's
+// history of the last q steps lives in shared memory as q+1 full-field slots
+// (the slot written at step k is never one a read at step k can ask for), and
+// the members advance with one block barrier per step.  Every cross-PE read
+// uses the delay the reference draws for it: draw number k*D + off(i, side) of
+// the member's SplitMix64 stream in counter form (any partition, n = 1 too).
+// The paper's experiments (Fig. 3/6: N = 100, one point per PE, q = 5,
+// 2e5 steps, 50-300 members) are latency-bound per member and embarrassingly
+// parallel across members -- 148 SMs run them side by side.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "async_pe.cuh"
+#include "runtime.cuh"
+
+namespace hb {
+namespace {
+
+struct EnsembleArgs {
+    const double* u0;   // prepared initial field [n]
+    int n;
+    double r, c, c1, c2;
+    int dirichlet;
+    int q;              // delays in {0..q-1}; q+1 history slots
+    int law;            // uniform or fixed
+    int fixed_d;
+    unsigned long long base_seed;
+    long long D;        // cross-PE reads per step
+    const int* offL;    // [n] draw rank of point i's left read (-1: same PE or pinned)
+    const int* offR;    // [n] ... right read
+    long long k_end;
+    long long stride;   // recording stride (norms at 0, stride, 2*stride, ..., k_end)
+    int n_rec;          // number of recorded steps
+    double* norms;      // [runs][n_rec]
+    double* terminals;  // [runs][n] (may be null)
+    unsigned int* flag; // [0] non-finite
+};
+
+__device__ __forceinline__ int draw_delay(const EnsembleArgs& a, unsigned long long seed,
+                                          long long k, int off) {
+    const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
+    if (bound == 0) return 0;
+    const uint64_t x = splitmix_draw(seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
+    if (a.law == 0) return int(bound < 65536 ? mod64_small(x, uint32_t(bound + 1))
+                                             : x % uint64_t(bound + 1));
+    return a.fixed_d < bound ? a.fixed_d : int(bound);
+}
+
+// l2_norm (core.cpp:50-56): sequential sum of squares, then sqrt -- one
+// thread, the reference's summation order.
+__device__ double seq_l2(const double* v, int n) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(v[i], v[i]));
+    return sqrt(s);
+}
+
+constexpr int kMaxPerThread = 4;
+
+__global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
+    extern __shared__ __align__(16) double hist[];  // [(q+1)][n]
+    const int n = a.n, Q = a.q + 1, T = blockDim.x, t = threadIdx.x;
+    const unsigned long long seed = a.base_seed + blockIdx.x;
+    using A = Arith<double>;
+    for (int i = t; i < n; i += T) hist[i] = a.u0[i];  // slot 0 = step 0
+    if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = 0.0;
+    __syncthreads();
+    if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = seq_l2(hist, n);
+
+    int offL[kMaxPerThread], offR[kMaxPerThread];
+#pragma unroll
+    for (int j = 0; j < kMaxPerThread; ++j) {
+        const int i = t + j * T;
+        offL[j] = i < n ? a.offL[i] : -1;
+        offR[j] = i < n ? a.offR[i] : -1;
+    }
+    long long next_rec = a.stride;
+    int rec = 1;
+    for (long long k = 0; k < a.k_end; ++k) {
+        const double* cur = hist + (k % Q) * n;
+        double* out = hist + ((k + 1) % Q) * n;
+#pragma unroll
+        for (int j = 0; j < kMaxPerThread; ++j) {
+            const int i = t + j * T;
+            if (i >= n) break;
+            double v;
+            if (a.dirichlet && (i == 0 || i == n - 1)) {
+                v = i == 0 ? a.c1 : a.c2;  // pinned, no draws (async_sim.cpp:92-95)
+            } else {
+                const int li = i == 0 ? n - 1 : i - 1;
+                const int ri = i == n - 1 ? 0 : i + 1;
+                // left before right: the draw order of async_sim.cpp:98-99
+                const double left = offL[j] < 0
+                    ? cur[li]
+                    : hist[((k - draw_delay(a, seed, k, offL[j])) % Q) * n + li];
+                const double right = offR[j] < 0
+                    ? cur[ri]
+                    : hist[((k - draw_delay(a, seed, k, offR[j])) % Q) * n + ri];
+                v = stencil_p(A::mul(a.r, right), A::mul(a.c, cur[i]), A::mul(a.r, left));
+            }
+            out[i] = v;
+        }
+        __syncthreads();
+        if (k + 1 == next_rec || (k + 1 == a.k_end && next_rec != k + 1)) {
+            if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec + rec] = seq_l2(out, n);
+            ++rec;
+            if (k + 1 == next_rec) next_rec += a.stride;
+        }
+    }
+    const double* fin = hist + (a.k_end % Q) * n;
+    bool bad = false;
+    for (int i = t; i < n; i += T) {
+        bad |= !isfinite(fin[i]);
+        if (a.terminals) a.terminals[(size_t)blockIdx.x * n + i] = fin[i];
+    }
+    if (bad) atomicOr(a.flag, 1u);
+}
+
+// In-step draw rank of every read of async_step_into (async_sim.cpp:86-101),
+// per point: ascending i, pinned ends skipped, left before right, only when
+// the neighbour lies in another PE.
+long long point_offsets(int n, int per_pe, bool dirichlet, std::vector<int>& offL,
+                        std::vector<int>& offR) {
+    offL.assign(n, -1);
+    offR.assign(n, -1);
+    long long cnt = 0;
+    for (int i = 0; i < n; ++i) {
+        if (dirichlet && (i == 0 || i == n - 1)) continue;
+        const int li = i == 0 ? n - 1 : i - 1;
+        const int ri = i == n - 1 ? 0 : i + 1;
+        if (i / per_pe != li / per_pe) offL[i] = int(cnt++);
+        if (i / per_pe != ri / per_pe) offR[i] = int(cnt++);
+    }
+    return cnt;
+}
+
+}  // namespace
+}  // namespace hb
+
+using namespace hb;
+
+extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_kind, double c1,
+                                 double c2, size_t per_pe, size_t q, int law, size_t fixed_delay,
+                                 size_t k_end, size_t stride, size_t runs, uint64_t base_seed,
+                                 size_t* steps_out, size_t max_steps, size_t* n_steps,
+                                 double* norms, double* terminals, double* mean_series,
+                                 double* std_series) {
+    // EnsembleConfig holds a TemperatureField, PartitionSpec and DelayModel
+    // (validated at construction); ensemble_run itself checks M.
+    if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u0) return fail(HEAT_EINVAL, "null field pointer");
+    if (per_pe == 0 || n % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
+    if (law == HEAT_DELAY_FIXED && fixed_delay >= q)
+        return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
+    if (law == HEAT_DELAY_GEOMETRIC)
+        return fail(HEAT_EINVAL, "GPU ensembles support the uniform and fixed laws "
+                                 "(the geometric law needs glibc log1p bits)");
+    if (law != HEAT_DELAY_UNIFORM && law != HEAT_DELAY_FIXED)
+        return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
+    if (runs == 0) return fail(HEAT_EDOMAIN, "ensemble_run: M >= 1 required");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+    if (stride == 0) stride = default_stride(n);
+    const int T = int(std::min<size_t>(1024, (n + 31) / 32 * 32));
+    if (n > size_t(T) * kMaxPerThread) return fail(HEAT_EINVAL, "GPU ensembles: N <= 4096");
+    const size_t smem = (q + 1) * n * sizeof(double);
+    if (smem > 200 * 1024) return fail(HEAT_EINVAL, "GPU ensembles: (q+1)*N*8 must fit in shared memory");
+
+    // recorded steps (analysis.cpp:56-60)
+    std::vector<size_t> steps{0};
+    for (size_t k = stride; k < k_end; k += stride) steps.push_back(k);
+    if (k_end > 0 && steps.back() != k_end) steps.push_back(k_end);
+    const size_t S = steps.size();
+    if (steps_out)
+        for (size_t s = 0; s < S && s < max_steps; ++s) steps_out[s] = steps[s];
+    if (n_steps) *n_steps = S;
+
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    std::lock_guard<std::mutex> lock(d->mu);
+    const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+    std::vector<int> offL, offR;
+    const long long D = point_offsets(int(n), int(per_pe), dir, offL, offR);
+    // device scratch: u0 | offL | offR | norms | terminals
+    auto a256 = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t o_u0 = 0, o_offL = o_u0 + a256(n * 8), o_offR = o_offL + a256(n * 4),
+                 o_norms = o_offR + a256(n * 4), o_term = o_norms + a256(runs * S * 8),
+                 total = o_term + a256(terminals ? runs * n * 8 : 8);
+    HB_TRY(ensure_scratch(*d, total));
+    char* base = static_cast<char*>(d->scratch);
+    cudaStream_t st = d->stream;
+    HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, reinterpret_cast<double*>(base + o_u0)));
+    HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), n * 4, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), n * 4, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemsetAsync(d->flag, 0, 2 * sizeof(unsigned int), st));
+
+    EnsembleArgs a{};
+    a.u0 = reinterpret_cast<const double*>(base + o_u0);
+    a.n = int(n);
+    a.r = r;
+    a.c = 1.0 - 2.0 * r;  // core.hpp:108
+    a.c1 = c1;
+    a.c2 = c2;
+    a.dirichlet = dir;
+    a.q = int(q);
+    a.law = law;
+    a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
+    a.base_seed = base_seed;
+    a.D = D;
+    a.offL = reinterpret_cast<const int*>(base + o_offL);
+    a.offR = reinterpret_cast<const int*>(base + o_offR);
+    a.k_end = (long long)k_end;
+    a.stride = (long long)stride;
+    a.n_rec = int(S);
+    a.norms = reinterpret_cast<double*>(base + o_norms);
+    a.terminals = terminals ? reinterpret_cast<double*>(base + o_term) : nullptr;
+    a.flag = d->flag;
+    if (smem > 48 * 1024)
+        HB_CUDA(cudaFuncSetAttribute(ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+    ensemble_kernel<<<unsigned(runs), T, smem, st>>>(a);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+
+    std::vector<double> hn(runs * S);
+    unsigned int flags[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(hn.data(), base + o_norms, runs * S * 8, cudaMemcpyDeviceToHost, st));
+    if (terminals)
+        HB_CUDA(cudaMemcpyAsync(terminals, base + o_term, runs * n * 8, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    if (norms) std::copy(hn.begin(), hn.end(), norms);
+    // mean / population std per recorded step, the reference's loop order
+    for (size_t s = 0; s < S; ++s) {
+        double mean = 0.0;
+        for (size_t j = 0; j < runs; ++j) mean += hn[j * S + s];
+        mean /= double(runs);
+        double var = 0.0;
+        for (size_t j = 0; j < runs; ++j) {
+            const double dd = hn[j * S + s] - mean;
+            var += dd * dd;
+        }
+        if (mean_series) mean_series[s] = mean;
+        if (std_series) std_series[s] = std::sqrt(var / double(runs));
+    }
+    return HEAT_OK;
+}

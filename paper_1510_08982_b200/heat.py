@@ -369,6 +369,94 @@ def async_free_run(u0, params: SolverParams, bc: BoundaryCondition, part: Partit
                            int(st.waits), float(st.residual_sum))
 
 
+# ---- analysis.hpp: ensembles -------------------------------------------------
+@dataclass
+class EnsembleConfig:
+    """analysis.hpp:14-23 (model.seed is ignored; members use base_seed + j)."""
+
+    u0: TemperatureField
+    params: SolverParams
+    bc: BoundaryCondition
+    part: PartitionSpec
+    model: DelayModel
+    k_end: int = 1
+    stride: int = 1
+
+
+@dataclass
+class EnsembleResult:
+    """analysis.hpp:25-32"""
+
+    steps: list
+    norm_series: list          # [run][recorded step]
+    terminal_fields: list      # [run]
+    mean_series: list
+    std_series: list
+    seeds: list
+
+
+def ensemble_run(cfg: EnsembleConfig, runs: int, base_seed: int,
+                 keep_terminals: bool = True) -> EnsembleResult:
+    """analysis.cpp:51-104 on the GPU: one CTA per member (K6, csrc/ensemble.cu)."""
+    v = _field(cfg.u0)
+    n = v.size
+    if cfg.part.total() != n:
+        raise InvalidArgument("AsyncSimulator: partition inconsistent with grid")
+    stride = cfg.stride or default_stride(n)
+    cap = 2 + cfg.k_end // stride
+    steps = np.zeros(cap, np.uintp)
+    ns = C.c_size_t(0)
+    norms = np.zeros(max(1, runs) * cap, np.float64)
+    terms = np.zeros((runs, n), np.float64) if keep_terminals and runs else None
+    mean = np.zeros(cap, np.float64)
+    std = np.zeros(cap, np.float64)
+    m = cfg.model
+    _lib.check(_lib.lib().heat_ensemble_run(
+        _lib.dptr(v), n, cfg.params.r(), cfg.bc.kind, cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(),
+        m.q, int(m.distribution), m.fixed_delay, cfg.k_end, stride, runs,
+        base_seed & 0xFFFFFFFFFFFFFFFF, _lib.szptr(steps), cap, C.byref(ns), _lib.dptr(norms),
+        _lib.dptr(terms), _lib.dptr(mean), _lib.dptr(std)), "ensemble_run")
+    S = ns.value
+    nrm = norms[:runs * S].reshape(runs, S)
+    return EnsembleResult([int(s) for s in steps[:S]], [list(map(float, row)) for row in nrm],
+                          [TemperatureField(t) for t in terms] if terms is not None else [],
+                          [float(x) for x in mean[:S]], [float(x) for x in std[:S]],
+                          [base_seed + j for j in range(runs)])
+
+
+def _population_std(xs):
+    mean = 0.0
+    for x in xs:
+        mean += x
+    mean /= float(len(xs))
+    var = 0.0
+    for x in xs:
+        var += (x - mean) * (x - mean)
+    return math.sqrt(var / float(len(xs)))
+
+
+def terminal_spread(res: EnsembleResult):
+    """analysis.cpp:122-132: (std of terminal mean temperature, std of terminal norm)."""
+    runs = len(res.terminal_fields)
+    if runs < 2:
+        raise DomainError("terminal_spread: M >= 2 required")
+    temps = [total_heat(f) / float(f.size()) for f in res.terminal_fields]
+    norms = [l2_norm(f) for f in res.terminal_fields]
+    return _population_std(temps), _population_std(norms)
+
+
+def convergence_check(traj: Trajectory, reference: TemperatureField, tol: float):
+    """analysis.cpp:106-120: first recorded step within `tol` (max-abs) of `reference`."""
+    if not (tol > 0.0):
+        raise DomainError("convergence_check: tol > 0 required")
+    for snap, k in zip(traj.snapshots, traj.steps):
+        if snap.size() != reference.size():
+            raise InvalidArgument("convergence_check: size mismatch")
+        if float(np.max(np.abs(snap.values() - reference.values()))) <= tol:
+            return k
+    return None
+
+
 # ---- async_exec.hpp ----------------------------------------------------------
 class ExecMode(enum.IntEnum):
     Barriered = _lib.EXEC_BARRIERED

@@ -88,6 +88,32 @@ def main():
                       "async_final": hexs(asy)})
     out["cases"] = cases
 
+    # --- ensembles (analysis.cpp:51-104) --------------------------------------
+    r_paper = R.checked_r(0.5, 0.01, 0.1)
+    cos100 = R.cosine_init(100)
+    ens = []
+    for (bc, c1, c2, per, law, q, fd, k, stride, runs, base) in (
+            (O.DIRICHLET, 1.0, 0.0, 1, O.UNIFORM, 5, 0, 3000, 1000, 4, 1000),
+            (O.PERIODIC, 0.0, 0.0, 10, O.FIXED, 4, 2, 2500, 700, 3, 7),
+            (O.PERIODIC, 0.0, 0.0, 1, O.UNIFORM, 3, 0, 2000, 0, 2, 42)):
+        steps, norms, terms, mean, std, spread = R.ensemble_run(
+            cos100, r_paper, bc, c1, c2, per, law, q, fd, k, stride, runs, base)
+        ens.append({"bc": bc, "c1": c1, "c2": c2, "per_pe": per, "law": law, "q": q, "d": fd,
+                    "k": k, "stride": stride, "runs": runs, "base": base, "steps": steps,
+                    "norms": [hexs(row) for row in norms],
+                    "terminal_fnv": [fnv1a64(t) for t in terms],
+                    "mean": hexs(mean), "std": hexs(std)})
+    out["ensembles"] = ens
+    # acceptance.cpp criteria 2-3 (M=50, N=100, one point per PE, q=5, 2e5 steps)
+    crit = {}
+    for name, bc, c1, c2 in (("dirichlet", O.DIRICHLET, 1.0, 0.0), ("periodic", O.PERIODIC, 0.0, 0.0)):
+        steps, norms, terms, mean, std, spread = R.ensemble_run(
+            cos100, r_paper, bc, c1, c2, 1, O.UNIFORM, 5, 0, 200000, 200000, 50, 1000)
+        crit[name] = {"terminal_fnv": [fnv1a64(t) for t in terms],
+                      "spread_mean_temp": float(spread[0]).hex(),
+                      "spread_norm": float(spread[1]).hex(), "mean": hexs(mean)}
+    out["acceptance_ensembles"] = crit
+
     # --- KATs of test_sync.cpp ------------------------------------------------
     out["kat_sync_step_dirichlet"] = hexs(R.sync_step([1.0, 0.0, 0.0], 0.5, O.DIRICHLET, 1.0, 0.0))
     out["kat_sync_step_periodic"] = hexs(R.sync_step([2.0, 0.0, 1.0], 0.25, O.PERIODIC))

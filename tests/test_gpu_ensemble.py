@@ -1,0 +1,92 @@
+"""GPU ensembles (K6, csrc/ensemble.cu) against the reference's ensemble_run
+(analysis.cpp:51-104): fixtures produced by the reference itself
+(tests/golden/golden.json) -- bit-exact norms, terminal fields, mean and std
+series -- plus the paper's experiment as acceptance.cpp criteria 2-3 run it
+(50 members, N = 100, one point per PE, q = 5, 2e5 steps)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal, fnv1a64
+
+pytestmark = pytest.mark.gpu
+
+G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+
+
+def unhex(v):
+    return np.array([float.fromhex(x) for x in v], np.float64)
+
+
+@pytest.fixture(scope="module")
+def H(gpu):
+    from paper_1510_08982_b200 import heat
+    return heat
+
+
+def _cfg(H, port, e):
+    u0 = port.cosine_init(100)
+    p = H.SolverParams.checked(0.5, 0.01, 0.1)
+    bc = H.BoundaryCondition.periodic() if e["bc"] else H.BoundaryCondition.dirichlet(e["c1"],
+                                                                                       e["c2"])
+    model = H.DelayModel(e["q"], H.Distribution(e["law"]), e["d"], 0.5, 0)
+    return H.EnsembleConfig(H.TemperatureField(u0), p, bc, H.PartitionSpec(100, e["per_pe"]),
+                            model, e["k"], e["stride"])
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2])
+def test_ensemble_matches_reference_fixture(H, port, idx):
+    e = G["ensembles"][idx]
+    res = H.ensemble_run(_cfg(H, port, e), e["runs"], e["base"])
+    assert res.steps == e["steps"]
+    for j in range(e["runs"]):
+        assert bits_equal(np.array(res.norm_series[j]), unhex(e["norms"][j])), j
+        assert fnv1a64(res.terminal_fields[j].values()) == e["terminal_fnv"][j]
+    assert bits_equal(np.array(res.mean_series), unhex(e["mean"]))
+    assert bits_equal(np.array(res.std_series), unhex(e["std"]))
+
+
+def test_ensemble_member_is_async_run(H, port):
+    # member j is async_run with seed base + j (analysis.cpp:16-38)
+    e = G["ensembles"][0]
+    res = H.ensemble_run(_cfg(H, port, e), 2, 555)
+    u0 = port.cosine_init(100)
+    r = H.SolverParams.checked(0.5, 0.01, 0.1).r()
+    for j in range(2):
+        fin = port.async_run(u0, r, 0, 1.0, 0.0, 1, 0, 5, seed=555 + j, k_end=e["k"])
+        assert bits_equal(res.terminal_fields[j].values(), fin)
+
+
+def test_paper_ensembles_acceptance_criteria_2_3(H, port):
+    # acceptance.cpp:103-137: Dirichlet members all reach the linear steady
+    # state (<= 1e-4); the periodic terminal mean temperature spreads (> 10x)
+    crit = G["acceptance_ensembles"]
+    out = {}
+    for name, bc in (("dirichlet", H.BoundaryCondition.dirichlet(1.0, 0.0)),
+                     ("periodic", H.BoundaryCondition.periodic())):
+        cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.checked(0.5, 0.01, 0.1), bc,
+                               H.PartitionSpec(100, 1), H.DelayModel.uniform(5, 0), 200000,
+                               200000)
+        res = H.ensemble_run(cfg, 50, 1000)
+        assert [fnv1a64(t.values()) for t in res.terminal_fields] == crit[name]["terminal_fnv"]
+        sm, sn = H.terminal_spread(res)
+        assert sm == float.fromhex(crit[name]["spread_mean_temp"])
+        assert sn == float.fromhex(crit[name]["spread_norm"])
+        out[name] = (res, sm)
+    steady = H.linear_steady_state(100, 1.0, 0.0).values()
+    worst = max(np.max(np.abs(f.values() - steady)) for f in out["dirichlet"][0].terminal_fields)
+    assert worst <= 1e-4
+    assert out["periodic"][1] > 1e-6 and out["periodic"][1] > 10 * out["dirichlet"][1]
+
+
+def test_ensemble_validation(H):
+    cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.from_r(0.5),
+                           H.BoundaryCondition.dirichlet(1, 0), H.PartitionSpec(100, 1),
+                           H.DelayModel.uniform(5, 0), 10, 10)
+    with pytest.raises(H.DomainError):
+        H.ensemble_run(cfg, 0, 1)
+    cfg.model = H.DelayModel.geometric(5, 0.5, 0)
+    with pytest.raises(H.InvalidArgument):
+        H.ensemble_run(cfg, 2, 1)
