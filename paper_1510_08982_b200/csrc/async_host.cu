@@ -193,6 +193,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     a.law = s.law;
     a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
     a.seed = s.seed;
+    a.modq = make_modq(unsigned(q));
     a.D = D;
     a.off_left = reinterpret_cast<const int*>(base + o_offL);
     a.off_right = reinterpret_cast<const int*>(base + o_offR);

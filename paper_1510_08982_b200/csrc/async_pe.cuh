@@ -50,6 +50,7 @@ struct AsyncPeArgs {
     int law;           // HEAT_DELAY_*
     int fixed_d;
     unsigned long long seed;
+    ModQ modq;              // x mod q (uniform law, steps k >= q-1)
     long long D;            // cross-PE reads (draws) per step
     const int* off_left;    // [P] in-step draw rank of the first point's left read, -1 none
     const int* off_right;   // [P] ... of the last point's right read, -1 none
@@ -102,26 +103,13 @@ struct RingOps<true> {
 };
 
 // Delay of the draw with in-step rank `off` at step k (async_sim.cpp:57-73).
-// x mod m for a 64-bit x and m <= 65536 with 32-bit divisions only (exact:
-// x = hi*2^32 + lo, and every intermediate stays below 2^32).  The generic
-// 64-bit remainder is a long software routine on the latency-critical path.
-__device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t m) {
-    if (m == 1) return 0;
-    const uint32_t hi = uint32_t(x >> 32), lo = uint32_t(x);
-    const uint32_t two32 = (0xFFFFFFFFu % m + 1u) % m;      // 2^32 mod m
-    const uint32_t a = (hi % m) * two32;                    // < m^2 <= 2^32
-    return ((a % m) + (lo % m)) % m;
-}
 
 __device__ __forceinline__ int det_delay(const AsyncPeArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
     if (bound == 0) return 0;  // every law yields 0 (the draw is still "consumed" by index)
     if (a.law == 2) return a.dtable[k * a.D + off];  // host-drawn, already bounded
     const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
-    if (a.law == 0) {
-        if (bound < 65536) return int(mod64_small(x, uint32_t(bound + 1)));
-        return int(x % uint64_t(bound + 1));
-    }
+    if (a.law == 0) return uniform_delay(x, bound, a.modq);
     return a.fixed_d < bound ? a.fixed_d : int(bound);
 }
 

@@ -72,6 +72,7 @@ struct AsyncStreamArgs {
     int q, R;
     int law, fixed_d;
     unsigned long long seed;
+    ModQ modq;
     long long D;
     const int* off_left;
     const int* off_right;
@@ -91,7 +92,7 @@ __device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
     if (a.law == 2) return a.dtable[k * a.D + off];
     const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
-    if (a.law == 0) return int(x % uint64_t(bound + 1));
+    if (a.law == 0) return uniform_delay(x, bound, a.modq);
     return a.fixed_d < bound ? a.fixed_d : int(bound);
 }
 

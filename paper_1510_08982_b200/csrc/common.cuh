@@ -47,6 +47,30 @@ __host__ __device__ __forceinline__ uint64_t splitmix_draw(uint64_t seed, uint64
     return splitmix_mix(seed + (j + 1) * 0x9e3779b97f4a7c15ULL);
 }
 
+// x mod m for a 32-bit m fixed per run (the uniform law's steady-state
+// modulus q).  With t = 2^32 mod m, x = hi*2^32 + lo ≡ v = hi*t + lo < 2^64,
+// and floor(v * floor((2^64-1)/m) / 2^64) is v's quotient or one less
+// (the error is below v/2^64 < 1), so one conditional subtract finishes.
+// Replaces a chain of variable 32-bit divisions on every cross-PE read.
+struct ModQ {
+    unsigned long long M;
+    unsigned int m, t;
+};
+__host__ __device__ inline ModQ make_modq(unsigned int m) {
+    return ModQ{~0ull / m, m, static_cast<unsigned int>((1ull << 32) % m)};
+}
+__device__ __forceinline__ unsigned int modq(uint64_t x, const ModQ& f) {
+    const uint64_t v = uint64_t(uint32_t(x >> 32)) * f.t + uint32_t(x);
+    const uint64_t r = v - __umul64hi(v, f.M) * f.m;
+    return uint32_t(r >= f.m ? r - f.m : r);
+}
+// Uniform-law delay x mod (bound + 1), bound = min(k, q-1)
+// (async_sim.cpp:57-73): the fast path for every step k >= q-1.
+__device__ __forceinline__ int uniform_delay(uint64_t x, long long bound, const ModQ& fq) {
+    if (bound + 1 == (long long)fq.m) return int(modq(x, fq));
+    return int(x % uint64_t(bound + 1));  // the first q-1 steps only
+}
+
 // ---- shared-memory / async-proxy PTX wrappers -----------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -34,6 +34,7 @@ struct EnsembleArgs {
     int law;            // uniform or fixed
     int fixed_d;
     unsigned long long base_seed;
+    ModQ modq;          // x mod q (uniform law, steps k >= q-1)
     long long D;        // cross-PE reads per step
     const int* offL;    // [n] draw rank of point i's left read (-1: same PE or pinned)
     const int* offR;    // [n] ... right read
@@ -45,16 +46,6 @@ struct EnsembleArgs {
     unsigned int* flag; // [0] non-finite
 };
 
-__device__ __forceinline__ int draw_delay(const EnsembleArgs& a, unsigned long long seed,
-                                          long long k, int off) {
-    const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
-    if (bound == 0) return 0;
-    const uint64_t x = splitmix_draw(seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
-    if (a.law == 0) return int(bound < 65536 ? mod64_small(x, uint32_t(bound + 1))
-                                             : x % uint64_t(bound + 1));
-    return a.fixed_d < bound ? a.fixed_d : int(bound);
-}
-
 // l2_norm (core.cpp:50-56): sequential sum of squares, then sqrt -- one
 // thread, the reference's summation order.
 __device__ double seq_l2(const double* v, int n) {
@@ -63,65 +54,139 @@ __device__ double seq_l2(const double* v, int n) {
     return sqrt(s);
 }
 
-constexpr int kMaxPerThread = 4;
+constexpr unsigned long long kGamma = 0x9e3779b97f4a7c15ULL;  // rng.hpp:21
 
+// PT points per thread (t, t+T, ...); LAW 0 uniform, 1 fixed.  The member is
+// latency-bound (one warp per scheduler), so the step is written for a short
+// dependent chain: per-point constants hoisted, SplitMix64 counters carried
+// incrementally (draw k*D + off of the member's stream is mix(z) with
+// z = seed + (k*D + off + 1)*gamma, advanced by D*gamma per step), the next
+// step's delays drawn before the barrier, and the steady state (k >= q-1:
+// bound = q-1, modulus q) free of branches.
+template <int PT, int LAW>
 __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
     extern __shared__ __align__(16) double hist[];  // [(q+1)][n]
-    const int n = a.n, Q = a.q + 1, T = blockDim.x, t = threadIdx.x;
+    const int n = a.n, q = a.q, Q = a.q + 1, T = blockDim.x, t = threadIdx.x;
     const unsigned long long seed = a.base_seed + blockIdx.x;
     using A = Arith<double>;
     for (int i = t; i < n; i += T) hist[i] = a.u0[i];  // slot 0 = step 0
-    if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = 0.0;
     __syncthreads();
     if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = seq_l2(hist, n);
 
-    int offL[kMaxPerThread], offR[kMaxPerThread];
+    int ci[PT], li[PT], ri[PT], offL[PT], offR[PT], dL[PT], dR[PT];
+    bool live[PT], pin[PT];
+    double pinv[PT];
+    unsigned long long zL[PT], zR[PT];
+    const unsigned long long zstep = (unsigned long long)a.D * kGamma;
 #pragma unroll
-    for (int j = 0; j < kMaxPerThread; ++j) {
+    for (int j = 0; j < PT; ++j) {
         const int i = t + j * T;
-        offL[j] = i < n ? a.offL[i] : -1;
-        offR[j] = i < n ? a.offR[i] : -1;
+        live[j] = i < n;
+        ci[j] = live[j] ? i : 0;
+        // pinned ends take no draws (async_sim.cpp:92-95)
+        pin[j] = a.dirichlet && (ci[j] == 0 || ci[j] == n - 1);
+        pinv[j] = ci[j] == 0 ? a.c1 : a.c2;
+        li[j] = ci[j] == 0 ? n - 1 : ci[j] - 1;
+        ri[j] = ci[j] == n - 1 ? 0 : ci[j] + 1;
+        offL[j] = live[j] ? a.offL[ci[j]] : -1;
+        offR[j] = live[j] ? a.offR[ci[j]] : -1;
+        zL[j] = seed + ((unsigned long long)(offL[j] < 0 ? 0 : offL[j]) + 1) * kGamma;
+        zR[j] = seed + ((unsigned long long)(offR[j] < 0 ? 0 : offR[j]) + 1) * kGamma;
     }
+    // delays of step kk for any kk (bound = min(kk, q-1)); advances z to kk+1
+    auto draw_generic = [&](long long kk) {
+        const long long bound = kk < q - 1 ? kk : q - 1;
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            if (LAW == 0) {
+                dL[j] = offL[j] < 0 || bound == 0
+                            ? 0 : int(splitmix_mix(zL[j]) % (unsigned long long)(bound + 1));
+                dR[j] = offR[j] < 0 || bound == 0
+                            ? 0 : int(splitmix_mix(zR[j]) % (unsigned long long)(bound + 1));
+            } else {
+                const int d = a.fixed_d < bound ? a.fixed_d : int(bound);
+                dL[j] = offL[j] < 0 ? 0 : d;
+                dR[j] = offR[j] < 0 ? 0 : d;
+            }
+            zL[j] += zstep;
+            zR[j] += zstep;
+        }
+    };
+    // delays of a step kk >= q-1 (modulus q; a fixed d < q is never clamped)
+    auto draw_steady = [&]() {
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+            if (LAW == 0) {
+                const int xl = int(modq(splitmix_mix(zL[j]), a.modq));
+                const int xr = int(modq(splitmix_mix(zR[j]), a.modq));
+                dL[j] = offL[j] < 0 ? 0 : xl;
+                dR[j] = offR[j] < 0 ? 0 : xr;
+                zL[j] += zstep;
+                zR[j] += zstep;
+            } else {
+                dL[j] = offL[j] < 0 ? 0 : a.fixed_d;
+                dR[j] = offR[j] < 0 ? 0 : a.fixed_d;
+            }
+        }
+    };
+    int slot = 0;  // k mod Q, a wrapped counter
     long long next_rec = a.stride;
     int rec = 1;
-    for (long long k = 0; k < a.k_end; ++k) {
-        const double* cur = hist + (k % Q) * n;
-        double* out = hist + ((k + 1) % Q) * n;
+    // step k: read slots of steps k-d, write slot k+1; left before right is
+    // the reference's draw order (async_sim.cpp:98-99), encoded in off*
+    auto compute = [&](int nslot) {
+        const double* cur = hist + slot * n;
+        double* out = hist + nslot * n;
 #pragma unroll
-        for (int j = 0; j < kMaxPerThread; ++j) {
-            const int i = t + j * T;
-            if (i >= n) break;
-            double v;
-            if (a.dirichlet && (i == 0 || i == n - 1)) {
-                v = i == 0 ? a.c1 : a.c2;  // pinned, no draws (async_sim.cpp:92-95)
-            } else {
-                const int li = i == 0 ? n - 1 : i - 1;
-                const int ri = i == n - 1 ? 0 : i + 1;
-                // left before right: the draw order of async_sim.cpp:98-99
-                const double left = offL[j] < 0
-                    ? cur[li]
-                    : hist[((k - draw_delay(a, seed, k, offL[j])) % Q) * n + li];
-                const double right = offR[j] < 0
-                    ? cur[ri]
-                    : hist[((k - draw_delay(a, seed, k, offR[j])) % Q) * n + ri];
-                v = stencil_p(A::mul(a.r, right), A::mul(a.c, cur[i]), A::mul(a.r, left));
-            }
-            out[i] = v;
+        for (int j = 0; j < PT; ++j) {
+            const int sl = slot - dL[j] < 0 ? slot - dL[j] + Q : slot - dL[j];
+            const int sr = slot - dR[j] < 0 ? slot - dR[j] + Q : slot - dR[j];
+            const double left = hist[sl * n + li[j]];
+            const double right = hist[sr * n + ri[j]];
+            const double v = stencil_p(A::mul(a.r, right), A::mul(a.c, cur[ci[j]]), A::mul(a.r, left));
+            if (live[j]) out[ci[j]] = pin[j] ? pinv[j] : v;
         }
+    };
+    auto finish = [&](long long k, int nslot) {
+        slot = nslot;
         __syncthreads();
         if (k + 1 == next_rec || (k + 1 == a.k_end && next_rec != k + 1)) {
-            if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec + rec] = seq_l2(out, n);
+            if (t == 0 && a.norms)
+                a.norms[(size_t)blockIdx.x * a.n_rec + rec] = seq_l2(hist + slot * n, n);
             ++rec;
             if (k + 1 == next_rec) next_rec += a.stride;
         }
+    };
+    draw_generic(0);
+    long long k = 0;
+    const long long k_gen = a.k_end < (long long)q - 2 ? a.k_end : (long long)(q > 2 ? q - 2 : 0);
+    for (; k < k_gen; ++k) {  // the next step still has bound < q-1
+        const int nslot = slot + 1 == Q ? 0 : slot + 1;
+        compute(nslot);
+        draw_generic(k + 1);
+        finish(k, nslot);
     }
-    const double* fin = hist + (a.k_end % Q) * n;
+    for (; k < a.k_end; ++k) {
+        const int nslot = slot + 1 == Q ? 0 : slot + 1;
+        compute(nslot);
+        draw_steady();  // next step's delays overlap this step's loads and the barrier
+        finish(k, nslot);
+    }
+    const double* fin = hist + slot * n;  // slot == k_end mod Q
     bool bad = false;
     for (int i = t; i < n; i += T) {
         bad |= !isfinite(fin[i]);
         if (a.terminals) a.terminals[(size_t)blockIdx.x * n + i] = fin[i];
     }
     if (bad) atomicOr(a.flag, 1u);
+}
+
+using EnsembleKernel = void (*)(const EnsembleArgs);
+EnsembleKernel pick_kernel(int pt, int law) {
+    const EnsembleKernel k[3][2] = {{ensemble_kernel<1, 0>, ensemble_kernel<1, 1>},
+                                    {ensemble_kernel<2, 0>, ensemble_kernel<2, 1>},
+                                    {ensemble_kernel<4, 0>, ensemble_kernel<4, 1>}};
+    return k[pt == 1 ? 0 : pt == 2 ? 1 : 2][law == HEAT_DELAY_UNIFORM ? 0 : 1];
 }
 
 // In-step draw rank of every read of async_step_into (async_sim.cpp:86-101),
@@ -170,8 +235,10 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     if (stride == 0) stride = default_stride(n);
-    const int T = int(std::min<size_t>(1024, (n + 31) / 32 * 32));
-    if (n > size_t(T) * kMaxPerThread) return fail(HEAT_EINVAL, "GPU ensembles: N <= 4096");
+    constexpr size_t kMaxPoints = 4096;
+    if (n > kMaxPoints) return fail(HEAT_EINVAL, "GPU ensembles: N <= 4096");
+    const int PT = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
+    const int T = int(((n + PT - 1) / PT + 31) / 32 * 32);
     const size_t smem = (q + 1) * n * sizeof(double);
     if (smem > 200 * 1024) return fail(HEAT_EINVAL, "GPU ensembles: (q+1)*N*8 must fit in shared memory");
 
@@ -215,6 +282,7 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     a.law = law;
     a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
     a.base_seed = base_seed;
+    a.modq = make_modq(unsigned(q));
     a.D = D;
     a.offL = reinterpret_cast<const int*>(base + o_offL);
     a.offR = reinterpret_cast<const int*>(base + o_offR);
@@ -224,10 +292,10 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     a.norms = reinterpret_cast<double*>(base + o_norms);
     a.terminals = terminals ? reinterpret_cast<double*>(base + o_term) : nullptr;
     a.flag = d->flag;
+    const EnsembleKernel kern = pick_kernel(PT, law);
     if (smem > 48 * 1024)
-        HB_CUDA(cudaFuncSetAttribute(ensemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem)));
-    ensemble_kernel<<<unsigned(runs), T, smem, st>>>(a);
+        HB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<unsigned(runs), T, smem, st>>>(a);
     HB_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 

@@ -284,6 +284,7 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.law = s.law;
     a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
     a.seed = s.seed;
+    a.modq = make_modq(unsigned(s.q));
     a.D = L.D;
     a.off_left = at<const int>(base, L.o_offL);
     a.off_right = at<const int>(base, L.o_offR);
