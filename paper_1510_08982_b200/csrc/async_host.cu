@@ -200,7 +200,8 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     a.dtable = reinterpret_cast<const unsigned char*>(base + o_dtab);
     a.ring = reinterpret_cast<double*>(base + o_ring);
     a.prog = reinterpret_cast<unsigned long long*>(base + o_prog);
-    a.stats = reinterpret_cast<unsigned long long*>(base + o_stats);
+    // statistics only when asked for: they sit on the latency-critical step
+    a.stats = host_stats ? reinterpret_cast<unsigned long long*>(base + o_stats) : nullptr;
     a.edge_log = s.want_logs ? reinterpret_cast<double*>(base + o_elog) : nullptr;
     a.used_log = s.want_logs ? reinterpret_cast<int*>(base + o_ulog) : nullptr;
     a.flag = d.flag;

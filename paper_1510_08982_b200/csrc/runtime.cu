@@ -46,6 +46,8 @@ int dev_ctx(int device, DevCtx** out) {
                                              " is not sm_100 (Blackwell); this build targets sm_100a only");
             d->sms = prop.multiProcessorCount;
             HB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+            HB_CUDA(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
+            HB_CUDA(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
             HB_CUDA(cudaMalloc(&d->flag, 4 * sizeof(unsigned int)));
             d->device = device;
         }

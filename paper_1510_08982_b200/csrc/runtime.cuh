@@ -68,6 +68,7 @@ struct DevCtx {
     int device = -1;
     int sms = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the streamed sync_run
     void* buf[2] = {nullptr, nullptr};
     size_t bytes = 0;
     unsigned int* flag = nullptr;  // [0] non-finite, [1] watchdog timeout

@@ -108,57 +108,87 @@ int sync_advance(int sms, Real* bufs[2], int& cur, long long n, double r, int pe
     return sync_advance_slab<Real>(sms, bufs, cur, g, r, c1, c2, steps, flag, st);
 }
 
+// One K1 configuration (array, pins, coefficients, tensor maps of both
+// ping-pong buffers) from which passes over any output range are launched.
+template <typename Real>
+struct SyncLauncher {
+    using T = SyncTB<Real, kV>;
+    SyncVariant* var = nullptr;
+    int sms = 0;
+    Real* bufs[2] = {nullptr, nullptr};
+    CUtensorMap load_map[2], store_map[2];
+    SyncPassArgs a{};
+
+    int init(int sms_, Real* b[2], const SlabGeom& g, double r, double c1, double c2,
+             unsigned int* flag) {
+        HB_TRY(sync_variant<Real>(&var));
+        sms = sms_;
+        bufs[0] = b[0];
+        bufs[1] = b[1];
+        a.len = g.len;
+        a.pin_lo = g.pin_lo;
+        a.pin_hi = g.pin_hi;
+        a.wrap = g.wrap;
+        a.r = r;
+        if (sizeof(Real) == 8) {
+            a.c = 1.0 - 2.0 * r;  // core.hpp:108: Real(1) - Real(2)*r, one rounding
+        } else {
+            const float rf = float(r);
+            a.c = double(1.0f - 2.0f * rf);
+        }
+        a.c1 = c1;
+        a.c2 = c2;
+        a.nonfinite = flag;
+        a.nchunks = g.len / kV;
+        // tensor maps: [chunk][row][16 doubles] views of both ping-pong arrays,
+        // 32-chunk boxes for window loads, 30-chunk boxes for output stores
+        for (int i = 0; i < 2; ++i) {
+            HB_TRY((make_chunk_map<Real, kV>(&load_map[i], bufs[i], a.nchunks, kWarp)));
+            HB_TRY((make_chunk_map<Real, kV>(&store_map[i], bufs[i], a.nchunks, kWarp - 2)));
+        }
+        return HEAT_OK;
+    }
+
+    // Advance outputs [out_lo, out_hi) by nsteps (<= V): reads bufs[src],
+    // writes bufs[src ^ 1].
+    int pass(int src, long long out_lo, long long out_hi, int nsteps, bool check,
+             cudaStream_t st) {
+        if (out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
+        if (out_hi <= out_lo) return HEAT_OK;
+        const long long tiles = (out_hi - out_lo + T::kOut - 1) / T::kOut;
+        const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
+        const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
+        SyncPassArgs p = a;
+        p.out_lo = out_lo;
+        p.out_hi = out_hi;
+        p.tiles = tiles;
+        p.src = bufs[src];
+        p.dst = bufs[src ^ 1];
+        p.nsteps = nsteps;
+        p.check_finite = check;
+        var->fn<<<grid, T::kThreads, T::smem_bytes(var->nbuf), st>>>(load_map[src],
+                                                                      store_map[src ^ 1], p);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return HEAT_OK;
+    }
+};
+
 template <typename Real>
 int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,
                       double c2, size_t steps, unsigned int* flag, cudaStream_t st,
                       int max_steps_per_pass) {
     using T = SyncTB<Real, kV>;
     if (steps == 0) return HEAT_OK;
-    SyncVariant* var = nullptr;
-    HB_TRY(sync_variant<Real>(&var));
-    const int occ = var->blocks_per_sm;
-    const long long tiles = (g.out_hi - g.out_lo + T::kOut - 1) / T::kOut;
-    const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
-    const int grid = int(std::min<long long>(want, (long long)sms * occ));
-    SyncPassArgs a{};
-    a.len = g.len;
-    a.out_lo = g.out_lo;
-    a.out_hi = g.out_hi;
-    a.pin_lo = g.pin_lo;
-    a.pin_hi = g.pin_hi;
-    a.wrap = g.wrap;
-    a.tiles = tiles;
-    a.r = r;
-    if (sizeof(Real) == 8) {
-        a.c = 1.0 - 2.0 * r;  // core.hpp:108: Real(1) - Real(2)*r, one rounding
-    } else {
-        const float rf = float(r);
-        a.c = double(1.0f - 2.0f * rf);
-    }
-    a.c1 = c1;
-    a.c2 = c2;
-    a.nonfinite = flag;
     if (g.out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
-    a.nchunks = g.len / kV;
-    // tensor maps: [chunk][row][16 doubles] views of both ping-pong arrays,
-    // 32-chunk boxes for window loads, 30-chunk boxes for output stores
-    CUtensorMap load_map[2], store_map[2];
-    for (int b = 0; b < 2; ++b) {
-        HB_TRY((make_chunk_map<Real, kV>(&load_map[b], bufs[b], a.nchunks, kWarp)));
-        HB_TRY((make_chunk_map<Real, kV>(&store_map[b], bufs[b], a.nchunks, kWarp - 2)));
-    }
+    SyncLauncher<Real> L;
+    HB_TRY(L.init(sms, bufs, g, r, c1, c2, flag));
     const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, T::kMaxSteps)
                                            : T::kMaxSteps;
     while (steps > 0) {
         const int s = int(std::min<size_t>(steps, size_t(cap)));
-        a.src = bufs[cur];
-        a.dst = bufs[cur ^ 1];
-        a.nsteps = s;
-        a.check_finite = size_t(s) == steps;  // last pass of this advance
-        var->fn<<<grid, T::kThreads, T::smem_bytes(var->nbuf), st>>>(load_map[cur],
-                                                                      store_map[cur ^ 1], a);
-        HB_CUDA(cudaGetLastError());
-        g_launches.fetch_add(1, std::memory_order_relaxed);
+        // finite check on the last pass of this advance only
+        HB_TRY(L.pass(cur, g.out_lo, g.out_hi, s, size_t(s) == steps, st));
         cur ^= 1;
         steps -= size_t(s);
     }
@@ -225,6 +255,150 @@ int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c
 
 namespace {
 
+// Validation + Dirichlet snap of one uploaded chunk [lo, hi) of the streamed
+// sync_run: flag[2] |= 1 on a non-finite value (core.hpp:45-51), then the
+// ends take c1 / c2 exactly (prepare_initial, sync_solver.cpp:25-37).
+__global__ void prep_chunk_kernel(double* __restrict__ u, long long lo, long long hi, long long n,
+                                  double c1, double c2, unsigned int* flag) {
+    bool bad = false;
+    for (long long i = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < hi;
+         i += (long long)gridDim.x * blockDim.x) {
+        bad |= !isfinite(u[i]);
+        if (i == 0) u[0] = c1;
+        if (i == n - 1) u[n - 1] = c2;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag + 2, 1u);
+}
+
+constexpr size_t kStreamMinPoints = size_t(1) << 24;  // below: copies are cheap, one shot
+constexpr int kStreamChunks = 16;
+constexpr size_t kStreamMaxPasses = 128;              // above: copies are a small share
+
+// Streamed sync_run (large Dirichlet fields, final state only): the field is
+// uploaded in C chunks on one copy stream, advanced chunk by chunk on the
+// compute stream, and downloaded chunk by chunk on a second copy stream, so
+// the 2 x 8N bytes of PCIe traffic overlap the temporal-blocked passes.
+//
+// Pass pi of chunk c advances outputs R(pi, c) = [c*cp - (pi+1)*32,
+// (c+1)*cp - (pi+1)*32) (first range from 0, last to n): shifting each
+// pass's ranges by 32 points -- the reach of one pass of <= 32 steps --
+// makes every input of R(pi, c) an output of passes already issued for
+// chunks <= c, and chunk c's first pass needs only uploaded chunks <= c.
+// Issued in chunk-major order on one stream, no launch overwrites values a
+// later launch still reads: the pass-(pi+2) write of chunk c ends exactly
+// where the pass-(pi+1) read of chunk c+1 begins.  Window reads beyond a
+// range's last output are stale values that cannot reach an exact output
+// within one pass.  The per-range kernels are the same K1 passes as the
+// one-shot path, so results are bit-identical.
+int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1, double c2,
+                      size_t k_end, double* final_out) {
+    using T = SyncTB<double, kV>;
+    const long long N = (long long)n;
+    const long long S = (long long)((k_end + T::kMaxSteps - 1) / T::kMaxSteps);  // passes
+    const long long shift = T::kMaxSteps;
+    const size_t pitch = (n + 63) / 64 * 64;
+    HB_TRY(ensure_buffers(d, 2 * pitch * sizeof(double)));
+    double* bufs[2] = {static_cast<double*>(d.buf[0]), static_cast<double*>(d.buf[0]) + pitch};
+    cudaStream_t st = d.stream;
+    SlabGeom g;
+    g.len = N;
+    g.out_lo = 0;
+    g.out_hi = N;
+    g.pin_lo = 0;
+    g.pin_hi = N - 1;
+    SyncLauncher<double> L;
+    HB_TRY(L.init(d.sms, bufs, g, r, c1, c2, d.flag));
+    // Chunk boundaries.  A "wave" is one tile per resident warp; chunks of
+    // whole waves keep every launch free of a ragged last wave.  Large fields
+    // get graded chunks (4, 6, 10, 16, 26, 41 waves, <= 64-wave middle, the
+    // head mirrored at the end): the first pass starts after a short upload
+    // and the last download is short, while neighbouring chunks differ by
+    // less than the compute/copy time ratio (~1.8), so neither the compute
+    // nor the download stream starves.  Smaller fields: 16 equal chunks.
+    const long long wave = (long long)d.sms * L.var->blocks_per_sm * T::kWarpsPerCta * T::kOut;
+    std::vector<long long> B{0};
+    if (N >= 128 * wave) {
+        std::vector<long long> head;
+        long long rem = N;
+        for (long long w = 4; w < 64 && rem > 8 * w * wave; w = (w * 8 + 4) / 5) {
+            head.push_back(w * wave);
+            rem -= 2 * w * wave;
+        }
+        for (long long h : head) B.push_back(B.back() + h);
+        const long long m = (rem + 64 * wave - 1) / (64 * wave);
+        const long long each = (rem / m) / wave * wave;  // whole waves; the last absorbs the rest
+        for (long long j = 0; j + 1 < m; ++j) B.push_back(B.back() + each);
+        long long tail = 0;
+        for (long long h : head) tail += h;
+        B.push_back((N - tail) / kV * kV);  // chunk starts stay 32-aligned
+        for (size_t j = head.size(); j-- > 1;) B.push_back(B.back() + head[j]);
+        B.push_back(N);                     // the last chunk absorbs N mod 32
+    } else {
+        const long long cp = ((N + kStreamChunks - 1) / kStreamChunks + kV - 1) / kV * kV;
+        for (long long b = cp; b < N; b += cp) B.push_back(b);
+        B.push_back(N);
+    }
+    const int C = int(B.size()) - 1;
+    for (int c = 0; c < C; ++c)
+        if (B[c + 1] - B[c] <= (S + 1) * shift || B[c] % kV)
+            return fail(HEAT_ELOGIC, "streamed sync_run: chunk plan violates the shift bound");
+    auto lo = [&](int c, long long pi) { return c == 0 ? 0 : B[c] - (pi + 1) * shift; };
+    auto hi = [&](int c, long long pi) { return c == C - 1 ? N : B[c + 1] - (pi + 1) * shift; };
+
+    std::vector<cudaEvent_t> ev(2 * C + 1, nullptr);  // up[c], done[c], ready
+    struct Cleanup {
+        std::vector<cudaEvent_t>& e;
+        ~Cleanup() {
+            for (auto x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } cleanup{ev};
+    for (auto& e : ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    cudaEvent_t* up = ev.data();
+    cudaEvent_t* done = ev.data() + C;
+
+    // the flag reset on the compute stream precedes every upload
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
+    HB_CUDA(cudaEventRecord(ev[2 * C], st));
+    HB_CUDA(cudaStreamWaitEvent(d.h2d, ev[2 * C], 0));
+    for (int c = 0; c < C; ++c) {
+        const long long a0 = B[c], a1 = B[c + 1];
+        HB_CUDA(cudaMemcpyAsync(bufs[0] + a0, u0 + a0, (a1 - a0) * sizeof(double),
+                                cudaMemcpyHostToDevice, d.h2d));
+        HB_CUDA(cudaEventRecord(up[c], d.h2d));
+        HB_CUDA(cudaStreamWaitEvent(st, up[c], 0));
+        prep_chunk_kernel<<<d.sms * 2, 256, 0, st>>>(bufs[0], a0, a1, N, c1, c2, d.flag);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        size_t left = k_end;
+        for (long long pi = 0; pi < S; ++pi) {
+            const int s = int(std::min<size_t>(left, size_t(T::kMaxSteps)));
+            HB_TRY(L.pass(int(pi & 1), lo(c, pi), hi(c, pi), s, pi == S - 1, st));
+            left -= size_t(s);
+        }
+        HB_CUDA(cudaEventRecord(done[c], st));
+    }
+    // downloads last: a pageable destination makes each copy block the host,
+    // which must not hold back the compute launches above
+    const int fin = int(S & 1);
+    for (int c = 0; c < C; ++c) {
+        const long long a0 = lo(c, S - 1), a1 = hi(c, S - 1);
+        HB_CUDA(cudaStreamWaitEvent(d.d2h, done[c], 0));
+        HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0, (a1 - a0) * sizeof(double),
+                                cudaMemcpyDeviceToHost, d.d2h));
+    }
+    unsigned int flags[4] = {0, 0, 0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    HB_CUDA(cudaStreamSynchronize(d.d2h));
+    if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    return HEAT_OK;
+}
+
 // Shared body of sync_run / sync_run_f32 (sync_solver.cpp:52-91).  Snapshots
 // and the final state are copied straight into the caller's buffers.
 template <typename Real>
@@ -240,8 +414,20 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
-    const size_t pitch = (n + 63) / 64 * 64;  // keep the second array 256-B aligned
     const bool f32 = sizeof(Real) == 4;
+    // Large Dirichlet runs that only want the final state: stream the copies
+    // under the compute.  The host end check (sync_solver.cpp:29-31) runs
+    // first; when it fails, the one-shot path reports the reference's errors
+    // in the reference's order (a non-finite field before the end check).
+    if (!f32 && final_out && !snapshots && !steps_out && bc_kind == HEAT_BC_DIRICHLET &&
+        n >= kStreamMinPoints && k_end > 0 &&
+        (k_end + SyncTB<double, kV>::kMaxSteps - 1) / SyncTB<double, kV>::kMaxSteps <=
+            kStreamMaxPasses &&
+        std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9 &&
+        !std::getenv("HEAT_NO_STREAMED_SYNC"))
+        return sync_run_streamed(*d, reinterpret_cast<const double*>(u0), n, r, c1, c2, k_end,
+                                 final_out);
+    const size_t pitch = (n + 63) / 64 * 64;  // keep the second array 256-B aligned
     const size_t need = 2 * pitch * sizeof(Real) + (f32 ? pitch * sizeof(double) : 0);
     HB_TRY(ensure_buffers(*d, need));
     Real* bufs[2] = {static_cast<Real*>(d->buf[0]), static_cast<Real*>(d->buf[0]) + pitch};
@@ -327,8 +513,9 @@ extern "C" int heat_sync_run(const double* u0, size_t n, double r, int bc_kind, 
     // reference (q = 1 reduces async_run to sync_run, test_async_sim.cpp:110-129).
     if (u0 && n >= 3 && n <= 8192 && k_end > 0 &&
         (bc_kind == HEAT_BC_DIRICHLET || bc_kind == HEAT_BC_PERIODIC)) {
-        size_t P = 0;
-        for (size_t cand = 16; cand >= 1 && !P; --cand)
+        size_t P = 0, maxP = 8;  // 8 PE warps: measured best at N = 100-4096
+        if (const char* e = std::getenv("HEAT_SMALL_SYNC_PES")) maxP = std::max(1, std::atoi(e));
+        for (size_t cand = maxP; cand >= 1 && !P; --cand)
             if (n % cand == 0 && n / cand <= 1024) P = cand;
         if (P)
             return async_run_core(u0, n, r, bc_kind, c1, c2, n / P, 1, HEAT_DELAY_UNIFORM, 0, 0.5,
