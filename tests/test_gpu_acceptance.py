@@ -1,10 +1,10 @@
 """The reference's OWN acceptance suite (proj/tests/acceptance.cpp, unmodified)
 linked with its hot path (sync_step, sync_run, sync_run_f32, async_run,
-exec_run) replaced by the B200 library through integration/heat_core_b200.cpp
+exec_run, ensemble_run) replaced by the B200 library through integration/heat_core_b200.cpp
 -- the drop-in proof.  Built by `make -C oracle acceptance` (needs
 /root/reference at build time; the binary ships to the GPU box prebuilt).
 
-Criteria 1-7 (bit-exact reductions, ensembles over the GPU async_run,
+Criteria 1-7 (bit-exact reductions, ensembles on the GPU ensemble_run,
 conservation, stability window, executor equivalence, barrier-free stability)
 must pass exactly as they do for the reference.  Criterion 8 is the
 reference's CPU timing methodology (median monotone in N and barrier-free

@@ -90,3 +90,28 @@ def test_ensemble_validation(H):
     cfg.model = H.DelayModel.geometric(5, 0.5, 0)
     with pytest.raises(H.InvalidArgument):
         H.ensemble_run(cfg, 2, 1)
+
+
+def test_paper_ensemble_speed_vs_reference(H, ref):
+    # The paper's Fig. 6 ensemble (M = 50, N = 100, q = 5, 2e5 steps, periodic)
+    # through the reference's own ensemble_run on this host and through the
+    # GPU; identical terminal means, GPU time printed for profiles/.
+    import time
+    cos = ref.cosine_init(100)
+    r = ref.checked_r(0.5, 0.01, 0.1)
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    steps, norms, terms, mean, std, spread = ref.ensemble_run(
+        cos, r, O.PERIODIC, 0.0, 0.0, 1, O.UNIFORM, 5, 0, 200000, 200000, 50, 1000)
+    t_ref = time.perf_counter() - t0
+    cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.checked(0.5, 0.01, 0.1),
+                           H.BoundaryCondition.periodic(), H.PartitionSpec(100, 1),
+                           H.DelayModel.uniform(5, 0), 200000, 200000)
+    H.ensemble_run(cfg, 2, 1)  # context + module load
+    t0 = time.perf_counter()
+    res = H.ensemble_run(cfg, 50, 1000)
+    t_gpu = time.perf_counter() - t0
+    assert [fnv1a64(t.values()) for t in res.terminal_fields] == [fnv1a64(t) for t in terms]
+    print(f"\npaper ensemble (M=50, N=100, q=5, 2e5 steps): reference {t_ref:.3f} s, "
+          f"GPU {t_gpu:.4f} s, x{t_ref / t_gpu:.0f}")
+    assert t_gpu < t_ref
