@@ -35,19 +35,26 @@ __global__ void stream_seed_kernel(const double* __restrict__ field, const SeedO
     }
 }
 
-int launch_seed(cudaStream_t st, const double* field, const std::vector<SeedOp>& ops) {
+// `dev` (capacity `cap` ops) is a persistent device table, e.g. in the run's
+// scratch; without one a temporary is allocated and the call synchronises.
+// (A pageable-source cudaMemcpyAsync has taken its copy when it returns, so
+// the host vector may go either way.)
+int launch_seed(cudaStream_t st, const double* field, const std::vector<SeedOp>& ops,
+                SeedOp* dev = nullptr, size_t cap = 0) {
     if (ops.empty()) return HEAT_OK;
-    SeedOp* d_ops = nullptr;
-    HB_CUDA(cudaMallocAsync(&d_ops, ops.size() * sizeof(SeedOp), st));
+    const bool tmp = dev == nullptr || ops.size() > cap;
+    SeedOp* d_ops = dev;
+    if (tmp) HB_CUDA(cudaMallocAsync(&d_ops, ops.size() * sizeof(SeedOp), st));
     HB_CUDA(cudaMemcpyAsync(d_ops, ops.data(), ops.size() * sizeof(SeedOp), cudaMemcpyHostToDevice,
                             st));
     stream_seed_kernel<<<int(std::min<size_t>(1024, (ops.size() + 255) / 256)), 256, 0, st>>>(
         field, d_ops, int(ops.size()));
     HB_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    HB_CUDA(cudaFreeAsync(d_ops, st));
-    // the host vector dies with the caller: make sure the copy has been taken
-    HB_CUDA(cudaStreamSynchronize(st));
+    if (tmp) {
+        HB_CUDA(cudaFreeAsync(d_ops, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+    }
     return HEAT_OK;
 }
 
@@ -188,6 +195,7 @@ int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, 
     L.o_stats = take(kStatWords * 8);
     L.o_abort = take(4);
     L.o_links = take(L.P * sizeof(PeLink));
+    L.o_seeds = take((2 * L.P + 2 * size_t(L.G)) * sizeof(SeedOp));
     L.bytes = off;
     return HEAT_OK;
 }
@@ -240,7 +248,8 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
             HB_CUDA(cudaMemcpyAsync(base + L.o_dtab, dtab.data(), dtab.size(),
                                     cudaMemcpyHostToDevice, st));
         }
-        HB_TRY(launch_seed(st, bufs[cur], seeds));  // synchronises: the host vectors may go
+        HB_TRY(launch_seed(st, bufs[cur], seeds, at<SeedOp>(base, L.o_seeds),
+                           2 * L.P + 2 * size_t(L.G)));
     }
     if (steps == 0) return HEAT_OK;
     HB_CUDA(cudaMemsetAsync(base + L.o_done, 0, L.P * L.Tp * 4, st));

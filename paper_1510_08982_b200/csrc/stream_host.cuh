@@ -31,7 +31,7 @@ struct StreamLayout {
     int R = 0, D = 0;
     int G = 1;  // device groups inside this launch (> 1: emulated device boundaries)
     size_t o_ringL, o_ringR, o_progL, o_progR, o_recvL, o_recvR, o_rprogL, o_rprogR, o_done,
-        o_counter, o_offL, o_offR, o_dtab, o_stats, o_abort, o_links, bytes;
+        o_counter, o_offL, o_offR, o_dtab, o_stats, o_abort, o_links, o_seeds, bytes;
 };
 
 int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, StreamLayout& L,
