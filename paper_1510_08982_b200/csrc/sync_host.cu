@@ -59,34 +59,63 @@ using SyncKernelFn = void (*)(CUtensorMap, CUtensorMap, SyncPassArgs);
 struct SyncVariant {
     SyncKernelFn fn;
     int nbuf;
-    int blocks_per_sm;  // filled by the occupancy query
+    int V;                    // points per lane
+    int out;                  // exact points per tile
+    int win_units, out_units; // tensor-map boxes (32-point units) of a window / its outputs
+    int smem;                 // dynamic shared memory per CTA
+    int blocks_per_sm;        // filled by the occupancy query
 };
-constexpr int kDefaultSyncVariant = 4;  // pipelined steps, 2 buffers: 3759-3765 GLUPS at 2^30
+template <typename Real, int V, int NBUF, int UNR>
+SyncVariant variant() {
+    using T = SyncTB<Real, V>;
+    return {sync_tb_kernel<Real, V, NBUF, UNR>, NBUF, V, T::kOut, T::kWinUnits, T::kOutUnits,
+            T::smem_bytes(NBUF), 0};
+}
+// 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows)
+template <typename Real, int NBUF>
+SyncVariant variant48() {
+    if constexpr (sizeof(Real) == 8)
+        return variant<Real, 48, NBUF, 0>();
+    else
+        return variant<Real, kV, 2, 0>();
+}
+// 6: 48-point lanes, 2 buffers: 3874 GLUPS at 2^30 (V = 32, variant 4: 3761)
+constexpr int kDefaultSyncVariant = 6;
+constexpr int kSyncVariants = 9;
 
+// The selected variant's table entry (no CUDA calls).
 template <typename Real>
-int sync_variant(SyncVariant** out) {
-    static SyncVariant table[] = {
-        {sync_tb_kernel<Real, kV, 2, 1>, 2, 0},
-        {sync_tb_kernel<Real, kV, 2, 2>, 2, 0},
-        {sync_tb_kernel<Real, kV, 1, 1>, 1, 0},
-        {sync_tb_kernel<Real, kV, 1, 2>, 1, 0},
-        {sync_tb_kernel<Real, kV, 2, 0>, 2, 0},  // 4: pipelined steps, 2 buffers
-        {sync_tb_kernel<Real, kV, 1, 0>, 1, 0},  // 5: pipelined steps, 1 buffer
+SyncVariant& sync_variant_entry() {
+    // 0-5: V = 32 (buffers x step schedule); 6-8: wider lanes, same 32-point
+    // halo (f64 only: an f32 lane of 48 points is not whole swizzle rows)
+    static SyncVariant table[kSyncVariants] = {
+        variant<Real, kV, 2, 1>(),
+        variant<Real, kV, 2, 2>(),
+        variant<Real, kV, 1, 1>(),
+        variant<Real, kV, 1, 2>(),
+        variant<Real, kV, 2, 0>(),  // 4: pipelined steps, 2 buffers
+        variant<Real, kV, 1, 0>(),  // 5: pipelined steps, 1 buffer
+        variant48<Real, 2>(),        // 6: 48-point lanes, 2 buffers
+        variant48<Real, 1>(),        // 7: 48-point lanes, 1 buffer
+        variant<Real, 64, 1, 0>(),   // 8: 64-point lanes, 1 buffer
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
         const int v = e ? std::atoi(e) : kDefaultSyncVariant;
-        return (v >= 0 && v < 6) ? v : kDefaultSyncVariant;
+        return (v >= 0 && v < kSyncVariants) ? v : kDefaultSyncVariant;
     }();
-    SyncVariant& v = table[idx];
+    return table[idx];
+}
+
+template <typename Real>
+int sync_variant(SyncVariant** out) {
+    SyncVariant& v = sync_variant_entry<Real>();
     if (v.blocks_per_sm == 0) {
-        using T = SyncTB<Real, kV>;
-        const int smem = T::smem_bytes(v.nbuf);
         HB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
         int per_sm = 0;
         HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, reinterpret_cast<const void*>(v.fn), T::kThreads, smem));
+            &per_sm, reinterpret_cast<const void*>(v.fn), SyncTB<Real, kV>::kThreads, v.smem));
         if (per_sm < 1) return fail(HEAT_ECUDA, "sync_tb_kernel does not fit on an SM");
         v.blocks_per_sm = per_sm;
     }
@@ -143,8 +172,8 @@ struct SyncLauncher {
         // tensor maps: [chunk][row][16 doubles] views of both ping-pong arrays,
         // 32-chunk boxes for window loads, 30-chunk boxes for output stores
         for (int i = 0; i < 2; ++i) {
-            HB_TRY((make_chunk_map<Real, kV>(&load_map[i], bufs[i], a.nchunks, kWarp)));
-            HB_TRY((make_chunk_map<Real, kV>(&store_map[i], bufs[i], a.nchunks, kWarp - 2)));
+            HB_TRY((make_chunk_map<Real, kV>(&load_map[i], bufs[i], a.nchunks, var->win_units)));
+            HB_TRY((make_chunk_map<Real, kV>(&store_map[i], bufs[i], a.nchunks, var->out_units)));
         }
         return HEAT_OK;
     }
@@ -155,7 +184,7 @@ struct SyncLauncher {
              cudaStream_t st) {
         if (out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
         if (out_hi <= out_lo) return HEAT_OK;
-        const long long tiles = (out_hi - out_lo + T::kOut - 1) / T::kOut;
+        const long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
         const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
         const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
         SyncPassArgs p = a;
@@ -166,8 +195,7 @@ struct SyncLauncher {
         p.dst = bufs[src ^ 1];
         p.nsteps = nsteps;
         p.check_finite = check;
-        var->fn<<<grid, T::kThreads, T::smem_bytes(var->nbuf), st>>>(load_map[src],
-                                                                      store_map[src ^ 1], p);
+        var->fn<<<grid, T::kThreads, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
@@ -315,7 +343,7 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // and the last download is short, while neighbouring chunks differ by
     // less than the compute/copy time ratio (~1.8), so neither the compute
     // nor the download stream starves.  Smaller fields: 16 equal chunks.
-    const long long wave = (long long)d.sms * L.var->blocks_per_sm * T::kWarpsPerCta * T::kOut;
+    const long long wave = (long long)d.sms * L.var->blocks_per_sm * T::kWarpsPerCta * L.var->out;
     std::vector<long long> B{0};
     if (N >= 128 * wave) {
         std::vector<long long> head;
@@ -495,6 +523,15 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
 }  // namespace hb
 
 using namespace hb;
+
+extern "C" int heat_sync_kernel_info(int* points_per_lane, int* buffers,
+                                     int* exact_points_per_tile) {
+    const SyncVariant& v = sync_variant_entry<double>();
+    if (points_per_lane) *points_per_lane = v.V;
+    if (buffers) *buffers = v.nbuf;
+    if (exact_points_per_tile) *exact_points_per_tile = v.out;
+    return HEAT_OK;
+}
 
 extern "C" int heat_sync_step(const double* u, size_t n, double r, int bc_kind, double c1,
                               double c2, double* out) {

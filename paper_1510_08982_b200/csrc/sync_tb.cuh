@@ -43,15 +43,29 @@ struct SyncTB {
     static constexpr int kRowElems = 128 / int(sizeof(Real));
     static constexpr int kPer16 = 16 / int(sizeof(Real));         // elements per 16-B unit
     static constexpr int kBufBytes = kWarp * kChunkBytes;         // dense window
-    static constexpr int kOut = (kWarp - 2) * V;                  // exact points per tile
+    // The halo is 32 points per side whatever V is: a pass of <= 32 steps
+    // leaves window points [32, 32V-32) exact.  At V = 32 that is lanes
+    // 1..30; wider lanes (V = 48, 64) waste a smaller share on the halo and
+    // pay the per-tile costs (TMA, staging, pipeline fill) over more points.
+    static constexpr int kHalo = 32;
+    static constexpr int kUnit = 32;  // tensor-map coordinate unit (points); windows start on one
+    static constexpr int kWinUnits = kWarp * V / kUnit;
+    static constexpr int kOutUnits = kWinUnits - 2 * kHalo / kUnit;
+    static constexpr int kOut = kWarp * V - 2 * kHalo;            // exact points per tile
+    static constexpr int kHaloRows = kHalo * int(sizeof(Real)) / 128;
     static constexpr int kWarpsPerCta = 4;
     static constexpr int kThreads = kWarpsPerCta * kWarp;
     // shared memory for NBUF window buffers per warp (+ mbarriers, + 1 KB alignment slack)
     static constexpr int smem_bytes(int nbuf) {
         return kWarpsPerCta * nbuf * kBufBytes + kWarpsPerCta * 2 * 8 + 1024;
     }
-    static constexpr int kMaxSteps = V;  // halo of one lane per side
+    static constexpr int kMaxSteps = kHalo;
+    // resident CTAs per SM the launch bounds promise (registers: V doubles per
+    // lane in registers; V > 32 needs ~210 registers)
+    static constexpr int min_blocks(int nbuf) { return V == 32 ? (nbuf == 1 ? 4 : 3) : 2; }
     static_assert(kChunkBytes % 128 == 0, "chunk must be whole 128-B swizzle rows");
+    static_assert(kBufBytes % 1024 == 0, "window buffers must keep the 1 KB swizzle alignment");
+    static_assert((kWarp * V) % kUnit == 0 && kHalo % kUnit == 0, "windows of whole units");
 };
 
 // Byte offset of 16-B unit `m` of lane-slot `slot`'s chunk in a 128B-swizzled
@@ -82,6 +96,27 @@ __device__ __forceinline__ void chunk_from_smem(const unsigned char* buf, int sl
         }
     }
 }
+// Stage the exact elements [el_lo, el_hi) of lane `lane`'s chunk for the TMA
+// store of the tile's output units: window row w lands at row w - kHaloRows,
+// so the store box starts at the (1 KB aligned) buffer start.  The halo
+// bounds are multiples of 32 elements, i.e. of whole 16-B units.
+template <typename Real, int V>
+__device__ __forceinline__ void chunk_to_smem_out(unsigned char* buf, int lane, const Real (&u)[V],
+                                                  int el_lo, int el_hi) {
+    using T = SyncTB<Real, V>;
+#pragma unroll
+    for (int m = 0; m < V / T::kPer16; ++m) {
+        const int e0 = m * T::kPer16;
+        if (e0 < el_lo || e0 + T::kPer16 > el_hi) continue;
+        const int row = lane * T::kRowsPerChunk + (m >> 3) - T::kHaloRows;
+        unsigned char* p = buf + row * 128 + (((m & 7) ^ (row & 7)) << 4);
+        if constexpr (sizeof(Real) == 8)
+            *reinterpret_cast<double2*>(p) = make_double2(u[e0], u[e0 + 1]);
+        else
+            *reinterpret_cast<float4*>(p) = make_float4(u[e0], u[e0 + 1], u[e0 + 2], u[e0 + 3]);
+    }
+}
+
 template <typename Real, int V>
 __device__ __forceinline__ void chunk_to_smem(unsigned char* buf, int slot, const Real (&u)[V]) {
     using T = SyncTB<Real, V>;
@@ -237,7 +272,7 @@ struct SyncPassArgs {
 // UNR:      unroll factor of the step loop; 0 = software-pipelined steps
 //           (warp_steps_pipelined) for tiles without pinned ends.
 template <typename Real, int V, int NBUF, int UNR>
-__global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
+__global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, SyncTB<Real, V>::min_blocks(NBUF))
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
     using T = SyncTB<Real, V>;
@@ -268,8 +303,8 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
     __syncwarp();
 
     const long long nwarps = (long long)gridDim.x * T::kWarpsPerCta;
-    const long long tma_len = a.nchunks * V;
-    auto window = [&](long long t) { return a.out_lo + t * T::kOut - V; };
+    const long long tma_len = a.nchunks * T::kUnit;  // points the tensor maps cover
+    auto window = [&](long long t) { return a.out_lo + t * T::kOut - T::kHalo; };
     auto in_window = [&](long long g, long long w0) {
         return g >= 0 && g >= w0 && g < w0 + kWarp * V;
     };
@@ -286,7 +321,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
         if (lane == 0) {
             if (NBUF == 2) bulk_wait_read_all();  // the TMA store that last used it has read it
             mbar_arrive_expect_tx(&bars[b], T::kBufBytes);
-            tma_load_3d(bufp(b), &tm_src, 0, 0, int(window(t) / V), &bars[b]);
+            tma_load_3d(bufp(b), &tm_src, 0, 0, int(window(t) / T::kUnit), &bars[b]);
         }
     };
 
@@ -335,40 +370,44 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, NBUF == 1 ? 4 : 3)
             }
         }
 
-        const bool out_lane = lane >= 1 && lane <= kWarp - 2;
+        // exact elements of this lane: window points [kHalo, 32V - kHalo)
+        const int el_lo = lane == 0 ? T::kHalo : 0;
+        const int el_hi = lane == kWarp - 1 ? V - T::kHalo : V;
         // Finite check only on the last pass of an advance: a non-finite value
         // at a non-pinned point never becomes finite again (c*NaN = NaN,
         // c*(+-Inf) = +-Inf or NaN), so the outcome of the reference's per-step
         // check (sync_solver.cpp:11-17) is decided by the final state.
-        if (a.check_finite && out_lane) {
+        if (a.check_finite) {
 #pragma unroll
             for (int i = 0; i < V; ++i)
-                if (g0 + i < a.out_hi && !isfinite(u[i])) bad = true;
+                if (i >= el_lo && i < el_hi && g0 + i < a.out_hi && !isfinite(u[i])) bad = true;
         }
-        const bool full = w0 + (kWarp - 1) * V <= a.out_hi;
+        const bool full = w0 + kWarp * V - T::kHalo <= a.out_hi;
         if (NBUF == 2 && inter && full) {
-            // stage the 30 exact chunks as a [30 x rows] box at the buffer start
-            if (out_lane) chunk_to_smem<Real, V>(buf, lane - 1, u);
+            // stage the exact units as a [kOutUnits x rows] box at the buffer start
+            chunk_to_smem_out<Real, V>(buf, lane, u, el_lo, el_hi);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d(&tm_dst, 0, 0, int((w0 + V) / V), buf);
+                tma_store_3d(&tm_dst, 0, 0, int((w0 + T::kHalo) / T::kUnit), buf);
                 bulk_commit();
             }
-        } else if (out_lane && full && g0 >= 0) {
-            // whole chunk in range: 16-B vector stores from registers
+        } else if (full && g0 >= 0) {
+            // whole exact 16-B units in range: vector stores from registers
 #pragma unroll
             for (int m = 0; m < V / T::kPer16; ++m) {
+                const int e0 = m * T::kPer16;
+                if (e0 < el_lo || e0 + T::kPer16 > el_hi) continue;
                 if constexpr (sizeof(Real) == 8)
-                    reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[2 * m], u[2 * m + 1]);
+                    reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[e0], u[e0 + 1]);
                 else
                     reinterpret_cast<float4*>(dst + g0)[m] =
-                        make_float4(u[4 * m], u[4 * m + 1], u[4 * m + 2], u[4 * m + 3]);
+                        make_float4(u[e0], u[e0 + 1], u[e0 + 2], u[e0 + 3]);
             }
-        } else if (out_lane) {
+        } else {
 #pragma unroll
             for (int i = 0; i < V; ++i)
-                if (g0 + i < a.out_hi) dst[g0 + i] = u[i];
+                if (i >= el_lo && i < el_hi && g0 + i < a.out_hi) dst[g0 + i] = u[i];
         }
     }
     if (NBUF == 2 && lane == 0) bulk_wait_all();
