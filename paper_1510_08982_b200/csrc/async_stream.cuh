@@ -8,15 +8,16 @@
 // replayed from the reference's SplitMix64 stream (deterministic mode, bit-
 // exact with async_run) or the newest value within the bound q (free mode).
 //
-// Execution: each PE's slab is cut into K1 tiles (30V exact points, V = 32)
-// advanced s <= V steps per HBM pass with redundant halo recompute (the same
+// Execution: each PE's slab is cut into K1 tiles (32V - 64 exact points,
+// V = 48 by default, 32-point halo) advanced s <= 32 steps per HBM pass with
+// redundant halo recompute (the same
 // warp_step, TMA tensor loads/stores and 128B-swizzled buffers as K1).  Work
 // items (pass, tile) are handed out in pass-major order by one atomic counter;
 // a tile may start pass pi once its same-PE neighbours finished pass pi-1
 // (per-tile pass counters, acquire/release) -- a local dependency, never a
 // barrier.  The two tiles at a PE boundary inject the neighbour's value into
-// the stencil every step: lane 1 (the PE's first point) and lane lR (its
-// last point) spin on the neighbour's progress counter, read the edge ring
+// the stencil every step: the lanes holding the PE's first and last point
+// (an element cut inside the lane) spin on the neighbour's progress counter, read the edge ring
 // slot, and publish their own new edge value + progress (release).  Within a
 // pass the boundary tiles are handed out first, in (right edge of PE b, left
 // edge of PE b+1) pairs, so every pair that handshakes is co-resident and the
@@ -145,6 +146,47 @@ __device__ __forceinline__ bool wait_done(const AsyncStreamArgs& a, const unsign
     return true;
 }
 
+// One Jacobi step of a lane's V points in a PE-boundary tile: on the lane
+// with cutL, element FE takes the ghost product gp as its LEFT neighbour
+// product; on the lane with cutR, element LE takes it as its RIGHT one.
+// Points beyond a cut belong to the neighbour PE's side of the window and are
+// never output.  FE / LE are compile-time (the edge positions are warp-
+// uniform and few), so the cut costs one select, not one per element.
+template <int V, int FE, int LE>
+__device__ __forceinline__ void chunk_step_cut(double (&u)[V], double r, double c, double pL,
+                                               double pR, double pFirst, double pLast, bool cutL,
+                                               bool cutR, double gp) {
+    using A = Arith<double>;
+    double pm1 = pL, p0 = pFirst;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+        const double p1 = i + 1 == V ? pR : (i + 1 == V - 1 ? pLast : A::mul(r, u[i + 1]));
+        const double right = (i == LE && cutR) ? gp : p1;
+        const double left = (i == FE && cutL) ? gp : pm1;
+        u[i] = stencil_p(right, A::mul(c, u[i]), left);
+        pm1 = p0;
+        p0 = p1;
+    }
+}
+
+// One boundary-tile step, edge writes and the new edge values: the PE's
+// first point is element FE of its lane, the last point element LE.
+template <int V, int FE, int LE>
+__device__ __forceinline__ void boundary_step(double (&u)[V], double r, double c, bool cutL,
+                                              bool cutR, double ghost, bool pinF, double c1,
+                                              bool pinL, double c2, double& first, double& last) {
+    using A = Arith<double>;
+    const double pFirst = A::mul(r, u[0]);
+    const double pLast = A::mul(r, u[V - 1]);
+    const double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
+    const double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
+    chunk_step_cut<V, FE, LE>(u, r, c, pL, pR, pFirst, pLast, cutL, cutR, A::mul(r, ghost));
+    if (pinF) u[FE] = c1;
+    if (pinL) u[LE] = c2;
+    first = u[FE];
+    last = u[LE];
+}
+
 // Decoded work item.
 struct StreamItem {
     long long pass;
@@ -176,13 +218,14 @@ __device__ __forceinline__ StreamItem decode_item(const AsyncStreamArgs& a, long
 }
 
 template <int V>
-__global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
+__global__ void __launch_bounds__(SyncTB<double, V>::kThreads, SyncTB<double, V>::min_blocks(2))
     async_stream_kernel(const __grid_constant__ CUtensorMap tm_load0,
                         const __grid_constant__ CUtensorMap tm_load1,
                         const __grid_constant__ CUtensorMap tm_store0,
                         const __grid_constant__ CUtensorMap tm_store1, const AsyncStreamArgs a) {
     using T = SyncTB<double, V>;
     using A = Arith<double>;
+    static_assert(V == 32 || V == 48, "PE last points sit at element 31 mod 32: 31 | 15, 31, 47");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -202,7 +245,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
     const double r = a.r, c = a.c;
     const long long T_all = (long long)a.P * a.Tp;
     const long long total = a.npass * T_all;
-    const long long tma_len = (a.N / V) * V;
+    const long long tma_len = (a.N / T::kUnit) * T::kUnit;
     uint32_t phase = 0;
     bool bad = false, abort = false;
     unsigned long long reads = 0, waits = 0, maxd = 0, lag_min = ~0ull, lag_max = 0;
@@ -219,7 +262,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
     };
     auto geometry = [&](const StreamItem& it, long long& lo, long long& w0, long long& out_hi) {
         lo = (long long)it.p * a.n;
-        w0 = lo + (long long)it.m * T::kOut - V;
+        w0 = lo + (long long)it.m * T::kOut - T::kHalo;
         out_hi = lo + a.n;
     };
     auto deps_ready = [&](const StreamItem& it, bool block) -> bool {
@@ -245,7 +288,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
             asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired data -> async proxy
             mbar_arrive_expect_tx(&bars[bb], T::kBufBytes);
             tma_load_3d(wbase + bb * T::kBufBytes, (it.pass & 1) ? &tm_load1 : &tm_load0, 0, 0,
-                        int(w0 / V), &bars[bb]);
+                        int(w0 / T::kUnit), &bars[bb]);
         }
     };
 
@@ -331,8 +374,12 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
             }
         };
 
-        // ---- step the tile; boundary tiles exchange edge values every step
-        const int lR = int((out_hi - 1 - w0) / V);  // lane holding the PE's last point
+        // ---- step the tile; boundary tiles exchange edge values every step.
+        // The PE's first point sits kHalo points into a left-edge window, its
+        // last point wherever the PE ends: (lane, element) of each.
+        const int fl = T::kHalo / V;  // lane of the first point (lo - w0 = kHalo)
+        const int lpos = int(out_hi - 1 - w0);
+        const int ll = lpos / V, le = lpos % V;
         if (!left_edge && !right_edge) {
             const int half = nst / 2;
             warp_steps_pipelined<double, V>(u, r, c, half);
@@ -347,9 +394,10 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
             const bool pin_last = it.p == a.pin_last_pe;
             const bool needL = left_edge && lk.srcL != nullptr && !pin_first;
             const bool needR = right_edge && lk.srcR != nullptr && !pin_last;
-            // lane 1 holds the PE's first point, lane lR its last one
-            const bool mine = (lane == 1 && needL) || (lane == lR && needR && !(lane == 1 && needL));
-            const bool left = lane == 1 && needL;
+            // lane fl holds the PE's first point, lane ll its last one (different
+            // tiles: Tp >= 2)
+            const bool left = lane == fl && needL;
+            const bool mine = left || (lane == ll && needR);
             const unsigned long long* pw = left ? lk.progL_src : lk.progR_src;
             const double* gring = left ? lk.srcL : lk.srcR;
             const bool gsys = (lk.flags & (left ? kLinkSrcLSys : kLinkSrcRSys)) != 0;
@@ -385,42 +433,49 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
                     abort = true;
                     break;
                 }
-                const double pFirst = A::mul(r, u[0]);
-                const double pLast = A::mul(r, u[V - 1]);
-                double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
-                double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
-                if (lane == 1 && needL) pL = A::mul(r, ghost);
-                if (lane == lR && needR) pR = A::mul(r, ghost);
-                chunk_step<double, V>(u, r, c, pL, pR, pFirst, pLast);
-                if (left_edge && pin_first && lane == 1) u[0] = a.c1;
-                if (right_edge && pin_last && lane == lR) u[V - 1] = a.c2;
+                // edge elements: first at kHalo % V (always), last at le, which
+                // is 31 mod 32 -- warp-uniform, dispatched to a compile-time cut
+                const bool cutR = lane == ll && needR;
+                const bool pinF = left_edge && pin_first && lane == fl;
+                const bool pinL = right_edge && pin_last && lane == ll;
+                double first, last;
+                constexpr int FE = T::kHalo % V;
+                if (V == 32 || le == 31)
+                    boundary_step<V, FE, 31>(u, r, c, left, cutR, ghost, pinF, a.c1, pinL, a.c2,
+                                             first, last);
+                else if (le == 15)
+                    boundary_step<V, FE, (V > 15 ? 15 : 0)>(u, r, c, left, cutR, ghost, pinF,
+                                                            a.c1, pinL, a.c2, first, last);
+                else
+                    boundary_step<V, FE, (V > 47 ? 47 : V - 1)>(u, r, c, left, cutR, ghost, pinF,
+                                                                 a.c1, pinL, a.c2, first, last);
                 // publish u_first(k+1) / u_last(k+1) to every ring that mirrors
                 // it (local, plus the neighbour device's receive ring for a
                 // device boundary -- a P2P store over NVLink), then release
                 // the progress word with the matching scope
                 const long long slot = (k + 1) & (a.R - 1);
-                if (left_edge && lane == 1) {
+                if (left_edge && lane == fl) {
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (!lk.pubF[t]) continue;
                         if (lk.flags & (t ? kLinkPubF1Sys : 0)) {
-                            st_relaxed_sys_f64(lk.pubF[t] + slot, u[0]);
+                            st_relaxed_sys_f64(lk.pubF[t] + slot, first);
                             st_release_sys(reinterpret_cast<uint64_t*>(lk.pubF_prog[t]), uint64_t(k + 1));
                         } else {
-                            st_relaxed_gpu_f64(lk.pubF[t] + slot, u[0]);
+                            st_relaxed_gpu_f64(lk.pubF[t] + slot, first);
                             st_release_gpu(reinterpret_cast<uint64_t*>(lk.pubF_prog[t]), uint64_t(k + 1));
                         }
                     }
                 }
-                if (right_edge && lane == lR) {
+                if (right_edge && lane == ll) {
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
                         if (!lk.pubL[t]) continue;
                         if (lk.flags & (t ? kLinkPubL1Sys : 0)) {
-                            st_relaxed_sys_f64(lk.pubL[t] + slot, u[V - 1]);
+                            st_relaxed_sys_f64(lk.pubL[t] + slot, last);
                             st_release_sys(reinterpret_cast<uint64_t*>(lk.pubL_prog[t]), uint64_t(k + 1));
                         } else {
-                            st_relaxed_gpu_f64(lk.pubL[t] + slot, u[V - 1]);
+                            st_relaxed_gpu_f64(lk.pubL[t] + slot, last);
                             st_release_gpu(reinterpret_cast<uint64_t*>(lk.pubL_prog[t]), uint64_t(k + 1));
                         }
                     }
@@ -429,26 +484,37 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, 3)
             if (abort) break;
         }
 
-        // ---- window out: lanes 1..30 that lie inside this PE
-        const bool out_lane = lane >= 1 && lane <= kWarp - 2 && g0 >= lo && g0 < out_hi;
-        if (out_lane && it.pass == a.npass - 1) {  // non-finite values are absorbing
-#pragma unroll
-            for (int i = 0; i < V; ++i) bad |= !isfinite(u[i]);
+        // ---- window out: the tile's exact points [w0 + kHalo, w0 + 32V - kHalo)
+        // that lie inside this PE (bounds are multiples of 32 points)
+        const bool full = w0 + kWarp * V - T::kHalo <= out_hi && w0 + T::kHalo >= lo;
+        int el_lo = lane == 0 ? T::kHalo : 0;  // a whole window inside the PE
+        int el_hi = lane == kWarp - 1 ? V - T::kHalo : V;
+        if (!full) {  // clipped to the PE
+            const long long ex_lo = max(w0 + T::kHalo, lo);
+            const long long ex_hi = min(w0 + kWarp * V - T::kHalo, out_hi);
+            el_lo = int(max(0LL, min((long long)V, ex_lo - g0)));
+            el_hi = int(max(0LL, min((long long)V, ex_hi - g0)));
         }
-        const bool full = w0 + (kWarp - 1) * V <= out_hi && w0 + V >= lo;
+        if (it.pass == a.npass - 1) {  // non-finite values are absorbing
+#pragma unroll
+            for (int i = 0; i < V; ++i)
+                if (i >= el_lo && i < el_hi) bad |= !isfinite(u[i]);
+        }
         unsigned char* bufb = wbase + b * T::kBufBytes;
         if (tma_ok(w0) && full) {
-            if (out_lane) chunk_to_smem<double, V>(bufb, lane - 1, u);
+            chunk_to_smem_out_split<double, V>(bufb, lane, u, el_lo, el_hi);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-                tma_store_3d((it.pass & 1) ? &tm_store0 : &tm_store1, 0, 0, int((w0 + V) / V), bufb);
+                tma_store_3d((it.pass & 1) ? &tm_store0 : &tm_store1, 0, 0,
+                             int((w0 + T::kHalo) / T::kUnit), bufb);
                 bulk_commit();
             }
-        } else if (out_lane) {
+        } else {
 #pragma unroll
             for (int m = 0; m < V / 2; ++m)
-                reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[2 * m], u[2 * m + 1]);
+                if (2 * m >= el_lo && 2 * m + 2 <= el_hi)
+                    reinterpret_cast<double2*>(dst + g0)[m] = make_double2(u[2 * m], u[2 * m + 1]);
         }
         // Declare the PREVIOUS item done (its store has had a whole compute
         // phase to land: wait until at most this item's store group is in

@@ -10,7 +10,17 @@ namespace hb {
 
 namespace {
 
-constexpr int kSV = 32;  // points per lane of the stream kernel (= K1's V)
+// Points per lane of the stream kernel for PEs of n points: 48 like K1 when a
+// PE still spans >= 2 such tiles, else 32 (HEAT_ASYNC_LANE_POINTS=32 forces
+// 32 for A/B); the halo is 32 points either way.
+int stream_lane_points(size_t n) {
+    static const bool force32 = [] {
+        const char* e = std::getenv("HEAT_ASYNC_LANE_POINTS");
+        return e && std::atoi(e) == 32;
+    }();
+    return (!force32 && n > size_t(SyncTB<double, 48>::kOut)) ? 48 : 32;
+}
+constexpr int kSU = 32;  // tensor-map unit (points); PEs are whole units
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
@@ -160,10 +170,12 @@ int virtual_device_groups(size_t P) {
 
 int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, StreamLayout& L,
                   std::vector<int>& offL, std::vector<int>& offR) {
-    if (s.n % kSV != 0)
+    if (s.n % kSU != 0)
         return fail(HEAT_EINVAL, "async: PEs wider than 1024 points must be a multiple of 32 points");
     L.P = s.N / s.n;
-    L.Tp = (s.n + SyncTB<double, kSV>::kOut - 1) / SyncTB<double, kSV>::kOut;
+    L.V = stream_lane_points(s.n);
+    const long long tile_out = L.V == 48 ? SyncTB<double, 48>::kOut : SyncTB<double, 32>::kOut;
+    L.Tp = (s.n + tile_out - 1) / tile_out;
     if (L.Tp < 2) return fail(HEAT_ELOGIC, "async stream: a PE needs >= 2 tiles");
     L.G = (groups >= 1 && L.P % size_t(groups) == 0) ? groups : 1;
     L.R = 64;
@@ -210,11 +222,38 @@ int stream_seed_external(cudaStream_t st, const double* field, const AsyncRunSpe
     return launch_seed(st, field, ops);
 }
 
+// Launch of the stream kernel with V-point lanes (tensor maps in 32-point units).
+template <int V>
+int launch_stream(int sms, cudaStream_t st, double* const bufs[2], int cur, long long N,
+                  const AsyncStreamArgs& a) {
+    using T = SyncTB<double, V>;
+    static int per_sm = 0;
+    const int smem = T::smem_bytes(2);
+    if (per_sm == 0) {
+        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<V>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<V>,
+                                                              T::kThreads, smem));
+        if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
+    }
+    const long long nunits = N / T::kUnit;
+    CUtensorMap ld[2], stm[2];
+    for (int b = 0; b < 2; ++b) {
+        HB_TRY(make_chunk_map_f64(&ld[b], bufs[b], nunits, T::kWinUnits));
+        HB_TRY(make_chunk_map_f64(&stm[b], bufs[b], nunits, T::kOutUnits));
+    }
+    // maps follow the pass parity: pass pi reads a.buf[pi & 1]
+    async_stream_kernel<V><<<sms * per_sm, T::kThreads, smem, st>>>(ld[cur], ld[cur ^ 1], stm[cur],
+                                                                   stm[cur ^ 1], a);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return HEAT_OK;
+}
+
 int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, const AsyncRunSpec& s,
                          const StreamLayout& L, char* base, const StreamExternal& ext,
                          const std::vector<int>& offL, const std::vector<int>& offR, size_t k0,
                          size_t steps, bool init, unsigned int* flag, float* device_ms) {
-    using T = SyncTB<double, kSV>;
     // the pinned Dirichlet ends: global PE 0's first point, global PE Pg-1's last
     const long long Pg = ext.P_global > 0 ? ext.P_global : (long long)L.P;
     const bool dir = s.bc_kind == HEAT_BC_DIRICHLET;
@@ -256,21 +295,6 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     HB_CUDA(cudaMemsetAsync(base + L.o_counter, 0, 8, st));
     HB_CUDA(cudaMemsetAsync(base + L.o_abort, 0, 4, st));
 
-    static int per_sm = 0;
-    const int smem = T::smem_bytes(2);
-    if (per_sm == 0) {
-        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<kSV>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<kSV>,
-                                                              T::kThreads, smem));
-        if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
-    }
-    const long long nchunks = (long long)(s.N / kSV);
-    CUtensorMap ld[2], stm[2];
-    for (int b = 0; b < 2; ++b) {
-        HB_TRY(make_chunk_map_f64(&ld[b], bufs[b], nchunks, kWarp));
-        HB_TRY(make_chunk_map_f64(&stm[b], bufs[b], nchunks, kWarp - 2));
-    }
     AsyncStreamArgs a{};
     a.buf[0] = bufs[cur];
     a.buf[1] = bufs[cur ^ 1];
@@ -285,7 +309,7 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.dirichlet = s.bc_kind == HEAT_BC_DIRICHLET;
     a.k0 = (long long)k0;
     a.steps = (long long)steps;
-    a.s = T::kMaxSteps;
+    a.s = SyncTB<double, 32>::kMaxSteps;  // 32: the halo, whatever the lane width
     a.npass = (a.steps + a.s - 1) / a.s;
     a.mode = s.mode;
     a.q = int(s.q);
@@ -307,17 +331,16 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.flag = flag;
     a.abort_word = at<unsigned int>(base, L.o_abort);
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;
-    // maps follow the pass parity: pass pi reads a.buf[pi & 1]
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (device_ms) {
         HB_CUDA(cudaEventCreate(&e0));
         HB_CUDA(cudaEventCreate(&e1));
         HB_CUDA(cudaEventRecord(e0, st));
     }
-    async_stream_kernel<kSV><<<sms * per_sm, T::kThreads, smem, st>>>(ld[cur], ld[cur ^ 1], stm[cur],
-                                                                     stm[cur ^ 1], a);
-    HB_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (L.V == 32)
+        HB_TRY(launch_stream<32>(sms, st, bufs, cur, (long long)s.N, a));
+    else
+        HB_TRY(launch_stream<48>(sms, st, bufs, cur, (long long)s.N, a));
     if (device_ms) {
         HB_CUDA(cudaEventRecord(e1, st));
         HB_CUDA(cudaEventSynchronize(e1));

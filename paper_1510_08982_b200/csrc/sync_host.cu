@@ -65,23 +65,23 @@ struct SyncVariant {
     int smem;                 // dynamic shared memory per CTA
     int blocks_per_sm;        // filled by the occupancy query
 };
-template <typename Real, int V, int NBUF, int UNR>
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true>
 SyncVariant variant() {
     using T = SyncTB<Real, V>;
-    return {sync_tb_kernel<Real, V, NBUF, UNR>, NBUF, V, T::kOut, T::kWinUnits, T::kOutUnits,
-            T::smem_bytes(NBUF), 0};
+    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST>, NBUF, V, T::kOut, T::kWinUnits,
+            T::kOutUnits, T::smem_bytes(NBUF), 0};
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows)
-template <typename Real, int NBUF>
+template <typename Real, int NBUF, bool TMA_ST = true>
 SyncVariant variant48() {
     if constexpr (sizeof(Real) == 8)
-        return variant<Real, 48, NBUF, 0>();
+        return variant<Real, 48, NBUF, 0, TMA_ST>();
     else
         return variant<Real, kV, 2, 0>();
 }
 // 6: 48-point lanes, 2 buffers: 3874 GLUPS at 2^30 (V = 32, variant 4: 3761)
 constexpr int kDefaultSyncVariant = 6;
-constexpr int kSyncVariants = 9;
+constexpr int kSyncVariants = 11;
 
 // The selected variant's table entry (no CUDA calls).
 template <typename Real>
@@ -98,6 +98,8 @@ SyncVariant& sync_variant_entry() {
         variant48<Real, 2>(),        // 6: 48-point lanes, 2 buffers
         variant48<Real, 1>(),        // 7: 48-point lanes, 1 buffer
         variant<Real, 64, 1, 0>(),   // 8: 64-point lanes, 1 buffer
+        variant48<Real, 2, false>(), // 9: 48-point lanes, 2 load buffers, register stores
+        variant<Real, kV, 2, 0, false>(),  // 10: 32-point lanes, 2 load buffers, register stores
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
