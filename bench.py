@@ -38,7 +38,7 @@ UNIT = "GLUPS"
 N_PER_GPU = 1 << 30
 R = 0.4
 STEPS_PER_BENCH_STEP = 1000
-STEPS_PER_PASS = 32
+STEPS_PER_PASS = 32  # fallback; the library reports its kernel's (heat_sync_kernel_info)
 BYTES_PER_UPDATE = 16  # one FP64 read + one FP64 write per point per step
 FP64_OPS_PER_UPDATE = 4  # 2 DMUL + 2 DADD with the shared r*u products
 CPU_SAMPLE_STEPS = 4
@@ -179,18 +179,31 @@ def run_reference(args, rank, world):
     return 0
 
 
-def sync_kernel_name():
+def sync_kernel_info():
     """The f64 pass kernel the library selected (heat_sync_kernel_info)."""
+    import ctypes
+    from paper_1510_08982_b200 import _lib
+    v, nb, out, sp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.lib().heat_sync_kernel_info(ctypes.byref(v), ctypes.byref(nb), ctypes.byref(out),
+                                     ctypes.byref(sp))
+    return {"V": v.value, "buffers": nb.value, "exact": out.value, "steps_per_pass": sp.value}
+
+
+def sync_kernel_name():
     try:
-        import ctypes
-        from paper_1510_08982_b200 import _lib
-        v, nb, out = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-        _lib.lib().heat_sync_kernel_info(ctypes.byref(v), ctypes.byref(nb), ctypes.byref(out))
-        return (f"sync_tb_kernel<double,{v.value},{nb.value},0> (temporal-blocked: "
-                f"{v.value}-point lanes, 32-point halo, {out.value} exact points per warp tile, "
-                f"32 steps per HBM pass)")
+        k = sync_kernel_info()
+        return (f"sync_tb_kernel<double,{k['V']},{k['buffers']},0,H={k['steps_per_pass']}> "
+                f"(temporal-blocked: {k['V']}-point lanes, {k['steps_per_pass']}-point halo, "
+                f"{k['exact']} exact points per warp tile, {k['steps_per_pass']} steps per HBM pass)")
     except Exception as e:  # the bench itself fails later if the library is missing
         return f"sync_tb_kernel (info unavailable: {e})"
+
+
+def steps_per_pass():
+    try:
+        return sync_kernel_info()["steps_per_pass"]
+    except Exception:
+        return STEPS_PER_PASS
 
 
 def config_dict(world):
@@ -199,7 +212,7 @@ def config_dict(world):
                     "10^4 FTCS steps (= 10 bench steps of 1000)" +
                     ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"),
         "N_per_gpu": N_PER_GPU, "N_total": N_PER_GPU * world, "r": R,
-        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": STEPS_PER_PASS,
+        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": steps_per_pass() if world == 1 else min(steps_per_pass(), 32),
         "kernel": sync_kernel_name(),
         "l2": "inputs larger than L2 (8 GiB per array vs 126 MB L2)",
         "parallelism": "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)",
@@ -269,10 +282,12 @@ def run_b200(args, rank, world, local):
     glups = total_updates / (ms * 1e-3) / 1e9
 
     # Roofline of the dominant kernel (sync_tb_kernel, one launch per pass of
-    # <= 32 steps; each 1000-step chunk is 31 passes of 32 + one of 8).
+    # <= steps_per_pass() steps, e.g. 31 passes of 32 + one of 8 per 1000 steps).
     # achieved = algorithmic bytes of all its launches / their device time;
     # the timed region is nothing but those back-to-back launches.
-    passes_per_step = -(-STEPS_PER_BENCH_STEP // STEPS_PER_PASS)
+    # multi-GPU slabs exchange 32-point ghosts: passes of <= 32 steps
+    spp = steps_per_pass() if world == 1 else min(steps_per_pass(), 32)
+    passes_per_step = -(-STEPS_PER_BENCH_STEP // spp)
     sync_launches = passes_per_step * args.steps
     per_launch_s = ms * 1e-3 / sync_launches
     alg_bytes_total = BYTES_PER_UPDATE * float(n) * STEPS_PER_BENCH_STEP * args.steps

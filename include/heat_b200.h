@@ -86,8 +86,10 @@ int heat_device_count(void);
 uint64_t heat_kernel_launches(void);
 /* The f64 synchronous pass kernel in use (HEAT_SYNC_VARIANT selects among
  * compiled variants): points per lane, window buffers per warp, exact points
- * per tile.  Host-only; no device needed. */
-int heat_sync_kernel_info(int* points_per_lane, int* buffers, int* exact_points_per_tile);
+ * per tile, steps per HBM pass (= halo points per side).  Host-only; no
+ * device needed. */
+int heat_sync_kernel_info(int* points_per_lane, int* buffers, int* exact_points_per_tile,
+                          int* steps_per_pass);
 
 /* set_strict_finite_checks / strict_finite_checks (sync_solver.hpp:77-78) */
 void heat_set_strict_finite_checks(int enabled);

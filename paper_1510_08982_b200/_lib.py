@@ -98,7 +98,7 @@ SIGNATURES = {
     "heat_version": (C.c_char_p, []),
     "heat_device_count": (_i, []),
     "heat_kernel_launches": (_u64, []),
-    "heat_sync_kernel_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "heat_sync_kernel_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "heat_set_strict_finite_checks": (None, [_i]),
     "heat_strict_finite_checks": (_i, []),
     "heat_trajectory_length": (_sz, [_sz, _sz, _sz]),

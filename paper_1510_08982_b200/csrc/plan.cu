@@ -120,7 +120,7 @@ int heat_plan_sync_advance(heat_plan* p, double r, int bc_kind, double c1, doubl
     g.pin_hi = (dir && p->rank == p->world - 1) ? kSlabHalo + (long long)p->n - 1 : -1;
     g.wrap = 0;
     return sync_advance_slab<double>(p->sms, p->ext, p->cur, g, r, c1, c2, steps, p->flag,
-                                     p->stream);
+                                     p->stream, kSlabHalo);
 }
 
 size_t heat_slab_halo(void) { return size_t(kSlabHalo); }

@@ -63,29 +63,34 @@ struct SyncVariant {
     int out;                  // exact points per tile
     int win_units, out_units; // tensor-map boxes (32-point units) of a window / its outputs
     int smem;                 // dynamic shared memory per CTA
+    int halo;                 // halo points per side = max steps per pass
     int blocks_per_sm;        // filled by the occupancy query
 };
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true>
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32>
 SyncVariant variant() {
-    using T = SyncTB<Real, V>;
-    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST>, NBUF, V, T::kOut, T::kWinUnits,
-            T::kOutUnits, T::smem_bytes(NBUF), 0};
+    using T = SyncTB<Real, V, H>;
+    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H>, NBUF, V, T::kOut, T::kWinUnits,
+            T::kOutUnits, T::smem_bytes(NBUF), H, 0};
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows)
-template <typename Real, int NBUF, bool TMA_ST = true>
+template <typename Real, int NBUF, bool TMA_ST = true, int H = 32>
 SyncVariant variant48() {
     if constexpr (sizeof(Real) == 8)
-        return variant<Real, 48, NBUF, 0, TMA_ST>();
+        return variant<Real, 48, NBUF, 0, TMA_ST, H>();
     else
         return variant<Real, kV, 2, 0>();
 }
-// 6: 48-point lanes, 2 buffers: 3874 GLUPS at 2^30 (V = 32, variant 4: 3761)
-constexpr int kDefaultSyncVariant = 6;
-constexpr int kSyncVariants = 11;
+// 11: 48-point lanes, 64-point halo, 2 buffers: +0.6% over variant 6 (48-point lanes,
+// 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Advances capped at
+// 32 steps per pass (multi-GPU slabs) use kHalo32Variant: a wider halo only wastes work there.
+constexpr int kDefaultSyncVariant = 11;
+constexpr int kHalo32Variant = 6;
+constexpr int kSyncVariants = 13;
 
-// The selected variant's table entry (no CUDA calls).
+// The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
+// the halo, i.e. the steps per pass the caller will ask for.
 template <typename Real>
-SyncVariant& sync_variant_entry() {
+SyncVariant& sync_variant_entry(int max_halo = 0) {
     // 0-5: V = 32 (buffers x step schedule); 6-8: wider lanes, same 32-point
     // halo (f64 only: an f32 lane of 48 points is not whole swizzle rows)
     static SyncVariant table[kSyncVariants] = {
@@ -100,18 +105,25 @@ SyncVariant& sync_variant_entry() {
         variant<Real, 64, 1, 0>(),   // 8: 64-point lanes, 1 buffer
         variant48<Real, 2, false>(), // 9: 48-point lanes, 2 load buffers, register stores
         variant<Real, kV, 2, 0, false>(),  // 10: 32-point lanes, 2 load buffers, register stores
+        variant48<Real, 2, true, 64>(),    // 11: 48-point lanes, 64-point halo (64 steps a pass)
+        variant<Real, 64, 1, 0, true, 64>(),  // 12: 64-point lanes, 64-point halo, 1 buffer
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
         const int v = e ? std::atoi(e) : kDefaultSyncVariant;
         return (v >= 0 && v < kSyncVariants) ? v : kDefaultSyncVariant;
     }();
+    if (max_halo > 0 && table[idx].halo > max_halo) {
+        // f32 keeps 32-point lanes (48 f32 values are not whole swizzle rows)
+        SyncVariant& h = table[sizeof(Real) == 8 ? kHalo32Variant : 4];
+        if (h.halo <= max_halo) return h;
+    }
     return table[idx];
 }
 
 template <typename Real>
-int sync_variant(SyncVariant** out) {
-    SyncVariant& v = sync_variant_entry<Real>();
+int sync_variant(SyncVariant** out, int max_halo = 0) {
+    SyncVariant& v = sync_variant_entry<Real>(max_halo);
     if (v.blocks_per_sm == 0) {
         HB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
@@ -151,8 +163,8 @@ struct SyncLauncher {
     SyncPassArgs a{};
 
     int init(int sms_, Real* b[2], const SlabGeom& g, double r, double c1, double c2,
-             unsigned int* flag) {
-        HB_TRY(sync_variant<Real>(&var));
+             unsigned int* flag, int max_halo = 0) {
+        HB_TRY(sync_variant<Real>(&var, max_halo));
         sms = sms_;
         bufs[0] = b[0];
         bufs[1] = b[1];
@@ -186,6 +198,7 @@ struct SyncLauncher {
              cudaStream_t st) {
         if (out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
         if (out_hi <= out_lo) return HEAT_OK;
+        if (nsteps > var->halo) return fail(HEAT_ELOGIC, "sync pass: more steps than the halo");
         const long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
         const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
         const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
@@ -208,13 +221,12 @@ template <typename Real>
 int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,
                       double c2, size_t steps, unsigned int* flag, cudaStream_t st,
                       int max_steps_per_pass) {
-    using T = SyncTB<Real, kV>;
     if (steps == 0) return HEAT_OK;
     if (g.out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
     SyncLauncher<Real> L;
-    HB_TRY(L.init(sms, bufs, g, r, c1, c2, flag));
-    const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, T::kMaxSteps)
-                                           : T::kMaxSteps;
+    HB_TRY(L.init(sms, bufs, g, r, c1, c2, flag, max_steps_per_pass));
+    const int halo = L.var->halo;
+    const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, halo) : halo;
     while (steps > 0) {
         const int s = int(std::min<size_t>(steps, size_t(cap)));
         // finite check on the last pass of this advance only
@@ -309,9 +321,10 @@ constexpr size_t kStreamMaxPasses = 128;              // above: copies are a sma
 // compute stream, and downloaded chunk by chunk on a second copy stream, so
 // the 2 x 8N bytes of PCIe traffic overlap the temporal-blocked passes.
 //
-// Pass pi of chunk c advances outputs R(pi, c) = [c*cp - (pi+1)*32,
-// (c+1)*cp - (pi+1)*32) (first range from 0, last to n): shifting each
-// pass's ranges by 32 points -- the reach of one pass of <= 32 steps --
+// Pass pi of chunk c advances outputs R(pi, c) = [B_c - (pi+1)*h,
+// B_{c+1} - (pi+1)*h) (first range from 0, last to n), h = the kernel's halo
+// (32 or 64 points): shifting each pass's ranges by h -- the reach of one
+// pass of <= h steps --
 // makes every input of R(pi, c) an output of passes already issued for
 // chunks <= c, and chunk c's first pass needs only uploaded chunks <= c.
 // Issued in chunk-major order on one stream, no launch overwrites values a
@@ -324,8 +337,6 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
                       size_t k_end, double* final_out) {
     using T = SyncTB<double, kV>;
     const long long N = (long long)n;
-    const long long S = (long long)((k_end + T::kMaxSteps - 1) / T::kMaxSteps);  // passes
-    const long long shift = T::kMaxSteps;
     const size_t pitch = (n + 63) / 64 * 64;
     HB_TRY(ensure_buffers(d, 2 * pitch * sizeof(double)));
     double* bufs[2] = {static_cast<double*>(d.buf[0]), static_cast<double*>(d.buf[0]) + pitch};
@@ -338,6 +349,8 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     g.pin_hi = N - 1;
     SyncLauncher<double> L;
     HB_TRY(L.init(d.sms, bufs, g, r, c1, c2, d.flag));
+    const long long shift = L.var->halo;  // steps per pass = reach of one pass
+    const long long S = ((long long)k_end + shift - 1) / shift;  // passes
     // Chunk boundaries.  A "wave" is one tile per resident warp; chunks of
     // whole waves keep every launch free of a ragged last wave.  Large fields
     // get graded chunks (4, 6, 10, 16, 26, 41 waves, <= 64-wave middle, the
@@ -402,7 +415,7 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
         g_launches.fetch_add(1, std::memory_order_relaxed);
         size_t left = k_end;
         for (long long pi = 0; pi < S; ++pi) {
-            const int s = int(std::min<size_t>(left, size_t(T::kMaxSteps)));
+            const int s = int(std::min<size_t>(left, size_t(shift)));
             HB_TRY(L.pass(int(pi & 1), lo(c, pi), hi(c, pi), s, pi == S - 1, st));
             left -= size_t(s);
         }
@@ -451,7 +464,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     // in the reference's order (a non-finite field before the end check).
     if (!f32 && final_out && !snapshots && !steps_out && bc_kind == HEAT_BC_DIRICHLET &&
         n >= kStreamMinPoints && k_end > 0 &&
-        (k_end + SyncTB<double, kV>::kMaxSteps - 1) / SyncTB<double, kV>::kMaxSteps <=
+        (k_end + sync_variant_entry<double>().halo - 1) / sync_variant_entry<double>().halo <=
             kStreamMaxPasses &&
         std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9 &&
         !std::getenv("HEAT_NO_STREAMED_SYNC"))
@@ -527,11 +540,12 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
 using namespace hb;
 
 extern "C" int heat_sync_kernel_info(int* points_per_lane, int* buffers,
-                                     int* exact_points_per_tile) {
+                                     int* exact_points_per_tile, int* steps_per_pass) {
     const SyncVariant& v = sync_variant_entry<double>();
     if (points_per_lane) *points_per_lane = v.V;
     if (buffers) *buffers = v.nbuf;
     if (exact_points_per_tile) *exact_points_per_tile = v.out;
+    if (steps_per_pass) *steps_per_pass = v.halo;
     return HEAT_OK;
 }
 

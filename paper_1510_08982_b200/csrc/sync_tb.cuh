@@ -36,18 +36,20 @@
 
 namespace hb {
 
-template <typename Real, int V>
+template <typename Real, int V, int H = 32>
 struct SyncTB {
     static constexpr int kChunkBytes = V * int(sizeof(Real));
     static constexpr int kRowsPerChunk = kChunkBytes / 128;       // 128-B swizzle rows
     static constexpr int kRowElems = 128 / int(sizeof(Real));
     static constexpr int kPer16 = 16 / int(sizeof(Real));         // elements per 16-B unit
     static constexpr int kBufBytes = kWarp * kChunkBytes;         // dense window
-    // The halo is 32 points per side whatever V is: a pass of <= 32 steps
-    // leaves window points [32, 32V-32) exact.  At V = 32 that is lanes
-    // 1..30; wider lanes (V = 48, 64) waste a smaller share on the halo and
-    // pay the per-tile costs (TMA, staging, pipeline fill) over more points.
-    static constexpr int kHalo = 32;
+    // The halo is H points per side (32 unless a variant asks for more): a
+    // pass of <= H steps leaves window points [H, 32V-H) exact.  At V = 32,
+    // H = 32 that is lanes 1..30; wider lanes (V = 48, 64) waste a smaller
+    // share on the halo and pay the per-tile costs (TMA, staging, pipeline
+    // fill) over more points; a wider halo (H = 64) pays the per-pass costs
+    // over more steps.
+    static constexpr int kHalo = H;
     static constexpr int kUnit = 32;  // tensor-map coordinate unit (points); windows start on one
     static constexpr int kWinUnits = kWarp * V / kUnit;
     static constexpr int kOutUnits = kWinUnits - 2 * kHalo / kUnit;
@@ -66,6 +68,7 @@ struct SyncTB {
     static_assert(kChunkBytes % 128 == 0, "chunk must be whole 128-B swizzle rows");
     static_assert(kBufBytes % 1024 == 0, "window buffers must keep the 1 KB swizzle alignment");
     static_assert((kWarp * V) % kUnit == 0 && kHalo % kUnit == 0, "windows of whole units");
+    static_assert(2 * kHalo < kWarp * V, "a window must keep exact points");
 };
 
 // Byte offset of 16-B unit `m` of lane-slot `slot`'s chunk in a 128B-swizzled
@@ -100,10 +103,10 @@ __device__ __forceinline__ void chunk_from_smem(const unsigned char* buf, int sl
 // store of the tile's output units: window row w lands at row w - kHaloRows,
 // so the store box starts at the (1 KB aligned) buffer start.  The halo
 // bounds are multiples of 32 elements, i.e. of whole 16-B units.
-template <typename Real, int V>
+template <typename Real, int V, int H = 32>
 __device__ __forceinline__ void chunk_to_smem_out(unsigned char* buf, int lane, const Real (&u)[V],
                                                   int el_lo, int el_hi) {
-    using T = SyncTB<Real, V>;
+    using T = SyncTB<Real, V, H>;
 #pragma unroll
     for (int m = 0; m < V / T::kPer16; ++m) {
         const int e0 = m * T::kPer16;
@@ -295,11 +298,11 @@ struct SyncPassArgs {
 //           (warp_steps_pipelined) for tiles without pinned ends.
 // TMA_ST: outputs leave through the window buffer with one TMA tensor store
 //         (NBUF = 2 only); false: 16-B vector stores straight from registers.
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true>
-__global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, SyncTB<Real, V>::min_blocks(NBUF))
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32>
+__global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, H>::min_blocks(NBUF))
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
-    using T = SyncTB<Real, V>;
+    using T = SyncTB<Real, V, H>;
     static_assert(NBUF == 1 || NBUF == 2, "one or two window buffers per warp");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 128B swizzle needs 1024-B aligned buffers
@@ -395,8 +398,8 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, SyncTB<Real, V>::mi
         }
 
         // exact elements of this lane: window points [kHalo, 32V - kHalo)
-        const int el_lo = lane == 0 ? T::kHalo : 0;
-        const int el_hi = lane == kWarp - 1 ? V - T::kHalo : V;
+        const int el_lo = min(V, max(0, T::kHalo - lane * V));
+        const int el_hi = min(V, max(0, kWarp * V - T::kHalo - lane * V));
         // Finite check only on the last pass of an advance: a non-finite value
         // at a non-pinned point never becomes finite again (c*NaN = NaN,
         // c*(+-Inf) = +-Inf or NaN), so the outcome of the reference's per-step
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V>::kThreads, SyncTB<Real, V>::mi
         const bool full = w0 + kWarp * V - T::kHalo <= a.out_hi;
         if (NBUF == 2 && TMA_ST && inter && full) {
             // stage the exact units as a [kOutUnits x rows] box at the buffer start
-            chunk_to_smem_out<Real, V>(buf, lane, u, el_lo, el_hi);
+            chunk_to_smem_out<Real, V, H>(buf, lane, u, el_lo, el_hi);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {

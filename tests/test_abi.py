@@ -56,9 +56,11 @@ def test_host_side_helpers_without_gpu():
     assert L.heat_trajectory_length(10, 10, 3) == 5      # steps 0,3,6,9,10
     assert L.heat_trajectory_length(2000, 250, 0) == 4    # default stride 100
     assert L.heat_slab_halo() == 32
-    v, nb, out = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    assert L.heat_sync_kernel_info(ctypes.byref(v), ctypes.byref(nb), ctypes.byref(out)) == 0
-    assert v.value in (32, 48, 64) and nb.value in (1, 2) and out.value == 32 * v.value - 64
+    v, nb, out, sp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    assert L.heat_sync_kernel_info(ctypes.byref(v), ctypes.byref(nb), ctypes.byref(out),
+                                   ctypes.byref(sp)) == 0
+    assert v.value in (32, 48, 64) and nb.value in (1, 2) and sp.value in (32, 64)
+    assert out.value == 32 * v.value - 2 * sp.value
     L.heat_set_strict_finite_checks(1)
     assert L.heat_strict_finite_checks() == 1
     L.heat_set_strict_finite_checks(0)
