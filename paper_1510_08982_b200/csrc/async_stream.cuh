@@ -217,15 +217,17 @@ __device__ __forceinline__ StreamItem decode_item(const AsyncStreamArgs& a, long
     return it;
 }
 
-template <int V>
-__global__ void __launch_bounds__(SyncTB<double, V>::kThreads, SyncTB<double, V>::min_blocks(2))
+template <int V, int H = 32>
+__global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double, V, H>::min_blocks(2))
     async_stream_kernel(const __grid_constant__ CUtensorMap tm_load0,
                         const __grid_constant__ CUtensorMap tm_load1,
                         const __grid_constant__ CUtensorMap tm_store0,
                         const __grid_constant__ CUtensorMap tm_store1, const AsyncStreamArgs a) {
-    using T = SyncTB<double, V>;
+    using T = SyncTB<double, V, H>;
     using A = Arith<double>;
     static_assert(V == 32 || V == 48, "PE last points sit at element 31 mod 32: 31 | 15, 31, 47");
+    // the host guarantees a PE's last tile holds >= H points, so no interior
+    // tile's window reaches into the next PE
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -487,8 +489,8 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, SyncTB<double, V>
         // ---- window out: the tile's exact points [w0 + kHalo, w0 + 32V - kHalo)
         // that lie inside this PE (bounds are multiples of 32 points)
         const bool full = w0 + kWarp * V - T::kHalo <= out_hi && w0 + T::kHalo >= lo;
-        int el_lo = lane == 0 ? T::kHalo : 0;  // a whole window inside the PE
-        int el_hi = lane == kWarp - 1 ? V - T::kHalo : V;
+        int el_lo = min(V, max(0, T::kHalo - lane * V));  // a whole window inside the PE
+        int el_hi = min(V, max(0, kWarp * V - T::kHalo - lane * V));
         if (!full) {  // clipped to the PE
             const long long ex_lo = max(w0 + T::kHalo, lo);
             const long long ex_hi = min(w0 + kWarp * V - T::kHalo, out_hi);
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(SyncTB<double, V>::kThreads, SyncTB<double, V>
         }
         unsigned char* bufb = wbase + b * T::kBufBytes;
         if (tma_ok(w0) && full) {
-            chunk_to_smem_out_split<double, V>(bufb, lane, u, el_lo, el_hi);
+            chunk_to_smem_out_split<double, V, H>(bufb, lane, u, el_lo, el_hi);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {

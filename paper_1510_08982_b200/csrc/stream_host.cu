@@ -10,15 +10,31 @@ namespace hb {
 
 namespace {
 
-// Points per lane of the stream kernel for PEs of n points: 48 like K1 when a
-// PE still spans >= 2 such tiles, else 32 (HEAT_ASYNC_LANE_POINTS=32 forces
-// 32 for A/B); the halo is 32 points either way.
-int stream_lane_points(size_t n) {
-    static const bool force32 = [] {
-        const char* e = std::getenv("HEAT_ASYNC_LANE_POINTS");
-        return e && std::atoi(e) == 32;
+// Tile geometry (points per lane V, halo H = steps per pass) of the stream
+// kernel for PEs of n points: the first of 48x64, 48x32, 32x32 under which
+// a PE spans >= 2 tiles and its last tile holds >= H points (an interior
+// tile's window must not reach into the next PE).  HEAT_ASYNC_GEOMETRY
+// ("48x64", "48x32", "32x32") forces one where it fits, for A/B.
+void stream_geometry(size_t n, int& V, int& H) {
+    static const int forced = [] {
+        const char* e = std::getenv("HEAT_ASYNC_GEOMETRY");
+        if (!e) return 0;
+        const std::string g(e);
+        return g == "48x64" ? 1 : g == "48x32" ? 2 : g == "32x32" ? 3 : 0;
     }();
-    return (!force32 && n > size_t(SyncTB<double, 48>::kOut)) ? 48 : 32;
+    const struct { int V, H; long long out; } cand[3] = {
+        {48, 64, SyncTB<double, 48, 64>::kOut},
+        {48, 32, SyncTB<double, 48, 32>::kOut},
+        {32, 32, SyncTB<double, 32, 32>::kOut}};
+    for (int i = forced ? forced - 1 : 0; i < 3; ++i) {
+        const long long rem = (long long)n % cand[i].out;
+        if ((long long)n > cand[i].out && (rem == 0 || rem >= cand[i].H)) {
+            V = cand[i].V;
+            H = cand[i].H;
+            return;
+        }
+    }
+    V = H = 32;
 }
 constexpr int kSU = 32;  // tensor-map unit (points); PEs are whole units
 
@@ -173,8 +189,8 @@ int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, 
     if (s.n % kSU != 0)
         return fail(HEAT_EINVAL, "async: PEs wider than 1024 points must be a multiple of 32 points");
     L.P = s.N / s.n;
-    L.V = stream_lane_points(s.n);
-    const long long tile_out = L.V == 48 ? SyncTB<double, 48>::kOut : SyncTB<double, 32>::kOut;
+    stream_geometry(s.n, L.V, L.H);
+    const long long tile_out = 32LL * L.V - 2LL * L.H;
     L.Tp = (s.n + tile_out - 1) / tile_out;
     if (L.Tp < 2) return fail(HEAT_ELOGIC, "async stream: a PE needs >= 2 tiles");
     L.G = (groups >= 1 && L.P % size_t(groups) == 0) ? groups : 1;
@@ -223,16 +239,16 @@ int stream_seed_external(cudaStream_t st, const double* field, const AsyncRunSpe
 }
 
 // Launch of the stream kernel with V-point lanes (tensor maps in 32-point units).
-template <int V>
+template <int V, int H>
 int launch_stream(int sms, cudaStream_t st, double* const bufs[2], int cur, long long N,
                   const AsyncStreamArgs& a) {
-    using T = SyncTB<double, V>;
+    using T = SyncTB<double, V, H>;
     static int per_sm = 0;
     const int smem = T::smem_bytes(2);
     if (per_sm == 0) {
-        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<V>,
+        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<V, H>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<V>,
+        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<V, H>,
                                                               T::kThreads, smem));
         if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
     }
@@ -243,8 +259,8 @@ int launch_stream(int sms, cudaStream_t st, double* const bufs[2], int cur, long
         HB_TRY(make_chunk_map_f64(&stm[b], bufs[b], nunits, T::kOutUnits));
     }
     // maps follow the pass parity: pass pi reads a.buf[pi & 1]
-    async_stream_kernel<V><<<sms * per_sm, T::kThreads, smem, st>>>(ld[cur], ld[cur ^ 1], stm[cur],
-                                                                   stm[cur ^ 1], a);
+    async_stream_kernel<V, H><<<sms * per_sm, T::kThreads, smem, st>>>(ld[cur], ld[cur ^ 1],
+                                                                      stm[cur], stm[cur ^ 1], a);
     HB_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return HEAT_OK;
@@ -309,7 +325,7 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.dirichlet = s.bc_kind == HEAT_BC_DIRICHLET;
     a.k0 = (long long)k0;
     a.steps = (long long)steps;
-    a.s = SyncTB<double, 32>::kMaxSteps;  // 32: the halo, whatever the lane width
+    a.s = L.H;  // steps per pass = the halo
     a.npass = (a.steps + a.s - 1) / a.s;
     a.mode = s.mode;
     a.q = int(s.q);
@@ -338,9 +354,11 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
         HB_CUDA(cudaEventRecord(e0, st));
     }
     if (L.V == 32)
-        HB_TRY(launch_stream<32>(sms, st, bufs, cur, (long long)s.N, a));
+        HB_TRY((launch_stream<32, 32>(sms, st, bufs, cur, (long long)s.N, a)));
+    else if (L.H == 32)
+        HB_TRY((launch_stream<48, 32>(sms, st, bufs, cur, (long long)s.N, a)));
     else
-        HB_TRY(launch_stream<48>(sms, st, bufs, cur, (long long)s.N, a));
+        HB_TRY((launch_stream<48, 64>(sms, st, bufs, cur, (long long)s.N, a)));
     if (device_ms) {
         HB_CUDA(cudaEventRecord(e1, st));
         HB_CUDA(cudaEventSynchronize(e1));

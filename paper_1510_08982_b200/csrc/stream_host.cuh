@@ -31,6 +31,7 @@ struct StreamLayout {
     int R = 0, D = 0;
     int G = 1;  // device groups inside this launch (> 1: emulated device boundaries)
     int V = 32; // points per lane of the stream kernel for this layout (48 or 32)
+    int H = 32; // halo points per side = steps per pass (64 or 32)
     size_t o_ringL, o_ringR, o_progL, o_progR, o_recvL, o_recvR, o_rprogL, o_rprogR, o_done,
         o_counter, o_offL, o_offR, o_dtab, o_stats, o_abort, o_links, o_seeds, bytes;
 };

@@ -122,12 +122,12 @@ __device__ __forceinline__ void chunk_to_smem_out(unsigned char* buf, int lane, 
 
 // chunk_to_smem_out with an unpredicated path for whole interior lanes
 // (measured: faster for the stream kernel K5, 0.5% slower for K1).
-template <typename Real, int V>
+template <typename Real, int V, int H = 32>
 __device__ __forceinline__ void chunk_to_smem_out_split(unsigned char* buf, int lane,
                                                         const Real (&u)[V], int el_lo, int el_hi) {
-    using T = SyncTB<Real, V>;
+    using T = SyncTB<Real, V, H>;
     if (el_lo != 0 || el_hi != V) {
-        chunk_to_smem_out<Real, V>(buf, lane, u, el_lo, el_hi);
+        chunk_to_smem_out<Real, V, H>(buf, lane, u, el_lo, el_hi);
         return;
     }
 #pragma unroll
