@@ -7,8 +7,9 @@ Workload (BASELINE.json configs[2], "cfg3"): N = 2^30 FP64 points per GPU,
 r = from_r(0.4), Dirichlet(0,0), sine initial profile, 10^4 FTCS time steps.
 One bench STEP = 1000 FTCS time steps over the whole field, so the default
 --steps 10 is exactly the cfg3 run.  For N > 1 GPUs (torchrun, one rank per
-GPU) each rank owns a 2^30-point slab of a G*2^30 domain (weak scaling) and
-exchanges 32-point ghosts with its neighbours every 32-step pass.
+GPU) each rank owns a 2^30-point slab of a G*2^30 domain (weak scaling; at
+G = 8 the total is cfg4's 2^33) and exchanges heat_slab_halo()-point ghosts
+(64) with its neighbours every pass of as many steps.
 
 Arms
   b200       the sm_100a kernels (libheat_b200.so) -- value is device-timed
@@ -199,6 +200,14 @@ def sync_kernel_name():
         return f"sync_tb_kernel (info unavailable: {e})"
 
 
+def slab_halo():
+    try:
+        from paper_1510_08982_b200 import _lib
+        return int(_lib.lib().heat_slab_halo())
+    except Exception:
+        return STEPS_PER_PASS
+
+
 def steps_per_pass():
     try:
         return sync_kernel_info()["steps_per_pass"]
@@ -212,7 +221,8 @@ def config_dict(world):
                     "10^4 FTCS steps (= 10 bench steps of 1000)" +
                     ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"),
         "N_per_gpu": N_PER_GPU, "N_total": N_PER_GPU * world, "r": R,
-        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": steps_per_pass() if world == 1 else min(steps_per_pass(), 32),
+        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": (steps_per_pass() if world == 1
+                           else min(steps_per_pass(), slab_halo())),
         "kernel": sync_kernel_name(),
         "l2": "inputs larger than L2 (8 GiB per array vs 126 MB L2)",
         "parallelism": "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)",
@@ -285,8 +295,8 @@ def run_b200(args, rank, world, local):
     # <= steps_per_pass() steps, e.g. 31 passes of 32 + one of 8 per 1000 steps).
     # achieved = algorithmic bytes of all its launches / their device time;
     # the timed region is nothing but those back-to-back launches.
-    # multi-GPU slabs exchange 32-point ghosts: passes of <= 32 steps
-    spp = steps_per_pass() if world == 1 else min(steps_per_pass(), 32)
+    # multi-GPU slabs exchange heat_slab_halo() ghosts: passes of at most as many steps
+    spp = steps_per_pass() if world == 1 else min(steps_per_pass(), slab_halo())
     passes_per_step = -(-STEPS_PER_BENCH_STEP // spp)
     sync_launches = passes_per_step * args.steps
     per_launch_s = ms * 1e-3 / sync_launches

@@ -98,7 +98,9 @@ struct SlabGeom {
     long long len = 0, out_lo = 0, out_hi = 0, pin_lo = -1, pin_hi = -1;
     int wrap = 0;
 };
-constexpr int kSlabHalo = 32;  // ghost points per side of a multi-GPU slab (= V)
+// ghost points per side of a multi-GPU slab = steps per exchange: the default
+// K1 variant's halo, so slab passes run the same 64-step kernel as one GPU
+constexpr int kSlabHalo = 64;
 
 template <typename Real>
 int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, double r, double c1,

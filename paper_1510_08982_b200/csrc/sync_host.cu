@@ -229,8 +229,15 @@ int sync_advance_slab(int sms, Real* bufs[2], int& cur, const SlabGeom& g, doubl
     const int cap = max_steps_per_pass > 0 ? std::min(max_steps_per_pass, halo) : halo;
     while (steps > 0) {
         const int s = int(std::min<size_t>(steps, size_t(cap)));
-        // finite check on the last pass of this advance only
-        HB_TRY(L.pass(cur, g.out_lo, g.out_hi, s, size_t(s) == steps, st));
+        // With `rem` steps still to go after this pass, the final outputs need
+        // this pass's values on [out_lo - rem, out_hi + rem): a slab whose
+        // ghosts were refreshed for the whole advance (ghost width >= steps)
+        // computes that shrinking light cone; a single domain clips it to
+        // [0, len).  The finite check runs on the last pass only.
+        const long long rem = (long long)(steps - size_t(s));
+        const long long lo = g.out_lo - rem > 0 ? (g.out_lo - rem) / kV * kV : 0;
+        const long long hi = std::min(g.len, g.out_hi + rem);
+        HB_TRY(L.pass(cur, lo, hi, s, rem == 0, st));
         cur ^= 1;
         steps -= size_t(s);
     }

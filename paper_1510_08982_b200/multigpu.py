@@ -1,7 +1,7 @@
 """Multi-GPU 1-D slab decomposition of the FTCS field.
 
 One process per GPU (torchrun).  Rank g owns points [g*n, (g+1)*n) of a global
-field of G*n points.  Every pass of s <= H steps (H = heat_slab_halo() = 32)
+field of G*n points.  Every pass of s <= H steps (H = heat_slab_halo() = 64)
 each rank needs the H points beyond each of its ends at the pass's start
 step: a nearest-neighbour halo exchange of 2 x H doubles (256 B each way),
 not a collective.  Only the true global ends are pinned (Dirichlet on rank 0

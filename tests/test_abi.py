@@ -55,7 +55,7 @@ def test_host_side_helpers_without_gpu():
     L = _lib.lib()
     assert L.heat_trajectory_length(10, 10, 3) == 5      # steps 0,3,6,9,10
     assert L.heat_trajectory_length(2000, 250, 0) == 4    # default stride 100
-    assert L.heat_slab_halo() == 32
+    assert L.heat_slab_halo() == 64
     v, nb, out, sp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     assert L.heat_sync_kernel_info(ctypes.byref(v), ctypes.byref(nb), ctypes.byref(out),
                                    ctypes.byref(sp)) == 0

@@ -1,11 +1,11 @@
 """Multi-GPU slab path of K1 (heat_plan_create_slab / halo_pack / halo_unpack,
 plan.cu) on ONE GPU: the G slabs of a world-G decomposition run one after
-another in this process (no kernel waits on another), their 32-point ghosts
+another in this process (no kernel waits on another), their H-point ghosts
 moved between passes exactly as multigpu.halo_exchange moves them over NCCL
 (send = [first H | last H] -> the neighbours' [left ghost | right ghost]).
 The gathered field must be bit-identical to the single-domain oracle; the
-slab advances run the 32-point-halo kernel whatever the default variant is
-(a 64-point halo would read past the 32 ghost points usefully exchanged)."""
+slab advances run the default kernel when its halo fits the 64 ghost points
+and the 32-point-halo variant otherwise (HEAT_SYNC_VARIANT=4 run)."""
 import numpy as np
 import pytest
 
