@@ -2,7 +2,9 @@
 // the small C-ABI entry points (errors, strict checks, trajectory sizing).
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <memory>
+#include <utility>
 
 #include "runtime.cuh"
 
@@ -68,6 +70,26 @@ int ensure_buffers(DevCtx& d, size_t bytes) {
                                      "): " + cudaGetErrorString(e));
     }
     d.bytes = bytes;
+    return HEAT_OK;
+}
+
+int kernel_smem_config(const void* fn, int smem, int threads, int* per_sm) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> cache;  // (kernel, device) -> CTAs/SM
+    int dev = 0;
+    HB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({fn, dev});
+    if (it != cache.end()) {
+        *per_sm = it->second;
+        return HEAT_OK;
+    }
+    HB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int n = 0;
+    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    if (n < 1) return fail(HEAT_ECUDA, "kernel does not fit on an SM");
+    cache[{fn, dev}] = n;
+    *per_sm = n;
     return HEAT_OK;
 }
 

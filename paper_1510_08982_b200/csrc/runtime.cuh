@@ -86,6 +86,11 @@ int dev_ctx(int device, DevCtx** out);
 int ensure_buffers(DevCtx& d, size_t bytes);
 int ensure_scratch(DevCtx& d, size_t bytes);
 
+// Sets `fn`'s dynamic shared memory limit to `smem` on the CURRENT device
+// (the attribute is per device) and returns its resident CTAs per SM for
+// `threads`-thread blocks; cached per (kernel, device).
+int kernel_smem_config(const void* fn, int smem, int threads, int* per_sm);
+
 // Validation helpers mirroring the reference's constructors.
 int check_field(const double* u, size_t n);  // BasicField ctor, core.hpp:45-51
 int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,

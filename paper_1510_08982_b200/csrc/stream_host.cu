@@ -243,15 +243,10 @@ template <int V, int H>
 int launch_stream(int sms, cudaStream_t st, double* const bufs[2], int cur, long long N,
                   const AsyncStreamArgs& a) {
     using T = SyncTB<double, V, H>;
-    static int per_sm = 0;
     const int smem = T::smem_bytes(2);
-    if (per_sm == 0) {
-        HB_CUDA(cudaFuncSetAttribute(async_stream_kernel<V, H>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, async_stream_kernel<V, H>,
-                                                              T::kThreads, smem));
-        if (per_sm < 1) return fail(HEAT_ECUDA, "async_stream_kernel does not fit on an SM");
-    }
+    int per_sm = 0;  // per device: the persistent grid is every resident CTA
+    HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(async_stream_kernel<V, H>), smem,
+                              T::kThreads, &per_sm));
     const long long nunits = N / T::kUnit;
     CUtensorMap ld[2], stm[2];
     for (int b = 0; b < 2; ++b) {

@@ -81,8 +81,8 @@ SyncVariant variant48() {
         return variant<Real, kV, 2, 0>();
 }
 // 11: 48-point lanes, 64-point halo, 2 buffers: +0.6% over variant 6 (48-point lanes,
-// 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Advances capped at
-// 32 steps per pass (multi-GPU slabs) use kHalo32Variant: a wider halo only wastes work there.
+// 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Callers that cap the
+// steps per pass below the default halo get kHalo32Variant.  tools/ab_sync.sh A/Bs them.
 constexpr int kDefaultSyncVariant = 11;
 constexpr int kHalo32Variant = 6;
 constexpr int kSyncVariants = 13;
@@ -92,7 +92,8 @@ constexpr int kSyncVariants = 13;
 template <typename Real>
 SyncVariant& sync_variant_entry(int max_halo = 0) {
     // 0-5: V = 32 (buffers x step schedule); 6-8: wider lanes, same 32-point
-    // halo (f64 only: an f32 lane of 48 points is not whole swizzle rows)
+    // halo (f64 only: an f32 lane of 48 points is not whole swizzle rows);
+    // 9-10: register stores instead of the TMA store; 11-12: 64-point halo
     static SyncVariant table[kSyncVariants] = {
         variant<Real, kV, 2, 1>(),
         variant<Real, kV, 2, 2>(),
@@ -124,15 +125,9 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
 template <typename Real>
 int sync_variant(SyncVariant** out, int max_halo = 0) {
     SyncVariant& v = sync_variant_entry<Real>(max_halo);
-    if (v.blocks_per_sm == 0) {
-        HB_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(v.fn),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem));
-        int per_sm = 0;
-        HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, reinterpret_cast<const void*>(v.fn), SyncTB<Real, kV>::kThreads, v.smem));
-        if (per_sm < 1) return fail(HEAT_ECUDA, "sync_tb_kernel does not fit on an SM");
-        v.blocks_per_sm = per_sm;
-    }
+    // per device (the current one): shared memory limit + occupancy
+    HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(v.fn), v.smem,
+                              SyncTB<Real, kV>::kThreads, &v.blocks_per_sm));
     *out = &v;
     return HEAT_OK;
 }
