@@ -149,6 +149,13 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
 // In-step draw ranks of the cross-PE reads (async_host.cu), returns D.
 int draw_offsets(size_t N, size_t n, int dirichlet, std::vector<int>& offL, std::vector<int>& offR);
 
+// K7 (sync_small.cu): the whole sync_run of a field of <= sync_small_max_points()
+// points in one CTA; arguments and errors as heat_sync_run (validated by the caller).
+size_t sync_small_max_points();
+int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                   size_t k_end, size_t stride, double* final_out, double* snapshots,
+                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots);
+
 // Synchronous advance on device buffers (ping-pong).  `cur` selects the
 // buffer holding u(k) on entry and is updated.  Does not synchronise.
 template <typename Real>

@@ -455,6 +455,11 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     if (stride == 0) stride = default_stride(n);
+    // Small f64 fields (the paper's regime): the whole run on one CTA (K7).
+    if (sizeof(Real) == 8 && n <= sync_small_max_points() && !std::getenv("HEAT_NO_SMALL_SYNC"))
+        return sync_run_small(reinterpret_cast<const double*>(u0), n, r, bc_kind, c1, c2, k_end,
+                              stride, final_out, snapshots, steps_out, max_snapshots,
+                              n_snapshots);
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
@@ -561,22 +566,8 @@ extern "C" int heat_sync_run(const double* u0, size_t n, double r, int bc_kind, 
                              double c2, size_t k_end, size_t stride, double* final_out,
                              double* snapshots, size_t* steps, size_t max_snapshots,
                              size_t* n_snapshots) {
-    // Small fields (the paper's regime): the exact synchronous trajectory via
-    // the warp-per-PE kernel with q = 1 -- one launch for all k_end steps,
-    // neighbour-only acquire/release flags instead of a launch per pass, and
-    // the trajectory written by the kernel.  Bit-identical to K1 and to the
-    // reference (q = 1 reduces async_run to sync_run, test_async_sim.cpp:110-129).
-    if (u0 && n >= 3 && n <= 8192 && k_end > 0 &&
-        (bc_kind == HEAT_BC_DIRICHLET || bc_kind == HEAT_BC_PERIODIC)) {
-        size_t P = 0, maxP = 8;  // 8 PE warps: measured best at N = 100-4096
-        if (const char* e = std::getenv("HEAT_SMALL_SYNC_PES")) maxP = std::max(1, std::atoi(e));
-        for (size_t cand = maxP; cand >= 1 && !P; --cand)
-            if (n % cand == 0 && n / cand <= 1024) P = cand;
-        if (P)
-            return async_run_core(u0, n, r, bc_kind, c1, c2, n / P, 1, HEAT_DELAY_UNIFORM, 0, 0.5,
-                                  0, k_end, stride, final_out, snapshots, steps, max_snapshots,
-                                  n_snapshots);
-    }
+    // Small fields go to K7 (one CTA, sync_small.cu), large Dirichlet runs
+    // that want only the final state to the streamed path, the rest to K1.
     return sync_run_impl<double>(u0, n, r, bc_kind, c1, c2, k_end, stride, final_out, snapshots,
                                  steps, max_snapshots, n_snapshots);
 }
