@@ -48,7 +48,7 @@ int heat_plan_create(heat_plan** out, size_t n, int device) {
     HB_CUDA(cudaMemset(p->base, 0, 2 * p->pitch * sizeof(double)));
     HB_CUDA(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking));
     p->stream = p->own;
-    HB_CUDA(cudaMalloc(&p->flag, 4 * sizeof(unsigned int)));
+    HB_CUDA(cudaMalloc(&p->flag, kFlagWords * sizeof(unsigned int)));
     HB_CUDA(cudaMemset(p->flag, 0, 4 * sizeof(unsigned int)));
     *out = p;
     return HEAT_OK;

@@ -61,6 +61,15 @@ extern std::atomic<bool> g_strict;
         if (s_ != HEAT_OK) return s_; \
     } while (0)
 
+// Flag words of a context (DevCtx / plan): [0] non-finite, [1] watchdog,
+// [2] input validation, [3] spare, [4..5] the K1 tile counter (u64) of the
+// context's stream -- one per stream owner, so concurrent contexts never
+// share it.
+constexpr int kFlagWords = 8;
+inline unsigned long long* tile_counter_of(unsigned int* flag) {
+    return reinterpret_cast<unsigned long long*>(flag + 4);
+}
+
 // Per-device state: a grow-only pair of field buffers for the one-shot
 // entry points, the non-finite flag word, and a private stream.
 struct DevCtx {

@@ -64,28 +64,30 @@ struct SyncVariant {
     int win_units, out_units; // tensor-map boxes (32-point units) of a window / its outputs
     int smem;                 // dynamic shared memory per CTA
     int halo;                 // halo points per side = max steps per pass
+    bool dyn;                 // tiles dealt by an atomic counter
     int blocks_per_sm;        // filled by the occupancy query
 };
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32>
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false>
 SyncVariant variant() {
     using T = SyncTB<Real, V, H>;
-    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H>, NBUF, V, T::kOut, T::kWinUnits,
-            T::kOutUnits, T::smem_bytes(NBUF), H, 0};
+    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H, DYN>, NBUF, V, T::kOut, T::kWinUnits,
+            T::kOutUnits, T::smem_bytes(NBUF), H, DYN, 0};
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows)
-template <typename Real, int NBUF, bool TMA_ST = true, int H = 32>
+template <typename Real, int NBUF, bool TMA_ST = true, int H = 32, bool DYN = false>
 SyncVariant variant48() {
     if constexpr (sizeof(Real) == 8)
-        return variant<Real, 48, NBUF, 0, TMA_ST, H>();
+        return variant<Real, 48, NBUF, 0, TMA_ST, H, DYN>();
     else
         return variant<Real, kV, 2, 0>();
 }
-// 11: 48-point lanes, 64-point halo, 2 buffers: +0.6% over variant 6 (48-point lanes,
-// 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Callers that cap the
-// steps per pass below the default halo get kHalo32Variant.  tools/ab_sync.sh A/Bs them.
-constexpr int kDefaultSyncVariant = 11;
+// 13: 48-point lanes, 64-point halo, 2 buffers, tiles dealt by an atomic counter:
+// +6.2% over its static-deal twin 11 (3980 vs 3748 GLUPS on one box), which was +0.6% over
+// 6 (48-point lanes, 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Callers
+// that cap the steps per pass below the default halo get kHalo32Variant.  tools/ab_sync.sh.
+constexpr int kDefaultSyncVariant = 13;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 13;
+constexpr int kSyncVariants = 14;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -108,6 +110,7 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant<Real, kV, 2, 0, false>(),  // 10: 32-point lanes, 2 load buffers, register stores
         variant48<Real, 2, true, 64>(),    // 11: 48-point lanes, 64-point halo (64 steps a pass)
         variant<Real, 64, 1, 0, true, 64>(),  // 12: 64-point lanes, 64-point halo, 1 buffer
+        variant48<Real, 2, true, 64, true>(),  // 13: as 11, tiles dealt by an atomic counter
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
@@ -205,6 +208,10 @@ struct SyncLauncher {
         p.dst = bufs[src ^ 1];
         p.nsteps = nsteps;
         p.check_finite = check;
+        if (var->dyn) {  // the stream owner's counter, zeroed in stream order
+            p.counter = tile_counter_of(a.nonfinite);
+            HB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
+        }
         var->fn<<<grid, T::kThreads, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);

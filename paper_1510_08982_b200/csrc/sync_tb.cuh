@@ -286,6 +286,7 @@ struct SyncPassArgs {
     int nsteps;
     unsigned int* nonfinite;  // set to 1 when an exact output value is not finite
     int check_finite;         // test the outputs of this pass (the last of an advance)
+    unsigned long long* counter;  // DYN kernels: tile counter, zero at launch
 };
 
 // NBUF = 2: the window of the next tile lands in the second buffer while this
@@ -298,7 +299,9 @@ struct SyncPassArgs {
 //           (warp_steps_pipelined) for tiles without pinned ends.
 // TMA_ST: outputs leave through the window buffer with one TMA tensor store
 //         (NBUF = 2 only); false: 16-B vector stores straight from registers.
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32>
+// DYN:    tiles handed out by an atomic counter (grabbed as soon as the
+//         current window is read) instead of a static round-robin deal.
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false>
 __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, H>::min_blocks(NBUF))
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
@@ -354,9 +357,14 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
 
     uint32_t phase = 0;
     bool bad = false;
-    long long t = (long long)blockIdx.x * T::kWarpsPerCta + warp;
+    auto grab = [&]() -> long long {
+        unsigned long long i = 0;
+        if (lane == 0) i = atomicAdd(a.counter, 1ull);
+        return (long long)__shfl_sync(0xffffffffu, i, 0);
+    };
+    long long t = DYN ? grab() : (long long)blockIdx.x * T::kWarpsPerCta + warp;
     if (t < a.tiles && interior(t)) issue(0, t);
-    for (int it = 0; t < a.tiles; ++it, t += nwarps) {
+    for (int it = 0; t < a.tiles; ++it) {
         const int b = NBUF == 2 ? (it & 1) : 0;
         unsigned char* buf = bufp(b);
         const long long w0 = window(t);
@@ -380,7 +388,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
                 }
             }
         }
-        const long long tn = t + nwarps;
+        const long long tn = DYN ? grab() : t + nwarps;
         if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
@@ -436,6 +444,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
             for (int i = 0; i < V; ++i)
                 if (i >= el_lo && i < el_hi && g0 + i < a.out_hi) dst[g0 + i] = u[i];
         }
+        t = tn;
     }
     if (NBUF == 2 && TMA_ST && lane == 0) bulk_wait_all();
     if (bad) atomicOr(a.nonfinite, 1u);
