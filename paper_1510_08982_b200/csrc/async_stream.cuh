@@ -294,26 +294,31 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         }
     };
 
-    long long pend_tile = -1;
-    unsigned int pend_pass = 0;
-    bool pend_generic = false;  // the pending tile left through per-lane stores
-    // Publish done[pend_tile] = pend_pass once its stores have landed
-    // (keep_groups = 1: the newest bulk store group may still be in flight).
+    // Done-signals are deferred and published in pairs: one release fence
+    // (fence.acq_rel.gpu, the costly part of a release store -- ncu: ERRBAR +
+    // MEMBAR were the largest non-FP64 stalls) then relaxed stores for both.
+    long long pend_tile[2] = {-1, -1};
+    unsigned int pend_pass[2] = {0, 0};
+    int npend = 0;
+    bool pend_generic = false;  // a pending tile left through per-lane stores
+    // Publish done[] of the pending tiles once their stores have landed.
+    // keep_groups = 1 only when the NEWEST bulk group is the current item's
+    // (not a pending one): every other group must be complete.
     auto signal_pending = [&](int keep_groups) {
+        if (npend == 0) return;
         if (pend_generic) __threadfence();  // every lane's generic stores first
         __syncwarp();
-        if (lane == 0) {  // TMA store group done, async-proxy writes ordered, release
+        if (lane == 0) {  // TMA store groups done, async-proxy writes ordered, release
             if (keep_groups)
                 asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
             else
                 bulk_wait_all();
-            if (pend_tile >= 0) {
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                st_release_gpu_u32(a.done + pend_tile, pend_pass);
-            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            fence_acq_rel_gpu();
+            for (int j = 0; j < npend; ++j) st_relaxed_gpu_u32(a.done + pend_tile[j], pend_pass[j]);
         }
         __syncwarp();
-        pend_tile = -1;
+        npend = 0;
         pend_generic = false;
     };
 
@@ -329,6 +334,10 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         const long long kbeg = a.k0 + it.pass * a.s;
         const int nst = int(min((long long)a.s, a.k0 + a.steps - kbeg));
 
+        // the next item's index: the atomic is issued now and read once this
+        // window is in, so its latency hides behind the window wait
+        unsigned long long nxt_raw = 0;
+        if (lane == 0) nxt_raw = atomicAdd(a.counter, 1ull);
         // ---- window in
         if (!cur_pref) {
             if (!deps_ready(it, false)) signal_pending(0);  // never block holding a signal
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         // tested half-way through this tile's steps, so the acquire latency
         // hides behind compute; the window prefetch then still has half a
         // tile of compute to land.
-        const long long nxt = grab();
+        const long long nxt = (long long)__shfl_sync(0xffffffffu, nxt_raw, 0);
         bool nxt_pref = false;
         StreamItem ni{};
         long long nlo = 0, nw0 = 0, nhi = 0;
@@ -521,10 +530,12 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         // Declare the PREVIOUS item done (its store has had a whole compute
         // phase to land: wait until at most this item's store group is in
         // flight), and keep this one pending.  Blocking waits flush first.
-        signal_pending(1);
-        pend_tile = (long long)it.p * a.Tp + it.m;
-        pend_pass = unsigned(it.pass + 1);
-        pend_generic = !(tma_ok(w0) && full);
+        const bool cur_bulk = tma_ok(w0) && full;  // this item's store is the newest group
+        if (npend == 2) signal_pending(cur_bulk ? 1 : 0);
+        pend_tile[npend] = (long long)it.p * a.Tp + it.m;
+        pend_pass[npend] = unsigned(it.pass + 1);
+        ++npend;
+        pend_generic |= !cur_bulk;
         cur = nxt;
         cur_pref = nxt_pref;
         if (nxt_pref) b ^= 1;

@@ -365,6 +365,10 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
     long long t = DYN ? grab() : (long long)blockIdx.x * T::kWarpsPerCta + warp;
     if (t < a.tiles && interior(t)) issue(0, t);
     for (int it = 0; t < a.tiles; ++it) {
+        // DYN: the next tile's index -- the atomic is issued now and read once
+        // this window is in, so its latency hides behind the window wait
+        unsigned long long nraw = 0;
+        if (DYN && lane == 0) nraw = atomicAdd(a.counter, 1ull);
         const int b = NBUF == 2 ? (it & 1) : 0;
         unsigned char* buf = bufp(b);
         const long long w0 = window(t);
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
                 }
             }
         }
-        const long long tn = DYN ? grab() : t + nwarps;
+        const long long tn = DYN ? (long long)__shfl_sync(0xffffffffu, nraw, 0) : t + nwarps;
         if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
