@@ -50,6 +50,7 @@ int dev_ctx(int device, DevCtx** out) {
             HB_CUDA(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
             HB_CUDA(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking));
             HB_CUDA(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking));
+            HB_CUDA(cudaStreamCreateWithFlags(&d->stream2, cudaStreamNonBlocking));
             HB_CUDA(cudaMalloc(&d->flag, kFlagWords * sizeof(unsigned int)));
             d->device = device;
         }

@@ -63,8 +63,8 @@ extern std::atomic<bool> g_strict;
 
 // Flag words of a context (DevCtx / plan): [0] non-finite, [1] watchdog,
 // [2] input validation, [3] spare, [4..5] the K1 tile counter (u64) of the
-// context's stream -- one per stream owner, so concurrent contexts never
-// share it.
+// context's stream, [6..7] that of its second compute stream (the streamed
+// sync_run) -- one per stream, so concurrent launches never share one.
 constexpr int kFlagWords = 8;
 inline unsigned long long* tile_counter_of(unsigned int* flag) {
     return reinterpret_cast<unsigned long long*>(flag + 4);
@@ -78,6 +78,7 @@ struct DevCtx {
     int sms = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the streamed sync_run
+    cudaStream_t stream2 = nullptr;             // its second compute stream
     void* buf[2] = {nullptr, nullptr};
     size_t bytes = 0;
     unsigned int* flag = nullptr;  // [0] non-finite, [1] watchdog timeout

@@ -192,8 +192,10 @@ struct SyncLauncher {
 
     // Advance outputs [out_lo, out_hi) by nsteps (<= V): reads bufs[src],
     // writes bufs[src ^ 1].
+    // counter_slot: which of the context's tile counters (one per stream that
+    // may run K1 concurrently) the launch uses.
     int pass(int src, long long out_lo, long long out_hi, int nsteps, bool check,
-             cudaStream_t st) {
+             cudaStream_t st, int counter_slot = 0) {
         if (out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
         if (out_hi <= out_lo) return HEAT_OK;
         if (nsteps > var->halo) return fail(HEAT_ELOGIC, "sync pass: more steps than the halo");
@@ -209,7 +211,7 @@ struct SyncLauncher {
         p.nsteps = nsteps;
         p.check_finite = check;
         if (var->dyn) {  // the stream owner's counter, zeroed in stream order
-            p.counter = tile_counter_of(a.nonfinite);
+            p.counter = tile_counter_of(a.nonfinite) + counter_slot;
             HB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
         }
         var->fn<<<grid, T::kThreads, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
@@ -397,7 +399,14 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     auto lo = [&](int c, long long pi) { return c == 0 ? 0 : B[c] - (pi + 1) * shift; };
     auto hi = [&](int c, long long pi) { return c == C - 1 ? N : B[c + 1] - (pi + 1) * shift; };
 
-    std::vector<cudaEvent_t> ev(2 * C + 1, nullptr);  // up[c], done[c], ready
+    // Chunks alternate between two compute streams.  Pass pi of chunk c needs
+    // pass pi-1 of chunks c and c-1 only (its inputs end inside R(pi-1, c) and
+    // begin inside R(pi-1, c-1)); every later pass of chunk c-1 touches its
+    // buffers only below where chunk c's pass-pi ranges begin.  So chunk c's
+    // early passes run beside chunk c-1's late ones, and each launch's last
+    // tiles share the GPU with the other stream's work instead of idling it.
+    cudaStream_t cs[2] = {st, d.stream2};
+    std::vector<cudaEvent_t> ev(size_t(C) + 1 + size_t(S) * C, nullptr);  // up[c], ready, E(pi,c)
     struct Cleanup {
         std::vector<cudaEvent_t>& e;
         ~Cleanup() {
@@ -407,38 +416,44 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     } cleanup{ev};
     for (auto& e : ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     cudaEvent_t* up = ev.data();
-    cudaEvent_t* done = ev.data() + C;
+    cudaEvent_t ready = ev[C];
+    auto E = [&](long long pi, int c) { return ev[size_t(C) + 1 + size_t(pi) * C + c]; };
 
-    // the flag reset on the compute stream precedes every upload
+    // the flag reset precedes every upload and every kernel on either stream
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
-    HB_CUDA(cudaEventRecord(ev[2 * C], st));
-    HB_CUDA(cudaStreamWaitEvent(d.h2d, ev[2 * C], 0));
+    HB_CUDA(cudaEventRecord(ready, st));
+    HB_CUDA(cudaStreamWaitEvent(d.h2d, ready, 0));
+    HB_CUDA(cudaStreamWaitEvent(cs[1], ready, 0));
     for (int c = 0; c < C; ++c) {
         const long long a0 = B[c], a1 = B[c + 1];
+        cudaStream_t s_c = cs[c & 1];
         HB_CUDA(cudaMemcpyAsync(bufs[0] + a0, u0 + a0, (a1 - a0) * sizeof(double),
                                 cudaMemcpyHostToDevice, d.h2d));
         HB_CUDA(cudaEventRecord(up[c], d.h2d));
-        HB_CUDA(cudaStreamWaitEvent(st, up[c], 0));
-        prep_chunk_kernel<<<d.sms * 2, 256, 0, st>>>(bufs[0], a0, a1, N, c1, c2, d.flag);
+        HB_CUDA(cudaStreamWaitEvent(s_c, up[c], 0));  // chunks <= c are in
+        prep_chunk_kernel<<<d.sms * 2, 256, 0, s_c>>>(bufs[0], a0, a1, N, c1, c2, d.flag);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         size_t left = k_end;
         for (long long pi = 0; pi < S; ++pi) {
+            if (c > 0 && pi > 0) HB_CUDA(cudaStreamWaitEvent(s_c, E(pi - 1, c - 1), 0));
             const int s = int(std::min<size_t>(left, size_t(shift)));
-            HB_TRY(L.pass(int(pi & 1), lo(c, pi), hi(c, pi), s, pi == S - 1, st));
+            HB_TRY(L.pass(int(pi & 1), lo(c, pi), hi(c, pi), s, pi == S - 1, s_c, c & 1));
+            HB_CUDA(cudaEventRecord(E(pi, c), s_c));
             left -= size_t(s);
         }
-        HB_CUDA(cudaEventRecord(done[c], st));
     }
     // downloads last: a pageable destination makes each copy block the host,
     // which must not hold back the compute launches above
     const int fin = int(S & 1);
     for (int c = 0; c < C; ++c) {
         const long long a0 = lo(c, S - 1), a1 = hi(c, S - 1);
-        HB_CUDA(cudaStreamWaitEvent(d.d2h, done[c], 0));
+        HB_CUDA(cudaStreamWaitEvent(d.d2h, E(S - 1, c), 0));
         HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0, (a1 - a0) * sizeof(double),
                                 cudaMemcpyDeviceToHost, d.d2h));
     }
+    HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 1), 0));  // both streams done
+    if (C > 1) HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 2), 0));
     unsigned int flags[4] = {0, 0, 0, 0};
     HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
     HB_CUDA(cudaStreamSynchronize(st));
