@@ -2,32 +2,36 @@
 //
 // Replaces detail::sync_step_into (sync_solver.hpp:26-39) iterated by
 // run_impl (sync_solver.cpp:70-75) and run_barriered (async_exec.cpp:57-114):
-// one launch advances the whole field by `nsteps` (<= V) Jacobi steps.
+// one launch advances a range of the field by `nsteps` (<= H) Jacobi steps.
 //
-// Layout / mapping
+// Layout / mapping (template V points per lane, halo H; default 48 x 64)
 //   * A WARP owns one tile: 32 lanes x V consecutive points (a "window" of
 //     32V points).  Lane l holds points [w0 + lV, w0 + (l+1)V) in registers.
 //   * Neighbour values inside a lane are registers; across lanes one
 //     __shfl_up / __shfl_down of the boundary PRODUCT r*u per step.
-//   * Lanes 0 and 31 are halo (redundant recompute).  After s <= V steps
-//     lanes 1..30 are exact, so a tile emits 30V points: tile t covers
-//     outputs [out_lo + 30Vt, out_lo + 30V(t+1)), window w0 = that - V.
-//   * No block barrier anywhere: warps are independent.  Each warp
-//     double-buffers its window in shared memory.  One elected lane moves a
-//     whole window with ONE TMA tensor copy (cp.async.bulk.tensor.3d, SASS
-//     UTMALDG) into a 128B-swizzled buffer -- the tensor map views the array
-//     as [chunk][row][16 doubles] so each lane's chunk is two 128-B rows and
-//     the swizzle makes the per-lane 16-B shared loads conflict-light -- while
-//     the previous tile is being stepped; results return through the same
-//     buffer with one TMA tensor store (UTMASTG) of the 30 exact chunks.
+//   * The first and last H points of the window are halo (redundant
+//     recompute): after s <= H steps points [H, 32V - H) are exact, so a tile
+//     emits 32V - 2H points: tile t covers outputs [out_lo + t*kOut,
+//     out_lo + (t+1)*kOut), window w0 = that - H.  (V = 32, H = 32: lanes
+//     1..30.)
+//   * No block barrier anywhere: warps are independent.  Tiles are dealt
+//     statically (warp w: tiles w, w + nwarps, ...) or, in the DYN variants
+//     (the default), by an atomic counter so no warp idles at a pass's end.
+//   * Each warp double-buffers its window in shared memory.  One elected lane
+//     moves a whole window with ONE TMA tensor copy (cp.async.bulk.tensor.3d,
+//     SASS UTMALDG) into a 128B-swizzled buffer -- the tensor map views the
+//     array in 32-point units of two 128-B rows, and the swizzle makes the
+//     per-lane 16-B shared loads conflict-light -- while the previous tile is
+//     being stepped; results return through the same buffer, staged shifted
+//     by the halo, with one TMA tensor store (UTMASTG) of the exact units.
 //   * Tiles whose window touches a pinned end, leaves [0, len) or whose
 //     outputs overrun out_hi take the generic path: per-lane element loads
 //     (zero fill or modular wrap), Dirichlet ends re-pinned after every
 //     step, bounds-checked stores.
 //
-// HBM traffic per pass: read 32V + write 30V points per 30V*s updates, i.e.
-// ~16.5/s bytes per lattice update (0.52 B at s = 32) -- the pass is bound by
-// the FP64 pipe (4 DP instructions per update), not by HBM.
+// HBM traffic per pass: read 32V + write 32V - 2H points per (32V - 2H)*s
+// updates, i.e. ~16/s bytes per lattice update (0.25 B at s = 64) -- the
+// pass is bound by the FP64 pipe (4 DP instructions per update), not by HBM.
 #pragma once
 
 #include <cuda.h>
