@@ -1,5 +1,5 @@
-"""Small-N synchronous path (heat_sync_run -> K3 barrier mode): device ns/step
-for the PE count HEAT_SMALL_SYNC_PES caps (A/B helper)."""
+"""Small-N synchronous path (exec_run(Barriered) -> heat_sync_run -> K7, or K1
+with HEAT_NO_SMALL_SYNC=1): device ns/step at N = 100, 1024, 4096."""
 import os
 import sys
 import numpy as np
@@ -14,4 +14,5 @@ for n in (100, 1024, 4096):
                          H.BoundaryCondition.dirichlet(0, 0), H.PartitionSpec(n, n // 4),
                          H.ExecConfig(4, K, H.ExecMode.Barriered, False, 0))
         best = res.duration_ns if best is None else min(best, res.duration_ns)
-    print(f"PES<={os.environ.get('HEAT_SMALL_SYNC_PES', '16')} n={n}: {best / K:.1f} ns/step")
+    path = "K1" if os.environ.get("HEAT_NO_SMALL_SYNC") else "K7"
+    print(f"{path} n={n}: {best / K:.1f} ns/step")
