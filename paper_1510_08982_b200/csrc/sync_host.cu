@@ -73,13 +73,14 @@ SyncVariant variant() {
     return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H, DYN>, NBUF, V, T::kOut, T::kWinUnits,
             T::kOutUnits, T::smem_bytes(NBUF), H, DYN, 0};
 }
-// 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows)
+// 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows);
+// f32 takes 64-point lanes (256 B, two rows) with the same halo, buffers and deal
 template <typename Real, int NBUF, bool TMA_ST = true, int H = 32, bool DYN = false>
 SyncVariant variant48() {
     if constexpr (sizeof(Real) == 8)
         return variant<Real, 48, NBUF, 0, TMA_ST, H, DYN>();
     else
-        return variant<Real, kV, 2, 0>();
+        return variant<Real, 64, NBUF, 0, TMA_ST, H, DYN>();
 }
 // 13: 48-point lanes, 64-point halo, 2 buffers, tiles dealt by an atomic counter:
 // +6.2% over its static-deal twin 11 (3980 vs 3748 GLUPS on one box), which was +0.6% over

@@ -111,6 +111,19 @@ def test_f32_bit_exact_vs_port(H, port):
     assert bits_equal(got.final().values(), port.sync_run_f32(u, 0.3, 1, 0, 0, 77))
 
 
+@pytest.mark.parametrize("periodic", [False, True])
+def test_f32_large_bit_exact_vs_port(H, port, periodic):
+    # many K1 f32 tiles (64-point lanes), two full passes and a partial one
+    n = (1 << 20) + 777
+    gen = SplitMix64(31 + periodic)
+    u = random_field(gen, n)
+    c1, c2 = (0.0, 0.0) if periodic else (float(u[0]), float(u[-1]))
+    bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(c1, c2)
+    got = H.sync_run_f32(H.TemperatureField(u), H.SolverParams.from_r(0.45), bc, 150, 150)
+    exp = port.sync_run_f32(u, 0.45, 1 if periodic else 0, c1, c2, 150)
+    assert bits_equal(got.final().values(), exp)
+
+
 def test_divergence_errors(H):
     # test_sync.cpp:151-162 (strict) and the TemperatureField ctor (non-strict).
     v = np.zeros(8)
