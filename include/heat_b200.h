@@ -78,6 +78,19 @@ typedef struct heat_async_stats {
     double   residual_sum; /* sum_k ||u(k+1) - A u(k)||_inf (a-posteriori bound), when logged */
 } heat_async_stats;
 
+/* ---- AsyncSimulator (async_sim.hpp:73-90) on the GPU ---------------------
+ * create = the ctor (prepared field, partition and q checks), step(count) =
+ * count x AsyncSimulator::step(), current = current() + step_index().  The
+ * handle owns its device state; any slicing of the steps is bit-identical to
+ * async_run over the whole (counter-form draws, persistent PE rings). */
+typedef struct heat_async_sim heat_async_sim;
+int heat_async_sim_create(heat_async_sim** sim, const double* u0, size_t n, double r, int bc_kind,
+                          double c1, double c2, size_t per_pe, size_t q, int law,
+                          size_t fixed_delay, double geometric_p, uint64_t seed);
+int heat_async_sim_step(heat_async_sim* sim, size_t count);
+int heat_async_sim_current(heat_async_sim* sim, double* field_out, size_t* step_index);
+int heat_async_sim_destroy(heat_async_sim* sim);
+
 /* ---- library state ---------------------------------------------------- */
 const char* heat_last_error(void);
 const char* heat_version(void);

@@ -113,6 +113,11 @@ SIGNATURES = {
                                _psz, _sz, _psz, _pd, _pd, _pd, _pd]),
     "heat_exec_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _i, _sz, _pd, _pu64,
                            _P(LagStatsC), _P(AsyncStatsC)]),
+    "heat_async_sim_create": (_i, [_P(_vp), _pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d,
+                                   _u64]),
+    "heat_async_sim_step": (_i, [_vp, _sz]),
+    "heat_async_sim_current": (_i, [_vp, _pd, _P(_sz)]),
+    "heat_async_sim_destroy": (_i, [_vp]),
     "heat_plan_create": (_i, [_P(_vp), _sz, _i]),
     "heat_plan_destroy": (_i, [_vp]),
     "heat_plan_set_stream": (_i, [_vp, _vp]),

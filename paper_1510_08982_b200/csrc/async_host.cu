@@ -631,3 +631,271 @@ static int plan_async(heat_plan* p, const AsyncRunSpec& s, heat_async_stats* sta
 }
 
 }  // extern "C"
+
+// ---- AsyncSimulator on the GPU (async_sim.hpp:73-90, async_sim.cpp:122-140) --
+// A handle owns its device state -- field(s), the PE rings and progress
+// words, the draw offsets -- and advances it in slices [k, k + count): the
+// kernels take absolute step numbers, the counter-form draws need no stream
+// state, and K3's rings / K5's scratch persist between slices, so stepping a
+// run in any slicing is bit-identical to async_run over the whole.
+struct heat_async_sim {
+    hb::DevCtx ctx;  // own stream, flag words, buffers, scratch
+    hb::AsyncRunSpec s{};
+    size_t P = 0;
+    bool wide = false;
+    double* field[2] = {nullptr, nullptr};
+    int cur = 0;
+    size_t k = 0;
+    bool started = false;
+    // K3 scratch layout
+    int R = 0, D = 0, V = 1;
+    size_t o_ring = 0, o_prog = 0, o_offL = 0, o_offR = 0, o_abort = 0;
+    bool shared = false;
+    size_t smem = 0;
+    // K5
+    hb::StreamLayout L;
+    std::vector<int> offL, offR;
+    // GEOMETRIC: host-drawn delays of the current slice
+    unsigned char* dtab = nullptr;
+    size_t dtab_bytes = 0;
+};
+
+namespace {
+
+void sim_free(heat_async_sim* sim) {
+    if (!sim) return;
+    cudaSetDevice(sim->ctx.device);
+    if (sim->ctx.stream) cudaStreamSynchronize(sim->ctx.stream);
+    if (sim->ctx.buf[0]) cudaFree(sim->ctx.buf[0]);
+    if (sim->ctx.scratch) cudaFree(sim->ctx.scratch);
+    if (sim->ctx.flag) cudaFree(sim->ctx.flag);
+    if (sim->dtab) cudaFree(sim->dtab);
+    if (sim->ctx.stream) cudaStreamDestroy(sim->ctx.stream);
+    delete sim;
+}
+
+// Delays of steps [k0, k0 + count) for the geometric law (glibc log1p, as
+// async_pe_run draws them), uploaded to the handle's table.
+int sim_geometric_table(heat_async_sim* sim, size_t k0, size_t count, int D) {
+    const auto& s = sim->s;
+    std::vector<unsigned char> t(std::max<size_t>(1, count * size_t(D)));
+    const double lp = std::log1p(-s.geometric_p);
+    for (size_t j = 0; j < count; ++j) {
+        const size_t k = k0 + j;
+        const size_t bound = std::min<size_t>(s.q - 1, k);
+        for (int o = 0; o < D; ++o) {
+            const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * uint64_t(D) + uint64_t(o));
+            const double u = double(x >> 11) * 0x1.0p-53;
+            double g = std::floor(std::log1p(-u) / lp);
+            if (!std::isfinite(g) || g < 0.0) g = 0.0;
+            t[j * D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
+        }
+    }
+    if (sim->dtab_bytes < t.size()) {
+        if (sim->dtab) cudaFree(sim->dtab);
+        sim->dtab = nullptr;
+        sim->dtab_bytes = 0;
+        HB_CUDA(cudaMalloc(&sim->dtab, t.size()));
+        sim->dtab_bytes = t.size();
+    }
+    HB_CUDA(cudaMemcpyAsync(sim->dtab, t.data(), t.size(), cudaMemcpyHostToDevice,
+                            sim->ctx.stream));
+    HB_CUDA(cudaStreamSynchronize(sim->ctx.stream));  // the host vector goes
+    return HEAT_OK;
+}
+
+int sim_step_k3(heat_async_sim* sim, size_t count) {
+    DevCtx& d = sim->ctx;
+    const auto& s = sim->s;
+    char* base = static_cast<char*>(d.scratch);
+    cudaStream_t st = d.stream;
+    if (!sim->started) {
+        async_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (sim->P * 2 * sim->R + 255) / 256)),
+                            256, 0, st>>>(sim->field[0], int(s.n), int(sim->P), sim->R,
+                                          reinterpret_cast<double*>(base + sim->o_ring),
+                                          reinterpret_cast<unsigned long long*>(base + sim->o_prog),
+                                          nullptr);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        HB_CUDA(cudaMemcpyAsync(base + sim->o_offL, sim->offL.data(), sim->P * sizeof(int),
+                                cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemcpyAsync(base + sim->o_offR, sim->offR.data(), sim->P * sizeof(int),
+                                cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaMemsetAsync(base + sim->o_abort, 0, sizeof(unsigned int), st));
+        sim->started = true;
+    }
+    if (s.law == HEAT_DELAY_GEOMETRIC) HB_TRY(sim_geometric_table(sim, sim->k, count, sim->D));
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
+    AsyncPeArgs a{};
+    a.field = sim->field[0];
+    a.N = (long long)s.N;
+    a.n = int(s.n);
+    a.P = int(sim->P);
+    a.r = s.r;
+    a.c = 1.0 - 2.0 * s.r;  // core.hpp:108
+    a.c1 = s.c1;
+    a.c2 = s.c2;
+    a.dirichlet = s.bc_kind == HEAT_BC_DIRICHLET;
+    a.k0 = (long long)sim->k;
+    a.k1 = (long long)(sim->k + count);
+    a.mode = 0;
+    a.q = int(s.q);
+    a.R = sim->R;
+    a.law = s.law;
+    a.fixed_d = int(std::min<size_t>(s.fixed_d, 1u << 30));
+    a.seed = s.seed;
+    a.modq = make_modq(unsigned(s.q));
+    a.D = sim->D;
+    a.off_left = reinterpret_cast<const int*>(base + sim->o_offL);
+    a.off_right = reinterpret_cast<const int*>(base + sim->o_offR);
+    a.dtable = sim->dtab;
+    a.dtab_k0 = (long long)sim->k;
+    a.ring = reinterpret_cast<double*>(base + sim->o_ring);
+    a.prog = reinterpret_cast<unsigned long long*>(base + sim->o_prog);
+    a.flag = d.flag;
+    a.abort_word = reinterpret_cast<unsigned int*>(base + sim->o_abort);
+    a.timeout_ns = 20ull * 1000 * 1000 * 1000;
+    return launch_pe(sim->V, sim->shared, true, a, int(sim->P), st, sim->smem);
+}
+
+int sim_step_k5(heat_async_sim* sim, size_t count) {
+    DevCtx& d = sim->ctx;
+    StreamExternal ext{};
+    if (sim->s.law == HEAT_DELAY_GEOMETRIC) {
+        HB_TRY(sim_geometric_table(sim, sim->k, count, sim->L.D));
+        ext.dtab = sim->dtab;
+        ext.dtab_k0 = (long long)sim->k;
+    }
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), d.stream));
+    const bool init = !sim->started;
+    sim->started = true;
+    return async_stream_advance(d.sms, d.stream, sim->field, sim->cur, sim->s, sim->L,
+                                static_cast<char*>(d.scratch), ext, sim->offL, sim->offR,
+                                sim->k, count, init, d.flag, nullptr);
+}
+
+}  // namespace
+
+extern "C" {
+
+int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, double r,
+                          int bc_kind, double c1, double c2, size_t per_pe, size_t q, int law,
+                          size_t fixed_delay, double geometric_p, uint64_t seed) {
+    if (!out) return fail(HEAT_EINVAL, "null simulator handle");
+    *out = nullptr;
+    // the caller's objects validate first (TemperatureField, DelayModel,
+    // PartitionSpec ctors), then AsyncSimulator's ctor (async_sim.cpp:122-134):
+    // prepare_initial, partition vs grid, q >= 1
+    if (N < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    if (!u0) return fail(HEAT_EINVAL, "null field pointer");
+    if (law == HEAT_DELAY_FIXED && q > 0 && fixed_delay >= q)
+        return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
+    if (law == HEAT_DELAY_GEOMETRIC && (!(geometric_p > 0.0) || geometric_p > 1.0))
+        return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
+    if (law < 0 || law > 2) return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
+    if (per_pe == 0 || N % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
+    if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
+        return fail(HEAT_EINVAL, "unknown boundary condition kind");
+    int dev = 0;
+    HB_CUDA(cudaGetDevice(&dev));
+    DevCtx* shared_ctx = nullptr;
+    HB_TRY(dev_ctx(dev, &shared_ctx));  // device checks (sm_100)
+    auto* sim = new heat_async_sim();
+    struct Guard {
+        heat_async_sim*& p;
+        ~Guard() {
+            if (p) sim_free(p);
+        }
+    } guard{sim};
+    DevCtx& d = sim->ctx;
+    d.device = dev;
+    d.sms = shared_ctx->sms;
+    HB_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    HB_CUDA(cudaMalloc(&d.flag, kFlagWords * sizeof(unsigned int)));
+    HB_CUDA(cudaMemset(d.flag, 0, kFlagWords * sizeof(unsigned int)));
+    sim->P = N / per_pe;
+    sim->wide = per_pe > 32 * 32 && sim->P > 1;
+    const size_t pitch = (N + 63) / 64 * 64;
+    // two buffers for K5 and for a single PE (K1 ping-pong), one for K3
+    HB_TRY(ensure_buffers(d, (sim->wide || sim->P == 1 ? 2 : 1) * pitch * sizeof(double)));
+    sim->field[0] = static_cast<double*>(d.buf[0]);
+    sim->field[1] = sim->field[0] + pitch;
+    HB_TRY(upload_prepared(d, u0, N, bc_kind, c1, c2, sim->field[0]));
+    // HistoryRing(q, prepare_initial(u0, bc)) in the ctor's initialiser list
+    if (q == 0) return fail(HEAT_EDOMAIN, "HistoryRing: depth >= 1 required");
+    sim->s = AsyncRunSpec{N, per_pe, r, bc_kind, c1, c2, 0, q, law, fixed_delay, geometric_p, seed,
+                          0, false};
+    if (sim->P == 1) {
+        // one PE never reads across: plain synchronous steps (K1 on field[0..1])
+        sim->wide = true;
+    }
+    if (sim->wide && sim->P > 1) {
+        HB_TRY(stream_layout(sim->s, 1, StreamExternal{}, sim->L, sim->offL, sim->offR));
+        HB_TRY(ensure_scratch(d, sim->L.bytes));
+    } else if (!sim->wide) {
+        sim->V = 1;
+        while (sim->V * 32 < int(per_pe)) sim->V *= 2;
+        sim->R = pick_ring(int(q));
+        sim->D = draw_offsets(N, per_pe, bc_kind == HEAT_BC_DIRICHLET, sim->offL, sim->offR);
+        size_t off = 0;
+        auto take = [&](size_t bytes) {
+            size_t o = off;
+            off += align256(bytes);
+            return o;
+        };
+        sim->o_ring = take(sim->P * 2 * sim->R * sizeof(double));
+        sim->o_prog = take(sim->P * sizeof(unsigned long long));
+        sim->o_offL = take(sim->P * sizeof(int));
+        sim->o_offR = take(sim->P * sizeof(int));
+        sim->o_abort = take(sizeof(unsigned int));
+        HB_TRY(ensure_scratch(d, off));
+        sim->smem = sim->P * 2 * sim->R * sizeof(double) + sim->P * sizeof(unsigned long long);
+        sim->shared = sim->P <= 16 && sim->smem <= 160 * 1024;
+    }
+    *out = sim;
+    sim = nullptr;  // owned by the caller now
+    return HEAT_OK;
+}
+
+int heat_async_sim_step(heat_async_sim* sim, size_t count) {
+    if (!sim) return fail(HEAT_EINVAL, "null simulator handle");
+    if (count == 0) return HEAT_OK;
+    HB_CUDA(cudaSetDevice(sim->ctx.device));
+    if (sim->P == 1) {  // a single PE: synchronous steps
+        HB_CUDA(cudaMemsetAsync(sim->ctx.flag, 0, 2 * sizeof(unsigned int), sim->ctx.stream));
+        HB_TRY(sync_advance<double>(sim->ctx.sms, sim->field, sim->cur, (long long)sim->s.N,
+                                    sim->s.r, sim->s.bc_kind == HEAT_BC_PERIODIC, sim->s.c1,
+                                    sim->s.c2, count, sim->ctx.flag, sim->ctx.stream));
+    } else if (sim->wide) {
+        HB_TRY(sim_step_k5(sim, count));
+    } else {
+        HB_TRY(sim_step_k3(sim, count));
+    }
+    unsigned int flags[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, sim->ctx.flag, sizeof flags, cudaMemcpyDeviceToHost,
+                            sim->ctx.stream));
+    HB_CUDA(cudaStreamSynchronize(sim->ctx.stream));
+    sim->k += count;
+    if (flags[1]) return fail(HEAT_ETIMEOUT, "async halo-ring wait exceeded its deadline");
+    // async_step_into checks only under strict finite checks (async_sim.cpp:102-104)
+    if (flags[0] && g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+    return HEAT_OK;
+}
+
+int heat_async_sim_current(heat_async_sim* sim, double* out, size_t* step_index) {
+    if (!sim) return fail(HEAT_EINVAL, "null simulator handle");
+    HB_CUDA(cudaSetDevice(sim->ctx.device));
+    if (out)
+        HB_CUDA(cudaMemcpyAsync(out, sim->field[sim->cur], sim->s.N * sizeof(double),
+                                cudaMemcpyDeviceToHost, sim->ctx.stream));
+    HB_CUDA(cudaStreamSynchronize(sim->ctx.stream));
+    if (step_index) *step_index = sim->k;
+    return HEAT_OK;
+}
+
+int heat_async_sim_destroy(heat_async_sim* sim) {
+    sim_free(sim);
+    return HEAT_OK;
+}
+
+}  // extern "C"

@@ -332,7 +332,8 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.D = L.D;
     a.off_left = at<const int>(base, L.o_offL);
     a.off_right = at<const int>(base, L.o_offR);
-    a.dtable = at<const unsigned char>(base, L.o_dtab);
+    a.dtable = ext.dtab ? ext.dtab : at<const unsigned char>(base, L.o_dtab);
+    a.dtab_k0 = ext.dtab ? ext.dtab_k0 : 0;
     a.links = at<const PeLink>(base, L.o_links);
     a.pin_first_pe = pin_first;
     a.pin_last_pe = pin_last;

@@ -23,6 +23,10 @@ struct StreamExternal {
     unsigned long long* right_push_prog = nullptr;
     long long pe_offset = 0;  // global index of local PE 0
     long long P_global = 0;   // 0 = this launch holds the whole domain
+    // GEOMETRIC law, stepping a run in slices (heat_async_sim_*): a device
+    // table of the delays of steps [dtab_k0, ...) replacing the layout's own
+    const unsigned char* dtab = nullptr;
+    long long dtab_k0 = 0;
 };
 
 // Device scratch of one streaming run (rings persist across its launches).

@@ -338,6 +338,56 @@ def async_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
                        extra=(part.per_pe(), *model._args()))
 
 
+class AsyncSimulator:
+    """AsyncSimulator (async_sim.hpp:73-90, async_sim.cpp:122-140) on the GPU.
+
+    The device holds the field, the PE edge rings and the draw offsets;
+    step(count) = count x AsyncSimulator::step().  Any slicing of the steps
+    is bit-identical to async_run over the whole run."""
+
+    def __init__(self, u0, params: SolverParams, bc: BoundaryCondition, part: PartitionSpec,
+                 model: DelayModel):
+        v = _field(u0)
+        self._h = C.c_void_p()
+        self.n = v.size
+        # prepare_initial runs before the partition check (async_sim.cpp:122-134):
+        # a mismatched partition is checked after a one-PE create has validated u0
+        per_pe = part.per_pe() if part.total() == v.size else v.size
+        _lib.check(_lib.lib().heat_async_sim_create(C.byref(self._h), _lib.dptr(v), v.size,
+                                                    params.r(), bc.kind, bc.c1, bc.c2, per_pe,
+                                                    *model._args()), "AsyncSimulator")
+        if part.total() != v.size:
+            self.close()
+            raise InvalidArgument("AsyncSimulator: partition inconsistent with grid")
+
+    def step(self, count: int = 1) -> None:
+        _lib.check(_lib.lib().heat_async_sim_step(self._h, count), "AsyncSimulator::step")
+
+    def step_index(self) -> int:
+        k = C.c_size_t(0)
+        _lib.check(_lib.lib().heat_async_sim_current(self._h, None, C.byref(k)), "step_index")
+        return int(k.value)
+
+    def current(self) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        _lib.check(_lib.lib().heat_async_sim_current(self._h, _lib.dptr(out), None), "current")
+        return out
+
+    def current_field(self) -> TemperatureField:
+        return TemperatureField(self.current())
+
+    def close(self):
+        if self._h:
+            _lib.lib().heat_async_sim_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def async_final(u0, params: SolverParams, bc: BoundaryCondition, part: PartitionSpec,
                 model: DelayModel, k_end: int) -> np.ndarray:
     """Final state of async_run without the trajectory copies."""
