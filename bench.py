@@ -343,13 +343,20 @@ def run_b200(args, rank, world, local):
         cpu = {"value": round(g, 4), "unit": UNIT, "cores": cores, "kind": kind,
                "sample": sample}
 
+    paper = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        try:
+            paper = run_paper_configs(H)
+        except Exception as exc:  # report, do not lose the line
+            paper = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     line = {
         "metric": METRIC, "value": round(glups, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (sine IC generated on device)", "config": config_dict(world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "clocks": clk.summary(), "async": async_info,
+        "clocks": clk.summary(), "async": async_info, "paper_configs": paper,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -357,6 +364,53 @@ def run_b200(args, rank, world, local):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_paper_configs(H):
+    """BASELINE configs[0] / [1], the paper's own runs: N = 1024, r = 0.25,
+    Dirichlet(0,0), sine IC, 1000 steps -- synchronous, and asynchronous with
+    8 PEs, q = 2, seeded delays.  GPU: wall time of one call through the
+    public API (upload, kernels, download), best of 20.  CPU: the reference's
+    own sync_run / async_run (oracle/_ref, one host thread), best of 5; the
+    GPU results must be bit-identical to it."""
+    from oracle import oracle as O
+    port = O.port()
+    ref = O.ref() if O.Ref.available() else port
+    n, k = 1024, 1000
+    u0 = port.prepare_initial(port.sine_init(n), O.DIRICHLET, 0.0, 0.0)
+    p = H.SolverParams.from_r(0.25)
+    bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
+    part = H.PartitionSpec(n, n // 8)
+    model = H.DelayModel.uniform(2, 1)
+
+    def best(f, reps):
+        out, ts = None, []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = f()
+            ts.append(time.perf_counter() - t0)
+        return out, min(ts) * 1e6
+
+    # the full API calls on both sides, each recording the trajectory every
+    # 100 steps (default_stride for N > 1000) -- 11 snapshots
+    f = H.TemperatureField(u0)
+    g_sync, t_gs = best(lambda: H.sync_run(f, p, bc, k, 100).final().values(), 20)
+    g_async, t_ga = best(lambda: H.async_run(f, p, bc, part, model, k, 100).final().values(), 20)
+    c_sync, t_cs = best(lambda: ref.sync_run(u0, p.r(), O.DIRICHLET, 0.0, 0.0, k, stride=100), 5)
+    c_async, t_ca = best(lambda: ref.async_run(u0, p.r(), O.DIRICHLET, 0.0, 0.0, n // 8,
+                                               O.UNIFORM, 2, seed=1, k_end=k, stride=100), 5)
+    kind = "reference" if ref is not port else "port"
+    return {
+        "workload": "N=1024, r=0.25, Dirichlet(0,0), sine IC, 1000 steps, trajectory every 100 "
+                    "steps; wall per sync_run / async_run call",
+        "cpu_kind": kind, "cpu_cores": 1,
+        "cfg1_sync": {"gpu_us": round(t_gs, 1), "cpu_us": round(t_cs, 1),
+                      "bit_exact": bool(np.array_equal(g_sync.view(np.uint64),
+                                                        np.asarray(c_sync).view(np.uint64)))},
+        "cfg2_async_q2": {"gpu_us": round(t_ga, 1), "cpu_us": round(t_ca, 1),
+                          "bit_exact": bool(np.array_equal(g_async.view(np.uint64),
+                                                            np.asarray(c_async).view(np.uint64)))},
+    }
 
 
 ASYNC_PES = 512  # 2^21 points per PE at N = 2^30

@@ -14,6 +14,8 @@
 // round, and the kernel writes the trajectory rows itself.  Bit-identical to
 // K1 and to the reference: the same stencil_p arithmetic on the same points.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 
 #include "runtime.cuh"
 #include "sync_tb.cuh"
@@ -30,16 +32,34 @@ struct SmallArgs {
     long long stride;  // 0: no trajectory
     double* snaps;     // [rows][n]: row 0 = step 0, row j = step j*stride, last row = k_end
     unsigned int* flag;
+    int prep;  // validate the raw upload (flag[2], no steps) and snap the Dirichlet ends
 };
 
 constexpr int kSmallHalo = 64;  // steps per round = halo points per side
 
 template <int V>
-__global__ void __launch_bounds__(V == 8 ? 1024 : 640, 1) sync_small_kernel(const SmallArgs a) {
+__global__ void __launch_bounds__(V <= 12 ? 1024 : 640, 1) sync_small_kernel(const SmallArgs a) {
     extern __shared__ double su[];
     constexpr int H = kSmallHalo, C = 32 * V - 2 * H;
     const int n = a.n, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) su[i] = a.field[i];
+    bool bad_in = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = a.field[i];
+        bad_in |= !isfinite(v);
+        su[i] = v;
+    }
+    if (a.prep) {
+        // TemperatureField ctor (core.hpp:45-51) on the raw upload, then
+        // prepare_initial's snap of the ends (the host checked |u - c| <= 1e-9)
+        if (__syncthreads_or(bad_in)) {
+            if (threadIdx.x == 0) atomicOr(a.flag + 2, 1u);
+            return;
+        }
+        if (a.dirichlet && threadIdx.x == 0) {
+            su[0] = a.c1;
+            su[n - 1] = a.c2;
+        }
+    }
     __syncthreads();
     if (a.snaps)
         for (int i = threadIdx.x; i < n; i += blockDim.x) a.snaps[i] = su[i];
@@ -121,7 +141,17 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
     HB_TRY(ensure_buffers(*d, pitch * sizeof(double)));
     double* field = static_cast<double*>(d->buf[0]);
     cudaStream_t st = d->stream;
-    HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, field));
+    // One round trip: the kernel validates the raw upload and snaps the ends
+    // itself when the host-side end check (sync_solver.cpp:29-31) passes; when
+    // it fails, upload_prepared reports the reference's errors in the
+    // reference's order (a non-finite field before the end check).
+    const bool ends_ok = bc_kind != HEAT_BC_DIRICHLET ||
+                         (std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9);
+    HB_CUDA(cudaMemsetAsync(d->flag, 0, 4 * sizeof(unsigned int), st));
+    if (ends_ok)
+        HB_CUDA(cudaMemcpyAsync(field, u0, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    else
+        HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, field));  // fails with the right error
     if (want && d->snaps_bytes < rows * n * sizeof(double)) {
         if (d->snaps) cudaFree(d->snaps);
         d->snaps = nullptr;
@@ -129,7 +159,6 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
         HB_CUDA(cudaMalloc(&d->snaps, rows * n * sizeof(double)));
         d->snaps_bytes = rows * n * sizeof(double);
     }
-    HB_CUDA(cudaMemsetAsync(d->flag, 0, 2 * sizeof(unsigned int), st));
     SmallArgs a{};
     a.field = field;
     a.n = int(n);
@@ -142,50 +171,65 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
     a.stride = want ? (long long)stride : 0;
     a.snaps = want ? static_cast<double*>(d->snaps) : nullptr;
     a.flag = d->flag;
+    a.prep = 1;
     const int smem = int(n * sizeof(double));
     const int kMaxSmem = int(sync_small_max_points() * sizeof(double));
-    if (n <= 4096) {
-        constexpr int V = 8, C = 32 * V - 2 * kSmallHalo;
+    // points per lane (measured, tools/probe_k3_pes.py): N <= 1024 8 (8 warps:
+    // 113 ns/step at 1024; 12 gives 173), N <= 8192 12 (4096: 302 vs 355 at 8),
+    // beyond 32.  HEAT_SMALL_V forces one for A/B.
+    static const int forced_v = [] {
+        const char* e = std::getenv("HEAT_SMALL_V");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int V = (forced_v == 8 && n <= 4096) || (forced_v == 12 && n <= 8192) ||
+                          forced_v == 32
+                      ? forced_v
+                      : n <= 1024 ? 8 : n <= 8192 ? 12 : 32;
+    if (V == 32 && n > 32 * 896) return fail(HEAT_ELOGIC, "K7: field too large");
+    auto launch = [&](auto kern, int lanes) -> int {
+        const int C = 32 * lanes - 2 * kSmallHalo;
         const int warps = int((n + C - 1) / C);
         int per_sm = 0;  // the limit is set once for the largest field this kernel takes
-        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(sync_small_kernel<V>), kMaxSmem,
-                                  32 * V == 256 ? 1024 : 640, &per_sm));
-        sync_small_kernel<V><<<1, warps * 32, smem, st>>>(a);
-    } else {
-        constexpr int V = 32, C = 32 * V - 2 * kSmallHalo;
-        const int warps = int((n + C - 1) / C);
-        int per_sm = 0;  // the limit is set once for the largest field this kernel takes
-        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(sync_small_kernel<V>), kMaxSmem,
-                                  32 * V == 256 ? 1024 : 640, &per_sm));
-        sync_small_kernel<V><<<1, warps * 32, smem, st>>>(a);
+        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(kern), kMaxSmem,
+                                  lanes <= 12 ? 1024 : 640, &per_sm));
+        if (warps * 32 > (lanes <= 12 ? 1024 : 640)) return fail(HEAT_ELOGIC, "K7: too many warps");
+        kern<<<1, warps * 32, smem, st>>>(a);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return HEAT_OK;
+    };
+    if (V == 12)
+        HB_TRY(launch(sync_small_kernel<12>, 12));
+    else if (V == 8)
+        HB_TRY(launch(sync_small_kernel<8>, 8));
+    else
+        HB_TRY(launch(sync_small_kernel<32>, 32));
+    // results and flags in one round trip
+    size_t ns = 0;
+    std::vector<size_t> ks;
+    if (want) {
+        // recorded steps: 0, stride, 2*stride, ..., and k_end when not a multiple
+        ks.push_back(0);
+        for (size_t kk = stride; kk <= k_end; kk += stride) ks.push_back(kk);
+        if (k_end % stride) ks.push_back(k_end);
+        ns = ks.size();
+        const size_t copy = std::min(ns, max_snapshots);
+        if (snapshots && copy)  // rows are contiguous on both sides: one copy
+            HB_CUDA(cudaMemcpyAsync(snapshots, d->snaps, copy * n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
     }
-    HB_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    unsigned int flags[2] = {0, 0};
+    if (final_out)
+        HB_CUDA(cudaMemcpyAsync(final_out, field, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    unsigned int flags[4] = {0, 0, 0, 0};
     HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
     HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     if (flags[0]) {
         if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
         return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     }
-    if (final_out)
-        HB_CUDA(cudaMemcpyAsync(final_out, field, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-    size_t ns = 0;
-    if (want) {
-        // recorded steps: 0, stride, 2*stride, ..., and k_end when not a multiple
-        std::vector<size_t> ks{0};
-        for (size_t kk = stride; kk <= k_end; kk += stride) ks.push_back(kk);
-        if (k_end % stride) ks.push_back(k_end);
-        ns = ks.size();
-        for (size_t j = 0; j < ns && j < max_snapshots; ++j) {
-            if (steps_out) steps_out[j] = ks[j];
-            if (snapshots)
-                HB_CUDA(cudaMemcpyAsync(snapshots + j * n,
-                                        static_cast<double*>(d->snaps) + j * n,
-                                        n * sizeof(double), cudaMemcpyDeviceToHost, st));
-        }
-    }
-    HB_CUDA(cudaStreamSynchronize(st));
+    if (steps_out)
+        for (size_t j = 0; j < ns && j < max_snapshots; ++j) steps_out[j] = ks[j];
     if (n_snapshots) *n_snapshots = ns;
     return HEAT_OK;
 }
