@@ -390,8 +390,7 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
             if (steps_out) steps_out[ns] = k;
         }
         ++ns;
-        HB_CUDA(cudaStreamSynchronize(st));
-        return HEAT_OK;
+        return HEAT_OK;  // stream order keeps the rows; one sync at the end
     };
     if (want_snaps) HB_TRY(record_from(0, bufs[0]));
     AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 0, q, law, fixed_delay, geometric_p, seed,
@@ -404,11 +403,10 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
                             record_from, nullptr, nullptr,
                             nullptr, nullptr));
     }
-    if (final_out) {
+    if (final_out)
         HB_CUDA(cudaMemcpyAsync(final_out, bufs[cur], N * sizeof(double), cudaMemcpyDeviceToHost,
                                 st));
-        HB_CUDA(cudaStreamSynchronize(st));
-    }
+    HB_CUDA(cudaStreamSynchronize(st));
     if (n_snapshots) *n_snapshots = ns;
     return HEAT_OK;
 }

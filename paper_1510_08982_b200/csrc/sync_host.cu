@@ -265,11 +265,17 @@ namespace {
 // Device-side TemperatureField validation (core.hpp:45-51): flag[2] |= 1 on a
 // non-finite value.  Runs right after the upload so the host never walks the
 // field (an O(N) host pass would dominate end-to-end time at N = 2^30).
-__global__ void validate_kernel(const double* __restrict__ u, long long n, unsigned int* flag) {
+// snap: also write the Dirichlet ends (each index is read, then written, by
+// the one thread that owns it).
+__global__ void validate_kernel(double* __restrict__ u, long long n, unsigned int* flag, int snap,
+                                double c1, double c2) {
     bool bad = false;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x)
+         i += (long long)gridDim.x * blockDim.x) {
         bad |= !isfinite(u[i]);
+        if (snap && i == 0) u[0] = c1;
+        if (snap && i == n - 1) u[n - 1] = c2;
+    }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag + 2, 1u);
 }
 
@@ -287,23 +293,22 @@ __global__ void narrow_kernel(const double* __restrict__ in, float* __restrict__
 int upload_prepared(DevCtx& d, const double* u0, size_t n, int bc_kind, double c1, double c2,
                     double* dst) {
     cudaStream_t st = d.stream;
+    // The end check reads the host field; the device finite check still comes
+    // first in the errors reported (the TemperatureField ctor precedes
+    // prepare_initial), and the same kernel snaps the ends: one round trip.
+    constexpr double kTol = 1e-9;  // kDirichletEndTol, sync_solver.hpp:44
+    const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+    const bool ends_ok = !dir || (std::abs(u0[0] - c1) <= kTol && std::abs(u0[n - 1] - c2) <= kTol);
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
     HB_CUDA(cudaMemcpyAsync(dst, u0, n * sizeof(double), cudaMemcpyHostToDevice, st));
-    validate_kernel<<<d.sms * 4, 256, 0, st>>>(dst, (long long)n, d.flag);
+    validate_kernel<<<d.sms * 4, 256, 0, st>>>(dst, (long long)n, d.flag, dir && ends_ok, c1, c2);
     HB_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
     unsigned int flags[4] = {0, 0, 0, 0};
     HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
     HB_CUDA(cudaStreamSynchronize(st));
     if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
-    if (bc_kind == HEAT_BC_DIRICHLET) {
-        constexpr double kTol = 1e-9;  // kDirichletEndTol, sync_solver.hpp:44
-        if (std::abs(u0[0] - c1) > kTol || std::abs(u0[n - 1] - c2) > kTol)
-            return fail(HEAT_EINVAL, "Dirichlet BC inconsistent with initial end values");
-        const double ends[2] = {c1, c2};
-        HB_CUDA(cudaMemcpy(dst, &ends[0], sizeof(double), cudaMemcpyHostToDevice));
-        HB_CUDA(cudaMemcpy(dst + n - 1, &ends[1], sizeof(double), cudaMemcpyHostToDevice));
-    }
+    if (!ends_ok) return fail(HEAT_EINVAL, "Dirichlet BC inconsistent with initial end values");
     return HEAT_OK;
 }
 
