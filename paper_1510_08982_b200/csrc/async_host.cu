@@ -3,6 +3,7 @@
 // heat_sample_delay, heat_exec_run.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <functional>
 
 #include "async_pe.cuh"
@@ -49,6 +50,36 @@ struct AsyncWork {
 
 size_t align256(size_t b) { return (b + 255) / 256 * 256; }
 
+// K3 geometry for PEs of n points, P of them: S lanes per PE (32/S PEs per
+// warp, shuffles confined to the segment) and V points per lane.  The
+// narrowest segment that keeps >= 4 warps (one per scheduler) and <= 32
+// points per lane: cfg2 (8 PEs of 128) runs 4 warps of two 16-lane PEs, not 8
+// warps of 4-point lanes.  HEAT_PE_SEG forces S for A/B.
+void pe_geometry(size_t n, size_t P, int& S, int& V, size_t& warps) {
+    static const int forced = [] {
+        const char* e = std::getenv("HEAT_PE_SEG");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ? v : 0;
+    }();
+    auto lanes_v = [&](int s) {
+        int v = 1;
+        while (v * s < int(n)) v *= 2;
+        return v;
+    };
+    S = 32;
+    if (forced && lanes_v(forced) <= 32) {
+        S = forced;
+    } else {
+        for (int cand = 16; cand >= 2; cand /= 2) {
+            const size_t w = (P + size_t(32 / cand) - 1) / size_t(32 / cand);
+            if (lanes_v(cand) > 32 || w < 4) break;
+            S = cand;
+        }
+    }
+    V = lanes_v(S);
+    warps = (P + size_t(32 / S) - 1) / size_t(32 / S);
+}
+
 int pick_ring(int q) {
     int R = 64;
     while (R < 4 * q) R *= 2;
@@ -58,9 +89,11 @@ int pick_ring(int q) {
 template <int V, bool S, bool B>
 int launch_v(const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
     if (S) {
-        if (smem > 48 * 1024)
-            HB_CUDA(cudaFuncSetAttribute(async_pe_kernel<V, S, B>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        // the dynamic rings plus the static histograms can pass 48 KB well below
+        // the rings' own 160 KB cap: raise the limit once, per device
+        int per_sm = 0;
+        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(async_pe_kernel<V, S, B>),
+                                  160 * 1024, 512, &per_sm));
         async_pe_kernel<V, S, B><<<1, 32 * P, smem, st>>>(a);
         HB_CUDA(cudaGetLastError());
     } else {
@@ -117,8 +150,9 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
         return fail(HEAT_ENODEV, "async: PEs wider than 1024 points need the streaming kernel "
                                  "(heat_plan_async_advance)");
     if (P > 65536) return fail(HEAT_EINVAL, "async: too many PEs");
-    int V = 1;
-    while (V * 32 < int(s.n)) V *= 2;
+    int S = 32, V = 1;
+    size_t warps = P;
+    pe_geometry(s.n, P, S, V, warps);
     const int q = int(s.q);
     const int R = pick_ring(q);
     const int dir = s.bc_kind == HEAT_BC_DIRICHLET;
@@ -209,7 +243,17 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s watchdog per wait
 
     const size_t smem = P * 2 * R * sizeof(double) + P * sizeof(unsigned long long);
-    const bool shared = P <= 16 && smem <= 160 * 1024;  // one CTA of <= 512 threads
+    bool shared = warps <= 16 && smem <= 160 * 1024;  // one CTA of <= 512 threads
+    if (s.mode != 0 || !shared) {
+        // segments pay off in the lockstep barrier mode only: with flags, two
+        // PEs in one warp serialise each other's spin-waits (measured +9%)
+        S = 32;
+        V = 1;
+        while (V * 32 < int(s.n)) V *= 2;
+        warps = P;
+        shared = P <= 16 && smem <= 160 * 1024;
+    }
+    a.seg = S;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (device_ms) {
@@ -239,7 +283,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
                                                    : s.k_end;
         a.k0 = (long long)k;
         a.k1 = (long long)next;
-        HB_TRY(launch_pe(V, shared, s.mode == 0, a, int(P), st, smem));
+        HB_TRY(launch_pe(V, shared, s.mode == 0, a, int(warps), st, smem));
         k = next;
         if (in_kernel) {
             unsigned int flags[2] = {0, 0};
@@ -646,7 +690,8 @@ struct heat_async_sim {
     size_t k = 0;
     bool started = false;
     // K3 scratch layout
-    int R = 0, D = 0, V = 1;
+    int R = 0, D = 0, V = 1, S = 32;
+    size_t warps = 0;
     size_t o_ring = 0, o_prog = 0, o_offL = 0, o_offR = 0, o_abort = 0;
     bool shared = false;
     size_t smem = 0;
@@ -753,7 +798,8 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
     a.flag = d.flag;
     a.abort_word = reinterpret_cast<unsigned int*>(base + sim->o_abort);
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;
-    return launch_pe(sim->V, sim->shared, true, a, int(sim->P), st, sim->smem);
+    a.seg = sim->S;
+    return launch_pe(sim->V, sim->shared, true, a, int(sim->warps), st, sim->smem);
 }
 
 int sim_step_k5(heat_async_sim* sim, size_t count) {
@@ -831,8 +877,7 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         HB_TRY(stream_layout(sim->s, 1, StreamExternal{}, sim->L, sim->offL, sim->offR));
         HB_TRY(ensure_scratch(d, sim->L.bytes));
     } else if (!sim->wide) {
-        sim->V = 1;
-        while (sim->V * 32 < int(per_pe)) sim->V *= 2;
+        pe_geometry(per_pe, sim->P, sim->S, sim->V, sim->warps);
         sim->R = pick_ring(int(q));
         sim->D = draw_offsets(N, per_pe, bc_kind == HEAT_BC_DIRICHLET, sim->offL, sim->offR);
         size_t off = 0;
@@ -848,7 +893,7 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         sim->o_abort = take(sizeof(unsigned int));
         HB_TRY(ensure_scratch(d, off));
         sim->smem = sim->P * 2 * sim->R * sizeof(double) + sim->P * sizeof(unsigned long long);
-        sim->shared = sim->P <= 16 && sim->smem <= 160 * 1024;
+        sim->shared = sim->warps <= 16 && sim->smem <= 160 * 1024;
     }
     *out = sim;
     sim = nullptr;  // owned by the caller now

@@ -69,6 +69,7 @@ struct AsyncPeArgs {
     double* snaps;
     long long snap_stride;
     long long k_final;
+    int seg;  // lanes per PE (a power of two, 2..32): 32/seg PEs share a warp
 };
 
 // stats layout (u64 words)
@@ -163,8 +164,12 @@ template <int V, bool kShared, bool kBarrier>
 __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const AsyncPeArgs a) {
     static_assert(kShared || !kBarrier, "barrier mode needs every PE in one CTA");
     extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31;
-    const int p = int((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+    // A PE is a segment of S lanes; the warp's 32/S segments are independent
+    // PEs, and every shuffle is confined to its segment (width S).
+    const int S = a.seg;
+    const int wl = threadIdx.x & 31;  // lane in the warp
+    const int lane = wl & (S - 1);    // lane in the PE's segment
+    const int p = int(((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5) * (32 / S) + wl / S);
     const int R = a.R;
     double* ring = a.ring;
     uint64_t* prog = reinterpret_cast<uint64_t*>(a.prog);
@@ -180,12 +185,14 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     }
     const bool active = p < a.P;
     if constexpr (!kShared) {
-        if (!active) return;  // warp-uniform; no block barrier in the global-ring variant
+        // no block barrier in the global-ring variant; inactive segments of a
+        // partly active warp stay for the shuffles (their writes are guarded)
+        if (!__any_sync(0xffffffffu, active)) return;
     }
     // [0,64) delay histogram, [64,128) writer-lag histogram, [128] lag overflow
     __shared__ unsigned int s_hist[16][129];
     unsigned int* whist = s_hist[(threadIdx.x >> 5) & 15];
-    for (int i = lane; i < 129; i += 32) whist[i] = 0;
+    for (int i = wl; i < 129; i += 32) whist[i] = 0;
     __syncwarp();
     const int n = a.n;
     const long long lo = (long long)p * n;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     // ghost (right PE's FIRST point); lane 0 publishes.  Everything a step
     // touches is precomputed here so the loop body stays short: the paper's
     // regime is latency-bound (one neighbour handshake per step).
-    const bool fetch = (lane == 0 && needL) || (lane == 31 && needR);
+    const bool fetch = (lane == 0 && needL) || (lane == S - 1 && needR);
     const int nb = lane == 0 ? lpe : rpe;
     const double* gring = ring + ((size_t)(nb < 0 ? 0 : nb) * 2 + (lane == 0 ? 1 : 0)) * R;
     const uint64_t* gprog = prog + (nb < 0 ? 0 : nb);
@@ -276,8 +283,8 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 break;
             }
         }
-        const double gL = __shfl_sync(0xffffffffu, ghost, 0);
-        const double gR = __shfl_sync(0xffffffffu, ghost, 31);
+        const double gL = __shfl_sync(0xffffffffu, ghost, 0, S);
+        const double gR = __shfl_sync(0xffffffffu, ghost, S - 1, S);
 
         // ---- 2. one step of the PE's points.  The PE's last point (lane
         // lastLane, element lastElem) takes r*gR as its right product; a
@@ -287,8 +294,8 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
         const bool last_lane = lane == lastLane;
         const double pFirst = A::mul(r, u[0]);
         const double pLast = A::mul(r, u[V - 1]);
-        double pL = __shfl_up_sync(0xffffffffu, pLast, 1);
-        double pR = __shfl_down_sync(0xffffffffu, pFirst, 1);
+        double pL = __shfl_up_sync(0xffffffffu, pLast, 1, S);
+        double pR = __shfl_down_sync(0xffffffffu, pFirst, 1, S);
         if (lane == 0) pL = A::mul(r, gL);
         {
             double pm1 = pL, p0 = pFirst;
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
 #pragma unroll
         for (int i = 0; i < V; ++i)
             if (i == lastElem) last = u[i];
-        last = __shfl_sync(0xffffffffu, last, lastLane);
+        last = __shfl_sync(0xffffffffu, last, lastLane, S);
         if (lane == 0 && active) {
             const int slot = (k + 1) & rmask;
             RingOps<kShared>::store_val(my0 + slot, u[0]);
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     if (bad) atomicOr(a.flag, 1u);
     __syncwarp();
     if (a.stats) {
-        for (int i = lane; i < 129; i += 32) {
+        for (int i = wl; i < 129; i += 32) {
             const unsigned int cnt = whist[i];
             if (cnt) atomicAdd(a.stats + (i < 64 ? kStatDelayHist + i : kStatLagHist + (i - 64)),
                                (unsigned long long)cnt);
