@@ -90,6 +90,14 @@ int heat_plan_download(heat_plan* p, double* host) {
     return HEAT_OK;
 }
 
+int heat_plan_download_device(heat_plan* p, void* dst_device) {
+    if (!p || !dst_device) return fail(HEAT_EINVAL, "null plan or device pointer");
+    HB_CUDA(cudaSetDevice(p->device));
+    HB_CUDA(cudaMemcpyAsync(dst_device, p->bufs[p->cur], p->n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, p->stream));
+    return HEAT_OK;  // stream-ordered on the plan's stream
+}
+
 int heat_plan_fill_sine(heat_plan* p) {
     if (!p) return fail(HEAT_EINVAL, "null plan");
     HB_CUDA(cudaSetDevice(p->device));

@@ -692,6 +692,11 @@ class Plan:
         _lib.check(_lib.lib().heat_plan_download(self._h, host.ctypes.data), "download")
         return host
 
+    def download_device(self, dst_device_ptr: int):
+        """Owned points into device memory (stream-ordered on the plan's stream)."""
+        _lib.check(_lib.lib().heat_plan_download_device(self._h, dst_device_ptr),
+                   "download_device")
+
     def fill_sine(self):
         _lib.check(_lib.lib().heat_plan_fill_sine(self._h), "fill_sine")
 

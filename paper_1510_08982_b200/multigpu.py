@@ -109,6 +109,23 @@ class PlanEngine(SlabEngine):
         self.plan.sync_advance(self.r, self.bc, steps)
 
 
+def gather_slabs(local: torch.Tensor, world: int, group=None) -> torch.Tensor:
+    """The final gather: every rank's slab (equal sizes, rank order) -> the
+    global field on every rank (all_gather_into_tensor; NCCL over NVLink on
+    device tensors, gloo on CPU ones)."""
+    out = torch.empty(world * local.numel(), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    return out
+
+
+def plan_gather(plan, world: int, group=None) -> torch.Tensor:
+    """gather_slabs of a plan's owned points, device to device."""
+    local = torch.empty(plan.n, dtype=torch.float64, device=f"cuda:{plan.device}")
+    plan.download_device(local.data_ptr())
+    plan.synchronize()
+    return gather_slabs(local, world, group)
+
+
 def exchange_handles(handle: bytes, rank: int, world: int, periodic: bool, group=None):
     """All-gather the 64-byte IPC handles (setup only) and pick the neighbours'."""
     handles = [None] * world
@@ -148,6 +165,10 @@ class AsyncSlabSolver:
         dist.barrier(group=self.group)
         return self.plan.xlink_advance(r, self.bc, steps, model)
 
+    def gather(self) -> torch.Tensor:
+        """The global field (device tensor on every rank)."""
+        return plan_gather(self.plan, self.world, self.group)
+
 
 class SlabSolver:
     """Sync FTCS on a G-way slab decomposition, one rank per GPU."""
@@ -171,3 +192,7 @@ class SlabSolver:
     def advance(self, steps: int) -> None:
         run_passes(self.engine, steps, self.rank, self.world, self.periodic, self.send,
                    self.recv, self.group)
+
+    def gather(self) -> torch.Tensor:
+        """The global field (device tensor on every rank)."""
+        return plan_gather(self.plan, self.world, self.group)

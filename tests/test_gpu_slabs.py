@@ -77,3 +77,29 @@ def test_slab_advance_caps_steps(H):
     with pytest.raises(H.InvalidArgument):
         p.sync_advance(0.25, H.BoundaryCondition.dirichlet(0.0, 0.0), H.Plan.halo() + 1)
     p.close()
+
+
+def test_plan_gather_device_to_device(H):
+    # the final gather's device path (heat_plan_download_device + NCCL
+    # all_gather_into_tensor) on a one-rank group: the gathered field is the plan's
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_1510_08982_b200 import multigpu as M
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p = H.Plan(5000, 0)
+        u = np.linspace(0.0, 1.0, 5000)
+        p.upload(u)
+        p.sync_advance(0.3, H.BoundaryCondition.dirichlet(0.0, 1.0), 7)
+        got = M.plan_gather(p, 1).cpu().numpy()
+        assert bits_equal(got, p.download())
+        p.close()
+    finally:
+        dist.destroy_process_group()

@@ -78,11 +78,10 @@ def _worker(rank, world, port, u0, r, periodic, c1, c2, steps, q):
         send = torch.zeros(2 * eng.halo, dtype=torch.float64)
         recv = torch.zeros(2 * eng.halo, dtype=torch.float64)
         M.run_passes(eng, steps, rank, world, periodic, send, recv)
-        local = torch.from_numpy(eng.owned())
-        parts = [torch.zeros_like(local) for _ in range(world)] if rank == 0 else None
-        dist.gather(local, parts, dst=0)
+        # the product's final gather (multigpu.gather_slabs)
+        full = M.gather_slabs(torch.from_numpy(eng.owned()), world)
         if rank == 0:
-            q.put(torch.cat(parts).numpy())
+            q.put(full.numpy())
     finally:
         dist.destroy_process_group()
 
