@@ -42,7 +42,7 @@ STEPS_PER_BENCH_STEP = 1000
 STEPS_PER_PASS = 32  # fallback; the library reports its kernel's (heat_sync_kernel_info)
 BYTES_PER_UPDATE = 16  # one FP64 read + one FP64 write per point per step
 FP64_OPS_PER_UPDATE = 4  # 2 DMUL + 2 DADD with the shared r*u products
-CPU_SAMPLE_STEPS = 4
+CPU_SAMPLE_STEPS = 32  # ~5 s timed (+ ~8 s of the API's own 8 GiB copies) per sample at N = 2^30
 
 
 def measured_peaks():
@@ -123,15 +123,21 @@ def dist_env():
     return rank, world, local
 
 
+_CPU_FIELDS = {}
+
+
 def cpu_baseline_run(n: int, steps: int, warm: bool = True):
     """The reference's exec_run(Barriered) on all host threads (oracle/_ref),
     or the C port's threaded executor when the reference library is absent.
     Returns (GLUPS, cores, kind, sample description)."""
     from oracle import oracle as O
     port = O.port()
-    u0 = port.sine_init(n)
-    u0[0] = 0.0
-    u0[-1] = 0.0
+    u0 = _CPU_FIELDS.get(n)
+    if u0 is None:  # 8 GiB at N = 2^30: built once per process, reused by every sample
+        u0 = port.sine_init(n)
+        u0[0] = 0.0
+        u0[-1] = 0.0
+        _CPU_FIELDS[n] = u0
     kind = "reference" if O.Ref.available() else "port"
     eng = O.ref() if kind == "reference" else port
     hw = os.cpu_count() or 1
