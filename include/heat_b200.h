@@ -91,6 +91,16 @@ int heat_async_sim_step(heat_async_sim* sim, size_t count);
 int heat_async_sim_current(heat_async_sim* sim, double* field_out, size_t* step_index);
 int heat_async_sim_destroy(heat_async_sim* sim);
 
+/* ---- planning queries (host only, no device needed; for tests/tools) -----
+ * The streamed sync_run's chunk boundaries for n points and a "wave" of
+ * wave_points (one tile per resident warp); K3's layout (lanes per PE, points
+ * per lane, warps, shared rings) for P PEs of n points, bound q, mode (0
+ * lockstep, 1 free); K5's tile geometry (points per lane, halo) for PEs of n. */
+int heat_stream_chunk_plan(size_t n, size_t wave_points, size_t* bounds, size_t cap, size_t* count);
+int heat_k3_geometry(size_t n, size_t P, size_t q, int mode, int* lanes_per_pe, int* points_per_lane,
+                     size_t* warps, int* shared_rings);
+int heat_k5_geometry(size_t n, int* points_per_lane, int* halo);
+
 /* ---- library state ---------------------------------------------------- */
 const char* heat_last_error(void);
 const char* heat_version(void);

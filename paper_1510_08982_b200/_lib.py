@@ -99,6 +99,9 @@ SIGNATURES = {
     "heat_device_count": (_i, []),
     "heat_kernel_launches": (_u64, []),
     "heat_sync_kernel_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "heat_stream_chunk_plan": (_i, [_sz, _sz, _P(_sz), _sz, _P(_sz)]),
+    "heat_k3_geometry": (_i, [_sz, _sz, _sz, _i, _P(_i), _P(_i), _P(_sz), _P(_i)]),
+    "heat_k5_geometry": (_i, [_sz, _P(_i), _P(_i)]),
     "heat_set_strict_finite_checks": (None, [_i]),
     "heat_strict_finite_checks": (_i, []),
     "heat_trajectory_length": (_sz, [_sz, _sz, _sz]),

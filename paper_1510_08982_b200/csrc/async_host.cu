@@ -86,6 +86,32 @@ int pick_ring(int q) {
     return R;
 }
 
+// Full K3 layout for P PEs of n points, delay bound q, mode (0 deterministic
+// lockstep, 1 free-running flags): lane segments only in the lockstep
+// barrier mode (with flags, two PEs in one warp serialise each other's
+// spin-waits, measured +9%); shared rings when one CTA of <= 16 warps holds
+// every PE and the rings fit.
+struct K3Layout {
+    int S = 32, V = 1, R = 64;
+    size_t warps = 0, smem = 0;
+    bool shared = false;
+};
+K3Layout k3_layout(size_t n, size_t P, int q, int mode) {
+    K3Layout L;
+    pe_geometry(n, P, L.S, L.V, L.warps);
+    L.R = pick_ring(q);
+    L.smem = P * 2 * L.R * sizeof(double) + P * sizeof(unsigned long long);
+    L.shared = L.warps <= 16 && L.smem <= 160 * 1024;
+    if (mode != 0 || !L.shared) {
+        L.S = 32;
+        L.V = 1;
+        while (L.V * 32 < int(n)) L.V *= 2;
+        L.warps = P;
+        L.shared = P <= 16 && L.smem <= 160 * 1024;
+    }
+    return L;
+}
+
 template <int V, bool S, bool B>
 int launch_v(const AsyncPeArgs& a, int P, cudaStream_t st, size_t smem) {
     if (S) {
@@ -150,11 +176,10 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
         return fail(HEAT_ENODEV, "async: PEs wider than 1024 points need the streaming kernel "
                                  "(heat_plan_async_advance)");
     if (P > 65536) return fail(HEAT_EINVAL, "async: too many PEs");
-    int S = 32, V = 1;
-    size_t warps = P;
-    pe_geometry(s.n, P, S, V, warps);
     const int q = int(s.q);
-    const int R = pick_ring(q);
+    const K3Layout G = k3_layout(s.n, P, q, s.mode);
+    const int S = G.S, V = G.V, R = G.R;
+    const size_t warps = G.warps;
     const int dir = s.bc_kind == HEAT_BC_DIRICHLET;
     std::vector<int> offL, offR;
     const int D = draw_offsets(s.N, s.n, dir, offL, offR);
@@ -242,17 +267,8 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     a.abort_word = reinterpret_cast<unsigned int*>(base + o_abort);
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s watchdog per wait
 
-    const size_t smem = P * 2 * R * sizeof(double) + P * sizeof(unsigned long long);
-    bool shared = warps <= 16 && smem <= 160 * 1024;  // one CTA of <= 512 threads
-    if (s.mode != 0 || !shared) {
-        // segments pay off in the lockstep barrier mode only: with flags, two
-        // PEs in one warp serialise each other's spin-waits (measured +9%)
-        S = 32;
-        V = 1;
-        while (V * 32 < int(s.n)) V *= 2;
-        warps = P;
-        shared = P <= 16 && smem <= 160 * 1024;
-    }
+    const size_t smem = G.smem;
+    const bool shared = G.shared;  // one CTA of <= 512 threads
     a.seg = S;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -822,6 +838,17 @@ int sim_step_k5(heat_async_sim* sim, size_t count) {
 
 extern "C" {
 
+int heat_k3_geometry(size_t n, size_t P, size_t q, int mode, int* lanes_per_pe,
+                     int* points_per_lane, size_t* warps, int* shared_rings) {
+    if (n == 0 || P == 0 || q == 0) return fail(HEAT_EINVAL, "k3 geometry: n, P, q >= 1");
+    const K3Layout G = k3_layout(n, P, int(q), mode);
+    if (lanes_per_pe) *lanes_per_pe = G.S;
+    if (points_per_lane) *points_per_lane = G.V;
+    if (warps) *warps = G.warps;
+    if (shared_rings) *shared_rings = G.shared ? 1 : 0;
+    return HEAT_OK;
+}
+
 int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, double r,
                           int bc_kind, double c1, double c2, size_t per_pe, size_t q, int law,
                           size_t fixed_delay, double geometric_p, uint64_t seed) {
@@ -877,8 +904,11 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         HB_TRY(stream_layout(sim->s, 1, StreamExternal{}, sim->L, sim->offL, sim->offR));
         HB_TRY(ensure_scratch(d, sim->L.bytes));
     } else if (!sim->wide) {
-        pe_geometry(per_pe, sim->P, sim->S, sim->V, sim->warps);
-        sim->R = pick_ring(int(q));
+        const K3Layout G = k3_layout(per_pe, sim->P, int(q), 0);
+        sim->S = G.S;
+        sim->V = G.V;
+        sim->warps = G.warps;
+        sim->R = G.R;
         sim->D = draw_offsets(N, per_pe, bc_kind == HEAT_BC_DIRICHLET, sim->offL, sim->offR);
         size_t off = 0;
         auto take = [&](size_t bytes) {
@@ -892,8 +922,8 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         sim->o_offR = take(sim->P * sizeof(int));
         sim->o_abort = take(sizeof(unsigned int));
         HB_TRY(ensure_scratch(d, off));
-        sim->smem = sim->P * 2 * sim->R * sizeof(double) + sim->P * sizeof(unsigned long long);
-        sim->shared = sim->warps <= 16 && sim->smem <= 160 * 1024;
+        sim->smem = G.smem;
+        sim->shared = G.shared;
     }
     *out = sim;
     sim = nullptr;  // owned by the caller now

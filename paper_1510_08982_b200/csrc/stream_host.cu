@@ -177,6 +177,14 @@ void build_links(const StreamLayout& L, char* base, const AsyncRunSpec& s, const
 
 }  // namespace
 
+int heat_k5_geometry_query(size_t n, int* points_per_lane, int* halo) {
+    int V = 32, H = 32;
+    stream_geometry(n, V, H);
+    if (points_per_lane) *points_per_lane = V;
+    if (halo) *halo = H;
+    return HEAT_OK;
+}
+
 int virtual_device_groups(size_t P) {
     const char* e = std::getenv("HEAT_VIRTUAL_DEVICES");
     if (!e) return 1;
@@ -405,3 +413,7 @@ int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur
 }
 
 }  // namespace hb
+
+extern "C" int heat_k5_geometry(size_t n, int* points_per_lane, int* halo) {
+    return hb::heat_k5_geometry_query(n, points_per_lane, halo);
+}

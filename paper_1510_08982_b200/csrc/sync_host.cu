@@ -333,6 +333,44 @@ constexpr size_t kStreamMinPoints = size_t(1) << 24;  // below: copies are cheap
 constexpr int kStreamChunks = 16;
 constexpr size_t kStreamMaxPasses = 128;              // above: copies are a small share
 
+}  // namespace
+
+// Chunk boundaries of the streamed sync_run for N points and a "wave" (one
+// tile per resident warp, in points).  Chunks of whole waves keep every
+// launch free of a ragged last wave.  Large fields get graded chunks (4, 7,
+// 12, 20, 32, 52 waves, <= 64-wave middle, the head mirrored at the end):
+// the first pass starts after a short upload and the last download is short,
+// while neighbouring chunks differ by less than the compute/copy time ratio
+// (~1.8), so neither the compute nor the download stream starves.  Smaller
+// fields: 16 equal chunks.  Every chunk but the last starts on a 32-point unit.
+std::vector<long long> stream_chunk_plan(long long N, long long wave) {
+    std::vector<long long> B{0};
+    if (wave > 0 && N >= 128 * wave) {
+        std::vector<long long> head;
+        long long rem = N;
+        for (long long w = 4; w < 64 && rem > 8 * w * wave; w = (w * 8 + 4) / 5) {
+            head.push_back(w * wave);
+            rem -= 2 * w * wave;
+        }
+        for (long long h : head) B.push_back(B.back() + h);
+        const long long m = (rem + 64 * wave - 1) / (64 * wave);
+        const long long each = (rem / m) / wave * wave;  // whole waves; the last absorbs the rest
+        for (long long j = 0; j + 1 < m; ++j) B.push_back(B.back() + each);
+        long long tail = 0;
+        for (long long h : head) tail += h;
+        B.push_back((N - tail) / kV * kV);  // chunk starts stay 32-aligned
+        for (size_t j = head.size(); j-- > 1;) B.push_back(B.back() + head[j]);
+        B.push_back(N);                     // the last chunk absorbs N mod 32
+    } else {
+        const long long cp = ((N + kStreamChunks - 1) / kStreamChunks + kV - 1) / kV * kV;
+        for (long long b = cp; b < N; b += cp) B.push_back(b);
+        B.push_back(N);
+    }
+    return B;
+}
+
+namespace {
+
 // Streamed sync_run (large Dirichlet fields, final state only): the field is
 // uploaded in C chunks on one copy stream, advanced chunk by chunk on the
 // compute stream, and downloaded chunk by chunk on a second copy stream, so
@@ -376,28 +414,7 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // less than the compute/copy time ratio (~1.8), so neither the compute
     // nor the download stream starves.  Smaller fields: 16 equal chunks.
     const long long wave = (long long)d.sms * L.var->blocks_per_sm * T::kWarpsPerCta * L.var->out;
-    std::vector<long long> B{0};
-    if (N >= 128 * wave) {
-        std::vector<long long> head;
-        long long rem = N;
-        for (long long w = 4; w < 64 && rem > 8 * w * wave; w = (w * 8 + 4) / 5) {
-            head.push_back(w * wave);
-            rem -= 2 * w * wave;
-        }
-        for (long long h : head) B.push_back(B.back() + h);
-        const long long m = (rem + 64 * wave - 1) / (64 * wave);
-        const long long each = (rem / m) / wave * wave;  // whole waves; the last absorbs the rest
-        for (long long j = 0; j + 1 < m; ++j) B.push_back(B.back() + each);
-        long long tail = 0;
-        for (long long h : head) tail += h;
-        B.push_back((N - tail) / kV * kV);  // chunk starts stay 32-aligned
-        for (size_t j = head.size(); j-- > 1;) B.push_back(B.back() + head[j]);
-        B.push_back(N);                     // the last chunk absorbs N mod 32
-    } else {
-        const long long cp = ((N + kStreamChunks - 1) / kStreamChunks + kV - 1) / kV * kV;
-        for (long long b = cp; b < N; b += cp) B.push_back(b);
-        B.push_back(N);
-    }
+    const std::vector<long long> B = stream_chunk_plan(N, wave);
     const int C = int(B.size()) - 1;
     for (int c = 0; c < C; ++c)
         if (B[c + 1] - B[c] <= (S + 1) * shift || B[c] % kV)
@@ -573,6 +590,14 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
 }  // namespace hb
 
 using namespace hb;
+
+extern "C" int heat_stream_chunk_plan(size_t n, size_t wave_points, size_t* bounds, size_t cap,
+                                      size_t* count) {
+    const std::vector<long long> B = stream_chunk_plan((long long)n, (long long)wave_points);
+    for (size_t j = 0; j < B.size() && j < cap; ++j) bounds[j] = size_t(B[j]);
+    if (count) *count = B.size();
+    return HEAT_OK;
+}
 
 extern "C" int heat_sync_kernel_info(int* points_per_lane, int* buffers,
                                      int* exact_points_per_tile, int* steps_per_pass) {
