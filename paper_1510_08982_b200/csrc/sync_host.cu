@@ -489,6 +489,96 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     return HEAT_OK;
 }
 
+constexpr size_t kOverlapSnapPoints = size_t(1) << 20;  // below: one stream is fine
+
+// sync_run of a large f64 field with a recorded trajectory, snapshot
+// downloads overlapped with the compute (streaming the
+// trajectory).  A recorded step is copied device-to-device into one of two
+// staging buffers (HBM speed) and downloaded from there on the copy stream
+// while the next segment computes; events keep each staging buffer until its
+// download has read it.  The host issues snapshot j's download only after
+// enqueueing segment j+1, so even a pageable destination (whose copy blocks
+// the host) overlaps the GPU's next segment.  Non-finite values are
+// absorbing, so the finite check of the last pass decides the outcome.
+int sync_run_overlapped(DevCtx& d, double** bufs, size_t n, double r, int periodic, double c1,
+                        double c2, size_t k_end, size_t stride, double* final_out,
+                        double* snapshots, size_t* steps_out, size_t max_snapshots,
+                        size_t* n_snapshots) {
+    cudaStream_t st = d.stream;
+    const size_t pitch = (n + 63) / 64 * 64;
+    if (d.snaps_bytes < 2 * pitch * sizeof(double)) {
+        if (d.snaps) cudaFree(d.snaps);
+        d.snaps = nullptr;
+        d.snaps_bytes = 0;
+        HB_CUDA(cudaMalloc(&d.snaps, 2 * pitch * sizeof(double)));
+        d.snaps_bytes = 2 * pitch * sizeof(double);
+    }
+    double* stage[2] = {static_cast<double*>(d.snaps), static_cast<double*>(d.snaps) + pitch};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // ready[2], done[2]
+    struct Cleanup {
+        cudaEvent_t* e;
+        ~Cleanup() {
+            for (int i = 0; i < 4; ++i)
+                if (e[i]) cudaEventDestroy(e[i]);
+        }
+    } cleanup{ev};
+    for (auto& e : ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    bool done_recorded[2] = {false, false};
+    long long pend_row = -1;
+    int pend_slot = 0;
+    auto issue_pending = [&]() -> int {  // the download of the staged snapshot
+        if (pend_row < 0) return HEAT_OK;
+        HB_CUDA(cudaStreamWaitEvent(d.d2h, ev[pend_slot], 0));
+        HB_CUDA(cudaMemcpyAsync(snapshots + size_t(pend_row) * n, stage[pend_slot],
+                                n * sizeof(double), cudaMemcpyDeviceToHost, d.d2h));
+        HB_CUDA(cudaEventRecord(ev[2 + pend_slot], d.d2h));
+        done_recorded[pend_slot] = true;
+        pend_row = -1;
+        return HEAT_OK;
+    };
+    size_t ns = 0;
+    int cur = 0;
+    auto stage_row = [&](size_t kk) -> int {  // snapshot of step kk into a staging buffer
+        if (ns < max_snapshots) {
+            const int slot = int(ns & 1);
+            if (done_recorded[slot]) HB_CUDA(cudaStreamWaitEvent(st, ev[2 + slot], 0));
+            HB_CUDA(cudaMemcpyAsync(stage[slot], bufs[cur], n * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, st));
+            HB_CUDA(cudaEventRecord(ev[slot], st));
+            HB_TRY(issue_pending());  // the previous one, now that this segment is queued
+            pend_row = (long long)ns;
+            pend_slot = slot;
+            if (steps_out) steps_out[ns] = kk;
+        }
+        ++ns;
+        return HEAT_OK;
+    };
+    HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
+    HB_TRY(stage_row(0));
+    size_t k = 0;
+    while (k < k_end) {
+        const size_t next = std::min(k_end, (k / stride + 1) * stride);
+        HB_TRY(sync_advance<double>(d.sms, bufs, cur, (long long)n, r, periodic, c1, c2, next - k,
+                                    d.flag, st));
+        k = next;
+        HB_TRY(stage_row(k));
+    }
+    HB_TRY(issue_pending());
+    if (final_out)
+        HB_CUDA(cudaMemcpyAsync(final_out, bufs[cur], n * sizeof(double), cudaMemcpyDeviceToHost,
+                                st));
+    unsigned int flags[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d.flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    HB_CUDA(cudaStreamSynchronize(d.d2h));
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    if (n_snapshots) *n_snapshots = ns;
+    return HEAT_OK;
+}
+
 // Shared body of sync_run / sync_run_f32 (sync_solver.cpp:52-91).  Snapshots
 // and the final state are copied straight into the caller's buffers.
 template <typename Real>
@@ -560,11 +650,16 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
         return HEAT_OK;
     };
     const bool want_snaps = snapshots != nullptr || steps_out != nullptr;
-    if (want_snaps) HB_TRY(record(bufs[0], 0));
-
     int cur = 0;
     size_t k = 0;
     const int periodic = bc_kind == HEAT_BC_PERIODIC;
+    if (!f32 && snapshots && n >= kOverlapSnapPoints && max_snapshots > 0 &&
+        !std::getenv("HEAT_NO_OVERLAP_SNAPS"))
+        return sync_run_overlapped(*d, reinterpret_cast<double**>(bufs), n, r, periodic, c1, c2,
+                                   k_end, stride, final_out, snapshots, steps_out, max_snapshots,
+                                   n_snapshots);
+    if (want_snaps) HB_TRY(record(bufs[0], 0));
+
     while (k < k_end) {
         // advance to the next recorded step (or straight to k_end)
         size_t next = want_snaps ? std::min(k_end, (k / stride + 1) * stride) : k_end;

@@ -165,3 +165,21 @@ def test_periodic_conservation_and_steady_state(H):
 def test_sine_1k_matches_helper(port):
     # the sine IC helper agrees bit-for-bit with the oracle's libm sin
     assert bits_equal(sine_field(1024), port.prepare_initial(port.sine_init(1024), 0, 0.0, 0.0))
+
+
+@pytest.mark.parametrize("periodic", [False, True])
+def test_large_trajectory_overlapped_snapshots(H, periodic):
+    # N >= 2^20 with a trajectory: snapshots staged device-to-device and
+    # downloaded on the copy stream while the next segment computes
+    # (sync_run_overlapped); every row must equal an independent run to its step
+    n = (1 << 20) + 333
+    gen = SplitMix64(77 + periodic)
+    u = random_field(gen, n)
+    c1, c2 = (0.0, 0.0) if periodic else (float(u[0]), float(u[-1]))
+    bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(c1, c2)
+    p = H.SolverParams.from_r(0.41)
+    t = H.sync_run(H.TemperatureField(u), p, bc, 250, 64)
+    assert t.steps == [0, 64, 128, 192, 250]
+    assert bits_equal(t.snapshots[0].values(), u)  # the prepared field (ends already exact)
+    for k, snap in zip(t.steps[1:], t.snapshots[1:]):
+        assert bits_equal(snap.values(), H.sync_final(u, p, bc, k)), k
