@@ -206,6 +206,18 @@ def sync_kernel_name():
         return f"sync_tb_kernel (info unavailable: {e})"
 
 
+def k5_geometry(per_pe):
+    """The stream kernel's tile geometry for PEs of per_pe points (heat_k5_geometry)."""
+    try:
+        import ctypes
+        from paper_1510_08982_b200 import _lib
+        v, h = ctypes.c_int(), ctypes.c_int()
+        _lib.lib().heat_k5_geometry(per_pe, ctypes.byref(v), ctypes.byref(h))
+        return f"{v.value},{h.value}"
+    except Exception:
+        return "?"
+
+
 def slab_halo():
     try:
         from paper_1510_08982_b200 import _lib
@@ -221,12 +233,24 @@ def steps_per_pass():
         return STEPS_PER_PASS
 
 
-def config_dict(world):
+N_STRONG_TOTAL = 1 << 33  # BASELINE configs[3] (cfg4): strong scaling at N = 2^33
+
+
+def points_per_gpu(args, world):
+    return N_STRONG_TOTAL // world if getattr(args, "strong", False) else N_PER_GPU
+
+
+def config_dict(world, n=N_PER_GPU, strong=False):
+    if strong:
+        work = (f"cfg4: N=2^33 FP64 in total ({n} points per GPU), r=0.4, Dirichlet(0,0), "
+                f"sine IC, 1000-step bench steps; strong scaling over {world} GPU(s)")
+    else:
+        work = ("cfg3: N=2^30 FP64 per GPU, r=0.4, Dirichlet(0,0), sine IC, "
+                "10^4 FTCS steps (= 10 bench steps of 1000)" +
+                ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"))
     return {
-        "workload": "cfg3: N=2^30 FP64 per GPU, r=0.4, Dirichlet(0,0), sine IC, "
-                    "10^4 FTCS steps (= 10 bench steps of 1000)" +
-                    ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"),
-        "N_per_gpu": N_PER_GPU, "N_total": N_PER_GPU * world, "r": R,
+        "workload": work,
+        "N_per_gpu": n, "N_total": n * world, "r": R,
         "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": (steps_per_pass() if world == 1
                            else min(steps_per_pass(), slab_halo())),
         "kernel": sync_kernel_name(),
@@ -248,7 +272,7 @@ def run_b200(args, rank, world, local):
     # timing events all live on it
     stream = torch.cuda.Stream(local)
     torch.cuda.set_stream(stream)
-    n = N_PER_GPU
+    n = points_per_gpu(args, world)
     bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
     r = H.SolverParams.from_r(R).r()
 
@@ -315,7 +339,10 @@ def run_b200(args, rank, world, local):
         ms * 1e-3) / 1e12
     roofline = {
         "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4), "traffic": ncu_traffic_per_launch(),
+        "frac": round(achieved / peak, 4),
+        # the capture is one pass over 2^30 points; DRAM bytes scale with the points
+        "traffic": (None if ncu_traffic_per_launch() is None
+                    else ncu_traffic_per_launch() * n / N_PER_GPU),
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "algorithmic_bytes_per_launch": alg_bytes,
         "note": "effective bandwidth with temporal blocking (16 B/update counted for every "
@@ -359,8 +386,10 @@ def run_b200(args, rank, world, local):
     line = {
         "metric": METRIC, "value": round(glups, 3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (sine IC generated on device)", "config": config_dict(world),
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (sine IC generated on device)",
+        "config": config_dict(world, n, args.strong),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk.summary(), "async": async_info, "paper_configs": paper,
     }
@@ -426,7 +455,8 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
     """Async vs sync on the cfg3 workload: same steps, device-timed."""
     per_pe = n // ASYNC_PES
     out = {"pes": ASYNC_PES, "points_per_pe": per_pe,
-           "kernel": "async_stream_kernel<32> (persistent, PE-boundary acquire/release rings)"}
+           "kernel": f"async_stream_kernel<{k5_geometry(per_pe)}> (persistent, PE-boundary "
+                     f"acquire/release rings)"}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for name, call in (
@@ -543,7 +573,11 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-async", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="cfg4: N = 2^33 in total split over the GPUs (no host-buffer legs)")
     args = ap.parse_args()
+    if args.strong:  # the field does not fit the host-buffer legs (e2e, CPU, paper configs)
+        args.skip_e2e = args.skip_cpu = True
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)

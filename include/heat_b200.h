@@ -199,6 +199,8 @@ int heat_plan_download(heat_plan* plan, double* host);
 /* Device-to-device copy of the owned points (stream-ordered on the plan's
  * stream), e.g. into a buffer of the final gather. */
 int heat_plan_download_device(heat_plan* plan, void* dst_device);
+/* Points [offset, offset + count) of the owned field to the host. */
+int heat_plan_download_range(heat_plan* plan, size_t offset, size_t count, double* host);
 /* Device IC u_i = sin(pi*i/(N-1)) with Dirichlet(0,0) ends snapped (bench only). */
 int heat_plan_fill_sine(heat_plan* plan);
 /* Advance the resident field by `steps` synchronous steps (no host sync). */

@@ -127,6 +127,7 @@ SIGNATURES = {
     "heat_plan_upload": (_i, [_vp, _vp]),
     "heat_plan_download": (_i, [_vp, _vp]),
     "heat_plan_download_device": (_i, [_vp, _vp]),
+    "heat_plan_download_range": (_i, [_vp, _sz, _sz, _vp]),
     "heat_plan_fill_sine": (_i, [_vp]),
     "heat_plan_sync_advance": (_i, [_vp, _d, _i, _d, _d, _sz]),
     "heat_plan_async_advance": (_i, [_vp, _d, _i, _d, _d, _sz, _sz, _sz, _P(AsyncStatsC)]),

@@ -90,6 +90,16 @@ int heat_plan_download(heat_plan* p, double* host) {
     return HEAT_OK;
 }
 
+int heat_plan_download_range(heat_plan* p, size_t offset, size_t count, double* host) {
+    if (!p || !host) return fail(HEAT_EINVAL, "null plan or host pointer");
+    if (offset > p->n || count > p->n - offset) return fail(HEAT_EINVAL, "range outside the plan");
+    HB_CUDA(cudaSetDevice(p->device));
+    HB_CUDA(cudaMemcpyAsync(host, p->bufs[p->cur] + offset, count * sizeof(double),
+                            cudaMemcpyDeviceToHost, p->stream));
+    HB_CUDA(cudaStreamSynchronize(p->stream));
+    return HEAT_OK;
+}
+
 int heat_plan_download_device(heat_plan* p, void* dst_device) {
     if (!p || !dst_device) return fail(HEAT_EINVAL, "null plan or device pointer");
     HB_CUDA(cudaSetDevice(p->device));

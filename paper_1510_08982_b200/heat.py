@@ -692,6 +692,13 @@ class Plan:
         _lib.check(_lib.lib().heat_plan_download(self._h, host.ctypes.data), "download")
         return host
 
+    def download_range(self, offset: int, count: int) -> np.ndarray:
+        """Points [offset, offset + count) of the owned field."""
+        out = np.empty(count, np.float64)
+        _lib.check(_lib.lib().heat_plan_download_range(self._h, offset, count, out.ctypes.data),
+                   "download_range")
+        return out
+
     def download_device(self, dst_device_ptr: int):
         """Owned points into device memory (stream-ordered on the plan's stream)."""
         _lib.check(_lib.lib().heat_plan_download_device(self._h, dst_device_ptr),

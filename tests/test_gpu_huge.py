@@ -1,0 +1,51 @@
+"""N = 2^33 on one B200 (BASELINE cfg4's total, 2 x 64 GiB in HBM): K1 passes
+over 8.6e9 points must stay exact where 32-bit index arithmetic would break
+(around 2^31 and 2^32, the domain ends, unit boundaries).  The initial field
+is the device's sine profile; windows of it are downloaded before the run and
+each checked point is recomputed by the oracle's light cone from its window
+(the cone of k steps reaches k points each way; the windows' far ends cannot
+influence the centre)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+N = 1 << 33
+K = 300  # 4 passes of 64 and a partial one
+
+
+@pytest.fixture(scope="module")
+def H(gpu):
+    from paper_1510_08982_b200 import heat
+    return heat
+
+
+def test_huge_field_lightcone(H, port):
+    bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
+    r = H.SolverParams.from_r(0.4).r()
+    p = H.Plan(N, 0)
+    try:
+        p.fill_sine()
+        centres = [0, 1, 2, 1000, (1 << 31) - 1, 1 << 31, (1 << 31) + 1, (1 << 32) - 33,
+                   1 << 32, (1 << 32) + 31, 3 << 31, N - 1 - 1000, N - 2, N - 1]
+        wins = {}
+        for c in centres:
+            lo = max(0, c - K - 2)
+            hi = min(N, c + K + 3)
+            wins[c] = (lo, p.download_range(lo, hi - lo))
+        p.sync_advance(r, bc, K)
+        got = {c: p.download_range(c, 1)[0] for c in centres}
+    finally:
+        p.close()
+    for c in centres:
+        lo, w = wins[c]
+        # a window away from the true ends is an interior segment: its own
+        # ends (held by the oracle's Dirichlet pins) are > K points away
+        if lo == 0:
+            w = w.copy()
+            w[0] = 0.0  # the snapped global end
+        if lo + w.size == N:
+            w = w.copy()
+            w[-1] = 0.0
+        want = port.sync_lightcone(w, r, 0, float(w[0]), float(w[-1]), K, c - lo)
+        assert got[c] == want, (c, got[c], want)
