@@ -35,8 +35,20 @@ def test_huge_field_lightcone(H, port):
             wins[c] = (lo, p.download_range(lo, hi - lo))
         p.sync_advance(r, bc, K)
         got = {c: p.download_range(c, 1)[0] for c in centres}
+        # K5 free-running with q = 1 is the synchronous scheme: same bits,
+        # including at PE boundaries (512 PEs of 2^24 points)
+        pe = N // 512
+        extra = [pe - 1, pe, 300 * pe - 1, 300 * pe, (1 << 32) - 1]
+        got_k1 = {c: p.download_range(c, 1)[0] for c in extra}
+        p.fill_sine()
+        p.async_advance(r, bc, pe, 1, K)
+        got_k5 = {c: p.download_range(c, 1)[0] for c in centres + extra}
     finally:
         p.close()
+    for c in centres:
+        assert got_k5[c] == got[c], ("K5 q=1 vs K1", c)
+    for c in extra:
+        assert got_k5[c] == got_k1[c], ("K5 q=1 vs K1 at a PE boundary", c)
     for c in centres:
         lo, w = wins[c]
         # a window away from the true ends is an interior segment: its own
