@@ -75,20 +75,22 @@ SyncVariant variant() {
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows);
 // f32 takes 64-point lanes (256 B, two rows) with the same halo, buffers and deal
-template <typename Real, int NBUF, bool TMA_ST = true, int H = 32, bool DYN = false>
+template <typename Real, int NBUF, bool TMA_ST = true, int H = 32, bool DYN = false, int UNR = 0>
 SyncVariant variant48() {
     if constexpr (sizeof(Real) == 8)
-        return variant<Real, 48, NBUF, 0, TMA_ST, H, DYN>();
+        return variant<Real, 48, NBUF, UNR, TMA_ST, H, DYN>();
     else
-        return variant<Real, 64, NBUF, 0, TMA_ST, H, DYN>();
+        return variant<Real, 64, NBUF, UNR, TMA_ST, H, DYN>();
 }
 // 13: 48-point lanes, 64-point halo, 2 buffers, tiles dealt by an atomic counter:
 // +6.2% over its static-deal twin 11 (3980 vs 3748 GLUPS on one box), which was +0.6% over
 // 6 (48-point lanes, 32-point halo: 3874 GLUPS at 2^30; V = 32, variant 4: 3761).  Callers
 // that cap the steps per pass below the default halo get kHalo32Variant.  tools/ab_sync.sh.
-constexpr int kDefaultSyncVariant = 13;
+// 15: as 13 with the pipelined step loop unrolled x4 instead of x2: +0.45% (4017 vs 3998,
+// twice, same box); unrolled x1 (14) loses 1.7%.
+constexpr int kDefaultSyncVariant = 15;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 14;
+constexpr int kSyncVariants = 16;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -112,6 +114,8 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant48<Real, 2, true, 64>(),    // 11: 48-point lanes, 64-point halo (64 steps a pass)
         variant<Real, 64, 1, 0, true, 64>(),  // 12: 64-point lanes, 64-point halo, 1 buffer
         variant48<Real, 2, true, 64, true>(),  // 13: as 11, tiles dealt by an atomic counter
+        variant48<Real, 2, true, 64, true, -1>(),  // 14: as 13, step loop not unrolled
+        variant48<Real, 2, true, 64, true, -4>(),  // 15: as 13, step loop unrolled 4
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");

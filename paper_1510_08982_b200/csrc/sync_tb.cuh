@@ -199,7 +199,7 @@ __device__ __forceinline__ void warp_step(Real (&u)[V], Real r, Real c) {
 // interior points -- the shuffle latency hides behind them instead of
 // stalling the start of every step.  Same products, same rounding sequence
 // as warp_step (4 DP instructions per point).  No pinned ends allowed.
-template <typename Real, int V>
+template <typename Real, int V, int PU = 2>
 __device__ __forceinline__ void warp_steps_pipelined(Real (&u)[V], Real r, Real c, int nsteps) {
     static_assert(V >= 4, "pipelined step needs >= 4 points per lane");
     using A = Arith<Real>;
@@ -207,7 +207,7 @@ __device__ __forceinline__ void warp_steps_pipelined(Real (&u)[V], Real r, Real 
     Real pLs = A::mul(r, u[V - 1]);
     Real pL = __shfl_up_sync(0xffffffffu, pLs, 1);
     Real pR = __shfl_down_sync(0xffffffffu, pF, 1);
-#pragma unroll 2
+#pragma unroll PU
     for (int s = 0; s < nsteps; ++s) {
         const Real p1 = A::mul(r, u[1]);        // r*u[1]   (old)
         const Real pVm2 = A::mul(r, u[V - 2]);  // r*u[V-2] (old)
@@ -400,8 +400,8 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, 
         if (tn < a.tiles && interior(tn)) issue(NBUF == 2 ? (b ^ 1) : 0, tn);
 
         if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
-            if constexpr (UNR == 0) {
-                warp_steps_pipelined<Real, V>(u, r, c, a.nsteps);
+            if constexpr (UNR <= 0) {  // pipelined steps, unrolled 2 (UNR = 0) or -UNR
+                warp_steps_pipelined<Real, V, (UNR == 0 ? 2 : -UNR)>(u, r, c, a.nsteps);
             } else {
 #pragma unroll UNR
                 for (int s = 0; s < a.nsteps; ++s) warp_step<Real, V>(u, r, c);
