@@ -91,6 +91,30 @@ int heat_async_sim_step(heat_async_sim* sim, size_t count);
 int heat_async_sim_current(heat_async_sim* sim, double* field_out, size_t* step_index);
 int heat_async_sim_destroy(heat_async_sim* sim);
 
+/* ---- HistoryRing (async_sim.hpp:31-57) in HBM + async_step (:68-71) -------
+ * heat_history_create: a ring of `depth` snapshots of n points at step
+ * `step`, holding `count` = min(depth, step + 1) of them; row d of
+ * `snapshots` (n doubles each) is u(step - d).  HistoryRing(depth, initial)
+ * is step = 0, count = 1.  push / read / snapshot / info follow the class
+ * (logic_error -> HEAT_ELOGIC).  heat_async_step is async_step(hist, params,
+ * bc, part, model, rng) (async_sim.cpp:107-116): *rng_state is the caller's
+ * SplitMix64 state, advanced as the reference's stream (D draws per step;
+ * only through the failing draw on a logic_error).  `out` (host, may be
+ * NULL) gets the new field; push != 0 also pushes it (AsyncSimulator::step,
+ * async_sim.cpp:136-140) without a host round trip.  Kernels K8a/K8b. */
+typedef struct heat_history heat_history;
+int heat_history_create(heat_history** hist, size_t depth, size_t n, size_t step,
+                        const double* snapshots, size_t count, int device);
+int heat_history_destroy(heat_history* hist);
+int heat_history_info(const heat_history* hist, size_t* depth, size_t* current_step,
+                      size_t* grid_size);
+int heat_history_push(heat_history* hist, const double* state, size_t n);
+int heat_history_read(const heat_history* hist, size_t i, size_t d, double* value);
+int heat_history_snapshot(const heat_history* hist, size_t d, double* out);
+int heat_async_step(heat_history* hist, double r, int bc_kind, double c1, double c2,
+                    size_t part_total, size_t per_pe, size_t q, int law, size_t fixed_delay,
+                    double geometric_p, uint64_t* rng_state, double* out, int push);
+
 /* ---- planning queries (host only, no device needed; for tests/tools) -----
  * The streamed sync_run's chunk boundaries for n points and a "wave" of
  * wave_points (one tile per resident warp); K3's layout (lanes per PE, points
@@ -117,6 +141,12 @@ int heat_sync_kernel_info(int* points_per_lane, int* buffers, int* exact_points_
 /* set_strict_finite_checks / strict_finite_checks (sync_solver.hpp:77-78) */
 void heat_set_strict_finite_checks(int enabled);
 int heat_strict_finite_checks(void);
+
+/* detail::prepare_initial (sync_solver.cpp:25-37): copy u0 to out, and for
+ * Dirichlet check |u0[0]-c1|, |u0[n-1]-c2| <= 1e-9 (HEAT_EINVAL) and snap the
+ * ends.  Host-only. */
+int heat_prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
+                         double* out);
 
 /* Snapshot count sync_run / async_run record for (n, k_end, stride). */
 size_t heat_trajectory_length(size_t n, size_t k_end, size_t stride);

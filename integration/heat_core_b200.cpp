@@ -8,13 +8,16 @@
 //   heat::sync_run      sync_solver.hpp:64-67   -> heat_sync_run
 //   heat::sync_run_f32  sync_solver.hpp:69-73   -> heat_sync_run_f32
 //   heat::async_run     async_sim.hpp:97-101    -> heat_async_run
+//   heat::async_step    async_sim.hpp:68-71     -> heat_history_create + heat_async_step
 //   heat::exec_run      async_exec.hpp:68-70    -> heat_exec_run
 //   heat::ensemble_run  analysis.hpp:36-52      -> heat_ensemble_run
 //
 // Everything else (AsyncSimulator stepping, CSV, the CLI) keeps running on the
 // reference's CPU code.  oracle/Makefile target `acceptance-b200` links
 // the reference's acceptance suite (proj/tests/acceptance.cpp) this way.
+#include <algorithm>
 #include <chrono>
+#include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <vector>
@@ -73,6 +76,34 @@ Trajectory run_traj(RunFn fn, const TemperatureField& u0, const SolverParams& pa
     return t;
 }
 
+int law_of(const DelayModel& m) {
+    return m.distribution == DelayModel::Distribution::Uniform ? HEAT_DELAY_UNIFORM
+           : m.distribution == DelayModel::Distribution::Fixed ? HEAT_DELAY_FIXED
+                                                               : HEAT_DELAY_GEOMETRIC;
+}
+
+// SplitMix64 (rng.hpp:16-41) keeps its state private.  One next() returns
+// mix(s + gamma), and mix is a bijection (xorshifts and odd multipliers), so
+// the position s is recovered from that draw; the caller then owes the stream
+// one draw fewer.
+std::uint64_t unxorshift(std::uint64_t y, int s) {
+    std::uint64_t x = y;
+    for (int i = 0; i < 64 / s + 1; ++i) x = y ^ (x >> s);
+    return x;
+}
+std::uint64_t inverse_odd(std::uint64_t m) {  // m^-1 mod 2^64 (Newton)
+    std::uint64_t x = m;
+    for (int i = 0; i < 6; ++i) x *= 2 - m * x;
+    return x;
+}
+constexpr std::uint64_t kGamma = 0x9e3779b97f4a7c15ULL;
+std::uint64_t take_position(SplitMix64& rng) {
+    std::uint64_t z = unxorshift(rng.next(), 31);
+    z = unxorshift(z * inverse_odd(0x94d049bb133111ebULL), 27);
+    z = unxorshift(z * inverse_odd(0xbf58476d1ce4e5b9ULL), 30);
+    return z - kGamma;
+}
+
 }  // namespace
 
 TemperatureField sync_step(const TemperatureField& u, const SolverParams& params,
@@ -105,9 +136,7 @@ Trajectory async_run(const TemperatureField& u0, const SolverParams& params,
     std::vector<double> snaps(cap * n);
     std::vector<std::size_t> steps(cap);
     std::size_t count = 0;
-    const int law = model.distribution == DelayModel::Distribution::Uniform ? HEAT_DELAY_UNIFORM
-                    : model.distribution == DelayModel::Distribution::Fixed ? HEAT_DELAY_FIXED
-                                                                            : HEAT_DELAY_GEOMETRIC;
+    const int law = law_of(model);
     throw_on(heat_async_run(u0.values().data(), n, params.r(), bc_kind(bc), bc.c1, bc.c2,
                             part.per_pe(), model.q, law, model.fixed_delay, model.geometric_p,
                             model.seed, k_end, stride, nullptr, snaps.data(), steps.data(), cap,
@@ -119,6 +148,39 @@ Trajectory async_run(const TemperatureField& u0, const SolverParams& params,
         t.steps.push_back(steps[j]);
     }
     return t;
+}
+
+// async_step over the caller's (host) ring: the held snapshots go to a device
+// ring at the same step, K8a/K8b compute the step, and the caller's stream is
+// left where the reference would leave it (D draws, or through the failing
+// draw on a logic_error).  A one-PE partition draws nothing and is not touched.
+TemperatureField async_step(const HistoryRing& hist, const SolverParams& params,
+                            const BoundaryCondition& bc, const PartitionSpec& part,
+                            const DelayModel& model, SplitMix64& rng) {
+    sync_strict();
+    if (part.total() != hist.grid_size())  // async_sim.cpp:113-114
+        throw std::invalid_argument("async_step: partition inconsistent with grid");
+    const std::size_t n = hist.grid_size(), k = hist.current_step();
+    const std::size_t held = std::min(hist.depth(), k + 1);
+    std::vector<double> rows(held * n);
+    for (std::size_t d = 0; d < held; ++d)
+        std::memcpy(rows.data() + d * n, hist.snapshot(d).data(), n * sizeof(double));
+    heat_history* h = nullptr;
+    throw_on(heat_history_create(&h, hist.depth(), n, k, rows.data(), held, -1));
+    const bool draws = part.total() / part.per_pe() > 1;
+    const std::uint64_t s0 = draws ? take_position(rng) : 0;
+    std::uint64_t s = s0;
+    std::vector<double> out(n);
+    const int st = heat_async_step(h, params.r(), bc_kind(bc), bc.c1, bc.c2, part.total(),
+                                   part.per_pe(), model.q, law_of(model), model.fixed_delay,
+                                   model.geometric_p, &s, out.data(), 0);
+    heat_history_destroy(h);
+    if (draws) {  // s = s0 + m*gamma for the m draws consumed; one is already taken
+        const std::uint64_t m = (s - s0) * inverse_odd(kGamma);
+        for (std::uint64_t j = 1; j < m; ++j) rng.next();
+    }
+    throw_on(st);
+    return TemperatureField(std::move(out));
 }
 
 EnsembleResult ensemble_run(const EnsembleConfig& cfg, std::size_t runs,

@@ -112,6 +112,8 @@ class Port(_Lib):
         L.orc_sync_lightcone.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd]
         L.orc_sync_step_into.argtypes = [_pd, _pd, _sz, _d, _i, _d, _d]
         L.orc_sync_step_into.restype = None
+        L.orc_async_step.argtypes = [_pd, _sz, _sz, _sz, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz,
+                                     _sz, _d, _pu64, _i, _pd]
 
     # --- initial conditions / norms --------------------------------------
     def sine_init(self, n: int, threads: int | None = None) -> np.ndarray:
@@ -216,6 +218,19 @@ class Port(_Lib):
             return [int(x) for x in steps[:ns.value]], snaps[:ns.value].copy()
         return fin
 
+    def async_step(self, snaps, depth, step, r, bc, c1, c2, part_total, per_pe, law, q,
+                   fixed_d=0, p=0.5, rng_state=0, strict=False):
+        """async_step over a ring at `step` (rows of `snaps`: u(step - d)).
+        Returns (status, field or None, rng state after the call)."""
+        snaps = np.ascontiguousarray(np.asarray(snaps, np.float64))
+        count, n = snaps.shape
+        out = np.empty(n, np.float64)
+        st_rng = C.c_uint64(rng_state)
+        st = self.lib.orc_async_step(_ptr(snaps), count, depth, step, n, r, bc, c1, c2,
+                                     part_total, per_pe, law, q, fixed_d, p, C.byref(st_rng),
+                                     int(strict), _ptr(out))
+        return st, (out if st == 0 else None), int(st_rng.value)
+
     def exec_run(self, u0, r, bc, c1, c2, per_pe, workers, k_end, mode=BARRIERED):
         u0 = _f64(u0)
         fin = np.empty(u0.size, np.float64)
@@ -262,6 +277,8 @@ class Ref(_Lib):
         L.ref_sync_step_into_loop.restype = _u64
         L.ref_prepare_initial.argtypes = [_pd, _sz, _i, _d, _d, _pd]
         L.ref_cosine_init.argtypes = [_sz, _pd]
+        L.ref_async_step.argtypes = [_pd, _sz, _sz, _sz, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz,
+                                     _sz, _d, _pu64, _pd]
         L.ref_hardware_concurrency.restype = C.c_uint
 
     def set_strict(self, on: bool):
@@ -379,6 +396,19 @@ class Ref(_Lib):
         if record:
             return [int(x) for x in steps[:ns.value]], snaps[:ns.value].copy()
         return fin
+
+    def async_step(self, snaps, depth, step, r, bc, c1, c2, part_total, per_pe, law, q,
+                   fixed_d=0, p=0.5, rng_state=0):
+        """heat::async_step itself on a HistoryRing rebuilt at `step`; returns
+        (status, field or None, rng state after the call)."""
+        snaps = np.ascontiguousarray(np.asarray(snaps, np.float64))
+        count, n = snaps.shape
+        out = np.empty(n, np.float64)
+        st_rng = C.c_uint64(rng_state)
+        st = self.lib.ref_async_step(_ptr(snaps), count, depth, step, n, r, bc, c1, c2,
+                                     part_total, per_pe, law, q, fixed_d, p, C.byref(st_rng),
+                                     _ptr(out))
+        return st, (out if st == 0 else None), int(st_rng.value)
 
     def exec_run(self, u0, r, bc, c1, c2, per_pe, workers, k_end, mode=BARRIERED,
                  record_lag=False):

@@ -65,6 +65,25 @@ void copy_traj(const heat::Trajectory& t, double* final_out, double* snaps,
     if (n_snap) *n_snap = t.snapshots.size();
 }
 
+// Inverse of SplitMix64's finaliser: the class keeps its state private, so
+// the state after a call is recovered from one more next() = mix(s + gamma).
+std::uint64_t unxorshift(std::uint64_t y, int s) {
+    std::uint64_t x = y;
+    for (int i = 0; i < 64 / s + 1; ++i) x = y ^ (x >> s);
+    return x;
+}
+std::uint64_t inverse_odd(std::uint64_t m) {
+    std::uint64_t x = m;
+    for (int i = 0; i < 6; ++i) x *= 2 - m * x;
+    return x;
+}
+std::uint64_t state_of(heat::SplitMix64& rng) {
+    std::uint64_t z = unxorshift(rng.next(), 31);
+    z = unxorshift(z * inverse_odd(0x94d049bb133111ebULL), 27);
+    z = unxorshift(z * inverse_odd(0xbf58476d1ce4e5b9ULL), 30);
+    return z - 0x9e3779b97f4a7c15ULL;
+}
+
 }  // namespace
 
 extern "C" {
@@ -135,6 +154,32 @@ int ref_async_run(const double* u0, std::size_t n, double r, int bc, double c1, 
     } catch (...) {
         return classify();
     }
+}
+
+// heat::async_step (async_sim.cpp:107-116) on a HistoryRing rebuilt at step
+// `step` from `count` snapshots (row d = u(step - d)); *rng in/out is the
+// SplitMix64 state, read back after the call (also after a throw).
+int ref_async_step(const double* snaps, std::size_t count, std::size_t depth, std::size_t step,
+                   std::size_t n, double r, int bc, double c1, double c2, std::size_t part_total,
+                   std::size_t per_pe, int law, std::size_t q, std::size_t fixed_d, double p,
+                   std::uint64_t* rng_state, double* out) {
+    heat::SplitMix64 rng(*rng_state);
+    int st = 0;
+    try {
+        auto row = [&](std::size_t d) { return std::vector<double>(snaps + d * n, snaps + (d + 1) * n); };
+        heat::HistoryRing ring(depth, row(count - 1));
+        for (std::size_t j = 0; j + count - 1 < step; ++j) ring.push(row(count - 1));
+        for (std::size_t d = count - 1; d-- > 0;) ring.push(row(d));
+        heat::DelayModel m = make_model(law, q, fixed_d, p, 0);
+        heat::TemperatureField f = heat::async_step(ring, heat::SolverParams::from_r(r, true),
+                                                    make_bc(bc, c1, c2),
+                                                    heat::PartitionSpec(part_total, per_pe), m, rng);
+        std::memcpy(out, f.values().data(), n * sizeof(double));
+    } catch (...) {
+        st = classify();
+    }
+    *rng_state = state_of(rng);
+    return st;
 }
 
 // sample_delay stream (async_sim.cpp:57-73) for golden vectors.

@@ -104,6 +104,7 @@ SIGNATURES = {
     "heat_k5_geometry": (_i, [_sz, _P(_i), _P(_i)]),
     "heat_set_strict_finite_checks": (None, [_i]),
     "heat_strict_finite_checks": (_i, []),
+    "heat_prepare_initial": (_i, [_pd, _sz, _i, _d, _d, _pd]),
     "heat_trajectory_length": (_sz, [_sz, _sz, _sz]),
     "heat_sync_step": (_i, [_pd, _sz, _d, _i, _d, _d, _pd]),
     "heat_sync_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd, _pd, _psz, _sz, _psz]),
@@ -119,6 +120,13 @@ SIGNATURES = {
     "heat_async_sim_create": (_i, [_P(_vp), _pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d,
                                    _u64]),
     "heat_async_sim_step": (_i, [_vp, _sz]),
+    "heat_history_create": (_i, [_P(_vp), _sz, _sz, _sz, _pd, _sz, _i]),
+    "heat_history_destroy": (_i, [_vp]),
+    "heat_history_info": (_i, [_vp, _psz, _psz, _psz]),
+    "heat_history_push": (_i, [_vp, _pd, _sz]),
+    "heat_history_read": (_i, [_vp, _sz, _sz, _pd]),
+    "heat_history_snapshot": (_i, [_vp, _sz, _pd]),
+    "heat_async_step": (_i, [_vp, _d, _i, _d, _d, _sz, _sz, _sz, _i, _sz, _d, _pu64, _pd, _i]),
     "heat_async_sim_current": (_i, [_vp, _pd, _P(_sz)]),
     "heat_async_sim_destroy": (_i, [_vp]),
     "heat_plan_create": (_i, [_P(_vp), _sz, _i]),

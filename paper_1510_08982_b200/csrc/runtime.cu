@@ -154,6 +154,16 @@ uint64_t heat_kernel_launches(void) { return g_launches.load(); }
 void heat_set_strict_finite_checks(int enabled) { g_strict = enabled != 0; }
 int heat_strict_finite_checks(void) { return g_strict ? 1 : 0; }
 
+int heat_prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
+                         double* out) {
+    if (!u0 || !out) return fail(HEAT_EINVAL, "null field pointer");
+    if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
+    std::vector<double> v;
+    HB_TRY(prepare_initial(u0, n, bc_kind, c1, c2, v));
+    std::memcpy(out, v.data(), n * sizeof(double));
+    return HEAT_OK;
+}
+
 size_t heat_trajectory_length(size_t n, size_t k_end, size_t stride) {
     if (stride == 0) stride = default_stride(n);
     size_t count = 1 + k_end / stride;

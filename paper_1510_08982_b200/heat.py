@@ -224,6 +224,16 @@ def strict_finite_checks() -> bool:
     return bool(_lib.lib().heat_strict_finite_checks())
 
 
+def prepare_initial(u0: TemperatureField, bc: BoundaryCondition) -> np.ndarray:
+    """detail::prepare_initial (sync_solver.cpp:25-37): a copy of u0; for Dirichlet
+    InvalidArgument if an end is off by more than 1e-9, else the ends snapped."""
+    v = _field(u0)
+    out = np.empty_like(v)
+    _lib.check(_lib.lib().heat_prepare_initial(_lib.dptr(v), v.size, bc.kind, bc.c1, bc.c2,
+                                               _lib.dptr(out)), "prepare_initial")
+    return out
+
+
 def _field(u0) -> np.ndarray:
     if isinstance(u0, TemperatureField):
         return np.ascontiguousarray(u0.values())
@@ -326,6 +336,134 @@ def sample_delay_at(model: DelayModel, j: int, k: int) -> int:
     d = C.c_size_t(0)
     _lib.check(_lib.lib().heat_sample_delay(*model._args(), j, k, C.byref(d)), "sample_delay")
     return d.value
+
+
+_GAMMA = 0x9E3779B97F4A7C15
+_M64 = 0xFFFFFFFFFFFFFFFF
+
+
+class SplitMix64:
+    """rng.hpp:16-41.  `state` is the stream position; async_step advances it
+    on the device exactly as the reference's stream would be advanced."""
+
+    def __init__(self, seed: int):
+        self.state = int(seed) & _M64
+
+    def next(self) -> int:
+        self.state = (self.state + _GAMMA) & _M64
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        return z ^ (z >> 31)
+
+    def next_double(self) -> float:
+        return float(self.next() >> 11) * 2.0 ** -53
+
+    def next_bounded(self, bound: int) -> int:
+        return self.next() % (bound + 1)
+
+
+def sample_delay(rng: SplitMix64, model: DelayModel, k: int) -> int:
+    """sample_delay (async_sim.cpp:57-73): one draw of `rng`'s stream at step k."""
+    d = C.c_size_t(0)
+    q, law, fd, p, _ = model._args()
+    _lib.check(_lib.lib().heat_sample_delay(q, law, fd, p, rng.state, 0, k, C.byref(d)),
+               "sample_delay")
+    rng.state = (rng.state + _GAMMA) & _M64
+    return d.value
+
+
+class HistoryRing:
+    """HistoryRing (async_sim.hpp:31-57, async_sim.cpp:25-55) with its snapshots
+    in HBM: read(i, d) = u_i(current_step - d), LogicError when d >= depth,
+    d > k or d >= snapshots held.  push() of a host state rotates the ring
+    without moving device data; async_step() reads it on the device."""
+
+    def __init__(self, depth: int, initial, device: int = -1):
+        self._create(depth, 0, np.asarray(initial, np.float64).reshape(1, -1), device)
+
+    @classmethod
+    def at_step(cls, depth: int, step: int, snapshots, device: int = -1) -> "HistoryRing":
+        """A ring at `step` holding min(depth, step + 1) snapshots, row d = u(step - d)."""
+        ring = cls.__new__(cls)
+        rows = np.asarray(snapshots, np.float64)
+        ring._create(depth, step, rows.reshape(rows.shape[0], -1), device)
+        return ring
+
+    def _create(self, depth: int, step: int, rows: np.ndarray, device: int) -> None:
+        rows = np.ascontiguousarray(rows)
+        self._h = C.c_void_p()
+        self._n = rows.shape[1]
+        _lib.check(_lib.lib().heat_history_create(C.byref(self._h), depth, self._n, step,
+                                                  _lib.dptr(rows), rows.shape[0], device),
+                   "HistoryRing")
+
+    def _info(self):
+        d, k, n = C.c_size_t(), C.c_size_t(), C.c_size_t()
+        _lib.check(_lib.lib().heat_history_info(self._h, C.byref(d), C.byref(k), C.byref(n)),
+                   "HistoryRing")
+        return d.value, k.value, n.value
+
+    def depth(self) -> int:
+        return self._info()[0]
+
+    def current_step(self) -> int:
+        return self._info()[1]
+
+    def grid_size(self) -> int:
+        return self._n
+
+    def push(self, state) -> None:
+        v = np.ascontiguousarray(np.asarray(state, np.float64).reshape(-1))
+        _lib.check(_lib.lib().heat_history_push(self._h, _lib.dptr(v), v.size), "HistoryRing::push")
+
+    def read(self, i: int, d: int) -> float:
+        x = C.c_double()
+        _lib.check(_lib.lib().heat_history_read(self._h, i, d, C.byref(x)), "HistoryRing::read")
+        return x.value
+
+    def snapshot(self, d: int) -> np.ndarray:
+        out = np.empty(self._n, np.float64)
+        _lib.check(_lib.lib().heat_history_snapshot(self._h, d, _lib.dptr(out)),
+                   "HistoryRing::snapshot")
+        return out
+
+    def _step(self, params, bc, part, model, rng, out, push):
+        st = C.c_uint64(rng.state)
+        q, law, fd, p, _ = model._args()
+        try:
+            _lib.check(_lib.lib().heat_async_step(self._h, params.r(), bc.kind, bc.c1, bc.c2,
+                                                  part.total(), part.per_pe(), q, law, fd, p,
+                                                  C.byref(st), _lib.dptr(out), int(push)),
+                       "async_step")
+        finally:
+            rng.state = int(st.value)
+
+    def push_async_step(self, params: SolverParams, bc: BoundaryCondition, part: PartitionSpec,
+                        model: DelayModel, rng: SplitMix64) -> None:
+        """AsyncSimulator::step (async_sim.cpp:136-140) on this ring: async_step,
+        then push its result, all on the device."""
+        self._step(params, bc, part, model, rng, None, True)
+
+    def close(self):
+        if self._h:
+            _lib.lib().heat_history_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def async_step(hist: HistoryRing, params: SolverParams, bc: BoundaryCondition,
+               part: PartitionSpec, model: DelayModel, rng: SplitMix64) -> TemperatureField:
+    """async_step (async_sim.hpp:68-71, async_sim.cpp:107-116): one step of Eq. (4)
+    over the ring, drawing from `rng` in the reference's order (kernels K8a/K8b)."""
+    out = np.empty(hist.grid_size(), np.float64)
+    hist._step(params, bc, part, model, rng, out, False)
+    return TemperatureField(out)
 
 
 def async_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
@@ -604,6 +742,53 @@ def exec_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
                                [int(x) for x in st.delay_histogram], int(st.waits),
                                float(st.residual_sum))
     return res
+
+
+@dataclass
+class BenchRow:
+    """async_exec.hpp:72-78 (times are GPU device time, ns)."""
+
+    n_points: int = 0
+    mode: ExecMode = ExecMode.Barriered
+    reps: int = 0
+    median_ns: int = 0
+    min_ns: int = 0
+
+
+def measure(grid_sizes: Sequence[int], modes: Sequence[ExecMode], reps: int, k_end: int,
+            workers: int) -> list:
+    """measure (async_exec.cpp:281-307): cosine IC, r = 0.5, Dirichlet(1, 0),
+    `workers` PEs; median = times[reps // 2] and min of `reps` exec_run calls."""
+    if reps < 3:
+        raise InvalidArgument("measure: reps >= 3 required")
+    rows = []
+    for n in grid_sizes:
+        if n % workers != 0:
+            raise InvalidArgument("measure: workers must divide every N")
+        u0 = cosine_init(n)
+        params = SolverParams.from_r(0.5)
+        bc = BoundaryCondition.dirichlet(1.0, 0.0)
+        part = PartitionSpec(n, n // workers)
+        for mode in modes:
+            cfg = ExecConfig(workers, k_end, mode, False)
+            times = sorted(exec_run(u0, params, bc, part, cfg).duration_ns for _ in range(reps))
+            rows.append(BenchRow(n, mode, reps, times[len(times) // 2], times[0]))
+    return rows
+
+
+def speedup_ratio(rows: Sequence[BenchRow], n_points: int) -> float:
+    """speedup_ratio (async_exec.cpp:309-318): barriered median / barrier-free median."""
+    barriered = free_running = 0
+    for row in rows:
+        if row.n_points != n_points:
+            continue
+        if row.mode == ExecMode.Barriered:
+            barriered = row.median_ns
+        else:
+            free_running = row.median_ns
+    if barriered == 0 or free_running == 0:
+        raise InvalidArgument("speedup_ratio: missing mode for this N")
+    return float(barriered) / float(free_running)
 
 
 # ---- device-resident plan ------------------------------------------------------

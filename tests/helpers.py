@@ -60,3 +60,27 @@ def bits_equal(a: np.ndarray, b: np.ndarray) -> bool:
     a = np.ascontiguousarray(a, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     return a.shape == b.shape and bool(np.all(a.view(np.uint64) == b.view(np.uint64)))
+
+
+def async_step_cases(seed: int, count: int, n_max: int = 60):
+    """Random async_step inputs (async_sim.cpp:107-116): a ring at a random
+    step with min(depth, step + 1) snapshots, a random partition / BC / law,
+    and a random stream position.  One case in four has depth < q, so late
+    draws can reach past the ring (HistoryRing::read's logic_error)."""
+    gen = SplitMix64(seed)
+    cases = []
+    for _ in range(count):
+        n = 3 + gen.next_bounded(n_max - 3)
+        q = 1 + gen.next_bounded(7)
+        depth = q if gen.next_bounded(3) else 1 + gen.next_bounded(q - 1) if q > 1 else 1
+        step = gen.next_bounded(12)
+        held = min(depth, step + 1)
+        law = int(gen.next_bounded(2))
+        cases.append(dict(
+            snaps=np.stack([random_field(gen, n) for _ in range(held)]),
+            depth=depth, step=step, r=0.5 * (gen.next_double() * 0.999 + 0.001),
+            bc=int(gen.next() & 1), c1=gen.next_double(), c2=gen.next_double(),
+            part_total=n, per_pe=random_divisor(gen, n), law=law, q=q,
+            fixed_d=int(gen.next_bounded(q - 1)) if law == 1 else 0,
+            p=0.05 + 0.9 * gen.next_double(), rng_state=gen.next()))
+    return cases

@@ -296,3 +296,25 @@ def test_free_run_q1_exact(H, port):
                                H.PartitionSpec(1024, 128), 1, 700)
     assert bits_equal(fin, port.sync_run(u0, 0.3, 0, 0.0, 0.0, 700))
     assert st.max_delay == 0 and st.residual_sum < 1e-9
+
+
+def test_measure_and_speedup_ratio(gpu):
+    """measure / speedup_ratio (async_exec.cpp:281-318) over the GPU exec_run,
+    as test_exec.cpp:151-175 checks them: row shape, reps >= 3, median >= min,
+    a positive ratio, and cost growing with N in both modes."""
+    from paper_1510_08982_b200 import heat as H
+    one = H.measure([30], [H.ExecMode.Barriered], 3, 50, 1)
+    assert len(one) == 1
+    assert (one[0].n_points, one[0].reps) == (30, 3)
+    assert one[0].median_ns >= one[0].min_ns > 0
+    with pytest.raises(H.InvalidArgument):
+        H.measure([30], [H.ExecMode.Barriered], 2, 50, 1)
+    with pytest.raises(H.InvalidArgument):
+        H.measure([30], [H.ExecMode.Barriered], 3, 50, 7)
+    rows = H.measure([100, 10000], [H.ExecMode.Barriered, H.ExecMode.BarrierFree], 5, 200, 1)
+    assert H.speedup_ratio(rows, 100) > 0.0
+    for mode in (H.ExecMode.Barriered, H.ExecMode.BarrierFree):
+        med = {r.n_points: r.median_ns for r in rows if r.mode == mode}
+        assert med[10000] >= med[100]
+    with pytest.raises(H.InvalidArgument):
+        H.speedup_ratio(rows, 64)

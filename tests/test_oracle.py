@@ -134,3 +134,19 @@ def test_port_exec_vs_reference(port, ref):
     fp, _ = port.exec_run(u, 0.5, 0, 1.0, 0.0, 96, 1, 500, mode=1)
     fr, _, _ = ref.exec_run(u, 0.5, 0, 1.0, 0.0, 96, 1, 500, mode=1)
     assert bits_equal(fp, fr)
+
+
+@pytest.mark.parametrize("seed", [11, 12])
+def test_port_async_step_vs_reference(port, ref, seed):
+    """async_step over arbitrary rings: values, status and the stream position
+    after the call (D draws, or through the failing draw on a logic_error)."""
+    from helpers import async_step_cases
+    errors = 0
+    for c in async_step_cases(seed, 60):
+        sp, fp, rp = port.async_step(**c)
+        sr, fr, rr = ref.async_step(**c)
+        assert (sp, rp) == (sr, rr)
+        errors += sp == 3
+        if sp == 0:
+            assert bits_equal(fp, fr)
+    assert errors > 0  # the logic_error path was exercised
