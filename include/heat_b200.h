@@ -124,6 +124,10 @@ int heat_stream_chunk_plan(size_t n, size_t wave_points, size_t* bounds, size_t 
 int heat_k3_geometry(size_t n, size_t P, size_t q, int mode, int* lanes_per_pe, int* points_per_lane,
                      size_t* warps, int* shared_rings);
 int heat_k5_geometry(size_t n, int* points_per_lane, int* halo);
+/* The geometric law's q-1 delay thresholds on a draw's top 53 bits
+ * (thresholds[j-1] = first m = x >> 11 whose delay is >= j; 2^53 = never),
+ * as the device kernels use them; HEAT_EINVAL for p too small. */
+int heat_geometric_thresholds(double p, size_t q, uint64_t* thresholds);
 
 /* ---- library state ---------------------------------------------------- */
 const char* heat_last_error(void);
@@ -196,10 +200,13 @@ int heat_async_free_run(const double* u0, size_t n, double r, int bc_kind, doubl
  * seeds base_seed + j (analysis.cpp:51-104), each recording l2_norm at steps
  * 0, stride, 2*stride, ... and k_end.  Fills steps_out[S] (S via n_steps),
  * norms[runs][S], terminals[runs][n] (may be NULL), mean_series[S] and
- * std_series[S] (population std), bit-identical to the reference.  Uniform
- * and fixed delay laws; N <= 4096 and (q+1)*N*8 bytes of shared memory. */
+ * std_series[S] (population std), bit-identical to the reference.  All
+ * three delay laws.  One CTA per member (K6) when the member's history fits
+ * shared memory (N <= 4096, (q+1)*N*8 bytes <= 200 KB); otherwise members run
+ * one after another on AsyncSimulator handles (K3/K5). */
 int heat_ensemble_run(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
-                      size_t per_pe, size_t q, int law, size_t fixed_delay, size_t k_end,
+                      size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                      size_t k_end,
                       size_t stride, size_t runs, uint64_t base_seed, size_t* steps_out,
                       size_t max_steps, size_t* n_steps, double* norms, double* terminals,
                       double* mean_series, double* std_series);

@@ -196,12 +196,9 @@ EnsembleResult ensemble_run(const EnsembleConfig& cfg, std::size_t runs,
     std::vector<double> norms(std::max<std::size_t>(1, runs) * cap), terms(runs * n), mean(cap),
         stdv(cap);
     const DelayModel& m = cfg.model;
-    const int law = m.distribution == DelayModel::Distribution::Uniform ? HEAT_DELAY_UNIFORM
-                    : m.distribution == DelayModel::Distribution::Fixed ? HEAT_DELAY_FIXED
-                                                                        : HEAT_DELAY_GEOMETRIC;
     throw_on(heat_ensemble_run(cfg.u0.values().data(), n, cfg.params.r(), bc_kind(cfg.bc),
-                               cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(), m.q, law, m.fixed_delay,
-                               cfg.k_end, stride, runs, base_seed, steps.data(), cap, &S,
+                               cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(), m.q, law_of(m),
+                               m.fixed_delay, m.geometric_p, cfg.k_end, stride, runs, base_seed, steps.data(), cap, &S,
                                norms.data(), terms.data(), mean.data(), stdv.data()));
     EnsembleResult res;
     res.steps.assign(steps.begin(), steps.begin() + S);

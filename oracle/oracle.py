@@ -285,12 +285,12 @@ class Ref(_Lib):
         self.lib.ref_set_strict(int(on))
 
     def ensemble_run(self, u0, r, bc, c1, c2, per_pe, law, q, fixed_d, k_end, stride, runs,
-                     base_seed):
+                     base_seed, p=0.5):
         """heat::ensemble_run -> (steps, norms[runs][S], terminals[runs][n], mean, std, spread2)."""
         L = self.lib
         if not getattr(L.ref_ensemble_run, "argtypes", None):
-            L.ref_ensemble_run.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _i, _sz, _sz, _sz, _sz,
-                                           _sz, _u64, _psz, _psz, _pd, _pd, _pd, _pd, _pd]
+            L.ref_ensemble_run.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _i, _sz, _sz, _d, _sz,
+                                           _sz, _sz, _u64, _psz, _psz, _pd, _pd, _pd, _pd, _pd]
         u0 = _f64(u0)
         n = u0.size
         s_ = stride if stride else (1 if n <= 1000 else 100)
@@ -302,8 +302,8 @@ class Ref(_Lib):
         mean = np.zeros(cap)
         std = np.zeros(cap)
         spread = np.zeros(2)
-        st = L.ref_ensemble_run(_ptr(u0), n, r, bc, c1, c2, per_pe, law, q, fixed_d, k_end, stride,
-                                runs, base_seed, _ptr(steps, _psz), C.byref(ns), _ptr(norms),
+        st = L.ref_ensemble_run(_ptr(u0), n, r, bc, c1, c2, per_pe, law, q, fixed_d, p, k_end,
+                                stride, runs, base_seed, _ptr(steps, _psz), C.byref(ns), _ptr(norms),
                                 _ptr(terms), _ptr(mean), _ptr(std), _ptr(spread))
         if st:
             raise OracleError(st, "ensemble_run")

@@ -275,7 +275,7 @@ unsigned ref_hardware_concurrency() { return std::thread::hardware_concurrency()
 // ensemble_run (analysis.cpp:51-104): norms[runs][S], terminals[runs][n],
 // mean/std[S]; steps_out[S]; returns S through n_steps.
 int ref_ensemble_run(const double* u0, std::size_t n, double r, int bc, double c1, double c2,
-                     std::size_t per_pe, int law, std::size_t q, std::size_t fixed_d,
+                     std::size_t per_pe, int law, std::size_t q, std::size_t fixed_d, double p,
                      std::size_t k_end, std::size_t stride, std::size_t runs,
                      std::uint64_t base_seed, std::size_t* steps_out, std::size_t* n_steps,
                      double* norms, double* terminals, double* mean, double* stdv,
@@ -285,7 +285,7 @@ int ref_ensemble_run(const double* u0, std::size_t n, double r, int bc, double c
                                  heat::SolverParams::from_r(r, true),
                                  make_bc(bc, c1, c2),
                                  heat::PartitionSpec(n, per_pe),
-                                 make_model(law, q, fixed_d, 0.5, 0),
+                                 make_model(law, q, fixed_d, p, 0),
                                  k_end,
                                  stride};
         heat::EnsembleResult res = heat::ensemble_run(cfg, runs, base_seed);

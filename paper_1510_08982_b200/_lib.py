@@ -102,6 +102,7 @@ SIGNATURES = {
     "heat_stream_chunk_plan": (_i, [_sz, _sz, _P(_sz), _sz, _P(_sz)]),
     "heat_k3_geometry": (_i, [_sz, _sz, _sz, _i, _P(_i), _P(_i), _P(_sz), _P(_i)]),
     "heat_k5_geometry": (_i, [_sz, _P(_i), _P(_i)]),
+    "heat_geometric_thresholds": (_i, [_d, _sz, _pu64]),
     "heat_set_strict_finite_checks": (None, [_i]),
     "heat_strict_finite_checks": (_i, []),
     "heat_prepare_initial": (_i, [_pd, _sz, _i, _d, _d, _pd]),
@@ -113,7 +114,7 @@ SIGNATURES = {
                             _pd, _pd, _psz, _sz, _psz]),
     "heat_sample_delay": (_i, [_sz, _i, _sz, _d, _u64, _u64, _sz, _psz]),
     "heat_async_free_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _pd, _P(AsyncStatsC)]),
-    "heat_ensemble_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _sz, _sz, _sz, _u64,
+    "heat_ensemble_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _sz, _sz, _sz, _u64,
                                _psz, _sz, _psz, _pd, _pd, _pd, _pd]),
     "heat_exec_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _i, _sz, _pd, _pu64,
                            _P(LagStatsC), _P(AsyncStatsC)]),

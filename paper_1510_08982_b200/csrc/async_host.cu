@@ -41,7 +41,6 @@ struct AsyncWork {
     unsigned long long* prog;
     int* offL;
     int* offR;
-    unsigned char* dtable;
     unsigned long long* stats;
     unsigned int* abort_word;
     double* edge_log;
@@ -184,23 +183,10 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     std::vector<int> offL, offR;
     const int D = draw_offsets(s.N, s.n, dir, offL, offR);
 
-    // host-drawn geometric delays (glibc log1p, bit-identical to the reference)
-    std::vector<unsigned char> dtab;
-    if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {
-        if (q > 256) return fail(HEAT_EINVAL, "async: geometric law on the GPU needs q <= 256");
-        dtab.resize(std::max<size_t>(1, s.k_end * size_t(D)));
-        const double lp = std::log1p(-s.geometric_p);
-        for (size_t k = 0; k < s.k_end; ++k) {
-            const size_t bound = std::min<size_t>(size_t(q - 1), k);
-            for (int o = 0; o < D; ++o) {
-                const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * D + o);
-                const double u = double(x >> 11) * 0x1.0p-53;
-                double g = std::floor(std::log1p(-u) / lp);
-                if (!std::isfinite(g) || g < 0.0) g = 0.0;
-                dtab[k * D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
-            }
-        }
-    }
+    // geometric law: the delay thresholds (exact, runtime.cu geometric_thresholds)
+    std::vector<uint64_t> gthr;
+    if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC)
+        HB_TRY(geometric_thresholds(s.geometric_p, s.q, gthr));
 
     // scratch layout
     size_t off = 0;
@@ -209,7 +195,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     const size_t o_prog = take(P * sizeof(unsigned long long));
     const size_t o_offL = take(P * sizeof(int));
     const size_t o_offR = take(P * sizeof(int));
-    const size_t o_dtab = take(std::max<size_t>(1, dtab.size()));
+    const size_t o_gthr = take(std::max<size_t>(1, gthr.size()) * sizeof(uint64_t));
     const size_t o_stats = take(kStatWords * sizeof(unsigned long long));
     const size_t o_abort = take(sizeof(unsigned int));
     const size_t o_elog = take(s.want_logs ? (s.k_end + 1) * P * 2 * sizeof(double) : 0);
@@ -229,8 +215,9 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     stats0[kStatLagMin] = ~0ull;
     HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), P * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!dtab.empty())
-        HB_CUDA(cudaMemcpyAsync(base + o_dtab, dtab.data(), dtab.size(), cudaMemcpyHostToDevice, st));
+    if (!gthr.empty())
+        HB_CUDA(cudaMemcpyAsync(base + o_gthr, gthr.data(), gthr.size() * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemcpyAsync(base + o_stats, stats0.data(), kStatWords * sizeof(unsigned long long),
                             cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemsetAsync(base + o_abort, 0, sizeof(unsigned int), st));
@@ -256,7 +243,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     a.D = D;
     a.off_left = reinterpret_cast<const int*>(base + o_offL);
     a.off_right = reinterpret_cast<const int*>(base + o_offR);
-    a.dtable = reinterpret_cast<const unsigned char*>(base + o_dtab);
+    a.gthr = reinterpret_cast<const uint64_t*>(base + o_gthr);
     a.ring = reinterpret_cast<double*>(base + o_ring);
     a.prog = reinterpret_cast<unsigned long long*>(base + o_prog);
     // statistics only when asked for: they sit on the latency-critical step
@@ -714,9 +701,8 @@ struct heat_async_sim {
     // K5
     hb::StreamLayout L;
     std::vector<int> offL, offR;
-    // GEOMETRIC: host-drawn delays of the current slice
-    unsigned char* dtab = nullptr;
-    size_t dtab_bytes = 0;
+    // GEOMETRIC: the delay thresholds (device, uploaded once)
+    uint64_t* gthr = nullptr;
 };
 
 namespace {
@@ -728,39 +714,9 @@ void sim_free(heat_async_sim* sim) {
     if (sim->ctx.buf[0]) cudaFree(sim->ctx.buf[0]);
     if (sim->ctx.scratch) cudaFree(sim->ctx.scratch);
     if (sim->ctx.flag) cudaFree(sim->ctx.flag);
-    if (sim->dtab) cudaFree(sim->dtab);
+    if (sim->gthr) cudaFree(sim->gthr);
     if (sim->ctx.stream) cudaStreamDestroy(sim->ctx.stream);
     delete sim;
-}
-
-// Delays of steps [k0, k0 + count) for the geometric law (glibc log1p, as
-// async_pe_run draws them), uploaded to the handle's table.
-int sim_geometric_table(heat_async_sim* sim, size_t k0, size_t count, int D) {
-    const auto& s = sim->s;
-    std::vector<unsigned char> t(std::max<size_t>(1, count * size_t(D)));
-    const double lp = std::log1p(-s.geometric_p);
-    for (size_t j = 0; j < count; ++j) {
-        const size_t k = k0 + j;
-        const size_t bound = std::min<size_t>(s.q - 1, k);
-        for (int o = 0; o < D; ++o) {
-            const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * uint64_t(D) + uint64_t(o));
-            const double u = double(x >> 11) * 0x1.0p-53;
-            double g = std::floor(std::log1p(-u) / lp);
-            if (!std::isfinite(g) || g < 0.0) g = 0.0;
-            t[j * D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
-        }
-    }
-    if (sim->dtab_bytes < t.size()) {
-        if (sim->dtab) cudaFree(sim->dtab);
-        sim->dtab = nullptr;
-        sim->dtab_bytes = 0;
-        HB_CUDA(cudaMalloc(&sim->dtab, t.size()));
-        sim->dtab_bytes = t.size();
-    }
-    HB_CUDA(cudaMemcpyAsync(sim->dtab, t.data(), t.size(), cudaMemcpyHostToDevice,
-                            sim->ctx.stream));
-    HB_CUDA(cudaStreamSynchronize(sim->ctx.stream));  // the host vector goes
-    return HEAT_OK;
 }
 
 int sim_step_k3(heat_async_sim* sim, size_t count) {
@@ -783,7 +739,6 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
         HB_CUDA(cudaMemsetAsync(base + sim->o_abort, 0, sizeof(unsigned int), st));
         sim->started = true;
     }
-    if (s.law == HEAT_DELAY_GEOMETRIC) HB_TRY(sim_geometric_table(sim, sim->k, count, sim->D));
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), st));
     AsyncPeArgs a{};
     a.field = sim->field[0];
@@ -807,8 +762,7 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
     a.D = sim->D;
     a.off_left = reinterpret_cast<const int*>(base + sim->o_offL);
     a.off_right = reinterpret_cast<const int*>(base + sim->o_offR);
-    a.dtable = sim->dtab;
-    a.dtab_k0 = (long long)sim->k;
+    a.gthr = sim->gthr;
     a.ring = reinterpret_cast<double*>(base + sim->o_ring);
     a.prog = reinterpret_cast<unsigned long long*>(base + sim->o_prog);
     a.flag = d.flag;
@@ -821,11 +775,6 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
 int sim_step_k5(heat_async_sim* sim, size_t count) {
     DevCtx& d = sim->ctx;
     StreamExternal ext{};
-    if (sim->s.law == HEAT_DELAY_GEOMETRIC) {
-        HB_TRY(sim_geometric_table(sim, sim->k, count, sim->L.D));
-        ext.dtab = sim->dtab;
-        ext.dtab_k0 = (long long)sim->k;
-    }
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 2 * sizeof(unsigned int), d.stream));
     const bool init = !sim->started;
     sim->started = true;
@@ -924,6 +873,14 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         HB_TRY(ensure_scratch(d, off));
         sim->smem = G.smem;
         sim->shared = G.shared;
+        if (law == HEAT_DELAY_GEOMETRIC) {  // exact device delays of the law
+            std::vector<uint64_t> gthr;
+            HB_TRY(geometric_thresholds(geometric_p, q, gthr));
+            HB_CUDA(cudaMalloc(&sim->gthr, std::max<size_t>(1, gthr.size()) * sizeof(uint64_t)));
+            if (!gthr.empty())
+                HB_CUDA(cudaMemcpy(sim->gthr, gthr.data(), gthr.size() * sizeof(uint64_t),
+                                   cudaMemcpyHostToDevice));
+        }
     }
     *out = sim;
     sim = nullptr;  // owned by the caller now
@@ -972,3 +929,11 @@ int heat_async_sim_destroy(heat_async_sim* sim) {
 }
 
 }  // extern "C"
+
+namespace hb {
+// The simulator's current field on the device and its stream (ensemble.cu).
+void async_sim_device_field(heat_async_sim* sim, const double** field, cudaStream_t* st) {
+    *field = sim->field[sim->cur];
+    *st = sim->ctx.stream;
+}
+}  // namespace hb

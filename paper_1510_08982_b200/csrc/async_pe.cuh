@@ -54,8 +54,7 @@ struct AsyncPeArgs {
     long long D;            // cross-PE reads (draws) per step
     const int* off_left;    // [P] in-step draw rank of the first point's left read, -1 none
     const int* off_right;   // [P] ... of the last point's right read, -1 none
-    const unsigned char* dtable;  // GEOMETRIC: host-drawn delays [(k - dtab_k0)*D + off]
-    long long dtab_k0;            // first step the table covers (0 for whole runs)
+    const uint64_t* gthr;         // GEOMETRIC: the q-1 delay thresholds (geometric_thresholds)
     double* ring;                 // [P][2][R]: side 0 = first point, 1 = last point
     unsigned long long* prog;     // [P] published step count
     unsigned long long* stats;    // see kStat* offsets
@@ -109,10 +108,10 @@ struct RingOps<true> {
 __device__ __forceinline__ int det_delay(const AsyncPeArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
     if (bound == 0) return 0;  // every law yields 0 (the draw is still "consumed" by index)
-    if (a.law == 2) return a.dtable[(k - a.dtab_k0) * a.D + off];  // host-drawn, bounded
+    if (a.law == 1) return a.fixed_d < bound ? a.fixed_d : int(bound);
     const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
     if (a.law == 0) return uniform_delay(x, bound, a.modq);
-    return a.fixed_d < bound ? a.fixed_d : int(bound);
+    return geometric_delay(x, a.gthr, int(bound));
 }
 
 // Spin until prog[pe] >= need (acquire).  Returns the observed progress, or

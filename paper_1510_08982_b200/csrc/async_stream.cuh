@@ -77,8 +77,7 @@ struct AsyncStreamArgs {
     long long D;
     const int* off_left;
     const int* off_right;
-    const unsigned char* dtable;  // GEOMETRIC delays [(k - dtab_k0)*D + off]
-    long long dtab_k0;            // first step the table covers
+    const uint64_t* gthr;         // GEOMETRIC: the q-1 delay thresholds (geometric_thresholds)
     const struct PeLink* links;   // [P] neighbour sources / publish targets
     int pin_first_pe;             // PE whose first point is the pinned global end 0 (or -1)
     int pin_last_pe;              // PE whose last point is the pinned global end N-1 (or -1)
@@ -92,10 +91,10 @@ struct AsyncStreamArgs {
 
 __device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
-    if (a.law == 2) return a.dtable[(k - a.dtab_k0) * a.D + off];
+    if (a.law == 1) return a.fixed_d < bound ? a.fixed_d : int(bound);
     const uint64_t x = splitmix_draw(a.seed, uint64_t(k) * uint64_t(a.D) + uint64_t(off));
     if (a.law == 0) return uniform_delay(x, bound, a.modq);
-    return a.fixed_d < bound ? a.fixed_d : int(bound);
+    return geometric_delay(x, a.gthr, int(bound));
 }
 
 __device__ __forceinline__ uint64_t ld_acq(const unsigned long long* w, bool sys) {

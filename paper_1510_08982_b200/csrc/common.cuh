@@ -71,6 +71,15 @@ __device__ __forceinline__ int uniform_delay(uint64_t x, long long bound, const 
     return int(x % uint64_t(bound + 1));  // the first q-1 steps only
 }
 
+// Geometric-law delay from the thresholds of geometric_thresholds()
+// (runtime.cuh): T[j-1] is the first top-53-bits value whose delay is >= j.
+__device__ __forceinline__ int geometric_delay(uint64_t x, const uint64_t* T, int bound) {
+    const uint64_t m = x >> 11;
+    int d = 0;
+    while (d < bound && m >= T[d]) ++d;
+    return d;
+}
+
 // ---- shared-memory / async-proxy PTX wrappers -----------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -31,8 +31,9 @@ struct EnsembleArgs {
     double r, c, c1, c2;
     int dirichlet;
     int q;              // delays in {0..q-1}; q+1 history slots
-    int law;            // uniform or fixed
+    int law;            // uniform, fixed or geometric
     int fixed_d;
+    const uint64_t* gthr;  // geometric law: the q-1 delay thresholds (geometric_thresholds)
     unsigned long long base_seed;
     ModQ modq;          // x mod q (uniform law, steps k >= q-1)
     long long D;        // cross-PE reads per step
@@ -56,7 +57,7 @@ __device__ double seq_l2(const double* v, int n) {
 
 constexpr unsigned long long kGamma = 0x9e3779b97f4a7c15ULL;  // rng.hpp:21
 
-// PT points per thread (t, t+T, ...); LAW 0 uniform, 1 fixed.  The member is
+// PT points per thread (t, t+T, ...); LAW 0 uniform, 1 fixed, 2 geometric.  The member is
 // latency-bound (one warp per scheduler), so the step is written for a short
 // dependent chain: per-point constants hoisted, SplitMix64 counters carried
 // incrementally (draw k*D + off of the member's stream is mix(z) with
@@ -65,10 +66,13 @@ constexpr unsigned long long kGamma = 0x9e3779b97f4a7c15ULL;  // rng.hpp:21
 // bound = q-1, modulus q) free of branches.
 template <int PT, int LAW>
 __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
-    extern __shared__ __align__(16) double hist[];  // [(q+1)][n]
+    extern __shared__ __align__(16) double hist[];  // [(q+1)][n], then the q-1 thresholds
     const int n = a.n, q = a.q, Q = a.q + 1, T = blockDim.x, t = threadIdx.x;
     const unsigned long long seed = a.base_seed + blockIdx.x;
     using A = Arith<double>;
+    uint64_t* gthr = reinterpret_cast<uint64_t*>(hist + (size_t)Q * n);
+    if (LAW == 2)
+        for (int j = t; j < q - 1; j += T) gthr[j] = a.gthr[j];
     for (int i = t; i < n; i += T) hist[i] = a.u0[i];  // slot 0 = step 0
     __syncthreads();
     if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = seq_l2(hist, n);
@@ -103,10 +107,13 @@ __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
                             ? 0 : int(splitmix_mix(zL[j]) % (unsigned long long)(bound + 1));
                 dR[j] = offR[j] < 0 || bound == 0
                             ? 0 : int(splitmix_mix(zR[j]) % (unsigned long long)(bound + 1));
-            } else {
+            } else if (LAW == 1) {
                 const int d = a.fixed_d < bound ? a.fixed_d : int(bound);
                 dL[j] = offL[j] < 0 ? 0 : d;
                 dR[j] = offR[j] < 0 ? 0 : d;
+            } else {
+                dL[j] = offL[j] < 0 ? 0 : geometric_delay(splitmix_mix(zL[j]), gthr, int(bound));
+                dR[j] = offR[j] < 0 ? 0 : geometric_delay(splitmix_mix(zR[j]), gthr, int(bound));
             }
             zL[j] += zstep;
             zR[j] += zstep;
@@ -123,9 +130,16 @@ __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
                 dR[j] = offR[j] < 0 ? 0 : xr;
                 zL[j] += zstep;
                 zR[j] += zstep;
-            } else {
+            } else if (LAW == 1) {
                 dL[j] = offL[j] < 0 ? 0 : a.fixed_d;
                 dR[j] = offR[j] < 0 ? 0 : a.fixed_d;
+            } else {
+                const int xl = geometric_delay(splitmix_mix(zL[j]), gthr, q - 1);
+                const int xr = geometric_delay(splitmix_mix(zR[j]), gthr, q - 1);
+                dL[j] = offL[j] < 0 ? 0 : xl;
+                dR[j] = offR[j] < 0 ? 0 : xr;
+                zL[j] += zstep;
+                zR[j] += zstep;
             }
         }
     };
@@ -183,10 +197,11 @@ __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
 
 using EnsembleKernel = void (*)(const EnsembleArgs);
 EnsembleKernel pick_kernel(int pt, int law) {
-    const EnsembleKernel k[3][2] = {{ensemble_kernel<1, 0>, ensemble_kernel<1, 1>},
-                                    {ensemble_kernel<2, 0>, ensemble_kernel<2, 1>},
-                                    {ensemble_kernel<4, 0>, ensemble_kernel<4, 1>}};
-    return k[pt == 1 ? 0 : pt == 2 ? 1 : 2][law == HEAT_DELAY_UNIFORM ? 0 : 1];
+    const EnsembleKernel k[3][3] = {
+        {ensemble_kernel<1, 0>, ensemble_kernel<1, 1>, ensemble_kernel<1, 2>},
+        {ensemble_kernel<2, 0>, ensemble_kernel<2, 1>, ensemble_kernel<2, 2>},
+        {ensemble_kernel<4, 0>, ensemble_kernel<4, 1>, ensemble_kernel<4, 2>}};
+    return k[pt == 1 ? 0 : pt == 2 ? 1 : 2][law];
 }
 
 // In-step draw rank of every read of async_step_into (async_sim.cpp:86-101),
@@ -207,6 +222,94 @@ long long point_offsets(int n, int per_pe, bool dirichlet, std::vector<int>& off
     return cnt;
 }
 
+// mean / population std per recorded step, the reference's loop order
+// (analysis.cpp:88-103)
+void series_stats(const std::vector<double>& hn, size_t runs, size_t S, double* mean_series,
+                  double* std_series) {
+    for (size_t s = 0; s < S; ++s) {
+        double mean = 0.0;
+        for (size_t j = 0; j < runs; ++j) mean += hn[j * S + s];
+        mean /= double(runs);
+        double var = 0.0;
+        for (size_t j = 0; j < runs; ++j) {
+            const double dd = hn[j * S + s] - mean;
+            var += dd * dd;
+        }
+        if (mean_series) mean_series[s] = mean;
+        if (std_series) std_series[s] = std::sqrt(var / double(runs));
+    }
+}
+
+// l2_norm of a device field in the reference's order (one thread); flag |= 1
+// when the field holds a non-finite value (the terminal TemperatureField).
+__global__ void member_norm_kernel(const double* __restrict__ v, long long n, double* out,
+                                   unsigned int* flag) {
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (long long i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(v[i], v[i]));
+        *out = sqrt(s);
+    }
+    if (flag) {
+        bool bad = false;
+        for (long long i = threadIdx.x; i < n; i += blockDim.x) bad |= !isfinite(v[i]);
+        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1u);
+    }
+}
+
+// run_member (analysis.cpp:16-38) for each member on a GPU AsyncSimulator
+// handle: K3 for PEs <= 1024 points, K5 for wider ones.
+int ensemble_via_simulators(const double* u0, size_t n, double r, int bc_kind, double c1,
+                            double c2, size_t per_pe, size_t q, int law, size_t fixed_delay,
+                            double geometric_p, const std::vector<size_t>& steps, size_t runs,
+                            uint64_t base_seed, std::vector<double>& hn, double* terminals) {
+    const size_t S = steps.size();
+    double* dn = nullptr;
+    unsigned int* dflag = nullptr;
+    struct Bufs {
+        double*& dn;
+        unsigned int*& f;
+        ~Bufs() {
+            if (dn) cudaFree(dn);
+            if (f) cudaFree(f);
+        }
+    } bufs{dn, dflag};
+    HB_CUDA(cudaMalloc(&dn, S * sizeof(double)));
+    HB_CUDA(cudaMalloc(&dflag, sizeof(unsigned int)));
+    for (size_t j = 0; j < runs; ++j) {
+        heat_async_sim* sim = nullptr;
+        HB_TRY(heat_async_sim_create(&sim, u0, n, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
+                                     geometric_p, base_seed + j));
+        struct Guard {
+            heat_async_sim* s;
+            ~Guard() { heat_async_sim_destroy(s); }
+        } guard{sim};
+        size_t k = 0;
+        const double* field = nullptr;
+        cudaStream_t st = nullptr;
+        for (size_t s = 0; s < S; ++s) {
+            if (steps[s] > k) HB_TRY(heat_async_sim_step(sim, steps[s] - k));
+            k = steps[s];
+            async_sim_device_field(sim, &field, &st);
+            const bool last = s + 1 == S;
+            if (last) HB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(unsigned int), st));
+            member_norm_kernel<<<1, 256, 0, st>>>(field, (long long)n, dn + s,
+                                                  last ? dflag : nullptr);
+            HB_CUDA(cudaGetLastError());
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+        unsigned int bad = 0;
+        HB_CUDA(cudaMemcpyAsync(hn.data() + j * S, dn, S * sizeof(double), cudaMemcpyDeviceToHost,
+                                st));
+        HB_CUDA(cudaMemcpyAsync(&bad, dflag, sizeof bad, cudaMemcpyDeviceToHost, st));
+        if (terminals)
+            HB_CUDA(cudaMemcpyAsync(terminals + j * n, field, n * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
+        if (bad) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    return HEAT_OK;
+}
+
 }  // namespace
 }  // namespace hb
 
@@ -214,7 +317,7 @@ using namespace hb;
 
 extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_kind, double c1,
                                  double c2, size_t per_pe, size_t q, int law, size_t fixed_delay,
-                                 size_t k_end, size_t stride, size_t runs, uint64_t base_seed,
+                                 double geometric_p, size_t k_end, size_t stride, size_t runs, uint64_t base_seed,
                                  size_t* steps_out, size_t max_steps, size_t* n_steps,
                                  double* norms, double* terminals, double* mean_series,
                                  double* std_series) {
@@ -226,21 +329,13 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
     if (law == HEAT_DELAY_FIXED && fixed_delay >= q)
         return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
-    if (law == HEAT_DELAY_GEOMETRIC)
-        return fail(HEAT_EINVAL, "GPU ensembles support the uniform and fixed laws "
-                                 "(the geometric law needs glibc log1p bits)");
-    if (law != HEAT_DELAY_UNIFORM && law != HEAT_DELAY_FIXED)
-        return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
+    if (law == HEAT_DELAY_GEOMETRIC && (!(geometric_p > 0.0) || geometric_p > 1.0))
+        return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
+    if (law < 0 || law > 2) return fail(HEAT_ELOGIC, "sample_delay: unknown distribution");
     if (runs == 0) return fail(HEAT_EDOMAIN, "ensemble_run: M >= 1 required");
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     if (stride == 0) stride = default_stride(n);
-    constexpr size_t kMaxPoints = 4096;
-    if (n > kMaxPoints) return fail(HEAT_EINVAL, "GPU ensembles: N <= 4096");
-    const int PT = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
-    const int T = int(((n + PT - 1) / PT + 31) / 32 * 32);
-    const size_t smem = (q + 1) * n * sizeof(double);
-    if (smem > 200 * 1024) return fail(HEAT_EINVAL, "GPU ensembles: (q+1)*N*8 must fit in shared memory");
 
     // recorded steps (analysis.cpp:56-60)
     std::vector<size_t> steps{0};
@@ -251,16 +346,34 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
         for (size_t s = 0; s < S && s < max_steps; ++s) steps_out[s] = steps[s];
     if (n_steps) *n_steps = S;
 
+    std::vector<uint64_t> gthr;
+    if (law == HEAT_DELAY_GEOMETRIC) HB_TRY(geometric_thresholds(geometric_p, q, gthr));
+    constexpr size_t kMaxPoints = 4096;
+    const size_t smem = (q + 1) * n * sizeof(double) + gthr.size() * sizeof(uint64_t);
+    std::vector<double> hn(runs * S);
+    if (n > kMaxPoints || smem > 200 * 1024) {
+        // the field or its history does not fit one CTA: members through
+        // AsyncSimulator handles (K3 / K5) one after another
+        HB_TRY(ensemble_via_simulators(u0, n, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
+                                       geometric_p, steps, runs, base_seed, hn, terminals));
+        if (norms) std::copy(hn.begin(), hn.end(), norms);
+        series_stats(hn, runs, S, mean_series, std_series);
+        return HEAT_OK;
+    }
+    const int PT = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
+    const int T = int(((n + PT - 1) / PT + 31) / 32 * 32);
+
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
     const bool dir = bc_kind == HEAT_BC_DIRICHLET;
     std::vector<int> offL, offR;
     const long long D = point_offsets(int(n), int(per_pe), dir, offL, offR);
-    // device scratch: u0 | offL | offR | norms | terminals
+    // device scratch: u0 | offL | offR | thresholds | norms | terminals
     auto a256 = [](size_t b) { return (b + 255) / 256 * 256; };
     const size_t o_u0 = 0, o_offL = o_u0 + a256(n * 8), o_offR = o_offL + a256(n * 4),
-                 o_norms = o_offR + a256(n * 4), o_term = o_norms + a256(runs * S * 8),
+                 o_gthr = o_offR + a256(n * 4), o_norms = o_gthr + a256(gthr.size() * 8 + 8),
+                 o_term = o_norms + a256(runs * S * 8),
                  total = o_term + a256(terminals ? runs * n * 8 : 8);
     HB_TRY(ensure_scratch(*d, total));
     char* base = static_cast<char*>(d->scratch);
@@ -268,6 +381,9 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, reinterpret_cast<double*>(base + o_u0)));
     HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), n * 4, cudaMemcpyHostToDevice, st));
     HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), n * 4, cudaMemcpyHostToDevice, st));
+    if (!gthr.empty())
+        HB_CUDA(cudaMemcpyAsync(base + o_gthr, gthr.data(), gthr.size() * 8, cudaMemcpyHostToDevice,
+                                st));
     HB_CUDA(cudaMemsetAsync(d->flag, 0, 2 * sizeof(unsigned int), st));
 
     EnsembleArgs a{};
@@ -281,6 +397,7 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     a.q = int(q);
     a.law = law;
     a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
+    a.gthr = reinterpret_cast<const uint64_t*>(base + o_gthr);
     a.base_seed = base_seed;
     a.modq = make_modq(unsigned(q));
     a.D = D;
@@ -299,7 +416,6 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
     HB_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
 
-    std::vector<double> hn(runs * S);
     unsigned int flags[2] = {0, 0};
     HB_CUDA(cudaMemcpyAsync(hn.data(), base + o_norms, runs * S * 8, cudaMemcpyDeviceToHost, st));
     if (terminals)
@@ -311,18 +427,6 @@ extern "C" int heat_ensemble_run(const double* u0, size_t n, double r, int bc_ki
         return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     }
     if (norms) std::copy(hn.begin(), hn.end(), norms);
-    // mean / population std per recorded step, the reference's loop order
-    for (size_t s = 0; s < S; ++s) {
-        double mean = 0.0;
-        for (size_t j = 0; j < runs; ++j) mean += hn[j * S + s];
-        mean /= double(runs);
-        double var = 0.0;
-        for (size_t j = 0; j < runs; ++j) {
-            const double dd = hn[j * S + s] - mean;
-            var += dd * dd;
-        }
-        if (mean_series) mean_series[s] = mean;
-        if (std_series) std_series[s] = std::sqrt(var / double(runs));
-    }
+    series_stats(hn, runs, S, mean_series, std_series);
     return HEAT_OK;
 }

@@ -46,8 +46,9 @@ struct heat_history {
     size_t offs_key_pe = 0;
     int offs_key_bc = -1;
     int D = 0;
-    unsigned char* dtab = nullptr;
-    size_t dtab_cap = 0;
+    uint64_t* gthr = nullptr;      // geometric law: delay thresholds of (gthr_p, gthr_q)
+    double gthr_p = -1.0;
+    size_t gthr_q = 0;
     unsigned long long* flags = nullptr;  // [0] first failing draw, [1] non-finite
 };
 
@@ -99,7 +100,7 @@ struct EdgeArgs {
     double* out;
     const int* offL;
     const int* offR;
-    const unsigned char* dtab;  // geometric delays of this step, by draw rank
+    const uint64_t* gthr;       // geometric law: the q-1 delay thresholds
     unsigned long long* fail;   // lowest failing draw rank
     long long N, n, P;
     double r, c;
@@ -117,7 +118,7 @@ __device__ __forceinline__ double stale_read(const EdgeArgs& a, long long j, int
     } else if (a.law == HEAT_DELAY_FIXED) {
         d = a.fixed_d < a.bound ? a.fixed_d : a.bound;
     } else {
-        d = a.dtab[off];
+        d = geometric_delay(splitmix_draw(a.state, uint64_t(off)), a.gthr, int(a.bound));
     }
     if (d >= a.count) {
         atomicMin(a.fail, (unsigned long long)off);
@@ -167,7 +168,7 @@ void history_free(heat_history* h) {
     if (h->base) cudaFree(h->base);
     if (h->tab) cudaFree(h->tab);
     if (h->offs) cudaFree(h->offs);
-    if (h->dtab) cudaFree(h->dtab);
+    if (h->gthr) cudaFree(h->gthr);
     if (h->flags) cudaFree(h->flags);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -334,28 +335,19 @@ int heat_async_step(heat_history* h, double r, int bc_kind, double c1, double c2
     const size_t k = h->step;
     const long long bound = (long long)std::min(q - 1, k);
 
-    // host-drawn geometric delays (glibc log1p, sample_delay async_sim.cpp:64-69)
-    std::vector<unsigned char> dt;
-    if (law == HEAT_DELAY_GEOMETRIC && D > 0) {
-        dt.resize(size_t(D));
-        const double lp = std::log1p(-geometric_p);
-        for (int o = 0; o < D; ++o) {
-            const uint64_t x = splitmix_draw(*rng_state, uint64_t(o));
-            const double u = double(x >> 11) * 0x1.0p-53;
-            double g = std::floor(std::log1p(-u) / lp);
-            if (!std::isfinite(g) || g < 0.0) g = 0.0;
-            const size_t dd = std::min(size_t(g), size_t(bound));
-            dt[o] = (unsigned char)std::min<size_t>(dd, 255);  // >= 255 fails the depth check anyway
-        }
-        if (h->count > 255) return fail(HEAT_EINVAL, "async_step: geometric law needs depth <= 255");
-        if (h->dtab_cap < dt.size()) {
-            if (h->dtab) cudaFree(h->dtab);
-            h->dtab = nullptr;
-            h->dtab_cap = 0;
-            HB_CUDA(cudaMalloc(&h->dtab, dt.size()));
-            h->dtab_cap = dt.size();
-        }
-        HB_CUDA(cudaMemcpyAsync(h->dtab, dt.data(), dt.size(), cudaMemcpyHostToDevice, st));
+    // geometric law: exact device delays from the thresholds (geometric_thresholds)
+    if (law == HEAT_DELAY_GEOMETRIC && (h->gthr_p != geometric_p || h->gthr_q != q)) {
+        std::vector<uint64_t> gthr;
+        HB_TRY(geometric_thresholds(geometric_p, q, gthr));
+        if (h->gthr) cudaFree(h->gthr);
+        h->gthr = nullptr;
+        h->gthr_q = 0;
+        HB_CUDA(cudaMalloc(&h->gthr, std::max<size_t>(1, gthr.size()) * sizeof(uint64_t)));
+        if (!gthr.empty())
+            HB_CUDA(cudaMemcpy(h->gthr, gthr.data(), gthr.size() * sizeof(uint64_t),
+                               cudaMemcpyHostToDevice));
+        h->gthr_p = geometric_p;
+        h->gthr_q = q;
     }
 
     std::vector<const double*> tab(h->depth, nullptr);
@@ -380,7 +372,7 @@ int heat_async_step(heat_history* h, double r, int bc_kind, double c1, double c2
         a.out = nxt;
         a.offL = h->offs;
         a.offR = h->offs + P;
-        a.dtab = h->dtab;
+        a.gthr = h->gthr;
         a.fail = h->flags;
         a.N = (long long)N;
         a.n = (long long)per_pe;

@@ -117,6 +117,57 @@ int check_field(const double* u, size_t n) {
     return HEAT_OK;
 }
 
+namespace {
+// The reference's unclamped geometric delay of a draw with top bits m.
+double geometric_quotient(uint64_t m, double lp) {
+    return std::log1p(-(double(m) * 0x1.0p-53)) / lp;
+}
+size_t geometric_raw(uint64_t m, double lp) {
+    double g = std::floor(geometric_quotient(m, lp));
+    if (!std::isfinite(g) || g < 0.0) g = 0.0;
+    return size_t(g);
+}
+}  // namespace
+
+int geometric_thresholds(double p, size_t q, std::vector<uint64_t>& T) {
+    static std::mutex mu;
+    static std::map<std::pair<uint64_t, size_t>, std::vector<uint64_t>> cache;
+    uint64_t pbits;
+    std::memcpy(&pbits, &p, 8);
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_pair(pbits, q);
+    if (auto it = cache.find(key); it != cache.end()) {
+        T = it->second;
+        return HEAT_OK;
+    }
+    constexpr uint64_t kTop = uint64_t(1) << 53;  // m ranges over [0, 2^53)
+    const double lp = std::log1p(-p);
+    const double qmax = geometric_quotient(kTop - 1, lp);
+    if (!std::isfinite(qmax) || qmax >= 0x1.0p62)
+        return fail(HEAT_EINVAL, "geometric law: p too small for the device delay thresholds");
+    T.assign(q > 0 ? q - 1 : 0, kTop);
+    const double slope = std::max(1.0, std::ceil(std::fabs(lp)));
+    for (size_t j = 1; j < q; ++j) {
+        if (geometric_raw(kTop - 1, lp) < j) break;  // T[j-1..] stay 2^53: never reached
+        uint64_t lo = 0, hi = kTop - 1;               // smallest m with raw(m) >= j
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (geometric_raw(mid, lp) >= j) hi = mid;
+            else lo = mid + 1;
+        }
+        T[j - 1] = lo;
+        // rounding can move the crossing by a few ulps of the quotient (~j ulps of
+        // m per unit slope): check every m within a window far wider than that
+        const uint64_t W = std::min<uint64_t>(uint64_t(64.0 * double(j) * slope) + 4096, 1u << 22);
+        const uint64_t a = lo > W ? lo - W : 0, b = std::min(kTop, lo + W);
+        for (uint64_t m = a; m < b; ++m)
+            if ((geometric_raw(m, lp) >= j) != (m >= lo))
+                return fail(HEAT_EINVAL, "geometric law: delay not monotone near a threshold");
+    }
+    cache.emplace(key, T);
+    return HEAT_OK;
+}
+
 int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
                     std::vector<double>& out) {
     out.assign(u0, u0 + n);
@@ -161,6 +212,16 @@ int heat_prepare_initial(const double* u0, size_t n, int bc_kind, double c1, dou
     std::vector<double> v;
     HB_TRY(prepare_initial(u0, n, bc_kind, c1, c2, v));
     std::memcpy(out, v.data(), n * sizeof(double));
+    return HEAT_OK;
+}
+
+int heat_geometric_thresholds(double p, size_t q, uint64_t* thresholds) {
+    if (!thresholds) return fail(HEAT_EINVAL, "null output");
+    if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
+    if (!(p > 0.0) || p > 1.0) return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
+    std::vector<uint64_t> T;
+    HB_TRY(geometric_thresholds(p, q, T));
+    std::copy(T.begin(), T.end(), thresholds);
     return HEAT_OK;
 }
 

@@ -103,6 +103,19 @@ int kernel_smem_config(const void* fn, int smem, int threads, int* per_sm);
 
 // Validation helpers mirroring the reference's constructors.
 int check_field(const double* u, size_t n);  // BasicField ctor, core.hpp:45-51
+
+// The geometric law (sample_delay, async_sim.cpp:64-69) as thresholds on a
+// draw's top 53 bits m = x >> 11: d = #{j : m >= T[j-1]}, j = 1..q-1, then
+// min(d, bound).  Exact because the reference's floor(log1p(-u)/log1p(-p))
+// is non-decreasing in m away from each integer crossing, and every m in a
+// window around each threshold -- wider than log1p's rounding error can move
+// a crossing -- is checked with glibc's log1p itself.  HEAT_EINVAL when p is
+// so small that the quotient leaves size_t's range (the reference's
+// conversion is undefined there); cached per (p, q).
+int geometric_thresholds(double p, size_t q, std::vector<uint64_t>& T);
+
+// An AsyncSimulator handle's current field (device) and stream (async_host.cu).
+void async_sim_device_field(heat_async_sim* sim, const double** field, cudaStream_t* st);
 int prepare_initial(const double* u0, size_t n, int bc_kind, double c1, double c2,
                     std::vector<double>& out);  // sync_solver.cpp:25-37
 

@@ -227,7 +227,7 @@ int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, 
     L.o_counter = take(8);
     L.o_offL = take(L.P * 4);
     L.o_offR = take(L.P * 4);
-    L.o_dtab = take(s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC ? s.k_end * size_t(L.D) : 1);
+    L.o_gthr = take(std::max<size_t>(1, s.q - 1) * sizeof(uint64_t));
     L.o_stats = take(kStatWords * 8);
     L.o_abort = take(4);
     L.o_links = take(L.P * sizeof(PeLink));
@@ -290,26 +290,17 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
         HB_CUDA(cudaMemcpyAsync(base + L.o_offR, offR.data(), L.P * 4, cudaMemcpyHostToDevice, st));
         HB_CUDA(cudaMemcpyAsync(base + L.o_stats, stats0.data(), kStatWords * 8,
                                 cudaMemcpyHostToDevice, st));
-        if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {
-            std::vector<unsigned char> dtab(s.k_end * size_t(L.D));
-            const double lp = std::log1p(-s.geometric_p);
-            for (size_t k = 0; k < s.k_end; ++k) {
-                const size_t bound = std::min<size_t>(s.q - 1, k);
-                for (int o = 0; o < L.D; ++o) {
-                    const uint64_t x = splitmix_draw(s.seed, uint64_t(k) * L.D + o);
-                    const double u = double(x >> 11) * 0x1.0p-53;
-                    double g = std::floor(std::log1p(-u) / lp);
-                    if (!std::isfinite(g) || g < 0.0) g = 0.0;
-                    dtab[k * L.D + o] = (unsigned char)std::min<size_t>(size_t(g), bound);
-                }
-            }
-            HB_CUDA(cudaMemcpyAsync(base + L.o_dtab, dtab.data(), dtab.size(),
-                                    cudaMemcpyHostToDevice, st));
-        }
         HB_TRY(launch_seed(st, bufs[cur], seeds, at<SeedOp>(base, L.o_seeds),
                            2 * L.P + 2 * size_t(L.G)));
     }
     if (steps == 0) return HEAT_OK;
+    if (s.mode == 0 && s.law == HEAT_DELAY_GEOMETRIC) {  // exact device delays of the law
+        std::vector<uint64_t> gthr;
+        HB_TRY(geometric_thresholds(s.geometric_p, s.q, gthr));
+        if (!gthr.empty())
+            HB_CUDA(cudaMemcpyAsync(base + L.o_gthr, gthr.data(), gthr.size() * sizeof(uint64_t),
+                                    cudaMemcpyHostToDevice, st));
+    }
     HB_CUDA(cudaMemsetAsync(base + L.o_done, 0, L.P * L.Tp * 4, st));
     HB_CUDA(cudaMemsetAsync(base + L.o_counter, 0, 8, st));
     HB_CUDA(cudaMemsetAsync(base + L.o_abort, 0, 4, st));
@@ -340,8 +331,7 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.D = L.D;
     a.off_left = at<const int>(base, L.o_offL);
     a.off_right = at<const int>(base, L.o_offR);
-    a.dtable = ext.dtab ? ext.dtab : at<const unsigned char>(base, L.o_dtab);
-    a.dtab_k0 = ext.dtab ? ext.dtab_k0 : 0;
+    a.gthr = at<const uint64_t>(base, L.o_gthr);
     a.links = at<const PeLink>(base, L.o_links);
     a.pin_first_pe = pin_first;
     a.pin_last_pe = pin_last;

@@ -23,10 +23,6 @@ struct StreamExternal {
     unsigned long long* right_push_prog = nullptr;
     long long pe_offset = 0;  // global index of local PE 0
     long long P_global = 0;   // 0 = this launch holds the whole domain
-    // GEOMETRIC law, stepping a run in slices (heat_async_sim_*): a device
-    // table of the delays of steps [dtab_k0, ...) replacing the layout's own
-    const unsigned char* dtab = nullptr;
-    long long dtab_k0 = 0;
 };
 
 // Device scratch of one streaming run (rings persist across its launches).
@@ -37,7 +33,7 @@ struct StreamLayout {
     int V = 32; // points per lane of the stream kernel for this layout (48 or 32)
     int H = 32; // halo points per side = steps per pass (64 or 32)
     size_t o_ringL, o_ringR, o_progL, o_progR, o_recvL, o_recvR, o_rprogL, o_rprogR, o_done,
-        o_counter, o_offL, o_offR, o_dtab, o_stats, o_abort, o_links, o_seeds, bytes;
+        o_counter, o_offL, o_offR, o_gthr, o_stats, o_abort, o_links, o_seeds, bytes;
 };
 
 int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, StreamLayout& L,

@@ -123,8 +123,8 @@ int heat_plan_xlink_advance(heat_plan* p, double r, double c1, double c2, int mo
     if (!p || !p->xlink) return fail(HEAT_EINVAL, "xlink not set up");
     heat_xlink* x = static_cast<heat_xlink*>(p->xlink);
     if (mode != 0 && mode != 1) return fail(HEAT_EINVAL, "xlink: mode is 0 (replay) or 1 (free)");
-    if (law == HEAT_DELAY_GEOMETRIC)
-        return fail(HEAT_EINVAL, "xlink: the geometric law needs a host delay table (single GPU only)");
+    if (law == HEAT_DELAY_GEOMETRIC && (!(geometric_p > 0.0) || geometric_p > 1.0))
+        return fail(HEAT_EDOMAIN, "DelayModel: geometric p must lie in (0, 1]");
     if (law == HEAT_DELAY_FIXED && fixed_delay >= x->q)
         return fail(HEAT_EDOMAIN, "DelayModel: fixed delay must satisfy d < q");
     HB_CUDA(cudaSetDevice(p->device));

@@ -585,7 +585,8 @@ class EnsembleResult:
 
 def ensemble_run(cfg: EnsembleConfig, runs: int, base_seed: int,
                  keep_terminals: bool = True) -> EnsembleResult:
-    """analysis.cpp:51-104 on the GPU: one CTA per member (K6, csrc/ensemble.cu)."""
+    """analysis.cpp:51-104 on the GPU: one CTA per member (K6, csrc/ensemble.cu), or
+    AsyncSimulator handles (K3/K5) when a member's history exceeds shared memory."""
     v = _field(cfg.u0)
     n = v.size
     if cfg.part.total() != n:
@@ -601,7 +602,7 @@ def ensemble_run(cfg: EnsembleConfig, runs: int, base_seed: int,
     m = cfg.model
     _lib.check(_lib.lib().heat_ensemble_run(
         _lib.dptr(v), n, cfg.params.r(), cfg.bc.kind, cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(),
-        m.q, int(m.distribution), m.fixed_delay, cfg.k_end, stride, runs,
+        m.q, int(m.distribution), m.fixed_delay, m.geometric_p, cfg.k_end, stride, runs,
         base_seed & 0xFFFFFFFFFFFFFFFF, _lib.szptr(steps), cap, C.byref(ns), _lib.dptr(norms),
         _lib.dptr(terms), _lib.dptr(mean), _lib.dptr(std)), "ensemble_run")
     S = ns.value

@@ -318,3 +318,16 @@ def test_measure_and_speedup_ratio(gpu):
         assert med[10000] >= med[100]
     with pytest.raises(H.InvalidArgument):
         H.speedup_ratio(rows, 64)
+
+
+@pytest.mark.parametrize("N,n", [(1024, 128), (3 * 4096, 4096)])
+def test_geometric_large_q_device_thresholds(gpu, port, N, n):
+    """The geometric law with q = 300 (beyond a byte-table's range): K3 / K5
+    draw from the exact device thresholds and replay the reference's stream."""
+    from paper_1510_08982_b200 import heat as H
+    u0 = random_field(SplitMix64(N + 300), N)
+    bc = H.BoundaryCondition.dirichlet(float(u0[0]), float(u0[-1]))
+    got = H.async_final(u0, H.SolverParams.from_r(0.3), bc, H.PartitionSpec(N, n),
+                        H.DelayModel.geometric(300, 0.02, 5), 500)
+    want = port.async_run(u0, 0.3, 0, u0[0], u0[-1], n, 2, 300, 0, 0.02, 5, k_end=500)
+    assert bits_equal(got, want)

@@ -98,3 +98,65 @@ def test_k3_geometry_invariants(mode):
                     assert warps <= 16
     assert k3(128, 8, 2, 0)[:3] == (16, 8, 4)  # cfg2: two 16-lane PEs per warp, 4 warps
     assert k3(128, 8, 2, 1)[:3] == (32, 4, 8)  # free-running: one PE per warp
+
+
+# ---- geometric-law thresholds (runtime.cu geometric_thresholds) -------------
+GAMMA = 0x9E3779B97F4A7C15
+M64 = (1 << 64) - 1
+
+
+def _mix(z):
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def _unxorshift(y, s):
+    x = y
+    for _ in range(64 // s + 1):
+        x = y ^ (x >> s)
+    return x
+
+
+def _unmix(x):
+    z = _unxorshift(x, 31)
+    z = _unxorshift((z * pow(0x94D049BB133111EB, -1, 1 << 64)) & M64, 27)
+    return _unxorshift((z * pow(0xBF58476D1CE4E5B9, -1, 1 << 64)) & M64, 30)
+
+
+def thresholds(p, q):
+    out = (ctypes.c_uint64 * max(1, q - 1))()
+    assert _lib.lib().heat_geometric_thresholds(p, q, out) == 0
+    return [out[i] for i in range(q - 1)]
+
+
+def rule(x, T, bound):
+    m, d = x >> 11, 0
+    while d < bound and m >= T[d]:
+        d += 1
+    return d
+
+
+@pytest.mark.parametrize("p", [0.6, 0.3, 0.05, 0.999, 1e-6, 1.0])
+@pytest.mark.parametrize("q", [2, 5, 40])
+def test_geometric_thresholds_match_reference_draws(port, p, q):
+    """The device rule d = #{T_j <= x >> 11} (capped at the bound) equals the
+    reference's floor(log1p(-u)/log1p(-p)) (async_sim.cpp:64-69, through the
+    oracle) on random draws and on draws crafted to sit at every threshold
+    and one step either side of it."""
+    T = thresholds(p, q)
+    assert all(a <= b for a, b in zip(T, T[1:]))
+    seed = 12345
+    got = [rule(_mix((seed + (j + 1) * GAMMA) & M64), T, q - 1) for j in range(3000)]
+    assert got == port.delay_stream(2, q, 0, p, seed, 10 ** 6, 3000)
+    for t in T:
+        if t >= 1 << 53:
+            continue
+        for m in (t - 1, t, t + 1):
+            if not 0 <= m < 1 << 53:
+                continue
+            for low in (0, 0x7FF):
+                x = (m << 11) | low
+                s = (_unmix(x) - GAMMA) & M64  # the stream whose first draw is x
+                for k in (10 ** 6, 1):
+                    assert rule(x, T, min(q - 1, k)) == port.delay_stream(2, q, 0, p, s, k, 1)[0]
