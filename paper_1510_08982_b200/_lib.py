@@ -13,7 +13,10 @@ import threading
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libheat_b200.so")
+# HEAT_LIB_SUFFIX=x loads libheat_b200_x.so from the package (A/B builds only)
+LIB_PATH = os.path.join(
+    PKG, "libheat_b200" + ("_" + os.environ["HEAT_LIB_SUFFIX"] if os.environ.get("HEAT_LIB_SUFFIX") else "")
+    + ".so")
 
 HEAT_OK = 0
 HEAT_EDOMAIN = 1

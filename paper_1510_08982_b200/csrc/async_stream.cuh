@@ -87,7 +87,14 @@ struct AsyncStreamArgs {
     unsigned int* flag;
     unsigned int* abort_word;
     unsigned long long timeout_ns;
+    int pend_max;   // done-signals published per release fence (1..kMaxPend)
+    int pref_step;  // interior tiles: step at which the next window is issued (< 0: half-way)
 };
+constexpr int kMaxPend = 16;
+#ifndef HEAT_K5_UNROLL
+#define HEAT_K5_UNROLL 2
+#endif
+constexpr int kK5Unroll = HEAT_K5_UNROLL;  // interior step loop unroll (4: -2.4% here, though K1 gains 0.45% from it)
 
 __device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
@@ -297,8 +304,9 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
     // Done-signals are deferred and published in pairs: one release fence
     // (fence.acq_rel.gpu, the costly part of a release store -- ncu: ERRBAR +
     // MEMBAR were the largest non-FP64 stalls) then relaxed stores for both.
-    long long pend_tile[2] = {-1, -1};
-    unsigned int pend_pass[2] = {0, 0};
+    // Pending (tile, pass) pairs live in shared memory; only lane 0 uses them.
+    __shared__ uint2 s_pend[T::kWarpsPerCta][kMaxPend];
+    uint2* wpend = s_pend[warp];
     int npend = 0;
     bool pend_generic = false;  // a pending tile left through per-lane stores
     // Publish done[] of the pending tiles once their stores have landed.
@@ -315,7 +323,7 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
                 bulk_wait_all();
             asm volatile("fence.proxy.async.global;" ::: "memory");
             fence_acq_rel_gpu();
-            for (int j = 0; j < npend; ++j) st_relaxed_gpu_u32(a.done + pend_tile[j], pend_pass[j]);
+            for (int j = 0; j < npend; ++j) st_relaxed_gpu_u32(a.done + wpend[j].x, wpend[j].y);
         }
         __syncwarp();
         npend = 0;
@@ -392,10 +400,10 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         const int lpos = int(out_hi - 1 - w0);
         const int ll = lpos / V, le = lpos % V;
         if (!left_edge && !right_edge) {
-            const int half = nst / 2;
-            warp_steps_pipelined<double, V>(u, r, c, half);
+            const int half = a.pref_step < 0 ? nst / 2 : min(nst, a.pref_step);
+            warp_steps_pipelined<double, V, kK5Unroll>(u, r, c, half);
             try_prefetch();
-            warp_steps_pipelined<double, V>(u, r, c, nst - half);
+            warp_steps_pipelined<double, V, kK5Unroll>(u, r, c, nst - half);
         } else {
             try_prefetch();
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
@@ -531,9 +539,8 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         // phase to land: wait until at most this item's store group is in
         // flight), and keep this one pending.  Blocking waits flush first.
         const bool cur_bulk = tma_ok(w0) && full;  // this item's store is the newest group
-        if (npend == 2) signal_pending(cur_bulk ? 1 : 0);
-        pend_tile[npend] = (long long)it.p * a.Tp + it.m;
-        pend_pass[npend] = unsigned(it.pass + 1);
+        if (npend >= a.pend_max) signal_pending(cur_bulk ? 1 : 0);
+        if (lane == 0) wpend[npend] = make_uint2(unsigned(it.p * a.Tp + it.m), unsigned(it.pass + 1));
         ++npend;
         pend_generic |= !cur_bulk;
         cur = nxt;
