@@ -65,13 +65,15 @@ struct SyncVariant {
     int smem;                 // dynamic shared memory per CTA
     int halo;                 // halo points per side = max steps per pass
     bool dyn;                 // tiles dealt by an atomic counter
+    int warps;                // warps (tiles in flight) per CTA
     int blocks_per_sm;        // filled by the occupancy query
 };
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false>
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false,
+          int W = 4>
 SyncVariant variant() {
-    using T = SyncTB<Real, V, H>;
-    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H, DYN>, NBUF, V, T::kOut, T::kWinUnits,
-            T::kOutUnits, T::smem_bytes(NBUF), H, DYN, 0};
+    using T = SyncTB<Real, V, H, W>;
+    return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H, DYN, W>, NBUF, V, T::kOut, T::kWinUnits,
+            T::kOutUnits, T::smem_bytes(NBUF), H, DYN, W, 0};
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows);
 // f32 takes 64-point lanes (256 B, two rows) with the same halo, buffers and deal
@@ -90,7 +92,7 @@ SyncVariant variant48() {
 // twice, same box); unrolled x1 (14) loses 1.7%.
 constexpr int kDefaultSyncVariant = 15;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 16;
+constexpr int kSyncVariants = 18;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -116,6 +118,11 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant48<Real, 2, true, 64, true>(),  // 13: as 11, tiles dealt by an atomic counter
         variant48<Real, 2, true, 64, true, -1>(),  // 14: as 13, step loop not unrolled
         variant48<Real, 2, true, 64, true, -4>(),  // 15: as 13, step loop unrolled 4
+        // 16: 64-point lanes (f64), 64-point halo, 2 buffers, atomic deal, unrolled 4,
+        //     3 warps per CTA (2 x 3 x 32 KB of buffers per SM): 93.75% exact points
+        variant<Real, 64, 2, -4, true, 64, true, (sizeof(Real) == 8 ? 3 : 4)>(),
+        // 17: as 16, step loop unrolled 2
+        variant<Real, 64, 2, 0, true, 64, true, (sizeof(Real) == 8 ? 3 : 4)>(),
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
@@ -135,7 +142,7 @@ int sync_variant(SyncVariant** out, int max_halo = 0) {
     SyncVariant& v = sync_variant_entry<Real>(max_halo);
     // per device (the current one): shared memory limit + occupancy
     HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(v.fn), v.smem,
-                              SyncTB<Real, kV>::kThreads, &v.blocks_per_sm));
+                              v.warps * kWarp, &v.blocks_per_sm));
     *out = &v;
     return HEAT_OK;
 }
@@ -205,7 +212,7 @@ struct SyncLauncher {
         if (out_hi <= out_lo) return HEAT_OK;
         if (nsteps > var->halo) return fail(HEAT_ELOGIC, "sync pass: more steps than the halo");
         const long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
-        const long long want = (tiles + T::kWarpsPerCta - 1) / T::kWarpsPerCta;
+        const long long want = (tiles + var->warps - 1) / var->warps;
         const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
         SyncPassArgs p = a;
         p.out_lo = out_lo;
@@ -219,7 +226,7 @@ struct SyncLauncher {
             p.counter = tile_counter_of(a.nonfinite) + counter_slot;
             HB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
         }
-        var->fn<<<grid, T::kThreads, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
+        var->fn<<<grid, var->warps * kWarp, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
@@ -417,7 +424,7 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // and the last download is short, while neighbouring chunks differ by
     // less than the compute/copy time ratio (~1.8), so neither the compute
     // nor the download stream starves.  Smaller fields: 16 equal chunks.
-    const long long wave = (long long)d.sms * L.var->blocks_per_sm * T::kWarpsPerCta * L.var->out;
+    const long long wave = (long long)d.sms * L.var->blocks_per_sm * L.var->warps * L.var->out;
     const std::vector<long long> B = stream_chunk_plan(N, wave);
     const int C = int(B.size()) - 1;
     for (int c = 0; c < C; ++c)

@@ -40,7 +40,7 @@
 
 namespace hb {
 
-template <typename Real, int V, int H = 32>
+template <typename Real, int V, int H = 32, int W = 4>
 struct SyncTB {
     static constexpr int kChunkBytes = V * int(sizeof(Real));
     static constexpr int kRowsPerChunk = kChunkBytes / 128;       // 128-B swizzle rows
@@ -59,7 +59,7 @@ struct SyncTB {
     static constexpr int kOutUnits = kWinUnits - 2 * kHalo / kUnit;
     static constexpr int kOut = kWarp * V - 2 * kHalo;            // exact points per tile
     static constexpr int kHaloRows = kHalo * int(sizeof(Real)) / 128;
-    static constexpr int kWarpsPerCta = 4;
+    static constexpr int kWarpsPerCta = W;  // 3 for 64-point f64 lanes: 2 CTAs x 3 x 2 x 16 KB fit an SM
     static constexpr int kThreads = kWarpsPerCta * kWarp;
     // shared memory for NBUF window buffers per warp (+ mbarriers, + 1 KB alignment slack)
     static constexpr int smem_bytes(int nbuf) {
@@ -305,11 +305,12 @@ struct SyncPassArgs {
 //         (NBUF = 2 only); false: 16-B vector stores straight from registers.
 // DYN:    tiles handed out by an atomic counter (grabbed as soon as the
 //         current window is read) instead of a static round-robin deal.
-template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false>
-__global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, SyncTB<Real, V, H>::min_blocks(NBUF))
+template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false,
+          int W = 4>
+__global__ void __launch_bounds__(SyncTB<Real, V, H, W>::kThreads, SyncTB<Real, V, H, W>::min_blocks(NBUF))
     sync_tb_kernel(const __grid_constant__ CUtensorMap tm_src,
                    const __grid_constant__ CUtensorMap tm_dst, const SyncPassArgs a) {
-    using T = SyncTB<Real, V, H>;
+    using T = SyncTB<Real, V, H, W>;
     static_assert(NBUF == 1 || NBUF == 2, "one or two window buffers per warp");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 128B swizzle needs 1024-B aligned buffers

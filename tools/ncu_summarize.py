@@ -1,6 +1,6 @@
 """Summarise an ncu report / launch list into profiles/ (run here, no GPU needed).
 
-    python tools/ncu_summarize.py full   <report.ncu-rep> <kernel-key> <out.json>
+    python tools/ncu_summarize.py full   <report.ncu-rep> <kernel-key> <out.json> [<name regex>]
     python tools/ncu_summarize.py launches <launches.csv> <out.json>
 
 `full` extracts the metrics the roofline uses (DRAM bytes, duration, FP64 pipe,
@@ -38,8 +38,9 @@ def to_bytes(v, unit):
     return float(v) * scale.get(unit, 1)
 
 
-def full(rep, key, out):
-    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+def full(rep, key, out, kfilter=None):
+    sel = ["-k", "regex:" + kfilter] if kfilter else []
+    rows = list(csv.reader(io.StringIO(ncu("-i", rep, *sel, "--page", "raw", "--csv"))))
     h, units = rows[0], rows[1]
     launches = []
     for vals in rows[2:]:
@@ -58,7 +59,7 @@ def full(rep, key, out):
         d["kernel"] = vals[h.index("Kernel Name")] if "Kernel Name" in h else ""
         launches.append(d)
     # SASS opcode mix from the source page
-    src = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv",
+    src = list(csv.reader(io.StringIO(ncu("-i", rep, *sel, "--page", "source", "--csv",
                                           "--print-source", "sass"))))
     mix = Counter()
     if len(src) > 2:
@@ -69,6 +70,8 @@ def full(rep, key, out):
                 continue
             toks = r[iS].split()
             op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+            if not (r[iE] or "0").isdigit():
+                continue  # a repeated header
             mix[op.split(".")[0]] += int(r[iE] or 0)
     tot = sum(mix.values()) or 1
     L = launches[0]
@@ -106,6 +109,6 @@ def launches(path, out):
 
 if __name__ == "__main__":
     if sys.argv[1] == "full":
-        full(sys.argv[2], sys.argv[3], sys.argv[4])
+        full(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5] if len(sys.argv) > 5 else None)
     else:
         launches(sys.argv[2], sys.argv[3])
