@@ -415,6 +415,10 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
                    double* snapshots, size_t* steps_out, size_t max_snapshots,
                    size_t* n_snapshots) {
     if (stride == 0) stride = default_stride(N);
+    if (async_small_eligible(N, per_pe, q))  // K9: one CTA, temporal-blocked rounds
+        return async_run_small(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
+                               geometric_p, seed, k_end, stride, final_out, snapshots, steps_out,
+                               max_snapshots, n_snapshots);
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));

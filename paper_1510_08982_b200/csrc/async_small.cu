@@ -1,0 +1,466 @@
+// async_small.cu -- K9: deterministic asynchronous runs of small fields (the
+// paper's regime: cfg2 is N = 1024, 8 PEs, q = 2) in ONE CTA, temporal-blocked
+// like K7 (sync_small.cu).
+//
+// Replaces async_run (async_sim.cpp:118-160) -- Eq. (4): a PE's first/last
+// point reads its cross-PE neighbour at step k - d, d drawn from the run's
+// SplitMix64 stream in the reference's order (async_sim.cpp:86-101) -- for
+// N <= 2048 with PEs of a multiple of 8 points and q <= 8.
+//
+// Why temporal blocking still works with delays: a point at step k+1 depends
+// on its two neighbours at steps k - d (d <= q-1 <= k), i.e. still on points
+// one position away, so after s steps the exact region of a window has still
+// shrunk by at most s points per side.  What a window needs beyond K7 is the
+// delayed values themselves:
+//   * Warp w owns the chunk [128w, 128w+128) and steps a 256-point window
+//     (64-point halo each side, 8 points per lane) up to 64 steps per round.
+//     PE boundaries fall on lane boundaries (n is a multiple of 8 and windows
+//     start on multiples of 8), so every cross-PE read crosses a shuffle.
+//   * The SENDING lane applies the delay: the lane whose last point is a PE's
+//     last point sends r*u(k - d) up instead of r*u(k), d being the delay the
+//     receiving PE-first point draws for its left read (offL); the lane whose
+//     first point is a PE's first point sends r*u(k - d) down with the delay of
+//     the neighbour PE's right read (offR).  Each lane keeps the products of
+//     its two end points for the last QH-1 steps in registers.
+//   * Draw j of step k is mix(seed + (k*D + off + 1)*gamma): the counter
+//     advances by D*gamma per step, no multiply.  Every lane that holds a
+//     boundary (as exact point or as halo) draws the same delay.
+//   * Histories cross rounds through a shared table [P][first|last][QH] of
+//     products at steps k1, k1-1, ..., written by the exact owners at the end
+//     of a round and read by every window holding the point at the next start.
+// Bit-identical to async_run: the same stencil_p arithmetic, the same draws,
+// the same delayed operands (tests/test_gpu_async.py).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "runtime.cuh"
+#include "sync_tb.cuh"
+
+namespace hb {
+namespace {
+
+constexpr int kAsV = 8;                       // points per lane
+constexpr int kAsHalo = 64;                   // steps per round = halo points per side
+constexpr int kAsChunk = 32 * kAsV - 2 * kAsHalo;  // 128 exact points per warp
+constexpr int kAsMaxN = 2048;                 // 16 warps (128 registers per thread)
+constexpr int kAsMaxQ = 8;
+constexpr int kAsSub = 16;  // steps per delay word (16 nibbles)
+
+struct AsyncSmallArgs {
+    double* field;  // [N]: raw initial field in, final field out
+    int N, n, P;
+    double r, c, c1, c2;
+    int dirichlet;
+    long long k_end;
+    long long stride;  // 0: no trajectory
+    double* snaps;     // [rows][N]
+    unsigned int* flag;
+    int law, fixed_d, q;
+    unsigned long long seed;
+    ModQ modq;
+    long long D;
+    const int* offL;  // [P] draw rank of PE p's first-point left read, -1 none
+    const int* offR;  // [P] ... last-point right read
+    const uint64_t* gthr;  // geometric thresholds (q-1)
+};
+
+template <int LAW>
+__device__ __forceinline__ int small_delay(const AsyncSmallArgs& a, uint64_t z, int bound,
+                                           const uint64_t* gthr) {
+    if (LAW == 1) return a.fixed_d < bound ? a.fixed_d : bound;
+    if (bound == 0) return 0;
+    const uint64_t x = splitmix_mix(z);
+    if (LAW == 0) return uniform_delay(x, bound, a.modq);
+    return geometric_delay(x, gthr, bound);
+}
+
+// 16 delay bytes (each < 16) -> one word of 16 nibbles, step j at bits 4j
+__device__ __forceinline__ uint64_t pack_nibbles(const unsigned char* p) {
+    const uint4 v = *reinterpret_cast<const uint4*>(p);
+    auto half = [](uint32_t x) -> uint64_t {  // 4 bytes -> 16 bits
+        x = (x | (x >> 4)) & 0x00ff00ffu;
+        return uint64_t((x | (x >> 8)) & 0xffffu);
+    };
+    return half(v.x) | (half(v.y) << 16) | (half(v.z) << 32) | (half(v.w) << 48);
+}
+
+// h[0] = product at step k (current), h[j] = product at step k - j
+template <int QH>
+__device__ __forceinline__ double pick(const double (&h)[QH], int d) {
+    double v = h[0];
+#pragma unroll
+    for (int j = 1; j < QH; ++j)
+        if (d == j) v = h[j];
+    return v;
+}
+
+template <int QH, int LAW>
+__global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArgs a) {
+    extern __shared__ double smem[];
+    __shared__ __align__(16) unsigned char sdel[kAsMaxN / kAsChunk][64 * kAsSub];  // per warp: [stream][step]
+    double* su = smem;                                  // [N]
+    double* tab = smem + ((a.N + 1) & ~1);              // [P][2][QH]
+    int* soffL = reinterpret_cast<int*>(tab + a.P * 2 * QH);
+    int* soffR = soffL + a.P;
+    uint64_t* sthr =  // [q-1] geometric thresholds, 8-B aligned after the offsets
+        reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(soffR + a.P) + 7) & ~uintptr_t(7));
+    constexpr int V = kAsV, H = kAsHalo, C = kAsChunk;
+    const int N = a.N, n = a.n, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    bool bad_in = false;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const double v = a.field[i];
+        bad_in |= !isfinite(v);
+        su[i] = v;
+    }
+    for (int i = threadIdx.x; i < a.P; i += blockDim.x) {
+        soffL[i] = a.offL[i];
+        soffR[i] = a.offR[i];
+    }
+    if (a.law == 2)
+        for (int i = threadIdx.x; i < a.q - 1; i += blockDim.x) sthr[i] = a.gthr[i];
+    // TemperatureField ctor (core.hpp:45-51) on the raw upload, then
+    // prepare_initial's snap of the ends (the host checked |u - c| <= 1e-9)
+    if (__syncthreads_or(bad_in)) {
+        if (threadIdx.x == 0) atomicOr(a.flag + 2, 1u);
+        return;
+    }
+    if (a.dirichlet && threadIdx.x == 0) {
+        su[0] = a.c1;
+        su[N - 1] = a.c2;
+    }
+    __syncthreads();
+    const double r = a.r, c = a.c;
+    // step-0 histories: every slot holds r*u(0) (slots beyond k are never read)
+    for (int i = threadIdx.x; i < a.P * 2 * QH; i += blockDim.x) {
+        const int p = i / (2 * QH), side = (i / QH) & 1;
+        tab[i] = __dmul_rn(r, su[side ? p * n + n - 1 : p * n]);
+    }
+    if (a.snaps)
+        for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[i] = su[i];
+    __syncthreads();
+
+    const long long w0 = (long long)w * C - H;  // window start (unwrapped)
+    const long long g0 = w0 + (long long)lane * V;
+    const bool active = (long long)w * C < N;  // warp-uniform
+    const bool pinned = a.dirichlet && active && (w0 <= 0 || w0 + 32LL * V > N - 1);
+    auto real = [&](long long g) { return !a.dirichlet || (g >= 0 && g < N); };
+    auto wrapg = [&](long long g) -> int {
+        long long x = g % N;
+        return int(x < 0 ? x + N : x);
+    };
+    // Up: my last point sends to the next lane's first point (its left read).
+    const long long gu = g0 + V;
+    const int guw = wrapg(gu);
+    const int peU = guw / n;
+    const bool isU = real(gu) && guw % n == 0 && soffL[peU] >= 0;
+    const int offU = isU ? soffL[peU] : 0;
+    const int peL = wrapg(g0 + V - 1) / n;  // PE of my last point (its history row)
+    // Down: my first point sends to the previous lane's last point (its right read).
+    const long long gd = g0 - 1;
+    const int gdw = wrapg(gd);
+    const bool isD = real(gd) && (gdw + 1) % n == 0 && soffR[gdw / n] >= 0;
+    const int offD = isD ? soffR[gdw / n] : 0;
+    const int peF = wrapg(g0) / n;  // PE of my first point
+    // my end points that are PE edges (history rows), and as exact outputs
+    // (history writers)
+    const bool edgeF = real(g0) && wrapg(g0) % n == 0;
+    const bool edgeL = real(g0 + V - 1) && (wrapg(g0 + V - 1) + 1) % n == 0;
+    const int idx0 = lane * V, idx7 = lane * V + V - 1;
+    const bool ex0 = active && edgeF && idx0 >= H && idx0 < H + C && g0 < N;
+    const bool ex7 = active && edgeL && idx7 >= H && idx7 < H + C && g0 + V - 1 < N;
+
+    const uint64_t gamma = 0x9e3779b97f4a7c15ULL;
+    // this warp's delay streams: one per sending-up lane, then one per
+    // sending-down lane (fixed for the whole run)
+    const unsigned mU = __ballot_sync(0xffffffffu, active && isU);
+    const unsigned mD = __ballot_sync(0xffffffffu, active && isD);
+    const int cU = __popc(mU), nstreams = cU + __popc(mD);
+    const unsigned below = (1u << lane) - 1u;
+    const int sU = __popc(mU & below), sD = cU + __popc(mD & below);
+    long long k = 0;
+    long long next_rec = a.stride > 0 ? a.stride : a.k_end + 1;
+    double u[V];
+    double hF[QH], hL[QH];  // products of my first / last point, hX[j] at step k - j
+    while (k < a.k_end) {
+        long long s = min((long long)H, a.k_end - k);
+        s = min(s, next_rec - k);
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                const long long g = g0 + i;
+                u[i] = real(g) ? su[wrapg(g)] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < QH; ++j) {  // rows of PE edge points only
+                hF[j] = edgeF ? tab[(peF * 2 + 0) * QH + j] : 0.0;
+                hL[j] = edgeL ? tab[(peL * 2 + 1) * QH + j] : 0.0;
+            }
+            for (int t0 = 0; t0 < int(s); t0 += kAsSub) {
+                const int len = min(kAsSub, int(s) - t0);
+                const long long kb = k + t0;
+                // -- the delays of this sub-round, one lane per (stream, step):
+                // stream i < cU is the i-th sending-up lane, then the sending-down ones
+                for (int base = 0; base < nstreams * kAsSub; base += 32) {
+                    const int it = base + lane;
+                    const int si = min(it / kAsSub, nstreams - 1), j = it % kAsSub;
+                    // both shuffles on every lane (convergent), then the pick
+                    const int oU = __shfl_sync(0xffffffffu, offU, __fns(mU, 0, min(si, cU - 1) + 1));
+                    const int oD = __shfl_sync(0xffffffffu, offD,
+                                               __fns(mD, 0, max(si - cU, 0) + 1));
+                    const int off = si < cU ? oU : oD;
+                    const long long kk = kb + j;
+                    const int bound = kk < (long long)(a.q - 1) ? int(kk) : a.q - 1;
+                    const uint64_t z =
+                        a.seed + (uint64_t(kk) * uint64_t(a.D) + uint64_t(off) + 1) * gamma;
+                    if (it < nstreams * kAsSub)
+                        sdel[w][it] = (unsigned char)small_delay<LAW>(a, z, bound, sthr);
+                }
+                __syncwarp();
+                uint64_t wU = 0, wD = 0;
+                if (isU) wU = pack_nibbles(&sdel[w][sU * kAsSub]);
+                if (isD) wD = pack_nibbles(&sdel[w][sD * kAsSub]);
+                __syncwarp();
+                if (pinned) {
+                    for (int t = 0; t < len; ++t) {
+                        const double pF = __dmul_rn(r, u[0]);
+                        const double pLs = __dmul_rn(r, u[V - 1]);
+                        hF[0] = pF;
+                        hL[0] = pLs;
+                        const int dU = int(wU >> (4 * t)) & 15, dD = int(wD >> (4 * t)) & 15;
+                        const double pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, dU), 1);
+                        const double pR = __shfl_down_sync(0xffffffffu, pick<QH>(hF, dD), 1);
+                        chunk_step<double, V>(u, r, c, pL, pR, pF, pLs);
+                        pin_ends<double, V>(u, g0, 0, N - 1, a.c1, a.c2);
+#pragma unroll
+                        for (int j = QH - 1; j > 0; --j) {
+                            hF[j] = hF[j - 1];
+                            hL[j] = hL[j - 1];
+                        }
+                    }
+                } else {
+                    // software-pipelined as warp_steps_pipelined: the end points
+                    // first, then the next step's (delayed) shuffles, then the
+                    // interior points
+                    double pF = __dmul_rn(r, u[0]);
+                    double pLs = __dmul_rn(r, u[V - 1]);
+                    hF[0] = pF;
+                    hL[0] = pLs;
+                    double pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, int(wU & 15)), 1);
+                    double pR = __shfl_down_sync(0xffffffffu, pick<QH>(hF, int(wD & 15)), 1);
+                    for (int t = 0; t < len; ++t) {
+                        const double p1 = __dmul_rn(r, u[1]);
+                        const double pVm2 = __dmul_rn(r, u[V - 2]);
+                        const double nF = stencil_p(p1, __dmul_rn(c, u[0]), pL);
+                        const double nL = stencil_p(pR, __dmul_rn(c, u[V - 1]), pVm2);
+                        const double pF2 = __dmul_rn(r, nF);
+                        const double pLs2 = __dmul_rn(r, nL);
+#pragma unroll
+                        for (int j = QH - 1; j > 0; --j) {
+                            hF[j] = hF[j - 1];
+                            hL[j] = hL[j - 1];
+                        }
+                        hF[0] = pF2;
+                        hL[0] = pLs2;
+                        if (t + 1 < len) {
+                            const int dU = int(wU >> (4 * (t + 1))) & 15;
+                            const int dD = int(wD >> (4 * (t + 1))) & 15;
+                            pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, dU), 1);
+                            pR = __shfl_down_sync(0xffffffffu, pick<QH>(hF, dD), 1);
+                        }
+                        double pm1 = pF, p0 = p1;
+#pragma unroll
+                        for (int i = 1; i <= V - 2; ++i) {
+                            double pn;
+                            if (i + 1 == V - 1)
+                                pn = pLs;
+                            else if (i + 1 == V - 2)
+                                pn = pVm2;
+                            else
+                                pn = __dmul_rn(r, u[i + 1]);
+                            u[i] = stencil_p(pn, __dmul_rn(c, u[i]), pm1);
+                            pm1 = p0;
+                            p0 = pn;
+                        }
+                        u[0] = nF;
+                        u[V - 1] = nL;
+                        pF = pF2;
+                        pLs = pLs2;
+                    }
+                }
+            }
+            hF[0] = __dmul_rn(r, u[0]);
+            hL[0] = __dmul_rn(r, u[V - 1]);
+        }
+        __syncthreads();  // every window (and history row) has been read
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < V; ++i) {
+                const int idx = lane * V + i;
+                const long long g = g0 + i;
+                if (idx >= H && idx < H + C && g < N) su[g] = u[i];
+            }
+            // a PE edge point's products at steps k+s, k+s-1, ... (hF/hL were
+            // maintained for every lane, so the exact owner has them whether
+            // or not it also sends them)
+            if (ex0)
+#pragma unroll
+                for (int j = 0; j < QH; ++j) tab[(peF * 2 + 0) * QH + j] = hF[j];
+            if (ex7)
+#pragma unroll
+                for (int j = 0; j < QH; ++j) tab[(peL * 2 + 1) * QH + j] = hL[j];
+        }
+        __syncthreads();
+        k += s;
+        if (a.snaps && (k == next_rec || k == a.k_end)) {
+            const long long row = k % a.stride == 0 ? k / a.stride : k / a.stride + 1;
+            for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[row * N + i] = su[i];
+            if (k == next_rec) next_rec += a.stride;
+        }
+    }
+    bool bad = false;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        bad |= !isfinite(su[i]);
+        a.field[i] = su[i];
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flag, 1u);
+}
+
+int history_slots(size_t q) { return q <= 2 ? 2 : q <= 4 ? 4 : 8; }
+
+size_t small_smem_bytes(size_t N, size_t P, int QH, size_t q) {
+    return ((N + 1) & ~size_t(1)) * 8 + P * 2 * QH * 8 + 2 * P * 4 + 8 + q * 8;
+}
+
+}  // namespace
+
+bool async_small_eligible(size_t N, size_t per_pe, size_t q) {
+    if (std::getenv("HEAT_NO_SMALL_ASYNC")) return false;
+    return N <= (size_t)kAsMaxN && per_pe % kAsV == 0 && per_pe < N && q <= (size_t)kAsMaxQ;
+}
+
+// Whole deterministic async_run of a small field on one CTA (K9).  The caller
+// validated the arguments (heat_async_run); field validation, the end snap and
+// the trajectory rows (0, stride, ..., k_end -- async_sim.cpp:122-160) happen
+// in the kernel, with one host round trip.
+int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                    size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                    uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                    double* snapshots, size_t* steps_out, size_t max_snapshots,
+                    size_t* n_snapshots) {
+    if (stride == 0) stride = default_stride(N);
+    const bool want = snapshots != nullptr || steps_out != nullptr;
+    const size_t rows = want ? 2 + k_end / stride : 0;
+    const size_t P = N / per_pe;
+    const int dir = bc_kind == HEAT_BC_DIRICHLET;
+    std::vector<int> offL, offR;
+    const int D = draw_offsets(N, per_pe, dir, offL, offR);
+    std::vector<uint64_t> gthr;
+    if (law == HEAT_DELAY_GEOMETRIC) HB_TRY(geometric_thresholds(geometric_p, q, gthr));
+
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    std::lock_guard<std::mutex> lock(d->mu);
+    const size_t pitch = (N + 63) / 64 * 64;
+    HB_TRY(ensure_buffers(*d, pitch * sizeof(double)));
+    // draw tables: offL, offR, thresholds in the scratch
+    const size_t tab_bytes = 2 * P * sizeof(int) + 8 + std::max<size_t>(1, gthr.size()) * 8;
+    HB_TRY(ensure_scratch(*d, tab_bytes));
+    double* field = static_cast<double*>(d->buf[0]);
+    cudaStream_t st = d->stream;
+    const bool ends_ok = !dir || (std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[N - 1] - c2) <= 1e-9);
+    HB_CUDA(cudaMemsetAsync(d->flag, 0, 4 * sizeof(unsigned int), st));
+    if (!ends_ok) HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));  // the right error
+    HB_CUDA(cudaMemcpyAsync(field, u0, N * sizeof(double), cudaMemcpyHostToDevice, st));
+    // one upload of the draw tables (pageable host staging is fine: tiny)
+    std::vector<unsigned char> host(tab_bytes, 0);
+    std::memcpy(host.data(), offL.data(), P * sizeof(int));
+    std::memcpy(host.data() + P * sizeof(int), offR.data(), P * sizeof(int));
+    const size_t o_thr = (2 * P * sizeof(int) + 7) / 8 * 8;
+    if (!gthr.empty()) std::memcpy(host.data() + o_thr, gthr.data(), gthr.size() * 8);
+    char* sbase = static_cast<char*>(d->scratch);
+    HB_CUDA(cudaMemcpyAsync(sbase, host.data(), tab_bytes, cudaMemcpyHostToDevice, st));
+    if (want && d->snaps_bytes < rows * N * sizeof(double)) {
+        if (d->snaps) cudaFree(d->snaps);
+        d->snaps = nullptr;
+        d->snaps_bytes = 0;
+        HB_CUDA(cudaMalloc(&d->snaps, rows * N * sizeof(double)));
+        d->snaps_bytes = rows * N * sizeof(double);
+    }
+    AsyncSmallArgs a{};
+    a.field = field;
+    a.N = int(N);
+    a.n = int(per_pe);
+    a.P = int(P);
+    a.r = r;
+    a.c = 1.0 - 2.0 * r;  // core.hpp:108
+    a.c1 = c1;
+    a.c2 = c2;
+    a.dirichlet = dir;
+    a.k_end = (long long)k_end;
+    a.stride = want ? (long long)stride : 0;
+    a.snaps = want ? static_cast<double*>(d->snaps) : nullptr;
+    a.flag = d->flag;
+    a.law = law;
+    a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
+    a.q = int(q);
+    a.seed = seed;
+    a.modq = make_modq(unsigned(q));
+    a.D = D;
+    a.offL = reinterpret_cast<const int*>(sbase);
+    a.offR = reinterpret_cast<const int*>(sbase) + P;
+    a.gthr = reinterpret_cast<const uint64_t*>(sbase + o_thr);
+    const int QH = history_slots(q);
+    const int smem = int(small_smem_bytes(N, P, QH, q));
+    const int warps = int((N + kAsChunk - 1) / kAsChunk);
+    auto launch = [&](auto kern) -> int {
+        int per_sm = 0;
+        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(kern),
+                                  int(small_smem_bytes(kAsMaxN, kAsMaxN / kAsV, kAsMaxQ, kAsMaxQ)),
+                                  warps * 32, &per_sm));
+        kern<<<1, warps * 32, smem, st>>>(a);
+        HB_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return HEAT_OK;
+    };
+    auto by_law = [&](auto k0, auto k1, auto k2) -> int {
+        return law == HEAT_DELAY_UNIFORM ? launch(k0) : law == HEAT_DELAY_FIXED ? launch(k1)
+                                                                               : launch(k2);
+    };
+    if (QH == 2)
+        HB_TRY(by_law(async_small_kernel<2, 0>, async_small_kernel<2, 1>, async_small_kernel<2, 2>));
+    else if (QH == 4)
+        HB_TRY(by_law(async_small_kernel<4, 0>, async_small_kernel<4, 1>, async_small_kernel<4, 2>));
+    else
+        HB_TRY(by_law(async_small_kernel<8, 0>, async_small_kernel<8, 1>, async_small_kernel<8, 2>));
+    size_t ns = 0;
+    std::vector<size_t> ks;
+    if (want) {
+        ks.push_back(0);
+        for (size_t kk = stride; kk <= k_end; kk += stride) ks.push_back(kk);
+        if (k_end % stride) ks.push_back(k_end);
+        ns = ks.size();
+        const size_t copy = std::min(ns, max_snapshots);
+        if (snapshots && copy)
+            HB_CUDA(cudaMemcpyAsync(snapshots, d->snaps, copy * N * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+    }
+    if (final_out)
+        HB_CUDA(cudaMemcpyAsync(final_out, field, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    unsigned int flags[4] = {0, 0, 0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    if (steps_out)
+        for (size_t j = 0; j < ns && j < max_snapshots; ++j) steps_out[j] = ks[j];
+    if (n_snapshots) *n_snapshots = ns;
+    return HEAT_OK;
+}
+
+}  // namespace hb

@@ -331,3 +331,54 @@ def test_geometric_large_q_device_thresholds(gpu, port, N, n):
                         H.DelayModel.geometric(300, 0.02, 5), 500)
     want = port.async_run(u0, 0.3, 0, u0[0], u0[-1], n, 2, 300, 0, 0.02, 5, k_end=500)
     assert bits_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", [9, 1510, 8982])
+def test_small_async_kernel_bit_exact(H, port, seed):
+    # K9 (csrc/async_small.cu): N <= 2048, PEs of a multiple of 8 points, q <= 8 --
+    # one CTA, 64-step rounds, delays applied by the sending lane.  Random shapes
+    # around its limits (rounds cut by the recording stride, k_end not a multiple
+    # of 64, windows wrapping small periodic rings), all laws, both BCs.
+    gen = SplitMix64(seed)
+    for _ in range(12):
+        m = 2 + gen.next_bounded(254)
+        n = 8 * m
+        per_pe = 8 * random_divisor(gen, m)
+        if per_pe == n:
+            per_pe = 8
+        q = 1 + gen.next_bounded(7)
+        r = 0.5 * (gen.next_double() * 0.999 + 0.001)
+        periodic = gen.next() & 1
+        u0 = random_field(gen, n)
+        k_end = 1 + gen.next_bounded(300)
+        stride = 1 + gen.next_bounded(97)
+        law, fd, gp = _law(gen, q)
+        mseed = gen.next()
+        bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(
+            u0[0], u0[-1])
+        model = H.DelayModel(q, H.Distribution(law), fd, gp, mseed)
+        params = H.SolverParams.from_r(r)
+        t = H.async_run(H.TemperatureField(u0), params, bc, H.PartitionSpec(n, per_pe), model,
+                        k_end, stride)
+        steps, snaps = port.async_run(u0, params.r(), bc.kind, bc.c1, bc.c2, per_pe, law, q, fd,
+                                      gp, mseed, k_end, stride, record=True)
+        assert t.steps == steps
+        for j, s in enumerate(t.snapshots):
+            assert bits_equal(s.values(), snaps[j]), (n, per_pe, q, law, periodic, k_end, stride, j)
+
+
+@pytest.mark.parametrize("n,per_pe,q,bc", [(2048, 8, 4, 0), (2048, 1024, 2, 1), (2048, 64, 8, 1),
+                                           (16, 8, 3, 1), (24, 8, 2, 0)])
+def test_small_async_kernel_equals_k3(H, port, monkeypatch, n, per_pe, q, bc):
+    # K9 and K3 (HEAT_NO_SMALL_ASYNC) both give the oracle's bits
+    gen = SplitMix64(n * 7 + q)
+    u0 = random_field(gen, n)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.45)
+    part = H.PartitionSpec(n, per_pe)
+    model = H.DelayModel.uniform(q, 5)
+    k9 = H.async_final(u0, p, b, part, model, 777)
+    monkeypatch.setenv("HEAT_NO_SMALL_ASYNC", "1")
+    k3 = H.async_final(u0, p, b, part, model, 777)
+    exp = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, 0, q, seed=5, k_end=777)
+    assert bits_equal(k9, exp) and bits_equal(k3, exp)
