@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                     hL[0] = pLs;
                     double pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, int(wU & 15)), 1);
                     double pR = __shfl_down_sync(0xffffffffu, pick<QH>(hF, int(wD & 15)), 1);
-                    for (int t = 0; t < len; ++t) {
+                    auto step = [&](int t, bool more) {  // more: step t+1 follows in this sub-round
                         const double p1 = __dmul_rn(r, u[1]);
                         const double pVm2 = __dmul_rn(r, u[V - 2]);
                         const double nF = stencil_p(p1, __dmul_rn(c, u[0]), pL);
@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                         }
                         hF[0] = pF2;
                         hL[0] = pLs2;
-                        if (t + 1 < len) {
+                        if (more) {
                             const int dU = int(wU >> (4 * (t + 1))) & 15;
                             const int dD = int(wD >> (4 * (t + 1))) & 15;
                             pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, dU), 1);
@@ -288,6 +288,12 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                         u[V - 1] = nL;
                         pF = pF2;
                         pLs = pLs2;
+                    };
+                    if (len == kAsSub) {  // whole sub-round: constant shifts
+#pragma unroll
+                        for (int t = 0; t < kAsSub; ++t) step(t, t + 1 < kAsSub);
+                    } else {
+                        for (int t = 0; t < len; ++t) step(t, t + 1 < len);
                     }
                 }
             }
