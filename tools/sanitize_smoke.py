@@ -4,8 +4,8 @@ it (this round's pool does not: it refuses runs under compute-sanitizer):
 
     python tools/sanitize_smoke.py [big]
 
-K1 (one-shot sync, f64 and f32), K3 (async_run, barrier / flags / global
-rings), K5 (wide PEs), K6 (ensemble), K7 (small sync), the simulator, slab
+K1 (one-shot sync, f64 and f32), K9 (small async_run), K3 (async_run, barrier /
+flags / global rings), K5 (wide PEs), K6 (ensemble), K7 (small sync), the simulator, slab
 plans.  `big` adds the streamed sync_run (N = 2^24, slow under memcheck)."""
 import sys
 
@@ -34,6 +34,10 @@ def main():
     bc = H.BoundaryCondition.dirichlet(float(u[0]), float(u[-1]))
     H.sync_run(H.TemperatureField(u), p, bc, 150, 50)             # K7 with trajectory
     H.async_run(H.TemperatureField(u), p, bc, H.PartitionSpec(1024, 128),
+                H.DelayModel.uniform(2, 1), 150, 50)               # K9 (PEs of 8k points)
+    u1 = field(1000)
+    bc1 = H.BoundaryCondition.dirichlet(float(u1[0]), float(u1[-1]))
+    H.async_run(H.TemperatureField(u1), p, bc1, H.PartitionSpec(1000, 125),
                 H.DelayModel.uniform(2, 1), 150, 50)               # K3 barrier, segments
     H.async_final(u, p, bc, H.PartitionSpec(1024, 1), H.DelayModel.uniform(3, 2), 60)  # K3 global
     H.exec_run(H.TemperatureField(u), p, bc, H.PartitionSpec(1024, 128),
