@@ -87,6 +87,14 @@ class TemperatureField:
         v.setflags(write=False)
         self._v = v
 
+    @classmethod
+    def _adopt(cls, v: np.ndarray) -> "TemperatureField":
+        """Wrap a read-only float64 row the library produced (its finiteness was
+        checked on the device: a non-finite result raises before we get here)."""
+        f = cls.__new__(cls)
+        f._v = v
+        return f
+
     def size(self) -> int:
         return int(self._v.size)
 
@@ -252,7 +260,8 @@ def _trajectory(fn, what, u0, params, bc, k_end, stride, extra=()) -> Trajectory
                   C.cast(None, _lib._pd), _lib.dptr(snaps), _lib.szptr(steps), count,
                   C.byref(ns)), what)
     m = ns.value
-    return Trajectory([TemperatureField(snaps[j]) for j in range(m)],
+    snaps.setflags(write=False)  # rows are shared by the snapshots, never copied
+    return Trajectory([TemperatureField._adopt(snaps[j]) for j in range(m)],
                       [int(s) for s in steps[:m]], params, bc)
 
 
