@@ -1,5 +1,6 @@
 // runtime.cu -- library state, per-device workspace, validation helpers and
 // the small C-ABI entry points (errors, strict checks, trajectory sizing).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -107,6 +108,22 @@ int ensure_scratch(DevCtx& d, size_t bytes) {
     }
     d.scratch_bytes = bytes;
     return HEAT_OK;
+}
+
+unsigned char* host_stage(DevCtx& d, size_t bytes) {
+    if (bytes > kHostStageMax) return nullptr;
+    if (d.host_bytes < bytes) {
+        if (d.host) cudaFreeHost(d.host);
+        d.host = nullptr;
+        d.host_bytes = 0;
+        const size_t want = std::max<size_t>(bytes, 1u << 20);
+        if (cudaMallocHost(&d.host, want) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        d.host_bytes = want;
+    }
+    return static_cast<unsigned char*>(d.host);
 }
 
 int check_field(const double* u, size_t n) {

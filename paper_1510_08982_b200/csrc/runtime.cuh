@@ -86,6 +86,8 @@ struct DevCtx {
     size_t scratch_bytes = 0;
     void* snaps = nullptr;         // in-kernel trajectories of small runs
     size_t snaps_bytes = 0;
+    void* host = nullptr;          // pinned staging of the small one-shot calls
+    size_t host_bytes = 0;
 };
 
 // Closes a plan's IPC mappings and frees its xlink state (xlink.cu).
@@ -95,6 +97,11 @@ void xlink_release(heat_plan* p);
 int dev_ctx(int device, DevCtx** out);
 int ensure_buffers(DevCtx& d, size_t bytes);
 int ensure_scratch(DevCtx& d, size_t bytes);
+// Pinned host staging for the small one-shot calls (K7 / K9): their copies are
+// a few KB, and pageable copies cost ~10 us each.  Returns nullptr above
+// kHostStageMax (callers then copy from / to the caller's pageable memory).
+constexpr size_t kHostStageMax = 64ull << 20;
+unsigned char* host_stage(DevCtx& d, size_t bytes);
 
 // Sets `fn`'s dynamic shared memory limit to `smem` on the CURRENT device
 // (the attribute is per device) and returns its resident CTAs per SM for

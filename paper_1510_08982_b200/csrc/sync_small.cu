@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "runtime.cuh"
 #include "sync_tb.cuh"
@@ -148,10 +149,19 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
     const bool ends_ok = bc_kind != HEAT_BC_DIRICHLET ||
                          (std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9);
     HB_CUDA(cudaMemsetAsync(d->flag, 0, 4 * sizeof(unsigned int), st));
-    if (ends_ok)
-        HB_CUDA(cudaMemcpyAsync(field, u0, n * sizeof(double), cudaMemcpyHostToDevice, st));
-    else
+    // pinned staging: [flags | input | final | trajectory rows]
+    const size_t nb = n * sizeof(double);
+    unsigned char* hs = host_stage(*d, 64 + 2 * nb + rows * nb);
+    if (ends_ok) {
+        const void* src = u0;
+        if (hs) {
+            std::memcpy(hs + 64, u0, nb);
+            src = hs + 64;
+        }
+        HB_CUDA(cudaMemcpyAsync(field, src, nb, cudaMemcpyHostToDevice, st));
+    } else {
         HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, field));  // fails with the right error
+    }
     if (want && d->snaps_bytes < rows * n * sizeof(double)) {
         if (d->snaps) cudaFree(d->snaps);
         d->snaps = nullptr;
@@ -215,14 +225,22 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
         ns = ks.size();
         const size_t copy = std::min(ns, max_snapshots);
         if (snapshots && copy)  // rows are contiguous on both sides: one copy
-            HB_CUDA(cudaMemcpyAsync(snapshots, d->snaps, copy * n * sizeof(double),
-                                    cudaMemcpyDeviceToHost, st));
+            HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs + 64 + 2 * nb) : snapshots, d->snaps,
+                                    copy * nb, cudaMemcpyDeviceToHost, st));
     }
     if (final_out)
-        HB_CUDA(cudaMemcpyAsync(final_out, field, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs + 64 + nb) : final_out, field, nb,
+                                cudaMemcpyDeviceToHost, st));
     unsigned int flags[4] = {0, 0, 0, 0};
-    HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs) : flags, d->flag, sizeof flags,
+                            cudaMemcpyDeviceToHost, st));
     HB_CUDA(cudaStreamSynchronize(st));
+    if (hs) {
+        std::memcpy(flags, hs, sizeof flags);
+        if (final_out) std::memcpy(final_out, hs + 64 + nb, nb);
+        if (want && snapshots)
+            std::memcpy(snapshots, hs + 64 + 2 * nb, std::min(ns, max_snapshots) * nb);
+    }
     if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     if (flags[0]) {
         if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
