@@ -145,7 +145,11 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     const long long w0 = (long long)w * C - H;  // window start (unwrapped)
     const long long g0 = w0 + (long long)lane * V;
     const bool active = (long long)w * C < N;  // warp-uniform
-    const bool pinned = a.dirichlet && active && (w0 <= 0 || w0 + 32LL * V > N - 1);
+    // N and the window starts are multiples of 8, so the Dirichlet ends are
+    // always a lane's first (point 0) or last (point N-1) element: the
+    // pipelined step re-pins them with two selects
+    const bool pinF = a.dirichlet && g0 == 0;
+    const bool pinL = a.dirichlet && g0 + V - 1 == N - 1;
     auto real = [&](long long g) { return !a.dirichlet || (g >= 0 && g < N); };
     auto wrapg = [&](long long g) -> int {
         long long x = g % N;
@@ -223,24 +227,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                 if (isU) wU = pack_nibbles(&sdel[w][sU * kAsSub]);
                 if (isD) wD = pack_nibbles(&sdel[w][sD * kAsSub]);
                 __syncwarp();
-                if (pinned) {
-                    for (int t = 0; t < len; ++t) {
-                        const double pF = __dmul_rn(r, u[0]);
-                        const double pLs = __dmul_rn(r, u[V - 1]);
-                        hF[0] = pF;
-                        hL[0] = pLs;
-                        const int dU = int(wU >> (4 * t)) & 15, dD = int(wD >> (4 * t)) & 15;
-                        const double pL = __shfl_up_sync(0xffffffffu, pick<QH>(hL, dU), 1);
-                        const double pR = __shfl_down_sync(0xffffffffu, pick<QH>(hF, dD), 1);
-                        chunk_step<double, V>(u, r, c, pL, pR, pF, pLs);
-                        pin_ends<double, V>(u, g0, 0, N - 1, a.c1, a.c2);
-#pragma unroll
-                        for (int j = QH - 1; j > 0; --j) {
-                            hF[j] = hF[j - 1];
-                            hL[j] = hL[j - 1];
-                        }
-                    }
-                } else {
+                {
                     // software-pipelined as warp_steps_pipelined: the end points
                     // first, then the next step's (delayed) shuffles, then the
                     // interior points
@@ -253,8 +240,10 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                     auto step = [&](int t, bool more) {  // more: step t+1 follows in this sub-round
                         const double p1 = __dmul_rn(r, u[1]);
                         const double pVm2 = __dmul_rn(r, u[V - 2]);
-                        const double nF = stencil_p(p1, __dmul_rn(c, u[0]), pL);
-                        const double nL = stencil_p(pR, __dmul_rn(c, u[V - 1]), pVm2);
+                        double nF = stencil_p(p1, __dmul_rn(c, u[0]), pL);
+                        double nL = stencil_p(pR, __dmul_rn(c, u[V - 1]), pVm2);
+                        if (pinF) nF = a.c1;  // the Dirichlet ends, re-pinned every step
+                        if (pinL) nL = a.c2;
                         const double pF2 = __dmul_rn(r, nF);
                         const double pLs2 = __dmul_rn(r, nL);
 #pragma unroll
