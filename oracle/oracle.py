@@ -110,6 +110,8 @@ class Port(_Lib):
         L.orc_fnv1a64.restype = _u64
         L.orc_prepare_initial.argtypes = [_pd, _sz, _i, _d, _d, _pd]
         L.orc_sync_lightcone.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd]
+        L.orc_async_lightcone.argtypes = [_pd, _sz, _sz, _sz, _d, _d, _d, _sz, _i, _sz, _sz, _d,
+                                          C.c_uint64, _sz, _sz, _pd]
         L.orc_sync_step_into.argtypes = [_pd, _pd, _sz, _d, _i, _d, _d]
         L.orc_sync_step_into.restype = None
         L.orc_async_step.argtypes = [_pd, _sz, _sz, _sz, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz,
@@ -247,6 +249,19 @@ class Port(_Lib):
         st = self.lib.orc_sync_lightcone(_ptr(u0), u0.size, r, bc, c1, c2, k, centre, C.byref(v))
         if st:
             raise OracleError(st, "sync_lightcone")
+        return v.value
+
+    def async_lightcone(self, win, lo, n, r, c1, c2, per_pe, law, q, fixed_d=0, p=0.5, seed=0,
+                        k=1, centre=0) -> float:
+        """u(k)[centre] of the deterministic async run (Dirichlet) from the window
+        win = u0[lo : lo + len(win)] (heat_oracle.c orc_async_lightcone)."""
+        w = _f64(win)
+        v = C.c_double(0.0)
+        st = self.lib.orc_async_lightcone(_ptr(w), w.size, lo, n, r, c1, c2, per_pe, law, q,
+                                          fixed_d, p, seed & 0xFFFFFFFFFFFFFFFF, k, centre,
+                                          C.byref(v))
+        if st:
+            raise OracleError(st, "async_lightcone")
         return v.value
 
 

@@ -61,3 +61,44 @@ def test_huge_field_lightcone(H, port):
             w[-1] = 0.0
         want = port.sync_lightcone(w, r, 0, float(w[0]), float(w[-1]), K, c - lo)
         assert got[c] == want, (c, got[c], want)
+
+
+def test_async_replay_full_size_lightcone(H, port):
+    # BASELINE cfg3's asynchronous leg at full size: N = 2^30, 512 PEs of 2^21
+    # points, the deterministic replay K5 runs in the bench (uniform q = 2,
+    # seed 1) and a geometric one, checked point by point against the oracle's
+    # light cone of the asynchronous run (orc_async_lightcone: the reference's
+    # draws k*D + off at every PE boundary) around PE boundaries, inside PEs
+    # and at both ends
+    n = 1 << 30
+    pe = n // 512
+    bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
+    r = H.SolverParams.from_r(0.4).r()
+    centres = [0, 1, 2, 700, pe - 2, pe - 1, pe, pe + 1, 255 * pe - 1, 255 * pe, 256 * pe - 1,
+               256 * pe, 256 * pe + 77, 511 * pe - 1, 511 * pe, n - 2, n - 1]
+    models = [(H.DelayModel.uniform(2, 1), 0, 2, 0, 0.5, 1),
+              (H.DelayModel.geometric(3, 0.4, 7), 2, 3, 0, 0.4, 7)]
+    p = H.Plan(n, 0)
+    try:
+        results = []
+        for model, law, q, fd, gp, seed in models:
+            p.fill_sine()
+            wins = {}
+            for c in centres:
+                lo, hi = max(0, c - K - 2), min(n, c + K + 3)
+                wins[c] = (lo, p.download_range(lo, hi - lo))
+            p.async_replay(r, bc, pe, model, K)
+            got = {c: p.download_range(c, 1)[0] for c in centres}
+            results.append((law, q, fd, gp, seed, wins, got))
+    finally:
+        p.close()
+    for law, q, fd, gp, seed, wins, got in results:
+        for c in centres:
+            lo, w = wins[c]
+            w = w.copy()
+            if lo == 0:
+                w[0] = 0.0  # the snapped global ends
+            if lo + w.size == n:
+                w[-1] = 0.0
+            want = port.async_lightcone(w, lo, n, r, 0.0, 0.0, pe, law, q, fd, gp, seed, K, c)
+            assert got[c] == want, (law, q, c, got[c], want)

@@ -150,3 +150,20 @@ def test_port_async_step_vs_reference(port, ref, seed):
         if sp == 0:
             assert bits_equal(fp, fr)
     assert errors > 0  # the logic_error path was exercised
+
+
+@pytest.mark.parametrize("law,q,fd,gp", [(0, 2, 0, 0.5), (0, 3, 0, 0.5), (1, 4, 2, 0.5),
+                                         (2, 5, 0, 0.3)])
+def test_async_lightcone_windows(port, law, q, fd, gp):
+    # the deterministic async run's light cone (orc_async_lightcone) equals the
+    # full async_run at PE boundaries, interior points and near the true ends
+    n, per_pe, k, seed = 4096, 256, 120, 99 + q
+    gen = SplitMix64(n + q)
+    u0 = random_field(gen, n)
+    u0[0], u0[-1] = 0.0, 0.0
+    full = port.async_run(u0, 0.4, 0, 0.0, 0.0, per_pe, law, q, fd, gp, seed=seed, k_end=k)
+    for c in [0, 1, 5, 255, 256, 257, 1023, 1024, 2000, 3839, 3840, n - 2, n - 1]:
+        lo, hi = max(0, c - k - 2), min(n, c + k + 3)
+        got = port.async_lightcone(u0[lo:hi], lo, n, 0.4, 0.0, 0.0, per_pe, law, q, fd, gp,
+                                   seed, k, c)
+        assert got == full[c], (c, got, full[c])
