@@ -133,6 +133,11 @@ int heat_geometric_thresholds(double p, size_t q, uint64_t* thresholds);
 const char* heat_last_error(void);
 const char* heat_version(void);
 int heat_device_count(void);
+/* Device of the calling thread's one-shot calls (sync_run, async_run,
+ * ensemble_run, ...): cudaSetDevice for this library.  One process per GPU
+ * under torchrun calls it with its local rank (multigpu.ensemble_run_sharded).
+ * HEAT_EINVAL for a device that does not exist. */
+int heat_set_device(int device);
 /* Number of kernels this library has launched in this process (all devices). */
 uint64_t heat_kernel_launches(void);
 /* The f64 synchronous pass kernel in use (HEAT_SYNC_VARIANT selects among

@@ -100,6 +100,7 @@ SIGNATURES = {
     "heat_last_error": (C.c_char_p, []),
     "heat_version": (C.c_char_p, []),
     "heat_device_count": (_i, []),
+    "heat_set_device": (_i, [_i]),
     "heat_kernel_launches": (_u64, []),
     "heat_sync_kernel_info": (_i, [C.POINTER(_i), C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "heat_stream_chunk_plan": (_i, [_sz, _sz, _P(_sz), _sz, _P(_sz)]),

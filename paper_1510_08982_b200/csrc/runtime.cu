@@ -208,6 +208,17 @@ const char* heat_last_error(void) { return t_error.c_str(); }
 
 const char* heat_version(void) { return "heat_b200 0.1 (sm_100a)"; }
 
+int heat_set_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(HEAT_ENODEV, "no CUDA device available");
+    }
+    if (device < 0 || device >= count) return fail(HEAT_EINVAL, "heat_set_device: no such device");
+    HB_CUDA(cudaSetDevice(device));
+    return HEAT_OK;
+}
+
 int heat_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

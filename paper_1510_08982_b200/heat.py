@@ -224,6 +224,11 @@ def default_stride(n_points: int) -> int:
     return 1 if n_points <= 1000 else 100
 
 
+def set_device(device: int) -> None:
+    """Device of this thread's one-shot calls (heat_set_device)."""
+    _lib.check(_lib.lib().heat_set_device(int(device)), "set_device")
+
+
 def set_strict_finite_checks(enabled: bool) -> None:
     _lib.lib().heat_set_strict_finite_checks(int(bool(enabled)))
 

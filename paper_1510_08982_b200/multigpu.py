@@ -15,6 +15,7 @@ host logic only; the stepping is the sm_100a kernel behind heat.Plan.
 """
 from __future__ import annotations
 
+import math
 from typing import Callable, Optional
 
 import torch
@@ -196,3 +197,56 @@ class SlabSolver:
     def gather(self) -> torch.Tensor:
         """The global field (device tensor on every rank)."""
         return plan_gather(self.plan, self.world, self.group)
+
+
+# ---- ensembles across GPUs (SURVEY §8f rank 1) -------------------------------
+def ensemble_run_sharded(cfg, runs: int, base_seed: int, device: Optional[int] = None,
+                         group=None, member_fn: Optional[Callable] = None,
+                         keep_terminals: bool = True):
+    """ensemble_run (analysis.cpp:51-104) with the members split over the ranks:
+    rank g runs members [g*M/G, (g+1)*M/G) (seeds base_seed + j) on its own GPU,
+    with no communication while they run. One all_gather_object then assembles
+    the norm series (and terminal fields) in member order, and every rank forms
+    mean/std in the reference's order: sequential sums over j, population std.
+    The result is bit-identical to a single-process ensemble_run of M members.
+
+    member_fn(cfg, count, first_seed) -> EnsembleResult defaults to the GPU
+    ensemble (heat.ensemble_run); the CPU tests pass the reference's."""
+    from . import heat as H
+    if runs == 0:
+        raise H.DomainError("ensemble_run: M >= 1 required")
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if device is not None:
+        H.set_device(device)
+    if member_fn is None:
+        def member_fn(c, count, first):
+            return H.ensemble_run(c, count, first, keep_terminals=keep_terminals)
+    start, end = rank * runs // world, (rank + 1) * runs // world
+    local = member_fn(cfg, end - start, base_seed + start) if end > start else None
+    mine = (start, local.steps if local else None,
+            [list(map(float, s)) for s in local.norm_series] if local else [],
+            [t.values() for t in local.terminal_fields] if (local and keep_terminals) else [])
+    parts = [mine]
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine, group=group)
+    parts.sort(key=lambda x: x[0])
+    steps = next(p[1] for p in parts if p[1] is not None)
+    norms = [s for p in parts for s in p[2]]
+    terms = [H.TemperatureField(t) for p in parts for t in p[3]]
+    S = len(steps)
+    mean_series, std_series = [0.0] * S, [0.0] * S
+    for s in range(S):  # analysis.cpp:90-101
+        mean = 0.0
+        for j in range(runs):
+            mean += norms[j][s]
+        mean /= float(runs)
+        var = 0.0
+        for j in range(runs):
+            d = norms[j][s] - mean
+            var += d * d
+        mean_series[s] = mean
+        std_series[s] = math.sqrt(var / float(runs))
+    return H.EnsembleResult(list(steps), norms, terms, mean_series, std_series,
+                            [base_seed + j for j in range(runs)])

@@ -153,3 +153,25 @@ def test_ensemble_beyond_shared_memory_matches_reference(H, ref, N, per_pe, law,
     bc = H.BoundaryCondition.dirichlet(float(u0[0]), float(u0[-1]))
     _check_against_reference(H, ref, u0, 0.4, bc, per_pe, law, q, 2 if law == 1 else 0, 0.5, 400,
                              150, 3, 9)
+
+
+def test_sharded_ensemble_one_rank_equals_ensemble_run(gpu, port):
+    # multigpu.ensemble_run_sharded on one process (no process group): the GPU
+    # members on the device heat_set_device picked, statistics formed on the
+    # host in the reference's order -- identical to heat.ensemble_run
+    from paper_1510_08982_b200 import heat as H
+    from paper_1510_08982_b200 import multigpu as M
+    cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.from_r(0.45),
+                           H.BoundaryCondition.periodic(), H.PartitionSpec(100, 1),
+                           H.DelayModel.uniform(3, 0), k_end=2000, stride=100)
+    a = M.ensemble_run_sharded(cfg, 9, 42, device=0)
+    b = H.ensemble_run(cfg, 9, 42)
+    assert a.steps == b.steps and a.seeds == b.seeds
+    assert np.array_equal(np.array(a.norm_series).view(np.uint64),
+                          np.array(b.norm_series).view(np.uint64))
+    assert np.array_equal(np.array(a.mean_series).view(np.uint64),
+                          np.array(b.mean_series).view(np.uint64))
+    assert np.array_equal(np.array(a.std_series).view(np.uint64),
+                          np.array(b.std_series).view(np.uint64))
+    with pytest.raises(H.InvalidArgument):
+        H.set_device(4096)

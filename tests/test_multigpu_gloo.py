@@ -111,3 +111,56 @@ def test_slab_decomposition_bit_exact(port, world, periodic):
     got = q.get(timeout=60)
     exp = port.sync_run(u0, r, 1 if periodic else 0, c1, c2, steps)
     assert bits_equal(got, exp)
+
+
+# ---- ensembles across ranks (multigpu.ensemble_run_sharded) -----------------
+def _ref_members(cfg, count, first_seed):
+    """The reference's own ensemble_run for one rank's members (CPU stand-in
+    for the GPU ensemble the product runs on each rank's device)."""
+    from oracle import oracle as O
+    from paper_1510_08982_b200 import heat as H
+    m = cfg.model
+    steps, norms, terms, mean, std, _ = O.ref().ensemble_run(
+        cfg.u0.values(), cfg.params.r(), cfg.bc.kind, cfg.bc.c1, cfg.bc.c2, cfg.part.per_pe(),
+        int(m.distribution), m.q, m.fixed_delay, cfg.k_end, cfg.stride, count, first_seed)
+    return H.EnsembleResult(steps, [list(r) for r in norms], [H.TemperatureField(t) for t in terms],
+                            list(mean), list(std), [first_seed + j for j in range(count)])
+
+
+def _ens_worker(rank, world, port, runs, base_seed, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08982_b200 import heat as H
+        cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.from_r(0.45),
+                               H.BoundaryCondition.dirichlet(1.0, 0.0), H.PartitionSpec(100, 1),
+                               H.DelayModel.uniform(4, 0), k_end=500, stride=50)
+        res = M.ensemble_run_sharded(cfg, runs, base_seed, member_fn=_ref_members)
+        if rank == 0:
+            q.put((res.steps, res.norm_series, res.mean_series, res.std_series,
+                   [t.values() for t in res.terminal_fields], res.seeds))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ensemble_sharded_bit_exact(world):
+    from oracle import oracle as O
+    if not O.Ref.available():
+        pytest.skip("reference library not built here")
+    runs, base = 7, 1000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_ens_worker, args=(world, _free_port(), runs, base, q), nprocs=world,
+                       join=True, start_method="spawn")
+    steps, norms, mean, std, terms, seeds = q.get(timeout=120)
+    port_ = O.port()
+    u0 = port_.cosine_init(100)
+    e_steps, e_norms, e_terms, e_mean, e_std, _ = O.ref().ensemble_run(
+        u0, 0.45, 0, 1.0, 0.0, 1, 0, 4, 0, 500, 50, runs, base)
+    assert steps == e_steps and seeds == [base + j for j in range(runs)]
+    assert np.array_equal(np.array(norms).view(np.uint64), e_norms.view(np.uint64))
+    assert np.array_equal(np.array(mean).view(np.uint64), np.asarray(e_mean).view(np.uint64))
+    assert np.array_equal(np.array(std).view(np.uint64), np.asarray(e_std).view(np.uint64))
+    assert np.array_equal(np.array(terms).view(np.uint64), e_terms.view(np.uint64))
