@@ -88,13 +88,14 @@ struct AsyncStreamArgs {
     unsigned int* abort_word;
     unsigned long long timeout_ns;
     int pend_max;   // done-signals published per release fence (1..kMaxPend)
-    int pref_step;  // interior tiles: step at which the next window is issued (< 0: half-way)
 };
 constexpr int kMaxPend = 16;
 #ifndef HEAT_K5_UNROLL
 #define HEAT_K5_UNROLL 2
 #endif
-constexpr int kK5Unroll = HEAT_K5_UNROLL;  // interior step loop unroll (4: -2.4% here, though K1 gains 0.45% from it)
+// interior step loop unroll: 2 (4: -1.4%, 1: -2.5%, measured with the single
+// interior loop; K1 gains 0.45% from 4)
+constexpr int kK5Unroll = HEAT_K5_UNROLL;
 
 __device__ __forceinline__ int det_delay_s(const AsyncStreamArgs& a, long long k, int off) {
     const long long bound = k < (long long)(a.q - 1) ? k : (long long)(a.q - 1);
@@ -330,7 +331,23 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         pend_generic = false;
     };
 
+    // this lane's share of an item's dependency flags (lanes 0..2: tiles m-1,
+    // m, m+1 of the same PE at the previous pass), loaded with acquire
+    auto dep_load = [&](const StreamItem& x) -> unsigned int {
+        unsigned int v = 0xffffffffu;
+        if (x.pass > 0 && lane < 3) {
+            const int mm = x.m + lane - 1;
+            if (mm >= 0 && mm < a.Tp) v = ld_acquire_gpu_u32(a.done + x.p * a.Tp + mm);
+        }
+        return v;
+    };
+    // Items are held two ahead: while item i runs, the warp already holds
+    // item i+1 (grabbed during item i-1, its flags loaded then), so i+1's
+    // window is issued as soon as i's window is in registers -- as K1 issues
+    // its next window -- and interior tiles step in one uninterrupted loop.
     long long cur = grab();
+    long long nxt = grab();
+    unsigned int nxt_dep = nxt < total ? dep_load(decode_item(a, nxt)) : 0xffffffffu;
     bool cur_pref = false;  // window of `cur` already in flight into buffer b
     while (cur < total && !abort) {
         const StreamItem it = decode_item(a, cur);
@@ -342,10 +359,9 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         const long long kbeg = a.k0 + it.pass * a.s;
         const int nst = int(min((long long)a.s, a.k0 + a.steps - kbeg));
 
-        // the next item's index: the atomic is issued now and read once this
-        // window is in, so its latency hides behind the window wait
-        unsigned long long nxt_raw = 0;
-        if (lane == 0) nxt_raw = atomicAdd(a.counter, 1ull);
+        // item i+2: the atomic is issued now and read once this window is in
+        unsigned long long nn_raw = 0;
+        if (lane == 0) nn_raw = atomicAdd(a.counter, 1ull);
         // ---- window in
         if (!cur_pref) {
             if (!deps_ready(it, false)) signal_pending(0);  // never block holding a signal
@@ -365,33 +381,29 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
                 u[i] = (g >= 0 && g < a.N) ? ld_relaxed_gpu_f64(src + g) : 0.0;
             }
         }
-        // ---- next item: grabbed now; its dependency flags are loaded now and
-        // tested half-way through this tile's steps, so the acquire latency
-        // hides behind compute; the window prefetch then still has half a
-        // tile of compute to land.
-        const long long nxt = (long long)__shfl_sync(0xffffffffu, nxt_raw, 0);
+        // ---- item i+1: its flags were loaded one item ago
         bool nxt_pref = false;
         StreamItem ni{};
         long long nlo = 0, nw0 = 0, nhi = 0;
         bool nxt_cand = false;
-        unsigned int dep_seen = 0xffffffffu;
         if (nxt < total) {
             ni = decode_item(a, nxt);
             geometry(ni, nlo, nw0, nhi);
             nxt_cand = tma_ok(nw0);
-            if (nxt_cand && ni.pass > 0 && lane < 3) {
-                const int mm = ni.m + lane - 1;
-                if (mm >= 0 && mm < a.Tp) dep_seen = ld_acquire_gpu_u32(a.done + ni.p * a.Tp + mm);
-            }
         }
+        unsigned int dep_seen = nxt_dep;
         auto try_prefetch = [&]() {
-            if (!nxt_cand) return;
+            if (!nxt_cand || nxt_pref) return;
             const bool ok = ni.pass == 0 || dep_seen >= unsigned(ni.pass);
             if (__all_sync(0xffffffffu, ok)) {
                 issue(b ^ 1, ni, nw0);
                 nxt_pref = true;
             }
         };
+        try_prefetch();
+        if (nxt_cand && !nxt_pref) dep_seen = dep_load(ni);  // tested again after the steps
+        const long long nn = (long long)__shfl_sync(0xffffffffu, nn_raw, 0);
+        const unsigned int nn_dep = nn < total ? dep_load(decode_item(a, nn)) : 0xffffffffu;
 
         // ---- step the tile; boundary tiles exchange edge values every step.
         // The PE's first point sits kHalo points into a left-edge window, its
@@ -400,10 +412,8 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         const int lpos = int(out_hi - 1 - w0);
         const int ll = lpos / V, le = lpos % V;
         if (!left_edge && !right_edge) {
-            const int half = a.pref_step < 0 ? nst / 2 : min(nst, a.pref_step);
-            warp_steps_pipelined<double, V, kK5Unroll>(u, r, c, half);
+            warp_steps_pipelined<double, V, kK5Unroll>(u, r, c, nst);
             try_prefetch();
-            warp_steps_pipelined<double, V, kK5Unroll>(u, r, c, nst - half);
         } else {
             try_prefetch();
             signal_pending(0);  // boundary tiles spin on other PEs: flush first
@@ -544,6 +554,8 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
         ++npend;
         pend_generic |= !cur_bulk;
         cur = nxt;
+        nxt = nn;
+        nxt_dep = nn_dep;
         cur_pref = nxt_pref;
         if (nxt_pref) b ^= 1;
     }

@@ -36,8 +36,7 @@ void stream_geometry(size_t n, int& V, int& H) {
     }
     V = H = 32;
 }
-// Done-signals deferred per release fence, and the step of an interior tile
-// at which the next window is issued (HEAT_K5_PEND / HEAT_K5_PREF, for A/B).
+// Done-signals deferred per release fence (HEAT_K5_PEND, for A/B).
 int env_int(const char* name, int dflt, int lo, int hi) {
     const char* e = std::getenv(name);
     if (!e || !*e) return dflt;
@@ -45,10 +44,6 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 }
 int stream_pend_max() {
     static const int v = env_int("HEAT_K5_PEND", 2, 1, kMaxPend);
-    return v;
-}
-int stream_pref_step() {
-    static const int v = env_int("HEAT_K5_PREF", -1, -1, 1 << 20);
     return v;
 }
 constexpr int kSU = 32;  // tensor-map unit (points); PEs are whole units
@@ -357,7 +352,6 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.abort_word = at<unsigned int>(base, L.o_abort);
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;
     a.pend_max = stream_pend_max();
-    a.pref_step = stream_pref_step();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (device_ms) {
         HB_CUDA(cudaEventCreate(&e0));
