@@ -14,6 +14,7 @@ p.fill_sine()
 bc = H.BoundaryCondition.dirichlet(0, 0)
 r = H.SolverParams.from_r(0.4).r()
 p.async_advance(r, bc, n // P, q, 64)
+p.sync_advance(r, bc, 128)  # both kernels warmed up (first-launch setup is not timed)
 p.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for mode in ("async", "sync", "async"):
