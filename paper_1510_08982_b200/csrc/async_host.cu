@@ -163,6 +163,30 @@ int launch_pe(int V, bool shared, bool barrier, const AsyncPeArgs& a, int P, cud
                    : launch_sb<true, false>(V, a, P, st, smem);
 }
 
+// K3 runs a PE wider than a warp's 1024 points as `upe` equal units of at
+// most 1024 points (the smallest such split).  The edges between units of
+// one PE read the neighbour's value of the same step (kUnitEdge), so the PE
+// stays synchronous inside; PE edges keep their draw ranks.
+int k3_units(size_t n, size_t& upe) {
+    upe = 1;
+    if (n <= 32 * 32) return HEAT_OK;
+    for (upe = 2; upe <= n && (n % upe != 0 || n / upe > 32 * 32); ++upe) {}
+    if (upe > n || n / upe < 2)
+        return fail(HEAT_EINVAL, "async: a PE of this width has no split into units of <= 1024 "
+                                 "points");
+    return HEAT_OK;
+}
+void unit_offsets(const std::vector<int>& peL, const std::vector<int>& peR, size_t upe,
+                  std::vector<int>& offL, std::vector<int>& offR) {
+    const size_t U = peL.size() * upe;
+    offL.resize(U);
+    offR.resize(U);
+    for (size_t u = 0; u < U; ++u) {
+        offL[u] = u % upe == 0 ? peL[u / upe] : kUnitEdge;
+        offR[u] = (u + 1) % upe == 0 ? peR[u / upe] : kUnitEdge;
+    }
+}
+
 }  // namespace
 
 
@@ -170,18 +194,23 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
                  const std::function<int(size_t, const double*)>& on_record,
                  unsigned long long* host_stats,
                  std::vector<double>* edge_log, std::vector<int>* used_log, float* device_ms) {
-    const size_t P = s.N / s.n;
-    if (s.n > 32 * 32)
-        return fail(HEAT_ENODEV, "async: PEs wider than 1024 points need the streaming kernel "
-                                 "(heat_plan_async_advance)");
+    // PEs wider than 1024 points run as units (k3_units; the callers send PEs
+    // of a multiple of 32 points to K5 instead)
+    size_t upe = 1;
+    HB_TRY(k3_units(s.n, upe));
+    if (upe > 1 && s.want_logs)
+        return fail(HEAT_EINVAL, "async: edge logs need PEs of <= 1024 points or a multiple of "
+                                 "32 points");
+    const size_t Ppe = s.N / s.n, P = Ppe * upe, nu = s.n / upe;  // PEs, units, unit width
     if (P > 65536) return fail(HEAT_EINVAL, "async: too many PEs");
     const int q = int(s.q);
-    const K3Layout G = k3_layout(s.n, P, q, s.mode);
+    const K3Layout G = k3_layout(nu, P, q, s.mode);
     const int S = G.S, V = G.V, R = G.R;
     const size_t warps = G.warps;
     const int dir = s.bc_kind == HEAT_BC_DIRICHLET;
-    std::vector<int> offL, offR;
-    const int D = draw_offsets(s.N, s.n, dir, offL, offR);
+    std::vector<int> peL, peR, offL, offR;
+    const int D = draw_offsets(s.N, s.n, dir, peL, peR);  // the PEs' draw ranks
+    unit_offsets(peL, peR, upe, offL, offR);
 
     // geometric law: the delay thresholds (exact, runtime.cu geometric_thresholds)
     std::vector<uint64_t> gthr;
@@ -206,7 +235,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
 
     // initial ring: slot 0 = step-0 edge values, prog = 0 (one small kernel)
     async_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (P * 2 * R + 255) / 256)), 256,
-                        0, st>>>(dfield, int(s.n), int(P), R, reinterpret_cast<double*>(base + o_ring),
+                        0, st>>>(dfield, int(nu), int(P), R, reinterpret_cast<double*>(base + o_ring),
                                  reinterpret_cast<unsigned long long*>(base + o_prog),
                                  s.want_logs ? reinterpret_cast<double*>(base + o_elog) : nullptr);
     HB_CUDA(cudaGetLastError());
@@ -226,7 +255,7 @@ int async_pe_run(DevCtx& d, const AsyncRunSpec& s, double* dfield, size_t stride
     AsyncPeArgs a{};
     a.field = dfield;
     a.N = (long long)s.N;
-    a.n = int(s.n);
+    a.n = int(nu);
     a.P = int(P);
     a.r = s.r;
     a.c = 1.0 - 2.0 * s.r;  // core.hpp:108
@@ -423,7 +452,8 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
-    const bool wide = per_pe > 32 * 32;  // K5 streaming kernel, else K3 warp-per-PE
+    // K5 streaming kernel for wide PEs of whole 32-point units, else K3
+    const bool wide = per_pe > 32 * 32 && per_pe % 32 == 0;
     const size_t pitch = (N + 63) / 64 * 64;
     HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
     double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
@@ -574,7 +604,7 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     }
 
     std::lock_guard<std::mutex> lock(d->mu);
-    const bool wide = per_pe > 32 * 32;
+    const bool wide = per_pe > 32 * 32 && per_pe % 32 == 0;  // K5; else K3 (units)
     const size_t pitch = (N + 63) / 64 * 64;
     HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
     double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
@@ -696,7 +726,9 @@ struct heat_async_sim {
     int cur = 0;
     size_t k = 0;
     bool started = false;
-    // K3 scratch layout
+    // K3 scratch layout (U units of nu points: PEs wider than 1024 points
+    // are split, k3_units)
+    size_t U = 0, nu = 0;
     int R = 0, D = 0, V = 1, S = 32;
     size_t warps = 0;
     size_t o_ring = 0, o_prog = 0, o_offL = 0, o_offR = 0, o_abort = 0;
@@ -729,16 +761,16 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
     char* base = static_cast<char*>(d.scratch);
     cudaStream_t st = d.stream;
     if (!sim->started) {
-        async_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (sim->P * 2 * sim->R + 255) / 256)),
-                            256, 0, st>>>(sim->field[0], int(s.n), int(sim->P), sim->R,
+        async_init_kernel<<<std::max<size_t>(1, std::min<size_t>(1024, (sim->U * 2 * sim->R + 255) / 256)),
+                            256, 0, st>>>(sim->field[0], int(sim->nu), int(sim->U), sim->R,
                                           reinterpret_cast<double*>(base + sim->o_ring),
                                           reinterpret_cast<unsigned long long*>(base + sim->o_prog),
                                           nullptr);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        HB_CUDA(cudaMemcpyAsync(base + sim->o_offL, sim->offL.data(), sim->P * sizeof(int),
+        HB_CUDA(cudaMemcpyAsync(base + sim->o_offL, sim->offL.data(), sim->U * sizeof(int),
                                 cudaMemcpyHostToDevice, st));
-        HB_CUDA(cudaMemcpyAsync(base + sim->o_offR, sim->offR.data(), sim->P * sizeof(int),
+        HB_CUDA(cudaMemcpyAsync(base + sim->o_offR, sim->offR.data(), sim->U * sizeof(int),
                                 cudaMemcpyHostToDevice, st));
         HB_CUDA(cudaMemsetAsync(base + sim->o_abort, 0, sizeof(unsigned int), st));
         sim->started = true;
@@ -747,8 +779,8 @@ int sim_step_k3(heat_async_sim* sim, size_t count) {
     AsyncPeArgs a{};
     a.field = sim->field[0];
     a.N = (long long)s.N;
-    a.n = int(s.n);
-    a.P = int(sim->P);
+    a.n = int(sim->nu);
+    a.P = int(sim->U);
     a.r = s.r;
     a.c = 1.0 - 2.0 * s.r;  // core.hpp:108
     a.c1 = s.c1;
@@ -838,7 +870,7 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
     HB_CUDA(cudaMalloc(&d.flag, kFlagWords * sizeof(unsigned int)));
     HB_CUDA(cudaMemset(d.flag, 0, kFlagWords * sizeof(unsigned int)));
     sim->P = N / per_pe;
-    sim->wide = per_pe > 32 * 32 && sim->P > 1;
+    sim->wide = per_pe > 32 * 32 && per_pe % 32 == 0 && sim->P > 1;  // K5; else K3 (units)
     const size_t pitch = (N + 63) / 64 * 64;
     // two buffers for K5 and for a single PE (K1 ping-pong), one for K3
     HB_TRY(ensure_buffers(d, (sim->wide || sim->P == 1 ? 2 : 1) * pitch * sizeof(double)));
@@ -857,22 +889,28 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         HB_TRY(stream_layout(sim->s, 1, StreamExternal{}, sim->L, sim->offL, sim->offR));
         HB_TRY(ensure_scratch(d, sim->L.bytes));
     } else if (!sim->wide) {
-        const K3Layout G = k3_layout(per_pe, sim->P, int(q), 0);
+        size_t upe = 1;
+        HB_TRY(k3_units(per_pe, upe));
+        sim->U = sim->P * upe;
+        sim->nu = per_pe / upe;
+        const K3Layout G = k3_layout(sim->nu, sim->U, int(q), 0);
         sim->S = G.S;
         sim->V = G.V;
         sim->warps = G.warps;
         sim->R = G.R;
-        sim->D = draw_offsets(N, per_pe, bc_kind == HEAT_BC_DIRICHLET, sim->offL, sim->offR);
+        std::vector<int> peL, peR;
+        sim->D = draw_offsets(N, per_pe, bc_kind == HEAT_BC_DIRICHLET, peL, peR);
+        unit_offsets(peL, peR, upe, sim->offL, sim->offR);
         size_t off = 0;
         auto take = [&](size_t bytes) {
             size_t o = off;
             off += align256(bytes);
             return o;
         };
-        sim->o_ring = take(sim->P * 2 * sim->R * sizeof(double));
-        sim->o_prog = take(sim->P * sizeof(unsigned long long));
-        sim->o_offL = take(sim->P * sizeof(int));
-        sim->o_offR = take(sim->P * sizeof(int));
+        sim->o_ring = take(sim->U * 2 * sim->R * sizeof(double));
+        sim->o_prog = take(sim->U * sizeof(unsigned long long));
+        sim->o_offL = take(sim->U * sizeof(int));
+        sim->o_offR = take(sim->U * sizeof(int));
         sim->o_abort = take(sizeof(unsigned int));
         HB_TRY(ensure_scratch(d, off));
         sim->smem = G.smem;

@@ -71,6 +71,11 @@ struct AsyncPeArgs {
     int seg;  // lanes per PE (a power of two, 2..32): 32/seg PEs share a warp
 };
 
+// off_left/off_right value of an edge between two units of the same PE (a
+// PE wider than one warp's 1024 points runs as several units, see
+// async_pe_run): exact, no draw
+constexpr int kUnitEdge = -2;
+
 // stats layout (u64 words)
 constexpr int kStatReads = 0, kStatWaits = 1, kStatMaxDelay = 2, kStatDelayHist = 3,
               kStatLagMin = 67, kStatLagMax = 68, kStatLagHist = 69, kStatLagOverflow = 133,
@@ -232,6 +237,9 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
     const double* gring = ring + ((size_t)(nb < 0 ? 0 : nb) * 2 + (lane == 0 ? 1 : 0)) * R;
     const uint64_t* gprog = prog + (nb < 0 ? 0 : nb);
     const int my_off = lane == 0 ? offL : offR;
+    // an edge between two units of one PE (kUnitEdge): read the neighbour's
+    // value of the same step, no draw (the PE is synchronous inside)
+    const bool exact_edge = my_off == kUnitEdge;
     double* my0 = ring + (size_t)(active ? p : 0) * 2 * R;
     double* my1 = my0 + R;
     const bool stats = a.stats != nullptr;
@@ -246,10 +254,10 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
             int m;
             uint64_t v;
             if (kBarrier) {
-                m = k - det_delay(a, k, my_off);
+                m = exact_edge ? k : k - det_delay(a, k, my_off);
                 v = uint64_t(k);  // lockstep: the neighbour has published step k
-            } else if (a.mode == 0) {
-                m = k - det_delay(a, k, my_off);
+            } else if (a.mode == 0 || exact_edge) {
+                m = exact_edge ? k : k - det_delay(a, k, my_off);
                 v = wait_prog<kShared>(a, gprog, m, &waited);
             } else {
                 v = wait_prog<kShared>(a, gprog, k - (a.q - 1), &waited);
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(kShared ? 512 : 256) async_pe_kernel(const Asy
                 abort = true;
             } else {
                 ghost = RingOps<kShared>::load_val(gring + (m & rmask));
-                if (stats) {
+                if (stats && !exact_edge) {
                     const unsigned used = unsigned(k - m);
                     // writer lag as LagStats measures it: producer progress - step consumed
                     const unsigned long long lag = v - (unsigned long long)m;

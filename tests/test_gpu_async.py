@@ -382,3 +382,49 @@ def test_small_async_kernel_equals_k3(H, port, monkeypatch, n, per_pe, q, bc):
     k3 = H.async_final(u0, p, b, part, model, 777)
     exp = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, 0, q, seed=5, k_end=777)
     assert bits_equal(k9, exp) and bits_equal(k3, exp)
+
+
+@pytest.mark.parametrize("n_total,per_pe,q,bc,law", [
+    (10000, 2500, 3, 0, 0), (10000, 2500, 2, 1, 2), (6000, 2000, 4, 1, 1), (4 * 1100, 1100, 2, 0, 0)])
+def test_wide_pes_off_the_32_grid_bit_exact(H, port, n_total, per_pe, q, bc, law):
+    # PEs wider than 1024 points that are not a multiple of 32 (K5 needs whole
+    # 32-point units) run on K3 as equal units of <= 1024 points, synchronous
+    # inside the PE: the reference's measure() sweep (N = 10000 over 4 or 8
+    # workers) and any such partition stay exact
+    gen = SplitMix64(n_total + per_pe + q)
+    u0 = random_field(gen, n_total)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.41)
+    fd, gp = (1, 0.5) if law == 1 else (0, 0.35)
+    model = H.DelayModel(q, H.Distribution(law), fd, gp, 77)
+    part = H.PartitionSpec(n_total, per_pe)
+    t = H.async_run(H.TemperatureField(u0), p, b, part, model, 150, 40)
+    steps, snaps = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, law, q, fd, gp, seed=77,
+                                  k_end=150, stride=40, record=True)
+    assert t.steps == steps
+    for j, s in enumerate(t.snapshots):
+        assert bits_equal(s.values(), snaps[j]), j
+    # AsyncSimulator in uneven slices (the same units, resumed) = async_run
+    sim = H.AsyncSimulator(H.TemperatureField(u0), p, b, part, model)
+    for c in (1, 37, 50, 62):
+        sim.step(c)
+    assert bits_equal(sim.current(), snaps[-1])
+    sim.close()
+
+
+def test_wide_pes_off_the_32_grid_executors(H, port):
+    # exec_run over such PEs: BarrierFree with q = 1 is the synchronous scheme;
+    # the reference's measure() sweep {100, 1000, 10000} x 4 workers runs
+    n = 10000
+    u0 = port.cosine_init(n)
+    p = H.SolverParams.from_r(0.5)
+    bc = H.BoundaryCondition.dirichlet(1.0, 0.0)
+    res = H.exec_run(H.TemperatureField(u0), p, bc, H.PartitionSpec(n, 2500),
+                     H.ExecConfig(4, 300, H.ExecMode.BarrierFree, False, 1))
+    assert bits_equal(res.field.values(), port.sync_run(u0, p.r(), 0, 1.0, 0.0, 300))
+    rows = H.measure([100, 1000, 10000], [H.ExecMode.Barriered, H.ExecMode.BarrierFree], 3, 200, 4)
+    assert len(rows) == 6 and all(r.median_ns > 0 for r in rows)
+    # a prime PE width above 1024 has no split into units
+    with pytest.raises(H.InvalidArgument, match="no split"):
+        H.async_final(random_field(SplitMix64(3), 2 * 1031), p, H.BoundaryCondition.periodic(),
+                      H.PartitionSpec(2 * 1031, 1031), H.DelayModel.uniform(2, 1), 5)
