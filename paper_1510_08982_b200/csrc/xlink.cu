@@ -62,6 +62,10 @@ int heat_plan_xlink_setup(heat_plan* p, size_t per_pe, size_t q, int bc_kind, vo
     p->async_bytes = 0;
     HB_CUDA(cudaMalloc(&p->async_scratch, x->L.bytes));
     HB_CUDA(cudaMemset(p->async_scratch, 0, x->L.bytes));
+    // cudaMemset may return before it runs: the zeroing must be done before the
+    // handle leaves this process, or it could land after a neighbour's seed
+    // stores into our receive rings (seen once with 3 ranks sharing one GPU)
+    HB_CUDA(cudaDeviceSynchronize());
     p->async_bytes = x->L.bytes;
     cudaIpcMemHandle_t h;
     HB_CUDA(cudaIpcGetMemHandle(&h, p->async_scratch));
