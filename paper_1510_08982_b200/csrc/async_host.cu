@@ -436,6 +436,52 @@ int heat_async_run(const double* u0, size_t N, double r, int bc_kind, double c1,
 
 namespace hb {
 
+// async_run for PEs no kernel geometry covers (wider than 1024 points, off
+// the 32-point grid, with no split into units of <= 1024 points: a prime
+// width): the reference's own loop, one async_step per step over a device
+// HistoryRing (K8a/K8b, history.cu) -- async_sim.cpp:118-160 literally.
+// Slow (a host round trip per step) but any partition works.
+int async_run_history(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
+                      size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                      uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                      double* snapshots, size_t* steps_out, size_t max_snapshots,
+                      size_t* n_snapshots) {
+    std::vector<double> cur;
+    HB_TRY(prepare_initial(u0, N, bc_kind, c1, c2, cur));
+    heat_history* h = nullptr;
+    HB_TRY(heat_history_create(&h, q, N, 0, cur.data(), 1, -1));
+    struct Guard {
+        heat_history* h;
+        ~Guard() { heat_history_destroy(h); }
+    } guard{h};
+    size_t ns = 0;
+    auto record = [&](size_t k, const double* v) -> int {
+        for (size_t i = 0; i < N; ++i)  // a snapshot is a TemperatureField (core.hpp:45-51)
+            if (!std::isfinite(v[i])) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+        if (ns < max_snapshots) {
+            if (snapshots) std::memcpy(snapshots + ns * N, v, N * sizeof(double));
+            if (steps_out) steps_out[ns] = k;
+        }
+        ++ns;
+        return HEAT_OK;
+    };
+    const bool want = snapshots != nullptr || steps_out != nullptr;
+    if (want) HB_TRY(record(0, cur.data()));
+    uint64_t rng = seed;
+    for (size_t k = 0; k < k_end; ++k) {
+        const bool rec = want && ((k + 1) % stride == 0 || k + 1 == k_end);
+        HB_TRY(heat_async_step(h, r, bc_kind, c1, c2, N, per_pe, q, law, fixed_delay, geometric_p,
+                               &rng, rec || k + 1 == k_end ? cur.data() : nullptr, 1));
+        if (rec) HB_TRY(record(k + 1, cur.data()));
+    }
+    if (final_out) {
+        if (k_end == 0) HB_TRY(heat_history_snapshot(h, 0, cur.data()));
+        std::memcpy(final_out, cur.data(), N * sizeof(double));
+    }
+    if (n_snapshots) *n_snapshots = ns;
+    return HEAT_OK;
+}
+
 // Body of async_run after validation; also the small-N exact sync path
 // (q = 1 replays d = 0 for every read: bit-identical to sync_run).
 int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
@@ -444,6 +490,13 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
                    double* snapshots, size_t* steps_out, size_t max_snapshots,
                    size_t* n_snapshots) {
     if (stride == 0) stride = default_stride(N);
+    {
+        size_t upe = 1;
+        if (per_pe > 32 * 32 && per_pe % 32 != 0 && k3_units(per_pe, upe) != HEAT_OK)
+            return async_run_history(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
+                                     geometric_p, seed, k_end, stride, final_out, snapshots,
+                                     steps_out, max_snapshots, n_snapshots);
+    }
     if (async_small_eligible(N, per_pe, q))  // K9: one CTA, temporal-blocked rounds
         return async_run_small(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
                                geometric_p, seed, k_end, stride, final_out, snapshots, steps_out,

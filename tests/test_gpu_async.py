@@ -424,7 +424,18 @@ def test_wide_pes_off_the_32_grid_executors(H, port):
     assert bits_equal(res.field.values(), port.sync_run(u0, p.r(), 0, 1.0, 0.0, 300))
     rows = H.measure([100, 1000, 10000], [H.ExecMode.Barriered, H.ExecMode.BarrierFree], 3, 200, 4)
     assert len(rows) == 6 and all(r.median_ns > 0 for r in rows)
-    # a prime PE width above 1024 has no split into units
+    # a prime PE width above 1024 has no split into units: async_run takes the
+    # reference's own loop over a device HistoryRing (K8a/K8b); the free-running
+    # executor refuses it
+    u1 = random_field(SplitMix64(3), 2 * 1031)
+    for bc in (H.BoundaryCondition.periodic(), H.BoundaryCondition.dirichlet(u1[0], u1[-1])):
+        t = H.async_run(H.TemperatureField(u1), p, bc, H.PartitionSpec(2 * 1031, 1031),
+                        H.DelayModel.geometric(3, 0.4, 1), 40, 15)
+        steps, snaps = port.async_run(u1, p.r(), bc.kind, bc.c1, bc.c2, 1031, 2, 3, 0, 0.4,
+                                      seed=1, k_end=40, stride=15, record=True)
+        assert t.steps == steps
+        for j, s in enumerate(t.snapshots):
+            assert bits_equal(s.values(), snaps[j]), j
     with pytest.raises(H.InvalidArgument, match="no split"):
-        H.async_final(random_field(SplitMix64(3), 2 * 1031), p, H.BoundaryCondition.periodic(),
-                      H.PartitionSpec(2 * 1031, 1031), H.DelayModel.uniform(2, 1), 5)
+        H.exec_run(H.TemperatureField(u1), p, H.BoundaryCondition.periodic(),
+                   H.PartitionSpec(2 * 1031, 1031), H.ExecConfig(2, 5, H.ExecMode.BarrierFree))
