@@ -42,7 +42,6 @@ STEPS_PER_BENCH_STEP = 1000
 STEPS_PER_PASS = 32  # fallback; the library reports its kernel's (heat_sync_kernel_info)
 BYTES_PER_UPDATE = 16  # one FP64 read + one FP64 write per point per step
 FP64_OPS_PER_UPDATE = 4  # 2 DMUL + 2 DADD with the shared r*u products
-CPU_SAMPLE_STEPS = 32  # ~5 s timed (+ ~8 s of the API's own 8 GiB copies) per sample at N = 2^30
 
 
 def measured_peaks():
@@ -124,61 +123,111 @@ def dist_env():
 
 
 _CPU_FIELDS = {}
+REF_SAMPLE_STEPS = 16  # FTCS steps per CPU sample at N = 2^30 (~2.6 s on 16 host threads)
 
 
-def cpu_baseline_run(n: int, steps: int, warm: bool = True):
-    """The reference's exec_run(Barriered) on all host threads (oracle/_ref),
-    or the C port's threaded executor when the reference library is absent.
-    Returns (GLUPS, cores, kind, sample description)."""
+def _cpu_field(n):
     from oracle import oracle as O
-    port = O.port()
     u0 = _CPU_FIELDS.get(n)
     if u0 is None:  # 8 GiB at N = 2^30: built once per process, reused by every sample
-        u0 = port.sine_init(n)
+        u0 = O.port().sine_init(n)
         u0[0] = 0.0
         u0[-1] = 0.0
         _CPU_FIELDS[n] = u0
+    return u0
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def cpu_exec_samples(n, steps, reps, mode=0):
+    """The reference's exec_run (oracle/_ref; the C port's threaded executor when
+    the reference library is absent) on all host threads, `reps` calls on one
+    field.  Returns (list of GLUPS per call, workers, kind)."""
+    from oracle import oracle as O
+    u0 = _cpu_field(n)
     kind = "reference" if O.Ref.available() else "port"
-    eng = O.ref() if kind == "reference" else port
-    hw = os.cpu_count() or 1
-    if kind == "reference":
-        hw = eng.hardware_concurrency() or hw
+    eng = O.ref() if kind == "reference" else O.port()
+    hw = (eng.hardware_concurrency() if kind == "reference" else 0) or os.cpu_count() or 1
     workers = 1
     while workers * 2 <= hw and n % (workers * 2) == 0:
         workers *= 2
     if kind == "reference":
-        fin, dur, _ = eng.exec_run(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
-                                   O.BARRIERED)
+        durs, _ = eng.exec_run_reps(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
+                                    mode, reps)
     else:
-        fin, dur = eng.exec_run(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
-                                O.BARRIERED)
-    glups = n * steps / (dur * 1e-9) / 1e9
-    sample = (f"N=2^{n.bit_length() - 1} FP64, {steps} FTCS steps, exec_run(Barriered) with P={workers} "
-              f"threads; time = exec_run's own duration (thread spawn..join, async_exec.cpp:101-106)")
-    return glups, workers, kind, sample
+        durs = [eng.exec_run(u0, R, O.DIRICHLET, 0.0, 0.0, n // workers, workers, steps,
+                             O.BARRIERED if mode == 0 else O.BARRIER_FREE)[1]
+                for _ in range(reps)]
+    return [n * steps / (d * 1e-9) / 1e9 for d in durs], workers, kind
+
+
+def cpu_baseline_b200_arm(n):
+    """BASELINE.md §3 on the GPU box's host: exec_run(Barriered) on all host
+    threads (the value, median of 3), exec_run(BarrierFree) (median of 3), and
+    the single-core detail::sync_step_into loop."""
+    from oracle import oracle as O
+    vals, workers, kind = cpu_exec_samples(n, REF_SAMPLE_STEPS, 3, 0)
+    free, _, _ = cpu_exec_samples(n, REF_SAMPLE_STEPS, 3, 1)
+    one = None
+    if kind == "reference":
+        k1 = 2
+        _, ns = O.ref().sync_step_into_loop(_cpu_field(n), R, O.DIRICHLET, 0.0, 0.0, k1)
+        one = round(n * k1 / (ns * 1e-9) / 1e9, 4)
+    return {
+        "value": round(statistics.median(vals), 4), "unit": UNIT, "cores": workers, "kind": kind,
+        "sample": (f"N=2^{n.bit_length() - 1} FP64, {REF_SAMPLE_STEPS} FTCS steps per sample, "
+                   f"exec_run(Barriered) with P={workers} threads, median of 3 samples "
+                   f"{[round(v, 3) for v in vals]}; time = exec_run's own duration (thread "
+                   f"spawn..join, async_exec.cpp:101-106)"),
+        "barrier_free": {"value": round(statistics.median(free), 4), "unit": UNIT,
+                         "cores": workers, "samples": [round(v, 3) for v in free],
+                         "what": "exec_run(BarrierFree), same N/P/steps (async_exec.cpp:156-259)"},
+        "sync_step_into_1core": {"value": one, "unit": UNIT, "cores": 1,
+                                 "what": f"detail::sync_step_into loop, 2 steps at N=2^{n.bit_length() - 1} "
+                                         "(sync_solver.hpp:26-39)"},
+        **cpu_info(),
+    }
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the reference's own exec_run(Barriered) (oracle/_ref,
+    compiled from /root/reference) on all host threads, rank 0 only.  One
+    bench step = one exec_run call of REF_SAMPLE_STEPS FTCS steps at N = 2^30,
+    timed by the reference's own duration; ms_per_step is that measured time.
+    One untimed warm-up call (page first touch) stands in for --warmup: the CPU
+    path has no clocks or caches to warm beyond it."""
     if rank != 0:
         return 0
     n = N_PER_GPU
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        g, cores, kind, sample = cpu_baseline_run(n, CPU_SAMPLE_STEPS)
-        if i >= args.warmup:
-            vals.append(g)
-        info = (cores, kind, sample)
+    warm = min(1, args.warmup)
+    vals, workers, kind = cpu_exec_samples(n, REF_SAMPLE_STEPS, warm + args.steps, 0)
+    vals = vals[warm:]
     v = statistics.median(vals)
-    ms = n * CPU_SAMPLE_STEPS / (v * 1e9) * 1e3 * (STEPS_PER_BENCH_STEP / CPU_SAMPLE_STEPS)
+    ms = n * REF_SAMPLE_STEPS / (v * 1e9) * 1e3
+    cfg = config_dict(world, impl="reference", steps=args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (sine IC)",
-        "config": config_dict(world),
-        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": info[0], "kind": info[1],
-                         "sample": info[2] + f"; median of {args.steps} samples"},
+        "config": cfg,
+        "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": workers, "kind": kind,
+                         "sample": (f"N=2^30 FP64, {REF_SAMPLE_STEPS} FTCS steps per bench step, "
+                                    f"exec_run(Barriered) with P={workers} threads; time = "
+                                    f"exec_run's own duration; median of {args.steps} measured "
+                                    f"calls after {warm} warm-up call"),
+                         **cpu_info()},
         "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -240,23 +289,32 @@ def points_per_gpu(args, world):
     return N_STRONG_TOTAL // world if getattr(args, "strong", False) else N_PER_GPU
 
 
-def config_dict(world, n=N_PER_GPU, strong=False):
+def config_dict(world, n=N_PER_GPU, strong=False, impl="b200", steps=10):
     if strong:
         work = (f"cfg4: N=2^33 FP64 in total ({n} points per GPU), r=0.4, Dirichlet(0,0), "
                 f"sine IC, 1000-step bench steps; strong scaling over {world} GPU(s)")
+    elif impl == "reference":
+        work = (f"cfg3: N=2^30 FP64, r=0.4, Dirichlet(0,0), sine IC; each bench step is a "
+                f"bounded sample of {REF_SAMPLE_STEPS} FTCS steps (the cfg3 run is 10^4)")
     else:
-        work = ("cfg3: N=2^30 FP64 per GPU, r=0.4, Dirichlet(0,0), sine IC, "
-                "10^4 FTCS steps (= 10 bench steps of 1000)" +
+        work = (f"cfg3: N=2^30 FP64 per GPU, r=0.4, Dirichlet(0,0), sine IC; {steps} bench steps "
+                f"of 1000 FTCS steps = {steps * 1000} steps timed (cfg3 is 10^4)" +
                 ("" if world == 1 else f"; {world}-GPU slab decomposition, N=2^30*{world}"))
-    return {
+    d = {
         "workload": work,
         "N_per_gpu": n, "N_total": n * world, "r": R,
-        "time_steps_per_bench_step": STEPS_PER_BENCH_STEP, "steps_per_pass": (steps_per_pass() if world == 1
-                           else min(steps_per_pass(), slab_halo())),
-        "kernel": sync_kernel_name(),
+        "time_steps_per_bench_step": REF_SAMPLE_STEPS if impl == "reference"
+        else STEPS_PER_BENCH_STEP,
         "l2": "inputs larger than L2 (8 GiB per array vs 126 MB L2)",
-        "parallelism": "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)",
     }
+    if impl == "reference":  # nothing of the GPU library is loaded on this arm
+        d["kernel"] = "reference exec_run(Barriered), std::barrier per step, host threads"
+        d["parallelism"] = "host threads"
+        return d
+    d["steps_per_pass"] = steps_per_pass() if world == 1 else min(steps_per_pass(), slab_halo())
+    d["kernel"] = sync_kernel_name()
+    d["parallelism"] = "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)"
+    return d
 
 
 def run_b200(args, rank, world, local):
@@ -300,6 +358,14 @@ def run_b200(args, rank, world, local):
         advance(STEPS_PER_BENCH_STEP)
     plan.synchronize()
     barrier()
+    # parity of the timed run: light-cone windows of the field as it enters
+    # the timed region, checked against the oracle after it (outside the timing)
+    chk = None
+    if world == 1 and not args.skip_parity:
+        from oracle.lightcone import WindowCheck
+        chk = WindowCheck(n, STEPS_PER_BENCH_STEP * args.steps, sync_centres(n))
+        chk.capture(plan.download_range)
+        torch.cuda.synchronize()
 
     launches0 = H.kernel_launches()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -314,6 +380,13 @@ def run_b200(args, rank, world, local):
     plan.synchronize()
     launches = H.kernel_launches() - launches0
     ms = e0.elapsed_time(e1)
+    parity = {}
+    if chk is not None:
+        from oracle import oracle as O
+        port = O.port()
+        kk = STEPS_PER_BENCH_STEP * args.steps
+        parity["sync"] = chk.verify(plan.download_range,
+                                    lambda w, lo: port.sync_window(w, lo, n, r, 0.0, 0.0, kk))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -322,34 +395,45 @@ def run_b200(args, rank, world, local):
     glups = total_updates / (ms * 1e-3) / 1e9
 
     # Roofline of the dominant kernel (sync_tb_kernel, one launch per pass of
-    # <= steps_per_pass() steps, e.g. 31 passes of 32 + one of 8 per 1000 steps).
-    # achieved = algorithmic bytes of all its launches / their device time;
-    # the timed region is nothing but those back-to-back launches.
-    # multi-GPU slabs exchange heat_slab_halo() ghosts: passes of at most as many steps
+    # <= steps_per_pass() steps: 15 passes of 64 + one of 40 per 1000 steps).
+    # The timed region is nothing but those back-to-back launches, so the
+    # average launch duration is the timed region / launches.  With 64-step
+    # temporal blocking a pass moves 0.25 B per lattice update through HBM;
+    # the bound is the FP64 pipe (4 DP instructions per update: 2 DMUL +
+    # 2 DADD with the shared r*u products), reported as the headline, and the
+    # 16 B/update effective bandwidth beside it.
     spp = steps_per_pass() if world == 1 else min(steps_per_pass(), slab_halo())
     passes_per_step = -(-STEPS_PER_BENCH_STEP // spp)
     sync_launches = passes_per_step * args.steps
     per_launch_s = ms * 1e-3 / sync_launches
-    alg_bytes_total = BYTES_PER_UPDATE * float(n) * STEPS_PER_BENCH_STEP * args.steps
-    alg_bytes = alg_bytes_total / sync_launches  # per launch (average)
+    updates = float(n) * STEPS_PER_BENCH_STEP * args.steps
+    alg_bytes = BYTES_PER_UPDATE * updates / sync_launches  # per launch (average)
+    alg_ops = FP64_OPS_PER_UPDATE * updates / sync_launches
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / per_launch_s / 1e9
-    fp64_peak = 148 * 64 * 1.965e9 / 1e12  # DP lanes x SMs x boost clock, T ops/s (nominal)
-    fp64_achieved = FP64_OPS_PER_UPDATE * float(n) * STEPS_PER_BENCH_STEP * args.steps / (
-        ms * 1e-3) / 1e12
+    clk_mhz = clk.summary()["sm_mhz"] or 1965.0
+    fp64_peak = 148 * 64 * 1.965e9 / 1e12  # SMs x FP64 lanes x max SM clock (T DP ops/s)
+    fp64_achieved = alg_ops / per_launch_s / 1e12
+    traffic = ncu_traffic_per_launch()
     roofline = {
-        "bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-        "frac": round(achieved / peak, 4),
-        # the capture is one pass over 2^30 points; DRAM bytes scale with the points
-        "traffic": (None if ncu_traffic_per_launch() is None
-                    else ncu_traffic_per_launch() * n / N_PER_GPU),
-        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-        "algorithmic_bytes_per_launch": alg_bytes,
-        "note": "effective bandwidth with temporal blocking (16 B/update counted for every "
-                "step); the pass itself is FP64-pipe bound, see fp64",
-        "fp64": {"ops_per_update": FP64_OPS_PER_UPDATE, "achieved_tops": round(fp64_achieved, 3),
-                 "peak_tops_nominal": round(fp64_peak, 3),
-                 "frac": round(fp64_achieved / fp64_peak, 4)},
+        "bound": "fp64", "achieved": round(fp64_achieved, 3), "peak": round(fp64_peak, 3),
+        "unit": "TFLOP/s", "frac": round(fp64_achieved / fp64_peak, 4),
+        # ncu DRAM bytes of one 64-step pass over 2^30 points (scales with the points)
+        "traffic": None if traffic is None else traffic * n / N_PER_GPU,
+        "peak_source": ("nominal 148 SMs x 64 FP64 lanes x 1965 MHz (MEASURED_PEAKS.json has no "
+                        "FP64 figure; tools/fp64_micro.cu measured 18.55 T DMUL/DADD per s)"),
+        "ops_per_update": FP64_OPS_PER_UPDATE,
+        "algorithmic_ops_per_launch": alg_ops,
+        "launch_ms": round(per_launch_s * 1e3, 3),
+        "frac_at_measured_clock": round(fp64_achieved / (148 * 64 * clk_mhz * 1e6 / 1e12), 4),
+        "hbm": {"achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                "algorithmic_bytes_per_launch": alg_bytes,
+                "dram_bytes_per_launch": None if traffic is None else traffic * n / N_PER_GPU,
+                "note": "16 B per lattice update counted for every step (BASELINE.md §2): the "
+                        "effective bandwidth temporal blocking buys; physical DRAM traffic is "
+                        "one read + one write of the field per 64-step pass"},
     }
 
     # Asynchronous scheme on the same workload (single GPU): K5 streaming
@@ -357,7 +441,7 @@ def run_b200(args, rank, world, local):
     # deterministic replay of a seeded q=2 stream.
     async_info = None
     if world == 1 and not args.skip_async:
-        async_info = run_async(args, H, torch, plan, stream, n, r, bc, glups)
+        async_info = run_async(args, H, torch, plan, stream, n, r, bc, glups, parity)
     elif world > 1 and not args.skip_async:
         try:
             async_info = run_async_multi(args, H, MG, torch, stream, n, r, bc, glups, rank, world,
@@ -368,13 +452,11 @@ def run_b200(args, rank, world, local):
     # End to end through the public API with host buffers (copies timed).
     e2e = None
     if not args.skip_e2e:
-        e2e = run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance)
+        e2e = run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance, parity)
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        g, cores, kind, sample = cpu_baseline_run(n, CPU_SAMPLE_STEPS)
-        cpu = {"value": round(g, 4), "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": sample}
+        cpu = cpu_baseline_b200_arm(n)
 
     paper = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -389,7 +471,8 @@ def run_b200(args, rank, world, local):
         "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (sine IC generated on device)",
-        "config": config_dict(world, n, args.strong),
+        "config": config_dict(world, n, args.strong, steps=args.steps),
+        "parity": parity_summary(parity) if parity else None,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk.summary(), "async": async_info, "paper_configs": paper,
     }
@@ -451,7 +534,40 @@ def run_paper_configs(H):
 ASYNC_PES = 512  # 2^21 points per PE at N = 2^30
 
 
-def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
+def sync_centres(n):
+    """Points the parity leg checks: both ends, the points next to them, the
+    middle, K1 tile boundaries (1408 exact points per tile, tiles start at 0),
+    K5 PE boundaries (2^21 points) and a few seeded random points."""
+    rng = np.random.default_rng(12345)
+    c = [1, 2, n // 2 - 1, n // 2, 1408 * 1000, 1408 * 1000 - 1, 1408 * 381301,
+         (n // ASYNC_PES) * 7, (n // ASYNC_PES) * 7 - 1, n - 3, n - 2]
+    c += [int(x) for x in rng.integers(0, n, 6)]
+    return c
+
+
+def async_centres(n):
+    pe = n // ASYNC_PES
+    rng = np.random.default_rng(54321)
+    c = [1, pe - 1, pe, 100 * pe - 1, 100 * pe, (ASYNC_PES // 2) * pe, n - pe - 1, n - pe,
+         n - 2]
+    c += [int(x) for x in rng.integers(0, n, 3)]
+    return c
+
+
+def parity_summary(parity):
+    out = {k: bool(v["ok"]) for k, v in parity.items()}
+    out["points"] = {k: int(v["points"]) for k, v in parity.items()}
+    out["windows"] = {k: int(v["windows"]) for k, v in parity.items()}
+    bad = {k: v["bad"] for k, v in parity.items() if v["bad"]}
+    if bad:
+        out["bad"] = bad
+    out["oracle"] = ("oracle/heat_oracle.c orc_sync_window / orc_async_window: light-cone windows "
+                     "of the field entering the timed region, every point > k from a held window "
+                     "end compared bit for bit (SURVEY §8c)")
+    return out
+
+
+def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups, parity):
     """Async vs sync on the cfg3 workload: same steps, device-timed."""
     per_pe = n // ASYNC_PES
     out = {"pes": ASYNC_PES, "points_per_pe": per_pe,
@@ -468,6 +584,12 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
             call()
         plan.synchronize()
         torch.cuda.synchronize()
+        chk = None
+        if name == "deterministic" and not args.skip_parity:
+            from oracle.lightcone import WindowCheck
+            chk = WindowCheck(n, STEPS_PER_BENCH_STEP * args.steps, async_centres(n))
+            chk.capture(plan.download_range)
+            torch.cuda.synchronize()
         e0.record(stream)
         stats = [call() for _ in range(args.steps)]
         e1.record(stream)
@@ -475,6 +597,16 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups):
         ms = e0.elapsed_time(e1)
         v = float(n) * STEPS_PER_BENCH_STEP * args.steps / (ms * 1e-3) / 1e9
         st = stats[-1]
+        if chk is not None:
+            from oracle import oracle as O
+            port = O.port()
+
+            def replay(w, lo):  # each bench step is a fresh run: k from 0, stream restarted
+                for _ in range(args.steps):
+                    w = port.async_window(w, lo, n, r, 0.0, 0.0, per_pe, O.UNIFORM, 2, seed=1,
+                                          k=STEPS_PER_BENCH_STEP)
+                return w
+            parity["async_det"] = chk.verify(plan.download_range, replay)
         out[name] = {
             "value": round(v, 3), "unit": UNIT, "ms_per_step": round(ms / args.steps, 3),
             "q": 8 if name == "free" else 2,
@@ -524,7 +656,7 @@ def run_async_multi(args, H, MG, torch, stream, n, r, bc, sync_glups, rank, worl
     return out
 
 
-def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance):
+def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance, parity):
     """Same metric through the public API with HOST buffers: per step the
     pinned host field goes H2D, 1000 FTCS steps run, the result comes back D2H."""
     k = max(1, min(args.steps, 3))
@@ -551,6 +683,15 @@ def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance):
             t1 = time.perf_counter()
         if i > 0:
             times.append(t1 - t0)
+    if world == 1 and not args.skip_parity:  # the last call's output against its input
+        from oracle import oracle as O
+        from oracle.lightcone import WindowCheck
+        port = O.port()
+        chk = WindowCheck(n, STEPS_PER_BENCH_STEP, sync_centres(n))
+        chk.capture(lambda lo, c: a_in[lo:lo + c])
+        parity["e2e"] = chk.verify(
+            lambda lo, c: a_out[lo:lo + c],
+            lambda w, lo: port.sync_window(w, lo, n, r, 0.0, 0.0, STEPS_PER_BENCH_STEP))
     t = statistics.median(times)
     if world > 1:
         import torch.distributed as dist
@@ -573,6 +714,8 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-async", action="store_true")
+    ap.add_argument("--skip-parity", action="store_true",
+                    help="do not check the timed runs against the oracle's light cones")
     ap.add_argument("--strong", action="store_true",
                     help="cfg4: N = 2^33 in total split over the GPUs (no host-buffer legs)")
     args = ap.parse_args()

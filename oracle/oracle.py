@@ -112,6 +112,9 @@ class Port(_Lib):
         L.orc_sync_lightcone.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd]
         L.orc_async_lightcone.argtypes = [_pd, _sz, _sz, _sz, _d, _d, _d, _sz, _i, _sz, _sz, _d,
                                           C.c_uint64, _sz, _sz, _pd]
+        L.orc_sync_window.argtypes = [_pd, _sz, _sz, _sz, _d, _d, _d, _sz]
+        L.orc_async_window.argtypes = [_pd, _sz, _sz, _sz, _d, _d, _d, _sz, _i, _sz, _sz, _d,
+                                       C.c_uint64, _sz]
         L.orc_sync_step_into.argtypes = [_pd, _pd, _sz, _d, _i, _d, _d]
         L.orc_sync_step_into.restype = None
         L.orc_async_step.argtypes = [_pd, _sz, _sz, _sz, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz,
@@ -251,6 +254,27 @@ class Port(_Lib):
             raise OracleError(st, "sync_lightcone")
         return v.value
 
+    def sync_window(self, win, lo, n, r, c1, c2, k) -> np.ndarray:
+        """The window win = u[lo : lo + len(win)] of an n-point Dirichlet run
+        advanced k steps with held window ends (heat_oracle.c orc_sync_window);
+        points more than k from a held end are exact."""
+        a = np.array(win, dtype=np.float64, copy=True)
+        st = self.lib.orc_sync_window(_ptr(a), a.size, lo, n, r, c1, c2, k)
+        if st:
+            raise OracleError(st, "sync_window")
+        return a
+
+    def async_window(self, win, lo, n, r, c1, c2, per_pe, law, q, fixed_d=0, p=0.5, seed=0,
+                     k=1) -> np.ndarray:
+        """orc_async_window: the deterministic asynchronous run of k steps from
+        step 0 on a window with held ends."""
+        a = np.array(win, dtype=np.float64, copy=True)
+        st = self.lib.orc_async_window(_ptr(a), a.size, lo, n, r, c1, c2, per_pe, law, q, fixed_d,
+                                       p, seed & 0xFFFFFFFFFFFFFFFF, k)
+        if st:
+            raise OracleError(st, "async_window")
+        return a
+
     def async_lightcone(self, win, lo, n, r, c1, c2, per_pe, law, q, fixed_d=0, p=0.5, seed=0,
                         k=1, centre=0) -> float:
         """u(k)[centre] of the deterministic async run (Dirichlet) from the window
@@ -288,6 +312,8 @@ class Ref(_Lib):
                                     _pd, _pd, _psz, _sz, _psz]
         L.ref_delay_stream.argtypes = [_i, _sz, _sz, _d, _u64, _sz, _sz, _pu64]
         L.ref_exec_run.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _i, _pd, _pu64, _pu64]
+        L.ref_exec_run_reps.argtypes = [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _i, _sz, _pu64,
+                                         _pd]
         L.ref_sync_step_into_loop.argtypes = [_pd, _pd, _sz, _d, _i, _d, _d, _sz]
         L.ref_sync_step_into_loop.restype = _u64
         L.ref_prepare_initial.argtypes = [_pd, _sz, _i, _d, _d, _pd]
@@ -436,6 +462,18 @@ class Ref(_Lib):
         if st:
             raise OracleError(st, "exec_run")
         return fin, int(dur.value), lag
+
+    def exec_run_reps(self, u0, r, bc, c1, c2, per_pe, workers, k_end, mode, reps,
+                      want_final=False):
+        """exec_run called `reps` times on one field: (durations_ns list, final or None)."""
+        u0 = _f64(u0)
+        durs = np.zeros(reps, np.uint64)
+        fin = np.empty(u0.size, np.float64) if want_final else None
+        st = self.lib.ref_exec_run_reps(_ptr(u0), u0.size, r, bc, c1, c2, per_pe, workers, k_end,
+                                        mode, reps, _ptr(durs, _pu64), _ptr(fin))
+        if st:
+            raise OracleError(st, "exec_run")
+        return [int(x) for x in durs], fin
 
     def sync_step_into_loop(self, u_prepared, r, bc, c1, c2, k):
         """Runs detail::sync_step_into k times; returns (field, loop_ns)."""

@@ -228,6 +228,35 @@ int ref_exec_run(const double* u0, std::size_t n, double r, int bc, double c1, d
     }
 }
 
+// exec_run repeated `reps` times on ONE TemperatureField (built once from the
+// caller's buffer), each call's own duration (thread spawn..join,
+// async_exec.cpp:101-106 / 227-231) into durations_ns[rep]; the last call's
+// field goes to final_out (may be null).  The bench's CPU baseline at
+// N = 2^30: it saves the shim's per-call 8 GiB field copies, not the
+// reference's own (prepare_initial, the result field).
+int ref_exec_run_reps(const double* u0, std::size_t n, double r, int bc, double c1, double c2,
+                      std::size_t per_pe, std::size_t workers, std::size_t k_end, int mode,
+                      std::size_t reps, std::uint64_t* durations_ns, double* final_out) {
+    try {
+        heat::TemperatureField f(std::vector<double>(u0, u0 + n));
+        heat::ExecConfig cfg{workers, k_end,
+                             mode == 0 ? heat::ExecMode::Barriered : heat::ExecMode::BarrierFree,
+                             false};
+        const auto params = heat::SolverParams::from_r(r, true);
+        const auto bcv = make_bc(bc, c1, c2);
+        const heat::PartitionSpec part(n, per_pe);
+        for (std::size_t i = 0; i < reps; ++i) {
+            heat::ExecResult res = heat::exec_run(f, params, bcv, part, cfg);
+            durations_ns[i] = std::uint64_t(res.duration.count());
+            if (final_out && i + 1 == reps)
+                std::memcpy(final_out, res.field.values().data(), n * sizeof(double));
+        }
+        return 0;
+    } catch (...) {
+        return classify();
+    }
+}
+
 // detail::sync_step_into loop (sync_solver.hpp:26-39) in place on caller buffers:
 // the single-core CPU baseline.  `a` holds u(0) (already prepared) and receives
 // u(k); `b` is scratch of the same size.  Returns elapsed ns of the loop.

@@ -167,11 +167,16 @@ int launch_pe(int V, bool shared, bool barrier, const AsyncPeArgs& a, int P, cud
 // most 1024 points (the smallest such split).  The edges between units of
 // one PE read the neighbour's value of the same step (kUnitEdge), so the PE
 // stays synchronous inside; PE edges keep their draw ranks.
-int k3_units(size_t n, size_t& upe) {
+// The smallest split of a PE of n points into equal units of <= 1024 points;
+// false when there is none (no side effects: a probe).
+bool k3_split(size_t n, size_t& upe) {
     upe = 1;
-    if (n <= 32 * 32) return HEAT_OK;
+    if (n <= 32 * 32) return true;
     for (upe = 2; upe <= n && (n % upe != 0 || n / upe > 32 * 32); ++upe) {}
-    if (upe > n || n / upe < 2)
+    return !(upe > n || n / upe < 2);
+}
+int k3_units(size_t n, size_t& upe) {
+    if (!k3_split(n, upe))
         return fail(HEAT_EINVAL, "async: a PE of this width has no split into units of <= 1024 "
                                  "points");
     return HEAT_OK;
@@ -476,6 +481,12 @@ int async_run_history(const double* u0, size_t N, double r, int bc_kind, double 
     }
     if (final_out) {
         if (k_end == 0) HB_TRY(heat_history_snapshot(h, 0, cur.data()));
+        // the reference records the final step as a TemperatureField
+        // (async_sim.cpp:150-158), whose ctor rejects non-finite values
+        if (!want)
+            for (size_t i = 0; i < N; ++i)
+                if (!std::isfinite(cur[i]))
+                    return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
         std::memcpy(final_out, cur.data(), N * sizeof(double));
     }
     if (n_snapshots) *n_snapshots = ns;
@@ -492,7 +503,7 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
     if (stride == 0) stride = default_stride(N);
     {
         size_t upe = 1;
-        if (per_pe > 32 * 32 && per_pe % 32 != 0 && k3_units(per_pe, upe) != HEAT_OK)
+        if (per_pe > 32 * 32 && per_pe % 32 != 0 && !k3_split(per_pe, upe))
             return async_run_history(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
                                      geometric_p, seed, k_end, stride, final_out, snapshots,
                                      steps_out, max_snapshots, n_snapshots);
@@ -638,18 +649,11 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     if (sync_path) {
         // Barriered is bit-identical to sync_run (acceptance.cpp:225-229); so is
         // BarrierFree with one PE (test_exec.cpp:69-87).
-        cudaEvent_t e0, e1;
-        HB_CUDA(cudaEventCreate(&e0));
-        HB_CUDA(cudaEventCreate(&e1));
-        HB_CUDA(cudaEventRecord(e0, d->stream));
-        int st = heat_sync_run(u0, N, r, bc_kind, c1, c2, k_end, k_end, field_out, nullptr,
-                               nullptr, 0, nullptr);
-        HB_CUDA(cudaEventRecord(e1, d->stream));
-        HB_CUDA(cudaEventSynchronize(e1));
+        // Timed like the BarrierFree kernels below: the compute launches'
+        // device time only, not the staging and copies around them (the
+        // reference's duration brackets the workers, async_exec.cpp:101-106).
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        int st = sync_run_timed(u0, N, r, bc_kind, c1, c2, k_end, field_out, &ms);
         if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
         if (lag) std::memset(lag, 0, sizeof *lag);
         if (stats) std::memset(stats, 0, sizeof *stats);

@@ -61,6 +61,33 @@ extern std::atomic<bool> g_strict;
         if (s_ != HEAT_OK) return s_; \
     } while (0)
 
+// A pair of timing events on one stream (destroyed with the pair).
+struct EventPair {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    EventPair() = default;
+    EventPair(const EventPair&) = delete;
+    EventPair& operator=(const EventPair&) = delete;
+    ~EventPair() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+    int begin(cudaStream_t st) {
+        if (!e0) HB_CUDA(cudaEventCreate(&e0));
+        if (!e1) HB_CUDA(cudaEventCreate(&e1));
+        HB_CUDA(cudaEventRecord(e0, st));
+        return HEAT_OK;
+    }
+    int end(cudaStream_t st) {
+        HB_CUDA(cudaEventRecord(e1, st));
+        return HEAT_OK;
+    }
+    int elapsed(float* ms) {
+        HB_CUDA(cudaEventSynchronize(e1));
+        HB_CUDA(cudaEventElapsedTime(ms, e0, e1));
+        return HEAT_OK;
+    }
+};
+
 // Flag words of a context (DevCtx / plan): [0] non-finite, [1] watchdog,
 // [2] input validation, [3] spare, [4..5] the K1 tile counter (u64) of the
 // context's stream, [6..7] that of its second compute stream (the streamed
@@ -191,7 +218,13 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
 size_t sync_small_max_points();
 int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                    size_t k_end, size_t stride, double* final_out, double* snapshots,
-                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots);
+                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots,
+                   float* kernel_ms = nullptr);
+// exec_run(Barriered) (async_exec.cpp:57-114): sync_run to the final state
+// with the compute kernels' device time (events on the run's stream around
+// the launches only -- the bracket BarrierFree's kernels are timed over).
+int sync_run_timed(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                   size_t k_end, double* final_out, float* kernel_ms);
 
 // Synchronous advance on device buffers (ping-pong).  `cur` selects the
 // buffer holding u(k) on entry and is updated.  Does not synchronise.

@@ -595,7 +595,8 @@ int sync_run_overlapped(DevCtx& d, double** bufs, size_t n, double r, int period
 template <typename Real>
 int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                   size_t k_end, size_t stride, double* final_out, double* snapshots,
-                  size_t* steps_out, size_t max_snapshots, size_t* n_snapshots) {
+                  size_t* steps_out, size_t max_snapshots, size_t* n_snapshots,
+                  float* kernel_ms = nullptr) {
     if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
     if (!u0) return fail(HEAT_EINVAL, "null field pointer");
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
@@ -605,7 +606,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     if (sizeof(Real) == 8 && n <= sync_small_max_points() && !std::getenv("HEAT_NO_SMALL_SYNC"))
         return sync_run_small(reinterpret_cast<const double*>(u0), n, r, bc_kind, c1, c2, k_end,
                               stride, final_out, snapshots, steps_out, max_snapshots,
-                              n_snapshots);
+                              n_snapshots, kernel_ms);
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
@@ -619,7 +620,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
         n >= kStreamMinPoints && k_end > 0 &&
         (k_end + sync_variant_entry<double>().halo - 1) / sync_variant_entry<double>().halo <=
             kStreamMaxPasses &&
-        std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9 &&
+        std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9 && !kernel_ms &&
         !std::getenv("HEAT_NO_STREAMED_SYNC"))
         return sync_run_streamed(*d, reinterpret_cast<const double*>(u0), n, r, c1, c2, k_end,
                                  final_out);
@@ -664,7 +665,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     int cur = 0;
     size_t k = 0;
     const int periodic = bc_kind == HEAT_BC_PERIODIC;
-    if (!f32 && snapshots && n >= kOverlapSnapPoints && max_snapshots > 0 &&
+    if (!f32 && snapshots && n >= kOverlapSnapPoints && max_snapshots > 0 && !kernel_ms &&
         !std::getenv("HEAT_NO_OVERLAP_SNAPS"))
         return sync_run_overlapped(*d, reinterpret_cast<double**>(bufs), n, r, periodic, c1, c2,
                                    k_end, stride, final_out, snapshots, steps_out, max_snapshots,
@@ -674,12 +675,20 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     while (k < k_end) {
         // advance to the next recorded step (or straight to k_end)
         size_t next = want_snaps ? std::min(k_end, (k / stride + 1) * stride) : k_end;
+        EventPair ev;
+        if (kernel_ms) HB_TRY(ev.begin(st));
         HB_TRY(sync_advance<Real>(d->sms, bufs, cur, (long long)n, r, periodic, c1, c2, next - k,
                                   d->flag, st));
+        if (kernel_ms) HB_TRY(ev.end(st));
         k = next;
         unsigned int flags[2] = {0, 0};
         HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
         HB_CUDA(cudaStreamSynchronize(st));
+        if (kernel_ms) {
+            float seg = 0.f;
+            HB_TRY(ev.elapsed(&seg));
+            *kernel_ms += seg;
+        }
         if (flags[0]) {
             if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");
             return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
@@ -696,6 +705,15 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
 }  // namespace hb
 
 using namespace hb;
+
+namespace hb {
+int sync_run_timed(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                   size_t k_end, double* final_out, float* kernel_ms) {
+    *kernel_ms = 0.f;
+    return sync_run_impl<double>(u0, n, r, bc_kind, c1, c2, k_end, k_end, final_out, nullptr,
+                                 nullptr, 0, nullptr, kernel_ms);
+}
+}  // namespace hb
 
 extern "C" int heat_stream_chunk_plan(size_t n, size_t wave_points, size_t* bounds, size_t cap,
                                       size_t* count) {

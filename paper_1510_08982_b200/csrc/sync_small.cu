@@ -131,7 +131,8 @@ size_t sync_small_max_points() { return 16384; }
 // 2*stride, ..., k_end -- sync_solver.cpp:58-88).
 int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                    size_t k_end, size_t stride, double* final_out, double* snapshots,
-                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots) {
+                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots,
+                   float* kernel_ms) {
     if (stride == 0) stride = default_stride(n);
     const bool want = snapshots != nullptr || steps_out != nullptr;
     const size_t rows = want ? 2 + k_end / stride : 0;  // upper bound (k_end not a multiple)
@@ -208,12 +209,15 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
     };
+    EventPair ev;
+    if (kernel_ms) HB_TRY(ev.begin(st));
     if (V == 12)
         HB_TRY(launch(sync_small_kernel<12>, 12));
     else if (V == 8)
         HB_TRY(launch(sync_small_kernel<8>, 8));
     else
         HB_TRY(launch(sync_small_kernel<32>, 32));
+    if (kernel_ms) HB_TRY(ev.end(st));
     // results and flags in one round trip
     size_t ns = 0;
     std::vector<size_t> ks;
@@ -241,6 +245,7 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
         if (want && snapshots)
             std::memcpy(snapshots, hs + 64 + 2 * nb, std::min(ns, max_snapshots) * nb);
     }
+    if (kernel_ms) HB_TRY(ev.elapsed(kernel_ms));
     if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     if (flags[0]) {
         if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by step");

@@ -10,6 +10,7 @@
 // on the data path goes through the host or a collective, and no rank ever
 // waits for more than its two neighbours.
 #include <cstring>
+#include <memory>
 
 #include "stream_host.cuh"
 
@@ -38,7 +39,10 @@ int heat_plan_xlink_setup(heat_plan* p, size_t per_pe, size_t q, int bc_kind, vo
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     HB_CUDA(cudaSetDevice(p->device));
-    auto* x = new heat_xlink();
+    // a second setup replaces the first: close its IPC mappings before the
+    // scratch they point into is freed and re-exported
+    xlink_release(p);
+    std::unique_ptr<heat_xlink> x(new heat_xlink());  // owned until stored in p->xlink
     x->per_pe = per_pe;
     x->q = q;
     x->bc_kind = bc_kind;
@@ -50,11 +54,7 @@ int heat_plan_xlink_setup(heat_plan* p, size_t per_pe, size_t q, int bc_kind, vo
     const bool periodic = bc_kind == HEAT_BC_PERIODIC;
     x->ext.left = p->rank > 0 || periodic;
     x->ext.right = p->rank + 1 < p->world || periodic;
-    int st = stream_layout(x->spec, 1, x->ext, x->L, x->offL, x->offR);
-    if (st != HEAT_OK) {
-        delete x;
-        return st;
-    }
+    HB_TRY(stream_layout(x->spec, 1, x->ext, x->L, x->offL, x->offR));
     // the whole K5 scratch is one IPC-exportable allocation; peers address
     // its receive rings at the layout's offsets (identical on every rank)
     if (p->async_scratch) cudaFree(p->async_scratch);
@@ -70,8 +70,7 @@ int heat_plan_xlink_setup(heat_plan* p, size_t per_pe, size_t q, int bc_kind, vo
     cudaIpcMemHandle_t h;
     HB_CUDA(cudaIpcGetMemHandle(&h, p->async_scratch));
     std::memcpy(handle_out, &h, sizeof h);
-    if (p->xlink) delete static_cast<heat_xlink*>(p->xlink);
-    p->xlink = x;
+    p->xlink = x.release();
     return HEAT_OK;
 }
 

@@ -161,6 +161,12 @@ class AsyncSlabSolver:
 
     def advance(self, r: float, steps: int, model=None):
         """One fresh run of `steps` steps from the current field."""
+        # No neighbour may still be consuming the previous run when seeding
+        # rewrites its receive ring and resets its progress words: every rank
+        # drains its own stream, then all meet, then all seed.
+        self.plan.synchronize()
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
         self.plan.xlink_seed()  # push my step-0 edges into the neighbours' rings
         torch.cuda.synchronize()
         dist.barrier(group=self.group)
@@ -223,14 +229,27 @@ def ensemble_run_sharded(cfg, runs: int, base_seed: int, device: Optional[int] =
         def member_fn(c, count, first):
             return H.ensemble_run(c, count, first, keep_terminals=keep_terminals)
     start, end = rank * runs // world, (rank + 1) * runs // world
-    local = member_fn(cfg, end - start, base_seed + start) if end > start else None
-    mine = (start, local.steps if local else None,
-            [list(map(float, s)) for s in local.norm_series] if local else [],
-            [t.values() for t in local.terminal_fields] if (local and keep_terminals) else [])
-    parts = [mine]
+    # A failing shard (DivergenceError, OOM, ...) must not leave the other
+    # ranks blocked in the gather: every rank gathers (ok, payload) and the
+    # first error (in rank order) is re-raised on all of them.
+    try:
+        local = member_fn(cfg, end - start, base_seed + start) if end > start else None
+        mine = (True, (start, local.steps if local else None,
+                       [list(map(float, s)) for s in local.norm_series] if local else [],
+                       [t.values() for t in local.terminal_fields]
+                       if (local and keep_terminals) else []))
+    except Exception as exc:  # noqa: BLE001 -- re-raised below on every rank
+        if world == 1:
+            raise
+        mine = (False, exc)
+    gathered = [mine]
     if world > 1:
-        parts = [None] * world
-        dist.all_gather_object(parts, mine, group=group)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine, group=group)
+    for ok, payload in gathered:
+        if not ok:
+            raise payload
+    parts = [payload for _, payload in gathered]
     parts.sort(key=lambda x: x[0])
     steps = next(p[1] for p in parts if p[1] is not None)
     norms = [s for p in parts for s in p[2]]

@@ -164,3 +164,45 @@ def test_ensemble_sharded_bit_exact(world):
     assert np.array_equal(np.array(mean).view(np.uint64), np.asarray(e_mean).view(np.uint64))
     assert np.array_equal(np.array(std).view(np.uint64), np.asarray(e_std).view(np.uint64))
     assert np.array_equal(np.array(terms).view(np.uint64), e_terms.view(np.uint64))
+
+
+def _failing_members(cfg, count, first_seed):
+    from paper_1510_08982_b200 import heat as H
+    if first_seed != 1000:  # every rank but 0 fails, as a diverging shard would
+        raise H.DivergenceError(f"shard at seed {first_seed} diverged")
+    return _ref_members(cfg, count, first_seed)
+
+
+def _ens_fail_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1510_08982_b200 import heat as H
+        cfg = H.EnsembleConfig(H.cosine_init(100), H.SolverParams.from_r(0.45),
+                               H.BoundaryCondition.dirichlet(1.0, 0.0), H.PartitionSpec(100, 1),
+                               H.DelayModel.uniform(4, 0), k_end=50, stride=10)
+        try:
+            M.ensemble_run_sharded(cfg, 6, 1000, member_fn=_failing_members)
+            q.put((rank, None))
+        except Exception as exc:  # noqa: BLE001
+            q.put((rank, f"{type(exc).__name__}: {exc}"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ensemble_sharded_error_reaches_every_rank():
+    """ADVICE r1: one failing shard must not hang the others in the gather;
+    every rank re-raises the first failing rank's error."""
+    from oracle import oracle as O
+    if not O.Ref.available():
+        pytest.skip("reference library not built here")
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_ens_fail_worker, args=(world, _free_port(), q), nprocs=world, join=True,
+                       start_method="spawn")
+    got = sorted(q.get(timeout=60) for _ in range(world))
+    assert [r for r, _ in got] == [0, 1, 2]
+    for _, err in got:
+        assert err == "DivergenceError: shard at seed 1002 diverged", err

@@ -167,3 +167,23 @@ def test_async_lightcone_windows(port, law, q, fd, gp):
         got = port.async_lightcone(u0[lo:hi], lo, n, 0.4, 0.0, 0.0, per_pe, law, q, fd, gp,
                                    seed, k, c)
         assert got == full[c], (c, got, full[c])
+
+
+@pytest.mark.parametrize("seed", [3, 11])
+def test_window_runs_vs_reference(port, ref, seed):
+    """orc_sync_window / orc_async_window (the bench's at-scale checkers):
+    every point more than k from a held window end equals the reference's own
+    full sync_run / async_run; true domain ends are pinned."""
+    rng = np.random.default_rng(seed)
+    n, per_pe, k = 2048, 256, 200
+    u0 = random_field(SplitMix64(seed), n)
+    u0[0], u0[-1] = 0.0, 0.0
+    full_s = ref.sync_run(u0, 0.4, 0, 0.0, 0.0, k)
+    full_a = ref.async_run(u0, 0.4, 0, 0.0, 0.0, per_pe, 0, 3, seed=seed, k_end=k)
+    for lo, w in [(0, 700), (n - 600, 600), (int(rng.integers(1, n - 900)), 900)]:
+        a = 0 if lo == 0 else k + 1
+        b = w if lo + w == n else w - k - 1
+        got = port.sync_window(u0[lo:lo + w], lo, n, 0.4, 0.0, 0.0, k)
+        assert bits_equal(got[a:b], np.asarray(full_s)[lo + a:lo + b]), ("sync", lo, w)
+        got = port.async_window(u0[lo:lo + w], lo, n, 0.4, 0.0, 0.0, per_pe, 0, 3, seed=seed, k=k)
+        assert bits_equal(got[a:b], np.asarray(full_a)[lo + a:lo + b]), ("async", lo, w)
