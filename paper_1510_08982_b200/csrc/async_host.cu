@@ -661,13 +661,31 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
     }
 
     std::lock_guard<std::mutex> lock(d->mu);
+    const size_t qf = q_free ? q_free : 8;
+    if (!record_lag && free_eligible(N, per_pe, qf)) {
+        // K10: one warp per PE in one thread-block cluster, DSMEM edge rings
+        std::vector<unsigned long long> hs(kStatWords, 0);
+        float ms = 0.f;
+        HB_TRY(exec_free_run(*d, u0, N, r, bc_kind, c1, c2, per_pe, qf, k_end, field_out,
+                             stats ? hs.data() : nullptr, &ms));
+        if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
+        if (lag) std::memset(lag, 0, sizeof *lag);
+        if (stats) {
+            std::memset(stats, 0, sizeof *stats);
+            stats->reads = hs[kStatReads];
+            stats->waits = hs[kStatWaits];
+            stats->max_delay = hs[kStatMaxDelay];
+            for (int i = 0; i < 64; ++i) stats->delay_histogram[i] = hs[kStatDelayHist + i];
+        }
+        return HEAT_OK;
+    }
     const bool wide = per_pe > 32 * 32 && per_pe % 32 == 0;  // K5; else K3 (units)
     const size_t pitch = (N + 63) / 64 * 64;
     HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
     double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
     int cur = 0;
     HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, bufs[0]));
-    const size_t q = q_free ? q_free : 8;
+    const size_t q = qf;
     AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, k_end,
                    false};
     std::vector<unsigned long long> hs(kStatWords, 0);

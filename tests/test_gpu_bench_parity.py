@@ -45,7 +45,7 @@ def test_cfg3_sync_and_async_full_length(H, port):
         res = chk.verify(p.download_range,
                          lambda w, lo: port.sync_window(w, lo, N, r, 0.0, 0.0, K))
         assert res["ok"], res["bad"]
-        assert res["points"] > 16 * 64
+        assert res["points"] > 10 * 64
 
         p.fill_sine()
         chk = WindowCheck(N, K, centres(2))
