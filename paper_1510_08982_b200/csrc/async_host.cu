@@ -662,7 +662,7 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
 
     std::lock_guard<std::mutex> lock(d->mu);
     const size_t qf = q_free ? q_free : 8;
-    if (!record_lag && free_eligible(N, per_pe, qf)) {
+    if (!record_lag && free_eligible(N, per_pe, qf, k_end)) {
         // K10: one warp per PE in one thread-block cluster, DSMEM edge rings
         std::vector<unsigned long long> hs(kStatWords, 0);
         float ms = 0.f;

@@ -101,9 +101,22 @@ __device__ __forceinline__ double slot_value(const FreeSlot& s) {
     return __hiloint2double(int(uint32_t(s.hi)), int(uint32_t(s.lo)));
 }
 
+// The ghost product a PE's edge lane consumes at step k, resolved from the
+// two probes issued one step earlier (slot k and the slot after the newest
+// one seen, m+1), branch-free.
+__device__ __forceinline__ void resolve_ghost(const FreeSlot& s0, const FreeSlot& s1, int k,
+                                              int& m, double& pg) {
+    const bool h0 = slot_is(s0, uint32_t(k));
+    const bool h1 = slot_is(s1, uint32_t(m + 1));
+    const double x = h0 ? slot_value(s0) : slot_value(s1);
+    pg = (h0 || h1) ? x : pg;
+    m = h0 ? k : (h1 ? m + 1 : m);
+}
+
 template <int V, bool STATS>
 __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const FreeArgs a) {
     extern __shared__ __align__(16) FreeSlot rings[];  // [W][2 sides][kFreeR]
+    __shared__ unsigned int s_hist[kFreeMaxW * 2][kFreeMaxQ];  // STATS: one row per edge lane
     const int W = a.W;
     const uint32_t cta = cluster_ctarank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,6 +126,9 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
     // invalidate every slot of this CTA's rings (tag 0xffffffff = no step)
     for (int i = threadIdx.x; i < W * 2 * kFreeR; i += blockDim.x)
         rings[i] = FreeSlot{~0ull, ~0ull};
+    if (STATS)
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x)
+            (&s_hist[0][0])[i] = 0;
     cluster_sync_all();  // no producer may write a slot before its owner cleared it
 
     const double r = a.r, c = a.c;
@@ -120,25 +136,32 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
     const bool dir = a.dirichlet != 0;
     const int lpe = p > 0 ? p - 1 : (dir ? -1 : P - 1);
     const int rpe = p + 1 < P ? p + 1 : (dir ? -1 : 0);
+    const bool first_lane = lane == 0, last_lane = lane == Lc - 1;
     const bool needL = active && lpe >= 0;  // Dirichlet PE 0 / P-1 have a pinned end instead
     const bool needR = active && rpe >= 0;
-    const bool first_lane = lane == 0, last_lane = lane == Lc - 1;
     const bool pin_first = active && dir && p == 0 && first_lane;
     const bool pin_last = active && dir && p == P - 1 && last_lane;
 
-    // lane 0 reads ring side 0 (left neighbour's last point) and publishes its
-    // first point into the left neighbour's side-1 ring; lane Lc-1 mirrors it
+    // lane 0 reads ring side 0 (its left neighbour's last product) and
+    // publishes its own first product into the left neighbour's side-1 ring;
+    // lane Lc-1 mirrors it.  Every other lane probes its warp's ring too (a
+    // valid address) and ignores the result: no divergent branch per step.
     const bool edge = (first_lane && needL) || (last_lane && needR);
     const int side = first_lane ? 0 : 1;
     const int nb = first_lane ? lpe : rpe;
-    const uint32_t my_ring =
-        smem_u32(rings + ((size_t)(active ? w : 0) * 2 + side) * kFreeR);
+    const uint32_t my_ring = smem_u32(rings + ((size_t)(active ? w : 0) * 2 + side) * kFreeR);
     uint32_t peer_ring = 0;
     if (edge) {
         const int nb_cta = nb / W, nb_w = nb % W;
         const uint32_t local = smem_u32(rings + ((size_t)nb_w * 2 + (1 - side)) * kFreeR);
         peer_ring = map_cluster(local, uint32_t(nb_cta));
     }
+    auto slot_addr = [&](uint32_t base, int k) { return base + uint32_t(k & (kFreeR - 1)) * 16u; };
+    auto publish = [&](int k, double prod) {
+        if (edge)
+            st_cluster_slot(slot_addr(peer_ring, k), pack_half(uint32_t(k), uint32_t(__double2loint(prod))),
+                            pack_half(uint32_t(k), uint32_t(__double2hiint(prod))));
+    };
 
     double u[V];
     const long long base = (long long)p * n + (long long)lane * V;
@@ -147,84 +170,101 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
     if (pin_first) u[0] = a.c1;  // prepare_initial snapped them already; keep exact
     if (pin_last) u[V - 1] = a.c2;
 
-    // step-0 edge values
-    if (edge) {
-        const double v = first_lane ? u[0] : u[V - 1];
-        st_cluster_slot(peer_ring, pack_half(0, uint32_t(__double2loint(v))),
-                        pack_half(0, uint32_t(__double2hiint(v))));
-    }
+    // products r*u of the lane's two end points; the step-0 edge products go out
+    double pF = A::mul(r, u[0]);
+    double pLs = A::mul(r, u[V - 1]);
+    double pL = __shfl_up_sync(0xffffffffu, pLs, 1);
+    double pR = __shfl_down_sync(0xffffffffu, pF, 1);
+    publish(0, first_lane ? pF : pLs);
 
-    long long m = -1;  // newest neighbour step seen (per edge lane)
-    double g = 0.0;    // its value
-    unsigned long long reads = 0, waits = 0, maxd = 0;
-    __shared__ unsigned int s_hist[64];
-    if (STATS) {
-        for (int i = threadIdx.x; i < 64; i += blockDim.x) s_hist[i] = 0;
-        __syncthreads();
-    }
-    bool abort = false;
-    const long long qm1 = a.q - 1;
+    int m = -1;        // newest neighbour step seen (edge lanes)
+    double pg = 0.0;   // its product r*u
+    unsigned long long waits = 0;
+    int maxd = 0;
+    bool dead = false;  // the watchdog fired somewhere: stop waiting
+    const int qm1 = a.q - 1;
+    const int k_end = int(a.k_end);
+    FreeSlot s0 = ld_slot(slot_addr(my_ring, 0)), s1 = s0;
     if (active) {
-        for (long long k = 0; k < a.k_end; ++k) {
-            // ---- ghost: the exact value (slot k) or the next unseen one (m+1)
-            if (edge) {
-                const uint32_t tk = uint32_t(k);
-                const FreeSlot sk = ld_slot(my_ring + uint32_t(k & (kFreeR - 1)) * 16u);
-                const FreeSlot sn = ld_slot(my_ring + uint32_t((m + 1) & (kFreeR - 1)) * 16u);
-                if (slot_is(sk, tk)) {
-                    m = k;
-                    g = slot_value(sk);
-                } else if (slot_is(sn, uint32_t(m + 1))) {
-                    ++m;
-                    g = slot_value(sn);
-                }
-                if (k - m > qm1) {  // too stale: wait for the neighbour (bounded delay)
-                    if (STATS) ++waits;
-                    const uint64_t t0 = globaltimer_ns();
-                    unsigned spins = 0;
-                    while (k - m > qm1) {
-                        const FreeSlot s = ld_slot(my_ring + uint32_t((m + 1) & (kFreeR - 1)) * 16u);
-                        if (slot_is(s, uint32_t(m + 1))) {
-                            ++m;
-                            g = slot_value(s);
-                        } else if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > a.timeout_ns) {
-                            atomicOr(a.flag + 1, 1u);
-                            abort = true;
-                            break;
-                        }
+        for (int k = 0; k < k_end; ++k) {
+            // ---- ghost for step k: probes from the previous step, then wait
+            // only when it would be more than q-1 steps old (bounded delay)
+            resolve_ghost(s0, s1, k, m, pg);
+            if (edge && !dead && k - m > qm1) {
+                if (STATS) ++waits;
+                const uint64_t t0 = globaltimer_ns();
+                unsigned spins = 0;
+                while (k - m > qm1) {
+                    const FreeSlot s = ld_slot(slot_addr(my_ring, m + 1));
+                    if (slot_is(s, uint32_t(m + 1))) {
+                        ++m;
+                        pg = slot_value(s);
+                    } else if ((++spins & 1023u) == 0 &&
+                               (globaltimer_ns() - t0 > a.timeout_ns ||
+                                *(volatile unsigned int*)(a.flag + 1))) {
+                        atomicOr(a.flag + 1, 1u);
+                        dead = true;
+                        break;
                     }
                 }
-                if (STATS) {
-                    const unsigned long long d = (unsigned long long)(k - m);
-                    ++reads;
-                    maxd = d > maxd ? d : maxd;
-                    atomicAdd(&s_hist[d < 64 ? d : 63], 1u);
-                }
             }
-            if (__any_sync(0xffffffffu, abort)) break;
-            // ---- one Jacobi step of the PE's points; the ghost products enter
-            // at the PE's two ends (lane 0's left, lane Lc-1's right)
-            const double pFirst = A::mul(r, u[0]);
-            const double pLast = A::mul(r, u[V - 1]);
-            const double up = __shfl_up_sync(0xffffffffu, pLast, 1);
-            const double dn = __shfl_down_sync(0xffffffffu, pFirst, 1);
-            const double pg = A::mul(r, g);
-            const double pL = first_lane ? pg : up;
-            const double pR = last_lane ? pg : dn;
-            chunk_step<double, V>(u, r, c, pL, pR, pFirst, pLast);
-            if (pin_first) u[0] = a.c1;
-            if (pin_last) u[V - 1] = a.c2;
-            // ---- publish step k+1's edge value into the neighbour's ring
-            if (edge) {
-                const double v = first_lane ? u[0] : u[V - 1];
-                const uint32_t t = uint32_t(k + 1);
-                st_cluster_slot(peer_ring + uint32_t((k + 1) & (kFreeR - 1)) * 16u,
-                                pack_half(t, uint32_t(__double2loint(v))),
-                                pack_half(t, uint32_t(__double2hiint(v))));
+            __syncwarp();  // reconverge: the shuffles below must not take the divergent path
+            if (STATS && edge) {
+                const int d = k - m;
+                maxd = d > maxd ? d : maxd;
+                ++s_hist[w * 2 + side][d < kFreeMaxQ ? d : kFreeMaxQ - 1];
+            }
+            // probes for step k+1, answered while this step computes
+            s0 = ld_slot(slot_addr(my_ring, k + 1));
+            s1 = ld_slot(slot_addr(my_ring, m + 1));
+            if (first_lane) pL = pg;  // the ghost product replaces the shuffle
+            if (last_lane) pR = pg;
+            // ---- one Jacobi step: the lane's end points first, their products
+            // shuffled and published, then the interior points (K1's
+            // software-pipelined order; same products, same roundings)
+            if constexpr (V == 1) {
+                double n0 = stencil_p(pR, A::mul(c, u[0]), pL);
+                if (pin_first) n0 = a.c1;
+                if (pin_last) n0 = a.c2;
+                const double p0 = A::mul(r, n0);
+                pL = __shfl_up_sync(0xffffffffu, p0, 1);
+                pR = __shfl_down_sync(0xffffffffu, p0, 1);
+                publish(k + 1, p0);
+                u[0] = n0;
+                pF = pLs = p0;
+            } else {
+                const double p1 = V == 2 ? pLs : A::mul(r, u[1]);
+                const double pVm2 = V == 2 ? pF : (V == 3 ? p1 : A::mul(r, u[V - 2]));
+                double nF = stencil_p(p1, A::mul(c, u[0]), pL);
+                double nL = stencil_p(pR, A::mul(c, u[V - 1]), pVm2);
+                if (pin_first) nF = a.c1;
+                if (pin_last) nL = a.c2;
+                const double pF2 = A::mul(r, nF);
+                const double pLs2 = A::mul(r, nL);
+                pL = __shfl_up_sync(0xffffffffu, pLs2, 1);  // for step k+1
+                pR = __shfl_down_sync(0xffffffffu, pF2, 1);
+                publish(k + 1, first_lane ? pF2 : pLs2);
+                double pm1 = pF, p0 = p1;
+#pragma unroll
+                for (int i = 1; i <= V - 2; ++i) {
+                    double pn;
+                    if (i + 1 == V - 1)
+                        pn = pLs;
+                    else if (i + 1 == V - 2)
+                        pn = pVm2;
+                    else
+                        pn = A::mul(r, u[i + 1]);
+                    u[i] = stencil_p(pn, A::mul(c, u[i]), pm1);
+                    pm1 = p0;
+                    p0 = pn;
+                }
+                u[0] = nF;
+                u[V - 1] = nL;
+                pF = pF2;
+                pLs = pLs2;
             }
         }
     }
-    // a watchdog abort anywhere ends every PE (their neighbours would spin)
     bool bad = false;
     if (active && lane < Lc) {
 #pragma unroll
@@ -236,13 +276,15 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
     if (STATS) {
         if (edge) {
-            atomicAdd(a.stats + kStatReads, reads);
+            atomicAdd(a.stats + kStatReads, (unsigned long long)k_end);
             atomicAdd(a.stats + kStatWaits, waits);
-            atomicMax(a.stats + kStatMaxDelay, maxd);
+            atomicMax(a.stats + kStatMaxDelay, (unsigned long long)maxd);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < 64; i += blockDim.x)
-            if (s_hist[i]) atomicAdd(a.stats + kStatDelayHist + i, (unsigned long long)s_hist[i]);
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x) {
+            const unsigned int v = (&s_hist[0][0])[i];
+            if (v) atomicAdd(a.stats + kStatDelayHist + i % kFreeMaxQ, (unsigned long long)v);
+        }
     }
     cluster_sync_all();  // no CTA leaves while a peer may still store into its shared memory
 }
@@ -301,9 +343,10 @@ bool free_layout(size_t P, int* W_out, int* C_out) {
     return true;
 }
 
-bool free_eligible(size_t N, size_t per_pe, size_t q) {
+bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end) {
     int V, Lc, W, C;
     return q >= 1 && q <= size_t(kFreeMaxQ) && per_pe < N && N % per_pe == 0 &&
+           k_end < size_t(1) << 31 &&
            free_geometry(per_pe, &V, &Lc) && free_layout(N / per_pe, &W, &C) &&
            !std::getenv("HEAT_NO_FREE_CLUSTER");
 }
@@ -384,7 +427,7 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
 extern "C" int heat_free_geometry(size_t N, size_t per_pe, size_t q, int* points_per_lane,
                                   int* lanes, int* warps_per_cta, int* cluster) {
     int V = 0, Lc = 0, W = 0, C = 0;
-    const bool ok = hb::free_eligible(N, per_pe, q) && hb::free_geometry(per_pe, &V, &Lc) &&
+    const bool ok = hb::free_eligible(N, per_pe, q, 1) && hb::free_geometry(per_pe, &V, &Lc) &&
                     hb::free_layout(N / per_pe, &W, &C);
     if (points_per_lane) *points_per_lane = ok ? V : 0;
     if (lanes) *lanes = ok ? Lc : 0;

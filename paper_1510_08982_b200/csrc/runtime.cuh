@@ -222,7 +222,7 @@ int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1,
                    float* kernel_ms = nullptr);
 // K10 (exec_free.cu): exec_run(BarrierFree) of PEs that fit one warp each, all
 // in one thread-block cluster; stats in the kStat layout (optional).
-bool free_eligible(size_t N, size_t per_pe, size_t q);
+bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end);
 int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, double c1,
                   double c2, size_t per_pe, size_t q, size_t k_end, double* field_out,
                   unsigned long long* stats_host, float* kernel_ms);

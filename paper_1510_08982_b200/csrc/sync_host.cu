@@ -7,6 +7,7 @@
 #include <cudaTypedefs.h>
 
 #include "runtime.cuh"
+#include "sync_cta.cuh"
 #include "sync_tb.cuh"
 
 namespace hb {
@@ -65,15 +66,31 @@ struct SyncVariant {
     int smem;                 // dynamic shared memory per CTA
     int halo;                 // halo points per side = max steps per pass
     bool dyn;                 // tiles dealt by an atomic counter
-    int warps;                // warps (tiles in flight) per CTA
+    int warps;                // warps per CTA
     int blocks_per_sm;        // filled by the occupancy query
+    bool cta_tiles;           // one tile per CTA (K1c) instead of one per warp
 };
 template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false,
           int W = 4>
 SyncVariant variant() {
     using T = SyncTB<Real, V, H, W>;
     return {sync_tb_kernel<Real, V, NBUF, UNR, TMA_ST, H, DYN, W>, NBUF, V, T::kOut, T::kWinUnits,
-            T::kOutUnits, T::smem_bytes(NBUF), H, DYN, W, 0};
+            T::kOutUnits, T::smem_bytes(NBUF), H, DYN, W, 0, false};
+}
+// K1c (sync_cta.cuh): G warps step one CTA-wide window, seams exchanged in
+// shared memory; f64 only (48-point lanes)
+template <typename Real, int V, int H, int G, int PU>
+SyncVariant variant_cta() {
+    using C = SyncCTA<Real, V, H, G>;
+    return {sync_cta_kernel<Real, V, H, G, PU>, 2, V, C::kOut, C::kWinUnits, C::kOutUnits,
+            C::smem_bytes(), H, true, G, 0, true};
+}
+template <typename Real, int PU>
+SyncVariant variant_cta48() {
+    if constexpr (sizeof(Real) == 8)
+        return variant_cta<Real, 48, 64, 4, PU>();
+    else
+        return variant<Real, 64, 2, -4, true, 64, true>();  // = variant 15 for f32
 }
 // 48-point lanes exist for f64 only (48 f32 values are not whole 128-B rows);
 // f32 takes 64-point lanes (256 B, two rows) with the same halo, buffers and deal
@@ -92,7 +109,7 @@ SyncVariant variant48() {
 // twice, same box); unrolled x1 (14) loses 1.7%.
 constexpr int kDefaultSyncVariant = 15;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 18;
+constexpr int kSyncVariants = 20;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -123,6 +140,11 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant<Real, 64, 2, -4, true, 64, true, (sizeof(Real) == 8 ? 3 : 4)>(),
         // 17: as 16, step loop unrolled 2
         variant<Real, 64, 2, 0, true, 64, true, (sizeof(Real) == 8 ? 3 : 4)>(),
+        // 18: K1c, 4 warps x 48-point lanes in one CTA window, 64-point halo,
+        //     atomic deal, step loop unrolled 4 (f32: variant 15's geometry)
+        variant_cta48<Real, 4>(),
+        // 19: as 18, step loop unrolled 2
+        variant_cta48<Real, 2>(),
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
@@ -212,7 +234,7 @@ struct SyncLauncher {
         if (out_hi <= out_lo) return HEAT_OK;
         if (nsteps > var->halo) return fail(HEAT_ELOGIC, "sync pass: more steps than the halo");
         const long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
-        const long long want = (tiles + var->warps - 1) / var->warps;
+        const long long want = var->cta_tiles ? tiles : (tiles + var->warps - 1) / var->warps;
         const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
         SyncPassArgs p = a;
         p.out_lo = out_lo;
@@ -424,7 +446,8 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // and the last download is short, while neighbouring chunks differ by
     // less than the compute/copy time ratio (~1.8), so neither the compute
     // nor the download stream starves.  Smaller fields: 16 equal chunks.
-    const long long wave = (long long)d.sms * L.var->blocks_per_sm * L.var->warps * L.var->out;
+    const long long wave = (long long)d.sms * L.var->blocks_per_sm *
+                           (L.var->cta_tiles ? 1 : L.var->warps) * L.var->out;
     const std::vector<long long> B = stream_chunk_plan(N, wave);
     const int C = int(B.size()) - 1;
     for (int c = 0; c < C; ++c)
