@@ -126,10 +126,10 @@ int heat_k3_geometry(size_t n, size_t P, size_t q, int mode, int* lanes_per_pe, 
 int heat_k5_geometry(size_t n, int* points_per_lane, int* halo);
 /* K10, exec_run(BarrierFree) in one thread-block cluster (exec_free.cu): for
  * N points in PEs of per_pe and delay bound q, the points per lane, lanes per
- * PE, PE warps per CTA and cluster size; HEAT_EINVAL (all 0) when the run
- * takes the K3/K5 path instead. */
+ * warp, warps per CTA, cluster size and warps per PE; HEAT_EINVAL (all 0)
+ * when the run takes the K3/K5 path instead. */
 int heat_free_geometry(size_t N, size_t per_pe, size_t q, int* points_per_lane, int* lanes,
-                       int* warps_per_cta, int* cluster);
+                       int* warps_per_cta, int* cluster, int* warps_per_pe);
 /* The geometric law's q-1 delay thresholds on a draw's top 53 bits
  * (thresholds[j-1] = first m = x >> 11 whose delay is >= j; 2^53 = never),
  * as the device kernels use them; HEAT_EINVAL for p too small. */

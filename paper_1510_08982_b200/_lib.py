@@ -106,7 +106,7 @@ SIGNATURES = {
     "heat_stream_chunk_plan": (_i, [_sz, _sz, _P(_sz), _sz, _P(_sz)]),
     "heat_k3_geometry": (_i, [_sz, _sz, _sz, _i, _P(_i), _P(_i), _P(_sz), _P(_i)]),
     "heat_k5_geometry": (_i, [_sz, _P(_i), _P(_i)]),
-    "heat_free_geometry": (_i, [_sz, _sz, _sz, _P(_i), _P(_i), _P(_i), _P(_i)]),
+    "heat_free_geometry": (_i, [_sz, _sz, _sz, _P(_i), _P(_i), _P(_i), _P(_i), _P(_i)]),
     "heat_geometric_thresholds": (_i, [_d, _sz, _pu64]),
     "heat_set_strict_finite_checks": (None, [_i]),
     "heat_strict_finite_checks": (_i, []),

@@ -49,6 +49,7 @@ constexpr int kFreeMaxW = 8;  // PE warps per CTA (registers: up to 40 points pe
 struct FreeArgs {
     double* field;  // [N] prepared initial field in, final field out
     int n, P, Lc, W;
+    int Wp;  // warps per PE (1, 2 or 4; divides W)
     double r, c, c1, c2;
     int dirichlet;
     long long k_end;
@@ -101,6 +102,21 @@ __device__ __forceinline__ double slot_value(const FreeSlot& s) {
     return __hiloint2double(int(uint32_t(s.hi)), int(uint32_t(s.lo)));
 }
 
+// Inner-PE seam slots (CTA shared memory): the same tagged halves, local.
+__device__ __forceinline__ void seam_store(uint32_t addr, uint32_t tag, double v) {
+    asm volatile("st.volatile.shared.v2.u64 [%0], {%1, %2};" ::"r"(addr),
+                 "l"(pack_half(tag, uint32_t(__double2loint(v)))),
+                 "l"(pack_half(tag, uint32_t(__double2hiint(v))))
+                 : "memory");
+}
+__device__ __forceinline__ FreeSlot seam_poll(uint32_t addr) {
+    FreeSlot s;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(s.lo), "=l"(s.hi)
+                 : "r"(addr)
+                 : "memory");
+    return s;
+}
 // The ghost product a PE's edge lane consumes at step k, resolved from the
 // two probes issued one step earlier (slot k and the slot after the newest
 // one seen, m+1), branch-free.
@@ -113,46 +129,61 @@ __device__ __forceinline__ void resolve_ghost(const FreeSlot& s0, const FreeSlot
     m = h0 ? k : (h1 ? m + 1 : m);
 }
 
-template <int V, bool STATS>
+// MW: PEs span several warps (seam exchange compiled in)
+template <int V, bool STATS, bool MW>
 __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const FreeArgs a) {
     extern __shared__ __align__(16) FreeSlot rings[];  // [W][2 sides][kFreeR]
+    __shared__ FreeSlot seams[4][kFreeMaxW][2];         // inner-PE warp seams, ring of 4
     __shared__ unsigned int s_hist[kFreeMaxW * 2][kFreeMaxQ];  // STATS: one row per edge lane
-    const int W = a.W;
+    const int W = a.W, Wp = MW ? a.Wp : 1;  // single-warp PEs: the v2 loop, folded
     const uint32_t cta = cluster_ctarank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int p = int(cta) * W + w;
+    const int gw = int(cta) * W + w;  // warp index in the cluster
+    const int p = gw / Wp, wi = gw - p * Wp;  // PE, warp inside the PE
     const bool active = w < W && p < a.P;  // warp-uniform
     const int n = a.n, P = a.P, Lc = a.Lc;
     // invalidate every slot of this CTA's rings (tag 0xffffffff = no step)
     for (int i = threadIdx.x; i < W * 2 * kFreeR; i += blockDim.x)
         rings[i] = FreeSlot{~0ull, ~0ull};
+    if (MW)
+        for (int i = threadIdx.x; i < 4 * kFreeMaxW * 2; i += blockDim.x)
+            (&seams[0][0][0])[i] = FreeSlot{~0ull, ~0ull};
     if (STATS)
         for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x)
             (&s_hist[0][0])[i] = 0;
     cluster_sync_all();  // no producer may write a slot before its owner cleared it
 
+    // r and c stay kernel parameters: ptxas keeps them in uniform registers,
+    // so every DMUL reads one vector register pair, not two (loading them
+    // into vector registers measured 40% slower per step)
     const double r = a.r, c = a.c;
     using A = Arith<double>;
     const bool dir = a.dirichlet != 0;
     const int lpe = p > 0 ? p - 1 : (dir ? -1 : P - 1);
     const int rpe = p + 1 < P ? p + 1 : (dir ? -1 : 0);
     const bool first_lane = lane == 0, last_lane = lane == Lc - 1;
+    const bool pe_first = first_lane && wi == 0;         // the PE's first point
+    const bool pe_last = last_lane && wi == Wp - 1;      // the PE's last point
     const bool needL = active && lpe >= 0;  // Dirichlet PE 0 / P-1 have a pinned end instead
     const bool needR = active && rpe >= 0;
-    const bool pin_first = active && dir && p == 0 && first_lane;
-    const bool pin_last = active && dir && p == P - 1 && last_lane;
+    const bool pin_first = active && dir && p == 0 && pe_first;
+    const bool pin_last = active && dir && p == P - 1 && pe_last;
+    // a PE wider than one warp is synchronous inside: its warps swap their
+    // seam products every step through shared memory (exact, never stale)
+    const bool seamL = active && first_lane && wi > 0;
+    const bool seamR = active && last_lane && wi < Wp - 1;
 
-    // lane 0 reads ring side 0 (its left neighbour's last product) and
-    // publishes its own first product into the left neighbour's side-1 ring;
-    // lane Lc-1 mirrors it.  Every other lane probes its warp's ring too (a
-    // valid address) and ignores the result: no divergent branch per step.
-    const bool edge = (first_lane && needL) || (last_lane && needR);
+    // The PE's first lane reads ring side 0 (its left neighbour PE's last
+    // product) and publishes its own first product into that PE's side-1
+    // ring; the last lane mirrors it.  Every other lane probes its warp's ring
+    // too (a valid address) and ignores the result: no divergent branch.
+    const bool edge = (pe_first && needL) || (pe_last && needR);
     const int side = first_lane ? 0 : 1;
-    const int nb = first_lane ? lpe : rpe;
+    const int nb_gw = first_lane ? lpe * Wp + Wp - 1 : rpe * Wp;  // neighbour PE's edge warp
     const uint32_t my_ring = smem_u32(rings + ((size_t)(active ? w : 0) * 2 + side) * kFreeR);
     uint32_t peer_ring = 0;
     if (edge) {
-        const int nb_cta = nb / W, nb_w = nb % W;
+        const int nb_cta = nb_gw / W, nb_w = nb_gw % W;
         const uint32_t local = smem_u32(rings + ((size_t)nb_w * 2 + (1 - side)) * kFreeR);
         peer_ring = map_cluster(local, uint32_t(nb_cta));
     }
@@ -161,10 +192,23 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
         if (edge)
             st_cluster_slot(slot_addr(peer_ring, k), pack_half(uint32_t(k), uint32_t(__double2loint(prod))),
                             pack_half(uint32_t(k), uint32_t(__double2hiint(prod))));
+        if (MW && (seamL || seamR))
+            seam_store(smem_u32(&seams[k & 3][w][side]), uint32_t(k), prod);
+    };
+    // the neighbouring warp's seam product of step k, polled by the whole
+    // warp until the seam lanes have theirs (it is exact: no staleness)
+    const bool seam_rd = seamL || seamR;
+    const int seam_w = seamL ? w - 1 : (seamR ? w + 1 : w);
+    auto seam_fetch = [&](int k) {
+        const uint32_t addr = smem_u32(&seams[k & 3][seam_w][first_lane ? 1 : 0]);
+        while (true) {
+            const FreeSlot s = seam_poll(addr);
+            if (__all_sync(0xffffffffu, !seam_rd || slot_is(s, uint32_t(k)))) return slot_value(s);
+        }
     };
 
     double u[V];
-    const long long base = (long long)p * n + (long long)lane * V;
+    const long long base = (long long)p * n + (long long)(wi * Lc + lane) * V;
 #pragma unroll
     for (int i = 0; i < V; ++i) u[i] = (active && lane < Lc) ? a.field[base + i] : 0.0;
     if (pin_first) u[0] = a.c1;  // prepare_initial snapped them already; keep exact
@@ -190,25 +234,56 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
             // ---- ghost for step k: probes from the previous step, then wait
             // only when it would be more than q-1 steps old (bounded delay)
             resolve_ghost(s0, s1, k, m, pg);
-            if (edge && !dead && k - m > qm1) {
-                if (STATS) ++waits;
-                const uint64_t t0 = globaltimer_ns();
-                unsigned spins = 0;
-                while (k - m > qm1) {
-                    const FreeSlot s = ld_slot(slot_addr(my_ring, m + 1));
-                    if (slot_is(s, uint32_t(m + 1))) {
-                        ++m;
-                        pg = slot_value(s);
-                    } else if ((++spins & 1023u) == 0 &&
-                               (globaltimer_ns() - t0 > a.timeout_ns ||
-                                *(volatile unsigned int*)(a.flag + 1))) {
-                        atomicOr(a.flag + 1, 1u);
-                        dead = true;
-                        break;
+            if (!MW) {
+                // v2 form (measured fastest for single-warp PEs): lanes that
+                // must wait spin alone, the warp reconverges below
+                if (edge && !dead && k - m > qm1) {
+                    if (STATS) ++waits;
+                    const uint64_t t0 = globaltimer_ns();
+                    unsigned spins = 0;
+                    while (k - m > qm1) {
+                        const FreeSlot s = ld_slot(slot_addr(my_ring, m + 1));
+                        if (slot_is(s, uint32_t(m + 1))) {
+                            ++m;
+                            pg = slot_value(s);
+                        } else if ((++spins & 1023u) == 0 &&
+                                   (globaltimer_ns() - t0 > a.timeout_ns ||
+                                    *(volatile unsigned int*)(a.flag + 1))) {
+                            atomicOr(a.flag + 1, 1u);
+                            dead = true;
+                            break;
+                        }
+                    }
+                }
+                __syncwarp();
+            } else {
+                // warp-uniform wait: the seam polls below shuffle-vote, and a
+                // loop that only some lanes run would leave the warp diverged
+                bool need = edge && !dead && k - m > qm1;
+                if (__any_sync(0xffffffffu, need)) {
+                    if (STATS && need) ++waits;
+                    const uint64_t t0 = globaltimer_ns();
+                    unsigned spins = 0;
+                    while (true) {
+                        if (need) {
+                            const FreeSlot s = ld_slot(slot_addr(my_ring, m + 1));
+                            if (slot_is(s, uint32_t(m + 1))) {
+                                ++m;
+                                pg = slot_value(s);
+                                need = k - m > qm1;
+                            }
+                        }
+                        if (!__any_sync(0xffffffffu, need)) break;
+                        if ((++spins & 1023u) == 0 &&
+                            (globaltimer_ns() - t0 > a.timeout_ns ||
+                             *(volatile unsigned int*)(a.flag + 1))) {
+                            if (lane == 0) atomicOr(a.flag + 1, 1u);
+                            dead = true;
+                            break;
+                        }
                     }
                 }
             }
-            __syncwarp();  // reconverge: the shuffles below must not take the divergent path
             if (STATS && edge) {
                 const int d = k - m;
                 maxd = d > maxd ? d : maxd;
@@ -217,8 +292,13 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
             // probes for step k+1, answered while this step computes
             s0 = ld_slot(slot_addr(my_ring, k + 1));
             s1 = ld_slot(slot_addr(my_ring, m + 1));
-            if (first_lane) pL = pg;  // the ghost product replaces the shuffle
-            if (last_lane) pR = pg;
+            if (pe_first) pL = pg;  // the ghost product replaces the shuffle
+            if (pe_last) pR = pg;
+            if constexpr (MW) {  // the neighbouring warps' seam products (exact)
+                const double x = seam_fetch(k);
+                if (seamL) pL = x;
+                if (seamR) pR = x;
+            }
             // ---- one Jacobi step: the lane's end points first, their products
             // shuffled and published, then the interior points (K1's
             // software-pipelined order; same products, same roundings)
@@ -290,64 +370,100 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
 }
 
 // Points per lane compiled in; a PE of n points runs as Lc = n / V lanes.
-constexpr int kFreeV[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 25, 32, 40};
+constexpr int kFreeV[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 25, 32, 40, 50};
 
 template <bool STATS>
-const void* free_kernel_ptr(int V) {
+const void* free_kernel_ptr(int V, bool MW) {
     switch (V) {
-        case 1: return (const void*)exec_free_kernel<1, STATS>;
-        case 2: return (const void*)exec_free_kernel<2, STATS>;
-        case 3: return (const void*)exec_free_kernel<3, STATS>;
-        case 4: return (const void*)exec_free_kernel<4, STATS>;
-        case 5: return (const void*)exec_free_kernel<5, STATS>;
-        case 6: return (const void*)exec_free_kernel<6, STATS>;
-        case 8: return (const void*)exec_free_kernel<8, STATS>;
-        case 10: return (const void*)exec_free_kernel<10, STATS>;
-        case 12: return (const void*)exec_free_kernel<12, STATS>;
-        case 16: return (const void*)exec_free_kernel<16, STATS>;
-        case 20: return (const void*)exec_free_kernel<20, STATS>;
-        case 24: return (const void*)exec_free_kernel<24, STATS>;
-        case 25: return (const void*)exec_free_kernel<25, STATS>;
-        case 32: return (const void*)exec_free_kernel<32, STATS>;
-        case 40: return (const void*)exec_free_kernel<40, STATS>;
+        case 1: return MW ? (const void*)exec_free_kernel<1, STATS, true> : (const void*)exec_free_kernel<1, STATS, false>;
+        case 2: return MW ? (const void*)exec_free_kernel<2, STATS, true> : (const void*)exec_free_kernel<2, STATS, false>;
+        case 3: return MW ? (const void*)exec_free_kernel<3, STATS, true> : (const void*)exec_free_kernel<3, STATS, false>;
+        case 4: return MW ? (const void*)exec_free_kernel<4, STATS, true> : (const void*)exec_free_kernel<4, STATS, false>;
+        case 5: return MW ? (const void*)exec_free_kernel<5, STATS, true> : (const void*)exec_free_kernel<5, STATS, false>;
+        case 6: return MW ? (const void*)exec_free_kernel<6, STATS, true> : (const void*)exec_free_kernel<6, STATS, false>;
+        case 8: return MW ? (const void*)exec_free_kernel<8, STATS, true> : (const void*)exec_free_kernel<8, STATS, false>;
+        case 10: return MW ? (const void*)exec_free_kernel<10, STATS, true> : (const void*)exec_free_kernel<10, STATS, false>;
+        case 12: return MW ? (const void*)exec_free_kernel<12, STATS, true> : (const void*)exec_free_kernel<12, STATS, false>;
+        case 16: return MW ? (const void*)exec_free_kernel<16, STATS, true> : (const void*)exec_free_kernel<16, STATS, false>;
+        case 20: return MW ? (const void*)exec_free_kernel<20, STATS, true> : (const void*)exec_free_kernel<20, STATS, false>;
+        case 24: return MW ? (const void*)exec_free_kernel<24, STATS, true> : (const void*)exec_free_kernel<24, STATS, false>;
+        case 25: return MW ? (const void*)exec_free_kernel<25, STATS, true> : (const void*)exec_free_kernel<25, STATS, false>;
+        case 32: return MW ? (const void*)exec_free_kernel<32, STATS, true> : (const void*)exec_free_kernel<32, STATS, false>;
+        case 40: return MW ? (const void*)exec_free_kernel<40, STATS, true> : (const void*)exec_free_kernel<40, STATS, false>;
+        case 50: return MW ? (const void*)exec_free_kernel<50, STATS, true> : (const void*)exec_free_kernel<50, STATS, false>;
         default: return nullptr;
     }
 }
 
 }  // namespace
 
-// The PE geometry K10 uses for PEs of n points: V points per lane, Lc = n / V
-// lanes (2 <= Lc <= 32), the smallest compiled V that fits; false if none.
-bool free_geometry(size_t n, int* V_out, int* Lc_out) {
-    for (int V : kFreeV) {
-        if (n % size_t(V) != 0) continue;
-        const size_t Lc = n / size_t(V);
-        if (Lc < 2) break;
-        if (Lc <= 32) {
-            *V_out = V;
-            *Lc_out = int(Lc);
-            return true;
-        }
+// PE warps per CTA and the cluster size for `warps` PE warps: one warp per SM
+// sub-partition while they fit 16 CTAs of 4, else 16 CTAs of up to
+// kFreeMaxW warps.
+bool free_layout(size_t warps, int* W_out, int* C_out) {
+    if (warps < 2 || warps > size_t(kFreeMaxCluster) * kFreeMaxW) return false;
+    int W = 4;
+    if (warps > size_t(kFreeMaxCluster) * 4) {
+        W = int((warps + kFreeMaxCluster - 1) / kFreeMaxCluster);
+        W = W <= 4 ? 4 : 8;  // a multiple of every warps-per-PE (1, 2, 4)
     }
-    return false;
+    *W_out = W;
+    *C_out = int((warps + W - 1) / W);
+    return true;
 }
 
-// PE warps per CTA and the cluster size: one warp per SM sub-partition while
-// the PEs fit 16 CTAs of 4, else 16 CTAs of up to kFreeMaxW warps.
-bool free_layout(size_t P, int* W_out, int* C_out) {
-    if (P < 2 || P > size_t(kFreeMaxCluster) * kFreeMaxW) return false;
-    int W = 4;
-    if (P > size_t(kFreeMaxCluster) * 4) W = int((P + kFreeMaxCluster - 1) / kFreeMaxCluster);
-    *W_out = W;
-    *C_out = int((P + W - 1) / W);
+// The PE geometry K10 uses for P PEs of n points: Wp warps per PE (1, 2 or
+// 4), Lc lanes per warp (2 <= Lc <= 32) and V points per lane, Wp*Lc*V = n.
+// Measured on B200 (tools/probe_k10.py), a PE warp's step costs ~210 cycles
+// of latency up to ~8 points per lane and ~8V + 150 cycles of issue beyond
+// (V = 20: 330, V = 40: 467); the seam exchange of a multi-warp PE adds
+// ~30.  The geometry with the lowest estimate wins, as long as every PE warp
+// keeps an SM sub-partition of its own (ties: fewer warps per PE).
+// HEAT_K10_MAX_WP caps Wp (A/B).
+bool free_geometry(size_t n, size_t P, int* V_out, int* Lc_out, int* Wp_out) {
+    static const int max_wp = [] {
+        const char* e = std::getenv("HEAT_K10_MAX_WP");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    int best_V = 0, best_Lc = 0, best_Wp = 0, best_cost = 0;
+    bool best_spread = false;
+    for (int Wp : {1, 2, 4}) {
+        if (Wp > max_wp || n % size_t(Wp) != 0) continue;
+        const size_t m = n / size_t(Wp);
+        int W, C;
+        if (!free_layout(P * size_t(Wp), &W, &C)) continue;
+        const bool spread = W == 4;  // one warp per SM sub-partition
+        for (int V : kFreeV) {
+            if (m % size_t(V) != 0) continue;
+            const size_t Lc = m / size_t(V);
+            if (Lc < 2) break;
+            if (Lc > 32) continue;
+            const int cost = std::max(210, 8 * V + 150) + (Wp > 1 ? 30 : 0);
+            const bool better = best_Wp == 0 || (spread && !best_spread) ||
+                                (spread == best_spread && cost < best_cost);
+            if (better) {
+                best_V = V;
+                best_Lc = int(Lc);
+                best_Wp = Wp;
+                best_cost = cost;
+                best_spread = spread;
+            }
+            break;  // the smallest V for this Wp
+        }
+    }
+    if (best_Wp == 0) return false;
+    *V_out = best_V;
+    *Lc_out = best_Lc;
+    *Wp_out = best_Wp;
     return true;
 }
 
 bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end) {
-    int V, Lc, W, C;
+    int V, Lc, Wp, W, C;
     return q >= 1 && q <= size_t(kFreeMaxQ) && per_pe < N && N % per_pe == 0 &&
            k_end < size_t(1) << 31 &&
-           free_geometry(per_pe, &V, &Lc) && free_layout(N / per_pe, &W, &C) &&
+           free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) &&
+           free_layout(N / per_pe * size_t(Wp), &W, &C) &&
            !std::getenv("HEAT_NO_FREE_CLUSTER");
 }
 
@@ -356,8 +472,9 @@ bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end) {
 int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, double c1,
                   double c2, size_t per_pe, size_t q, size_t k_end, double* field_out,
                   unsigned long long* stats_host, float* kernel_ms) {
-    int V = 0, Lc = 0, W = 0, C = 0;
-    if (!free_geometry(per_pe, &V, &Lc) || !free_layout(N / per_pe, &W, &C))
+    int V = 0, Lc = 0, Wp = 0, W = 0, C = 0;
+    if (!free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) ||
+        !free_layout(N / per_pe * size_t(Wp), &W, &C))
         return fail(HEAT_EINVAL, "exec_run: no K10 layout for this partition");
     const size_t pitch = (N + 63) / 64 * 64;
     HB_TRY(ensure_buffers(d, pitch * sizeof(double)));
@@ -377,6 +494,7 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     a.P = int(N / per_pe);
     a.Lc = Lc;
     a.W = W;
+    a.Wp = Wp;
     a.r = r;
     a.c = 1.0 - 2.0 * r;  // core.hpp:108
     a.c1 = c1;
@@ -387,7 +505,7 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     a.flag = d.flag;
     a.stats = dstats;
     a.timeout_ns = 20ull * 1000000000ull;
-    const void* fn = stats_host ? free_kernel_ptr<true>(V) : free_kernel_ptr<false>(V);
+    const void* fn = stats_host ? free_kernel_ptr<true>(V, Wp > 1) : free_kernel_ptr<false>(V, Wp > 1);
     if (!fn) return fail(HEAT_ELOGIC, "K10: points per lane not compiled");
     const int smem = W * 2 * kFreeR * int(sizeof(FreeSlot));
     if (C > 8) HB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -425,13 +543,15 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
 }  // namespace hb
 
 extern "C" int heat_free_geometry(size_t N, size_t per_pe, size_t q, int* points_per_lane,
-                                  int* lanes, int* warps_per_cta, int* cluster) {
-    int V = 0, Lc = 0, W = 0, C = 0;
-    const bool ok = hb::free_eligible(N, per_pe, q, 1) && hb::free_geometry(per_pe, &V, &Lc) &&
-                    hb::free_layout(N / per_pe, &W, &C);
+                                  int* lanes, int* warps_per_cta, int* cluster, int* warps_per_pe) {
+    int V = 0, Lc = 0, Wp = 0, W = 0, C = 0;
+    const bool ok = hb::free_eligible(N, per_pe, q, 1) &&
+                    hb::free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) &&
+                    hb::free_layout(N / per_pe * size_t(Wp), &W, &C);
     if (points_per_lane) *points_per_lane = ok ? V : 0;
     if (lanes) *lanes = ok ? Lc : 0;
     if (warps_per_cta) *warps_per_cta = ok ? W : 0;
     if (cluster) *cluster = ok ? C : 0;
+    if (warps_per_pe) *warps_per_pe = ok ? Wp : 0;
     return ok ? HEAT_OK : HEAT_EINVAL;
 }

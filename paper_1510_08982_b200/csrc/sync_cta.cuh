@@ -99,15 +99,23 @@ __device__ __forceinline__ void coef_reload(const Seam& s, double& r, double& c)
     asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r), "=d"(c) : "r"(s.coef)
                  : "memory");
 }
-// Lanes 0 / 31 poll while the others wait: the warp reconverges before the
-// next shuffle (else every later shuffle takes the divergent collective path,
-// 3x slower -- measured).
+// The whole warp polls until lanes 0 / 31 have their neighbours' products
+// (the others read their own dummy slot and are satisfied at once): a loop
+// that only some lanes run would leave the warp diverged, and every later
+// shuffle would take the slow collective path (measured: 3x slower).
 template <int G>
 __device__ __forceinline__ double seam_read(const Seam& s, double fallback) {
-    double x = fallback;
-    if (s.rd) x = seam_get(s.xch + s.entry(s.tag, G) + s.get, s.tag);
-    __syncwarp();
-    return x;
+    const uint32_t addr = s.rd ? s.xch + s.entry(s.tag, G) + s.get : s.xch + s.put;
+    while (true) {
+        unsigned long long lo, hi;
+        asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];"
+                     : "=l"(lo), "=l"(hi)
+                     : "r"(addr)
+                     : "memory");
+        const bool ok = !s.rd || (uint32_t(lo >> 32) == s.tag && uint32_t(hi >> 32) == s.tag);
+        if (__all_sync(0xffffffffu, ok))
+            return s.rd ? __hiloint2double(int(uint32_t(hi)), int(uint32_t(lo))) : fallback;
+    }
 }
 
 // nsteps software-pipelined steps (K1's warp_steps_pipelined) of a warp whose

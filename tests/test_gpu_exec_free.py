@@ -26,8 +26,11 @@ def H(gpu):
     return heat
 
 
+# single-warp PEs, then PEs over 2 or 4 warps with exact seams inside (10000/2500:
+# 4 x 25 lanes x 25 points; 10000/2000: 4 x 25 x 20; 10000/5000: 4 x 25 x 50)
 SHAPES = [(100, 10), (1000, 100), (10000, 1000), (1024, 128), (600, 24), (4096, 32),
-          (1000, 50), (10000, 500), (100, 5), (256, 2), (96, 3), (3000, 120)]
+          (1000, 50), (10000, 500), (100, 5), (256, 2), (96, 3), (3000, 120),
+          (10000, 2500), (10000, 2000), (10000, 5000), (2000, 500), (8000, 1000)]
 
 
 @pytest.mark.parametrize("N,n", SHAPES)
@@ -49,7 +52,8 @@ def test_k10_q1_is_sync(H, port, N, n, periodic):
     assert res.duration_ns > 0
 
 
-@pytest.mark.parametrize("N,n", [(100, 10), (1000, 100), (10000, 1000), (4096, 32)])
+@pytest.mark.parametrize("N,n", [(100, 10), (1000, 100), (10000, 1000), (4096, 32),
+                                 (10000, 2500)])
 def test_k10_free_bounded_delays(H, N, n):
     u0 = H.cosine_init(N)
     k = 3000

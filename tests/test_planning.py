@@ -164,24 +164,27 @@ def test_geometric_thresholds_match_reference_draws(port, p, q):
 
 def free_geometry(N, n, q=8):
     L = _lib.lib()
-    v = [ctypes.c_int(0) for _ in range(4)]
+    v = [ctypes.c_int(0) for _ in range(5)]
     st = L.heat_free_geometry(N, n, q, *[ctypes.byref(x) for x in v])
     return st, tuple(x.value for x in v)
 
 
 @pytest.mark.parametrize("N,n,expect", [
-    (100, 10, (1, 10, 4, 3)), (1000, 100, (4, 25, 4, 3)), (10000, 1000, (40, 25, 4, 3)),
-    (100, 5, (1, 5, 4, 5)), (1000, 50, (2, 25, 4, 5)), (10000, 500, (20, 25, 4, 5)),
-    (100, 25, (1, 25, 4, 1)), (1024, 128, (4, 32, 4, 2)), (4096, 32, (1, 32, 8, 16)),
-    (256, 2, (1, 2, 8, 16))])
+    (100, 10, (1, 10, 4, 3, 1)), (1000, 100, (4, 25, 4, 3, 1)), (10000, 1000, (10, 25, 4, 10, 4)),
+    (100, 5, (1, 5, 4, 5, 1)), (1000, 50, (2, 25, 4, 5, 1)), (10000, 500, (10, 25, 4, 10, 2)),
+    (100, 25, (1, 25, 4, 1, 1)), (1024, 128, (4, 32, 4, 2, 1)), (4096, 32, (1, 32, 8, 16, 1)),
+    (256, 2, (1, 2, 8, 16, 1)), (1000, 250, (10, 25, 4, 1, 1)), (10000, 2500, (25, 25, 4, 4, 4)),
+    (10000, 2000, (20, 25, 4, 5, 4)), (10000, 5000, (50, 25, 4, 2, 4))])
 def test_k10_free_geometry(N, n, expect):
-    """K10 (exec_free.cu): V * Lc = n exactly with 2 <= Lc <= 32 lanes and the
-    smallest compiled V; 4 PE warps per CTA (one per SM sub-partition) up to a
-    16-CTA cluster, then up to 8 per CTA."""
+    """K10 (exec_free.cu): Wp warps per PE of Lc lanes x V points, Wp*Lc*V = n
+    exactly with 2 <= Lc <= 32, chosen by the measured step-cost estimate; 4
+    warps per CTA (one per SM sub-partition) up to a 16-CTA cluster, then 8."""
     st, got = free_geometry(N, n)
     assert st == 0 and got == expect
-    V, Lc, W, C = got
-    assert V * Lc == n and 2 <= Lc <= 32 and W * C >= N // n and W * (C - 1) < N // n
+    V, Lc, W, C, Wp = got
+    P = N // n
+    assert V * Lc * Wp == n and 2 <= Lc <= 32 and W % Wp == 0
+    assert W * C >= P * Wp and W * (C - 1) < P * Wp
 
 
 @pytest.mark.parametrize("N,n,q", [(1031 * 2, 1031, 8),   # prime PE width: no lanes split
@@ -189,7 +192,7 @@ def test_k10_free_geometry(N, n, expect):
                                    (1000, 100, 17),       # q beyond the 32-slot ring
                                    (100, 100, 8),         # one PE: the sync path
                                    (129 * 4, 4, 8),       # 129 PEs > 16 x 8 warps
-                                   (41 * 32 * 2, 41 * 32, 8)])  # 1312 > 32 lanes x 40
+                                   (41 * 32 * 2, 41 * 32, 8)])  # 1312 = 41 x 32: no lanes split
 def test_k10_free_geometry_refusals(N, n, q):
     st, got = free_geometry(N, n, q)
-    assert st != 0 and got == (0, 0, 0, 0)
+    assert st != 0 and got == (0, 0, 0, 0, 0)

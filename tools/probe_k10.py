@@ -31,7 +31,7 @@ for P in (4, 5, 10, 20):
     for N in (100, 1000, 10000):
         if N % P:
             continue
-        geo = [C.c_int(0) for _ in range(4)]
+        geo = [C.c_int(0) for _ in range(5)]
         ok = lib.heat_free_geometry(N, N // P, 8, *[C.byref(x) for x in geo]) == 0
         geo = [x.value for x in geo]
         b = run(N, P, 0, False)
