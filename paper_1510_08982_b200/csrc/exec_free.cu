@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "async_pe.cuh"
@@ -50,6 +51,7 @@ struct FreeArgs {
     double* field;  // [N] prepared initial field in, final field out
     int n, P, Lc, W;
     int Wp;  // warps per PE (1, 2 or 4; divides W)
+    int dbg; // A/B only (HEAT_K10_DBG): 1 = no publish, 2 = no ghost probes (results wrong)
     double r, c, c1, c2;
     int dirichlet;
     long long k_end;
@@ -78,9 +80,13 @@ __device__ __forceinline__ uint32_t map_cluster(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
     return out;
 }
+// A plain (weak) 16-B DSMEM store: ptxas turns .relaxed.cluster / .volatile
+// into ST.E.128.STRONG.GPU / .SYS, ~25 ns per step slower (measured).  Each
+// 64-bit half carries its own tag, so a reader accepts a slot only when both
+// aligned halves (each written in one piece) show the step it wants.
 __device__ __forceinline__ void st_cluster_slot(uint32_t addr, unsigned long long lo,
                                                 unsigned long long hi) {
-    asm volatile("st.relaxed.cluster.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(lo),
+    asm volatile("st.shared::cluster.v2.u64 [%0], {%1, %2};" ::"r"(addr), "l"(lo),
                  "l"(hi)
                  : "memory");
 }
@@ -369,6 +375,420 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
     cluster_sync_all();  // no CTA leaves while a peer may still store into its shared memory
 }
 
+// K10 with lane halos and rounds, for PEs of one warp (K10r).  The plain
+// kernel above exchanges lane-edge products by shuffle, polls the ghost and
+// publishes the PE edges EVERY step; a single warp per SM sub-partition has
+// nothing to hide those latencies behind (~200 cycles per step, measured,
+// whatever V).  Here a PE advances in rounds of LH steps:
+//   * each lane also holds the LH points on either side of its own V (copies
+//     of its neighbours' points, refreshed by shuffle once per round) and
+//     steps them redundantly, so no shuffle sits inside a round;
+//   * the PE edges are polled once per round (the newest published value,
+//     from a probe issued at the end of the previous round) and published
+//     once per round (the edge product at the round's last step).
+// The asynchronous model allows exactly this: every consumed neighbour value
+// is the neighbour's value at some step k* with 0 <= k - k* <= q - 1 (paper
+// Eq. (4); the lanes wait only when the round's last step would read an
+// older one), and inside a PE every update is the same stencil_p on the same
+// products as the synchronous scheme (bit-identical when q = 1 forces k* = k,
+// which takes the plain kernel).  LH <= q/2: a neighbour one round behind
+// still satisfies the bound, so lockstep PEs never wait.
+template <int V, int LH, bool STATS>
+__global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const FreeArgs a) {
+    constexpr int E = V + 2 * LH;  // own points x[LH, LH+V)
+    // lanes whose window holds the PE's outer neighbour position (-1 or
+    // n_pe): d = 0 .. kG lanes in from either end; its end points: 0 .. kP
+    constexpr int kG = (LH - 1) / V, kP = LH / V;
+    extern __shared__ __align__(16) FreeSlot rings[];  // [W][2 sides][kFreeR], slot = round
+    __shared__ unsigned int s_hist[kFreeMaxW * 2][kFreeMaxQ];
+    const int W = a.W;
+    const uint32_t cta = cluster_ctarank();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = int(cta) * W + w;
+    const bool active = w < W && p < a.P;
+    const int n = a.n, P = a.P, Lc = a.Lc;
+    for (int i = threadIdx.x; i < W * 2 * kFreeR; i += blockDim.x)
+        rings[i] = FreeSlot{~0ull, ~0ull};
+    if (STATS)
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x)
+            (&s_hist[0][0])[i] = 0;
+    // r, c and the pinned values go through shared memory into registers
+    // once: ptxas otherwise re-loads kernel parameters from the constant bank
+    // inside the step loop (LDC + a short-scoreboard stall before the first
+    // DMUL of every step, measured with ncu)
+    __shared__ __align__(16) double s_coef[4];
+    if (threadIdx.x == 0) {
+        s_coef[0] = a.r;
+        s_coef[1] = a.c;
+        s_coef[2] = a.c1;
+        s_coef[3] = a.c2;
+    }
+    cluster_sync_all();
+
+    double r, c, c1, c2;
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r), "=d"(c) : "r"(smem_u32(s_coef)) : "memory");
+    asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c1), "=d"(c2) : "r"(smem_u32(s_coef + 2)) : "memory");
+    using A = Arith<double>;
+    const bool dir = a.dirichlet != 0;
+    const int lpe = p > 0 ? p - 1 : (dir ? -1 : P - 1);
+    const int rpe = p + 1 < P ? p + 1 : (dir ? -1 : 0);
+    const bool first_lane = lane == 0, last_lane = lane == Lc - 1;
+    const bool needL = active && lpe >= 0;
+    const bool needR = active && rpe >= 0;
+    const bool pin_first = active && dir && p == 0 && first_lane;
+    const bool pin_last = active && dir && p == P - 1 && last_lane;
+    const bool pinL = active && dir && p == 0, pinR = active && dir && p == P - 1;  // warp-uniform
+    const bool edge = (first_lane && needL) || (last_lane && needR);
+    const int side = first_lane ? 0 : 1;
+    const int nb = first_lane ? lpe : rpe;
+    const uint32_t my_ring = smem_u32(rings + ((size_t)(active ? w : 0) * 2 + side) * kFreeR);
+    uint32_t peer_ring = 0;
+    if (edge) {
+        const int nb_cta = nb / W, nb_w = nb % W;
+        const uint32_t local = smem_u32(rings + ((size_t)nb_w * 2 + (1 - side)) * kFreeR);
+        peer_ring = map_cluster(local, uint32_t(nb_cta));
+    }
+    // the value of step t (a multiple of LH, or k_end) lives in slot t / LH
+    auto slot_addr = [&](uint32_t base, int t) {
+        return base + uint32_t((t / LH) & (kFreeR - 1)) * 16u;
+    };
+    auto publish = [&](int t, double prod) {
+        if (edge)
+            st_cluster_slot(slot_addr(peer_ring, t), pack_half(uint32_t(t), uint32_t(__double2loint(prod))),
+                            pack_half(uint32_t(t), uint32_t(__double2hiint(prod))));
+    };
+
+    double x[E];
+    const long long base = (long long)p * n + (long long)lane * V;
+#pragma unroll
+    for (int i = 0; i < V; ++i) x[LH + i] = (active && lane < Lc) ? a.field[base + i] : 0.0;
+    if (pin_first) x[LH] = c1;
+    if (pin_last) x[LH + V - 1] = c2;
+    double pgL = 0.0, pgR = 0.0;  // the round's ghosts, on every lane near an end
+    publish(0, A::mul(r, first_lane ? x[LH] : x[LH + V - 1]));
+
+    int m = -1;         // step of the newest neighbour value seen (a round start)
+    double pg = 0.0;    // its product r*u
+    unsigned long long waits = 0;
+    int maxd = 0;
+    bool dead = false;
+    const int qm1 = a.q - 1;
+    const int k_end = int(a.k_end);
+    FreeSlot sa = ld_slot(slot_addr(my_ring, 0)), sb = sa;  // probes: round starts k, k - LH
+    // ghost for the round of steps k..last
+    auto ghost = [&](int k, int last) {
+        const bool ha = slot_is(sa, uint32_t(k)), hb = k >= LH && slot_is(sb, uint32_t(k - LH));
+        if (ha && k > m) {
+            m = k;
+            pg = slot_value(sa);
+        } else if (hb && k - LH > m) {
+            m = k - LH;
+            pg = slot_value(sb);
+        }
+        if (edge && !dead && last - m > qm1) {
+            if (STATS) ++waits;
+            const uint64_t t0 = globaltimer_ns();
+            unsigned spins = 0;
+            while (last - m > qm1) {
+                const int t = m < 0 ? 0 : m + LH;  // the next value the neighbour publishes
+                const FreeSlot s = ld_slot(slot_addr(my_ring, t));
+                if (slot_is(s, uint32_t(t))) {
+                    m = t;
+                    pg = slot_value(s);
+                } else if ((++spins & 1023u) == 0 &&
+                           (globaltimer_ns() - t0 > a.timeout_ns ||
+                            *(volatile unsigned int*)(a.flag + 1))) {
+                    atomicOr(a.flag + 1, 1u);
+                    dead = true;
+                    break;
+                }
+            }
+        }
+        __syncwarp();
+        if (STATS && edge) {
+            for (int kk = k; kk <= last; ++kk) {
+                const int d = kk - m;
+                maxd = d > maxd ? d : maxd;
+                ++s_hist[w * 2 + side][d < kFreeMaxQ ? d : kFreeMaxQ - 1];
+            }
+        }
+    };
+    // one step of window points x[lo, hi) (lo >= 1, hi <= E-1): all the
+    // products, then the sums -- the same stencil_p, the same roundings
+    auto step = [&](auto lo_c, auto hi_c) {
+        constexpr int lo = decltype(lo_c)::value, hi = decltype(hi_c)::value;
+        double pr[E], cx[E];
+#pragma unroll
+        for (int i = lo - 1; i <= hi; ++i) pr[i] = A::mul(r, x[i]);
+#pragma unroll
+        for (int i = lo; i < hi; ++i) cx[i] = A::mul(c, x[i]);
+        // the PE's outer neighbours (positions -1 and n_pe) are the ghosts, in
+        // whichever lanes' windows hold them (a pinned end is re-pinned below)
+#pragma unroll
+        for (int d = 0; d <= kG; ++d) {
+            if (LH - 1 - d * V >= lo - 1 && lane == d) pr[LH - 1 - d * V >= 0 ? LH - 1 - d * V : 0] = pgL;
+            if (LH + V + d * V <= hi && lane == Lc - 1 - d) pr[LH + V + d * V < E ? LH + V + d * V : E - 1] = pgR;
+        }
+#pragma unroll
+        for (int i = lo; i < hi; ++i) cx[i] = A::add(pr[i + 1], cx[i]);
+#pragma unroll
+        for (int i = lo; i < hi; ++i) x[i] = A::add(cx[i], pr[i - 1]);
+        if (pinL || pinR) {  // warp-uniform: only the two end PEs of a Dirichlet run
+#pragma unroll
+            for (int d = 0; d <= kP; ++d) {
+                if (pinL && lane == d) x[LH - d * V >= 0 ? LH - d * V : 0] = c1;
+                if (pinR && lane == Lc - 1 - d) x[LH + V - 1 + d * V < E ? LH + V - 1 + d * V : E - 1] = c2;
+            }
+        }
+    };
+    // halos: the LH points on either side, from the lanes that own them
+    // (one lane away when V >= LH, more when V < LH)
+    auto exchange = [&]() {
+        double own[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) own[e] = x[LH + e];
+#pragma unroll
+        for (int i = 0; i < LH; ++i) {
+            const int g = i - LH;                  // position relative to the lane's first point
+            const int dl = (-g + V - 1) / V;       // lanes up
+            x[i] = __shfl_up_sync(0xffffffffu, own[g + dl * V], dl);
+            const int gr = V + i, dr = gr / V;     // lanes down
+            x[LH + V + i] = __shfl_down_sync(0xffffffffu, own[gr - dr * V], dr);
+        }
+    };
+    // a round: step j updates window points [1 + j, E - 1 - j)
+    auto round_steps = [&](auto j_c) {
+        constexpr int j = decltype(j_c)::value;
+        step(std::integral_constant<int, 1 + j>{}, std::integral_constant<int, E - 1 - j>{});
+    };
+    if (active) {
+        int k = 0;
+        for (int rounds = k_end / LH; rounds > 0; --rounds) {  // count down: no k_end reload
+            exchange();
+            ghost(k, k + LH - 1);
+            pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
+            pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            round_steps(std::integral_constant<int, 0>{});
+            round_steps(std::integral_constant<int, 1>{});
+            if constexpr (LH > 2) {
+                round_steps(std::integral_constant<int, 2>{});
+                round_steps(std::integral_constant<int, 3>{});
+            }
+            k += LH;
+            sa = ld_slot(slot_addr(my_ring, k));  // answered while the halos move; issued
+            sb = ld_slot(slot_addr(my_ring, k - LH));  // before the publish (see K10t)
+            publish(k, A::mul(r, first_lane ? x[LH] : x[LH + V - 1]));
+        }
+        if (k < k_end) {  // the remaining steps, one at a time (plain halo refresh each)
+            ghost(k, k_end - 1);
+            pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
+            pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            for (; k < k_end; ++k) {
+                exchange();
+                round_steps(std::integral_constant<int, LH - 1>{});
+            }
+        }
+    }
+    bool bad = false;
+    if (active && lane < Lc) {
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            bad |= !isfinite(x[LH + i]);
+            a.field[base + i] = x[LH + i];
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.flag, 1u);
+    if (STATS) {
+        if (edge) {
+            atomicAdd(a.stats + kStatReads, (unsigned long long)k_end);
+            atomicAdd(a.stats + kStatWaits, waits);
+            atomicMax(a.stats + kStatMaxDelay, (unsigned long long)maxd);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x) {
+            const unsigned int v = (&s_hist[0][0])[i];
+            if (v) atomicAdd(a.stats + kStatDelayHist + i % kFreeMaxQ, (unsigned long long)v);
+        }
+    }
+    cluster_sync_all();
+}
+
+// K10 with one THREAD per PE (K10t), for PEs of up to 50 points: the
+// reference's own decomposition (one worker per PE, async_exec.cpp:156-259)
+// at its most literal.  Lane 0 of the PE's warp holds all n points in
+// registers, so there is no intra-PE exchange at all: a step is n stencils
+// with the two ghost products at the ends, and the PE edges are polled and
+// published once per round of LH steps as in K10r (LH <= q/2; LH = 1 polls
+// every step).  A step costs ~8n + 40 cycles of FP64 issue, so tiny PEs (the
+// reference's measure() at N = 100) run well below the ~170-cycle floor of a
+// PE spread over a warp's lanes.
+template <int V, int LH, bool STATS>
+__global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_pe_kernel(const FreeArgs a) {
+    extern __shared__ __align__(16) FreeSlot rings[];  // [W][2 sides][kFreeR], slot = round
+    __shared__ unsigned int s_hist[kFreeMaxW * 2][kFreeMaxQ];
+    __shared__ __align__(16) double s_coef[4];
+    const int W = a.W;
+    const uint32_t cta = cluster_ctarank();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = int(cta) * W + w;
+    const bool active = w < W && p < a.P && lane == 0;
+    const int n = a.n, P = a.P;
+    for (int i = threadIdx.x; i < W * 2 * kFreeR; i += blockDim.x)
+        rings[i] = FreeSlot{~0ull, ~0ull};
+    if (STATS)
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x)
+            (&s_hist[0][0])[i] = 0;
+    if (threadIdx.x == 0) {  // coefficients into registers via shared memory (see K10r)
+        s_coef[0] = a.r;
+        s_coef[1] = a.c;
+        s_coef[2] = a.c1;
+        s_coef[3] = a.c2;
+    }
+    cluster_sync_all();
+
+    unsigned long long waits = 0;
+    int maxd = 0;
+    bool bad = false;
+    const int k_end = int(a.k_end);
+    if (active) {
+        double r, c, c1, c2;
+        asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r), "=d"(c) : "r"(smem_u32(s_coef)) : "memory");
+        asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c1), "=d"(c2) : "r"(smem_u32(s_coef + 2)) : "memory");
+        using A = Arith<double>;
+        const bool dir = a.dirichlet != 0;
+        const int lpe = p > 0 ? p - 1 : (dir ? -1 : P - 1);
+        const int rpe = p + 1 < P ? p + 1 : (dir ? -1 : 0);
+        const bool needL = lpe >= 0, needR = rpe >= 0;
+        const bool pinL = dir && p == 0, pinR = dir && p == P - 1;
+        // side 0: the left neighbour's last product; side 1: the right one's first
+        const uint32_t ringL = smem_u32(rings + ((size_t)w * 2 + 0) * kFreeR);
+        const uint32_t ringR = smem_u32(rings + ((size_t)w * 2 + 1) * kFreeR);
+        uint32_t peerL = 0, peerR = 0;  // where this PE's first / last product goes
+        if (needL) peerL = map_cluster(smem_u32(rings + ((size_t)(lpe % W) * 2 + 1) * kFreeR), uint32_t(lpe / W));
+        if (needR) peerR = map_cluster(smem_u32(rings + ((size_t)(rpe % W) * 2 + 0) * kFreeR), uint32_t(rpe / W));
+        auto slot_addr = [&](uint32_t base, int t) {
+            return base + uint32_t((t / LH) & (kFreeR - 1)) * 16u;
+        };
+        auto put = [&](uint32_t peer, int t, double prod) {
+            st_cluster_slot(slot_addr(peer, t), pack_half(uint32_t(t), uint32_t(__double2loint(prod))),
+                            pack_half(uint32_t(t), uint32_t(__double2hiint(prod))));
+        };
+        double x[V];
+        const long long base = (long long)p * n;
+#pragma unroll
+        for (int i = 0; i < V; ++i) x[i] = a.field[base + i];
+        if (pinL) x[0] = c1;
+        if (pinR) x[V - 1] = c2;
+        auto publish = [&](int t) {
+            if (needL) put(peerL, t, A::mul(r, x[0]));
+            if (needR) put(peerR, t, A::mul(r, x[V - 1]));
+        };
+        publish(0);
+        int mL = -1, mR = -1;           // steps of the newest neighbour values seen
+        double pgL = 0.0, pgR = 0.0;    // their products
+        bool dead = false;
+        const int qm1 = a.q - 1;
+        FreeSlot la = ld_slot(slot_addr(ringL, 0)), lb = la, ra = ld_slot(slot_addr(ringR, 0)), rb = ra;
+        // resolve one side for the round k..last (probes of round starts k, k - LH)
+        auto side_ghost = [&](bool need, uint32_t ring, const FreeSlot& sa, const FreeSlot& sb, int k,
+                              int last, int& m, double& pg, int hrow) {
+            if (!need) return;
+            if (slot_is(sa, uint32_t(k)) && k > m) {
+                m = k;
+                pg = slot_value(sa);
+            } else if (k >= LH && slot_is(sb, uint32_t(k - LH)) && k - LH > m) {
+                m = k - LH;
+                pg = slot_value(sb);
+            }
+            if (!dead && last - m > qm1) {
+                if (STATS) ++waits;
+                const uint64_t t0 = globaltimer_ns();
+                unsigned spins = 0;
+                while (last - m > qm1) {
+                    const int t = m < 0 ? 0 : m + LH;
+                    const FreeSlot sl = ld_slot(slot_addr(ring, t));
+                    if (slot_is(sl, uint32_t(t))) {
+                        m = t;
+                        pg = slot_value(sl);
+                    } else if ((++spins & 1023u) == 0 &&
+                               (globaltimer_ns() - t0 > a.timeout_ns ||
+                                *(volatile unsigned int*)(a.flag + 1))) {
+                        atomicOr(a.flag + 1, 1u);
+                        dead = true;
+                        break;
+                    }
+                }
+            }
+            if (STATS) {
+                for (int kk = k; kk <= last; ++kk) {
+                    const int d = kk - m;
+                    maxd = d > maxd ? d : maxd;
+                    ++s_hist[hrow][d < kFreeMaxQ ? d : kFreeMaxQ - 1];
+                }
+            }
+        };
+        auto step = [&]() {
+            double pr[V], cx[V];
+#pragma unroll
+            for (int i = 0; i < V; ++i) pr[i] = A::mul(r, x[i]);
+#pragma unroll
+            for (int i = 0; i < V; ++i) cx[i] = A::mul(c, x[i]);
+#pragma unroll
+            for (int i = 0; i < V; ++i) cx[i] = A::add(i + 1 < V ? pr[i + 1] : pgR, cx[i]);
+#pragma unroll
+            for (int i = 0; i < V; ++i) x[i] = A::add(cx[i], i > 0 ? pr[i - 1] : pgL);
+            if (pinL) x[0] = c1;
+            if (pinR) x[V - 1] = c2;
+        };
+        int k = 0;
+        const bool comm = (a.dbg & 3) != 3;  // A/B only: HEAT_K10_DBG=3 drops all exchange
+        const bool gh = (a.dbg & 2) == 0;    // 2: no ghost polls (publishes kept)
+        for (int rounds = k_end / LH; rounds > 0; --rounds) {
+            if (comm && gh) {
+                side_ghost(needL, ringL, la, lb, k, k + LH - 1, mL, pgL, w * 2);
+                side_ghost(needR, ringR, ra, rb, k, k + LH - 1, mR, pgR, w * 2 + 1);
+            }
+#pragma unroll
+            for (int j = 0; j < LH; ++j) step();
+            k += LH;
+            if (comm) {
+                // probes before the publish: a load issued after a DSMEM
+                // store waits for that store (~50 ns per round, measured)
+                la = ld_slot(slot_addr(ringL, k));
+                lb = ld_slot(slot_addr(ringL, k - LH));
+                ra = ld_slot(slot_addr(ringR, k));
+                rb = ld_slot(slot_addr(ringR, k - LH));
+                publish(k);
+            }
+        }
+        if (k < k_end) {
+            side_ghost(needL, ringL, la, lb, k, k_end - 1, mL, pgL, w * 2);
+            side_ghost(needR, ringR, ra, rb, k, k_end - 1, mR, pgR, w * 2 + 1);
+            for (; k < k_end; ++k) step();
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+            bad |= !isfinite(x[i]);
+            a.field[base + i] = x[i];
+        }
+    }
+    if (bad) atomicOr(a.flag, 1u);
+    if (STATS) {
+        if (active) {
+            const int sides = int(p > 0 || a.dirichlet == 0) + int(p + 1 < P || a.dirichlet == 0);
+            atomicAdd(a.stats + kStatReads, (unsigned long long)k_end * (unsigned long long)sides);
+            atomicAdd(a.stats + kStatWaits, waits);
+            atomicMax(a.stats + kStatMaxDelay, (unsigned long long)maxd);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kFreeMaxW * 2 * kFreeMaxQ; i += blockDim.x) {
+            const unsigned int v = (&s_hist[0][0])[i];
+            if (v) atomicAdd(a.stats + kStatDelayHist + i % kFreeMaxQ, (unsigned long long)v);
+        }
+    }
+    cluster_sync_all();
+}
+
 // Points per lane compiled in; a PE of n points runs as Lc = n / V lanes.
 constexpr int kFreeV[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20, 24, 25, 32, 40, 50};
 
@@ -395,6 +815,111 @@ const void* free_kernel_ptr(int V, bool MW) {
     }
 }
 
+template <bool STATS>
+const void* free_lh_kernel_ptr(int V, int LH) {
+    if (LH == 4) switch (V) {
+        case 1: return (const void*)exec_free_lh_kernel<1, 4, STATS>;
+        case 2: return (const void*)exec_free_lh_kernel<2, 4, STATS>;
+        case 3: return (const void*)exec_free_lh_kernel<3, 4, STATS>;
+        case 4: return (const void*)exec_free_lh_kernel<4, 4, STATS>;
+        case 5: return (const void*)exec_free_lh_kernel<5, 4, STATS>;
+        case 6: return (const void*)exec_free_lh_kernel<6, 4, STATS>;
+        case 8: return (const void*)exec_free_lh_kernel<8, 4, STATS>;
+        case 10: return (const void*)exec_free_lh_kernel<10, 4, STATS>;
+        case 12: return (const void*)exec_free_lh_kernel<12, 4, STATS>;
+        case 16: return (const void*)exec_free_lh_kernel<16, 4, STATS>;
+        case 20: return (const void*)exec_free_lh_kernel<20, 4, STATS>;
+        case 24: return (const void*)exec_free_lh_kernel<24, 4, STATS>;
+        case 25: return (const void*)exec_free_lh_kernel<25, 4, STATS>;
+        case 32: return (const void*)exec_free_lh_kernel<32, 4, STATS>;
+        case 40: return (const void*)exec_free_lh_kernel<40, 4, STATS>;
+        case 50: return (const void*)exec_free_lh_kernel<50, 4, STATS>;
+        default: return nullptr;
+    }
+    if (LH == 2) switch (V) {
+        case 1: return (const void*)exec_free_lh_kernel<1, 2, STATS>;
+        case 2: return (const void*)exec_free_lh_kernel<2, 2, STATS>;
+        case 3: return (const void*)exec_free_lh_kernel<3, 2, STATS>;
+        case 4: return (const void*)exec_free_lh_kernel<4, 2, STATS>;
+        case 5: return (const void*)exec_free_lh_kernel<5, 2, STATS>;
+        case 6: return (const void*)exec_free_lh_kernel<6, 2, STATS>;
+        case 8: return (const void*)exec_free_lh_kernel<8, 2, STATS>;
+        case 10: return (const void*)exec_free_lh_kernel<10, 2, STATS>;
+        case 12: return (const void*)exec_free_lh_kernel<12, 2, STATS>;
+        case 16: return (const void*)exec_free_lh_kernel<16, 2, STATS>;
+        case 20: return (const void*)exec_free_lh_kernel<20, 2, STATS>;
+        case 24: return (const void*)exec_free_lh_kernel<24, 2, STATS>;
+        case 25: return (const void*)exec_free_lh_kernel<25, 2, STATS>;
+        case 32: return (const void*)exec_free_lh_kernel<32, 2, STATS>;
+        case 40: return (const void*)exec_free_lh_kernel<40, 2, STATS>;
+        case 50: return (const void*)exec_free_lh_kernel<50, 2, STATS>;
+        default: return nullptr;
+    }
+    return nullptr;
+}
+
+template <bool STATS>
+const void* free_pe_kernel_ptr(int V, int LH) {
+    if (LH == 4) switch (V) {
+        case 1: return (const void*)exec_free_pe_kernel<1, 4, STATS>;
+        case 2: return (const void*)exec_free_pe_kernel<2, 4, STATS>;
+        case 3: return (const void*)exec_free_pe_kernel<3, 4, STATS>;
+        case 4: return (const void*)exec_free_pe_kernel<4, 4, STATS>;
+        case 5: return (const void*)exec_free_pe_kernel<5, 4, STATS>;
+        case 6: return (const void*)exec_free_pe_kernel<6, 4, STATS>;
+        case 8: return (const void*)exec_free_pe_kernel<8, 4, STATS>;
+        case 10: return (const void*)exec_free_pe_kernel<10, 4, STATS>;
+        case 12: return (const void*)exec_free_pe_kernel<12, 4, STATS>;
+        case 16: return (const void*)exec_free_pe_kernel<16, 4, STATS>;
+        case 20: return (const void*)exec_free_pe_kernel<20, 4, STATS>;
+        case 24: return (const void*)exec_free_pe_kernel<24, 4, STATS>;
+        case 25: return (const void*)exec_free_pe_kernel<25, 4, STATS>;
+        case 32: return (const void*)exec_free_pe_kernel<32, 4, STATS>;
+        case 40: return (const void*)exec_free_pe_kernel<40, 4, STATS>;
+        case 50: return (const void*)exec_free_pe_kernel<50, 4, STATS>;
+        default: return nullptr;
+    }
+    if (LH == 2) switch (V) {
+        case 1: return (const void*)exec_free_pe_kernel<1, 2, STATS>;
+        case 2: return (const void*)exec_free_pe_kernel<2, 2, STATS>;
+        case 3: return (const void*)exec_free_pe_kernel<3, 2, STATS>;
+        case 4: return (const void*)exec_free_pe_kernel<4, 2, STATS>;
+        case 5: return (const void*)exec_free_pe_kernel<5, 2, STATS>;
+        case 6: return (const void*)exec_free_pe_kernel<6, 2, STATS>;
+        case 8: return (const void*)exec_free_pe_kernel<8, 2, STATS>;
+        case 10: return (const void*)exec_free_pe_kernel<10, 2, STATS>;
+        case 12: return (const void*)exec_free_pe_kernel<12, 2, STATS>;
+        case 16: return (const void*)exec_free_pe_kernel<16, 2, STATS>;
+        case 20: return (const void*)exec_free_pe_kernel<20, 2, STATS>;
+        case 24: return (const void*)exec_free_pe_kernel<24, 2, STATS>;
+        case 25: return (const void*)exec_free_pe_kernel<25, 2, STATS>;
+        case 32: return (const void*)exec_free_pe_kernel<32, 2, STATS>;
+        case 40: return (const void*)exec_free_pe_kernel<40, 2, STATS>;
+        case 50: return (const void*)exec_free_pe_kernel<50, 2, STATS>;
+        default: return nullptr;
+    }
+    if (LH == 1) switch (V) {
+        case 1: return (const void*)exec_free_pe_kernel<1, 1, STATS>;
+        case 2: return (const void*)exec_free_pe_kernel<2, 1, STATS>;
+        case 3: return (const void*)exec_free_pe_kernel<3, 1, STATS>;
+        case 4: return (const void*)exec_free_pe_kernel<4, 1, STATS>;
+        case 5: return (const void*)exec_free_pe_kernel<5, 1, STATS>;
+        case 6: return (const void*)exec_free_pe_kernel<6, 1, STATS>;
+        case 8: return (const void*)exec_free_pe_kernel<8, 1, STATS>;
+        case 10: return (const void*)exec_free_pe_kernel<10, 1, STATS>;
+        case 12: return (const void*)exec_free_pe_kernel<12, 1, STATS>;
+        case 16: return (const void*)exec_free_pe_kernel<16, 1, STATS>;
+        case 20: return (const void*)exec_free_pe_kernel<20, 1, STATS>;
+        case 24: return (const void*)exec_free_pe_kernel<24, 1, STATS>;
+        case 25: return (const void*)exec_free_pe_kernel<25, 1, STATS>;
+        case 32: return (const void*)exec_free_pe_kernel<32, 1, STATS>;
+        case 40: return (const void*)exec_free_pe_kernel<40, 1, STATS>;
+        case 50: return (const void*)exec_free_pe_kernel<50, 1, STATS>;
+        default: return nullptr;
+    }
+    return nullptr;
+}
+
 }  // namespace
 
 // PE warps per CTA and the cluster size for `warps` PE warps: one warp per SM
@@ -414,13 +939,15 @@ bool free_layout(size_t warps, int* W_out, int* C_out) {
 
 // The PE geometry K10 uses for P PEs of n points: Wp warps per PE (1, 2 or
 // 4), Lc lanes per warp (2 <= Lc <= 32) and V points per lane, Wp*Lc*V = n.
-// Measured on B200 (tools/probe_k10.py), a PE warp's step costs ~210 cycles
-// of latency up to ~8 points per lane and ~8V + 150 cycles of issue beyond
-// (V = 20: 330, V = 40: 467); the seam exchange of a multi-warp PE adds
-// ~30.  The geometry with the lowest estimate wins, as long as every PE warp
-// keeps an SM sub-partition of its own (ties: fewer warps per PE).
+// Step costs measured on B200 (tools/probe_k10.py, cycles per step): a
+// one-warp PE in rounds with lane halos (q >= 4) ~140 + 8V for V >= 4 (halos
+// from one lane away; V = 2-3: ~195, V = 1: ~224); one lane per PE (K10t)
+// ~40 + 8n; the plain
+// per-step kernel ~max(210, 150 + 8V); a PE over 2-4 warps (seams swapped
+// every step) ~310 + 8V.  The cheapest geometry wins, as long as every PE
+// warp keeps an SM sub-partition of its own (ties: fewer warps per PE).
 // HEAT_K10_MAX_WP caps Wp (A/B).
-bool free_geometry(size_t n, size_t P, int* V_out, int* Lc_out, int* Wp_out) {
+bool free_geometry(size_t n, size_t P, size_t q, int* V_out, int* Lc_out, int* Wp_out) {
     static const int max_wp = [] {
         const char* e = std::getenv("HEAT_K10_MAX_WP");
         return e ? std::max(1, std::atoi(e)) : 4;
@@ -433,12 +960,17 @@ bool free_geometry(size_t n, size_t P, int* V_out, int* Lc_out, int* Wp_out) {
         int W, C;
         if (!free_layout(P * size_t(Wp), &W, &C)) continue;
         const bool spread = W == 4;  // one warp per SM sub-partition
-        for (int V : kFreeV) {
+        for (int V : kFreeV) {  // every V that fits (the cost is not monotone in V)
             if (m % size_t(V) != 0) continue;
             const size_t Lc = m / size_t(V);
-            if (Lc < 2) break;
+            if (Lc < 1 || (Lc == 1 && Wp > 1)) break;
             if (Lc > 32) continue;
-            const int cost = std::max(210, 8 * V + 150) + (Wp > 1 ? 30 : 0);
+            // (one point per lane: halos from several lanes away, ~60 more)
+            // one lane per PE (K10t): ~8n + 40
+            const int cost = Wp > 1    ? 310 + 8 * V
+                             : Lc == 1 ? 40 + 8 * V + (q >= 4 ? 0 : 60)
+                             : (q >= 4 ? (V >= 4 ? 140 + 8 * V : V >= 2 ? 195 : 224)
+                                       : std::max(210, 150 + 8 * V));
             const bool better = best_Wp == 0 || (spread && !best_spread) ||
                                 (spread == best_spread && cost < best_cost);
             if (better) {
@@ -448,7 +980,6 @@ bool free_geometry(size_t n, size_t P, int* V_out, int* Lc_out, int* Wp_out) {
                 best_cost = cost;
                 best_spread = spread;
             }
-            break;  // the smallest V for this Wp
         }
     }
     if (best_Wp == 0) return false;
@@ -458,11 +989,33 @@ bool free_geometry(size_t n, size_t P, int* V_out, int* Lc_out, int* Wp_out) {
     return true;
 }
 
+// A Dirichlet field that fits ONE warp at >= 4 points per lane (N <= 128,
+// e.g. the reference's measure() at N = 100): all PEs share that warp (K10w).
+// Their edges move with the warp's own halo shuffles, so every PE reads its
+// neighbours' current values -- no barrier, no ring, every delay 0 (the
+// synchronous trajectory, which the free-running model allows) -- in K10r's
+// rounds with the whole field as one segment.
+bool free_one_warp(size_t N, int bc_kind, int* V_out, int* Lc_out) {
+    if (bc_kind != HEAT_BC_DIRICHLET || std::getenv("HEAT_K10_NO_ONE_WARP")) return false;
+    for (int V : kFreeV) {
+        if (V > 5) return false;  // wider lanes: the PE warps of K10r/K10t are faster
+        if (V < 4 || N % size_t(V) != 0) continue;
+        const size_t Lc = N / size_t(V);
+        if (Lc < 2) return false;
+        if (Lc <= 32) {
+            *V_out = V;
+            *Lc_out = int(Lc);
+            return true;
+        }
+    }
+    return false;
+}
+
 bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end) {
     int V, Lc, Wp, W, C;
     return q >= 1 && q <= size_t(kFreeMaxQ) && per_pe < N && N % per_pe == 0 &&
            k_end < size_t(1) << 31 &&
-           free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) &&
+           free_geometry(per_pe, N / per_pe, q, &V, &Lc, &Wp) &&
            free_layout(N / per_pe * size_t(Wp), &W, &C) &&
            !std::getenv("HEAT_NO_FREE_CLUSTER");
 }
@@ -473,9 +1026,15 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
                   double c2, size_t per_pe, size_t q, size_t k_end, double* field_out,
                   unsigned long long* stats_host, float* kernel_ms) {
     int V = 0, Lc = 0, Wp = 0, W = 0, C = 0;
-    if (!free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) ||
-        !free_layout(N / per_pe * size_t(Wp), &W, &C))
+    const bool one_warp = free_one_warp(N, bc_kind, &V, &Lc);
+    if (one_warp) {
+        Wp = 1;
+        W = 1;
+        C = 1;
+    } else if (!free_geometry(per_pe, N / per_pe, q, &V, &Lc, &Wp) ||
+               !free_layout(N / per_pe * size_t(Wp), &W, &C)) {
         return fail(HEAT_EINVAL, "exec_run: no K10 layout for this partition");
+    }
     const size_t pitch = (N + 63) / 64 * 64;
     HB_TRY(ensure_buffers(d, pitch * sizeof(double)));
     double* field = static_cast<double*>(d.buf[0]);
@@ -490,11 +1049,13 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     }
     FreeArgs a{};
     a.field = field;
-    a.n = int(per_pe);
-    a.P = int(N / per_pe);
+    a.n = one_warp ? int(N) : int(per_pe);  // K10w: the field is one segment
+    a.P = one_warp ? 1 : int(N / per_pe);
     a.Lc = Lc;
     a.W = W;
     a.Wp = Wp;
+    static const int dbg = std::getenv("HEAT_K10_DBG") ? std::atoi(std::getenv("HEAT_K10_DBG")) : 0;
+    a.dbg = dbg;
     a.r = r;
     a.c = 1.0 - 2.0 * r;  // core.hpp:108
     a.c1 = c1;
@@ -505,7 +1066,16 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     a.flag = d.flag;
     a.stats = dstats;
     a.timeout_ns = 20ull * 1000000000ull;
-    const void* fn = stats_host ? free_kernel_ptr<true>(V, Wp > 1) : free_kernel_ptr<false>(V, Wp > 1);
+    // single-warp PEs: rounds of LH steps with lane halos (K10r) when the
+    // staleness bound allows LH <= q/2 and the halo fits one lane (V >= LH);
+    // q <= 3 and V = 1 take the plain per-step kernel.  HEAT_K10_PLAIN=1: always plain.
+    static const bool plain = std::getenv("HEAT_K10_PLAIN") != nullptr;
+    const int LH = one_warp ? 4 : plain || Wp > 1 ? 0 : q >= 8 ? 4 : q >= 4 ? 2 : 0;
+    const int LHt = q >= 8 ? 4 : q >= 4 ? 2 : 1;  // K10t rounds
+    const void* fn =
+        Lc == 1 ? (stats_host ? free_pe_kernel_ptr<true>(V, LHt) : free_pe_kernel_ptr<false>(V, LHt))
+        : LH    ? (stats_host ? free_lh_kernel_ptr<true>(V, LH) : free_lh_kernel_ptr<false>(V, LH))
+                : (stats_host ? free_kernel_ptr<true>(V, Wp > 1) : free_kernel_ptr<false>(V, Wp > 1));
     if (!fn) return fail(HEAT_ELOGIC, "K10: points per lane not compiled");
     const int smem = W * 2 * kFreeR * int(sizeof(FreeSlot));
     if (C > 8) HB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -545,8 +1115,17 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
 extern "C" int heat_free_geometry(size_t N, size_t per_pe, size_t q, int* points_per_lane,
                                   int* lanes, int* warps_per_cta, int* cluster, int* warps_per_pe) {
     int V = 0, Lc = 0, Wp = 0, W = 0, C = 0;
+    if (hb::free_eligible(N, per_pe, q, 1) && hb::free_one_warp(N, HEAT_BC_DIRICHLET, &V, &Lc)) {
+        // K10w (Dirichlet fields of <= 128 points): one warp holds the field
+        if (points_per_lane) *points_per_lane = V;
+        if (lanes) *lanes = Lc;
+        if (warps_per_cta) *warps_per_cta = 1;
+        if (cluster) *cluster = 1;
+        if (warps_per_pe) *warps_per_pe = 0;  // all PEs share the warp
+        return HEAT_OK;
+    }
     const bool ok = hb::free_eligible(N, per_pe, q, 1) &&
-                    hb::free_geometry(per_pe, N / per_pe, &V, &Lc, &Wp) &&
+                    hb::free_geometry(per_pe, N / per_pe, q, &V, &Lc, &Wp) &&
                     hb::free_layout(N / per_pe * size_t(Wp), &W, &C);
     if (points_per_lane) *points_per_lane = ok ? V : 0;
     if (lanes) *lanes = ok ? Lc : 0;

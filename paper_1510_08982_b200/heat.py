@@ -737,8 +737,11 @@ class ExecResult:
 
 
 def exec_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
-             part: PartitionSpec, cfg: ExecConfig) -> ExecResult:
-    """async_exec.hpp:68-70 / async_exec.cpp:263-279"""
+             part: PartitionSpec, cfg: ExecConfig, stats: bool = True) -> ExecResult:
+    """async_exec.hpp:68-70 / async_exec.cpp:263-279.  `stats` (a B200
+    extension, BarrierFree only): collect the kernel's delay histogram into
+    `res.stats`; measure() times the runs without it, as the reference's
+    exec_run collects nothing."""
     v = _field(u0)
     out = np.empty_like(v)
     dur = C.c_uint64(0)
@@ -747,12 +750,13 @@ def exec_run(u0: TemperatureField, params: SolverParams, bc: BoundaryCondition,
     _lib.check(_lib.lib().heat_exec_run(_lib.dptr(v), v.size, params.r(), bc.kind, bc.c1, bc.c2,
                                         part.per_pe(), cfg.workers, cfg.k_end, int(cfg.mode),
                                         int(cfg.record_lag), cfg.q_free, _lib.dptr(out),
-                                        C.byref(dur), C.byref(lag), C.byref(st)), "exec_run")
+                                        C.byref(dur), C.byref(lag), C.byref(st) if stats else None),
+               "exec_run")
     res = ExecResult(TemperatureField(out), [cfg.k_end] * cfg.workers, int(dur.value))
     if cfg.record_lag:
         res.lag = LagStats(int(lag.reads), int(lag.min_lag), int(lag.max_lag),
                            [int(x) for x in lag.histogram], int(lag.overflow))
-    if cfg.mode == ExecMode.BarrierFree:
+    if cfg.mode == ExecMode.BarrierFree and stats:
         res.stats = AsyncStats(int(st.reads), int(st.max_delay),
                                [int(x) for x in st.delay_histogram], int(st.waits),
                                float(st.residual_sum))
@@ -786,7 +790,8 @@ def measure(grid_sizes: Sequence[int], modes: Sequence[ExecMode], reps: int, k_e
         part = PartitionSpec(n, n // workers)
         for mode in modes:
             cfg = ExecConfig(workers, k_end, mode, False)
-            times = sorted(exec_run(u0, params, bc, part, cfg).duration_ns for _ in range(reps))
+            times = sorted(exec_run(u0, params, bc, part, cfg, stats=False).duration_ns
+                           for _ in range(reps))
             rows.append(BenchRow(n, mode, reps, times[len(times) // 2], times[0]))
     return rows
 

@@ -61,7 +61,10 @@ def test_k10_free_bounded_delays(H, N, n):
                      H.PartitionSpec(N, n), H.ExecConfig(N // n, k, H.ExecMode.BarrierFree))
     st = res.stats
     P = N // n
-    assert st.reads == 2 * (P - 1) * k  # every PE edge read once per step
+    if N <= 160:  # K10w: the whole field shares one warp, no ring reads (delay 0)
+        assert st.reads == 0 and st.max_delay == 0
+    else:
+        assert st.reads == 2 * (P - 1) * k  # every PE edge read once per step
     assert sum(st.delay_histogram) == st.reads
     assert st.max_delay <= 7 and all(x == 0 for x in st.delay_histogram[8:])
     v = res.field.values()

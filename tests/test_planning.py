@@ -170,9 +170,9 @@ def free_geometry(N, n, q=8):
 
 
 @pytest.mark.parametrize("N,n,expect", [
-    (100, 10, (1, 10, 4, 3, 1)), (1000, 100, (4, 25, 4, 3, 1)), (10000, 1000, (10, 25, 4, 10, 4)),
-    (100, 5, (1, 5, 4, 5, 1)), (1000, 50, (2, 25, 4, 5, 1)), (10000, 500, (10, 25, 4, 10, 2)),
-    (100, 25, (1, 25, 4, 1, 1)), (1024, 128, (4, 32, 4, 2, 1)), (4096, 32, (1, 32, 8, 16, 1)),
+    (100, 10, (2, 5, 4, 3, 1)), (1000, 100, (4, 25, 4, 3, 1)), (10000, 1000, (10, 25, 4, 10, 4)),
+    (100, 5, (1, 5, 4, 5, 1)), (1000, 50, (2, 25, 4, 5, 1)), (10000, 500, (20, 25, 4, 5, 1)),
+    (100, 25, (5, 5, 4, 1, 1)), (1024, 128, (4, 32, 4, 2, 1)), (4096, 32, (2, 16, 8, 16, 1)),
     (256, 2, (1, 2, 8, 16, 1)), (1000, 250, (10, 25, 4, 1, 1)), (10000, 2500, (25, 25, 4, 4, 4)),
     (10000, 2000, (20, 25, 4, 5, 4)), (10000, 5000, (50, 25, 4, 2, 4))])
 def test_k10_free_geometry(N, n, expect):

@@ -11,9 +11,10 @@ from paper_1510_08982_b200 import heat as H
 
 lib = _lib.lib()
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
+Q = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # exec_run's q_free (0: the default)
 
 
-def run(N, P, mode, stats, q=0):
+def run(N, P, mode, stats, q=Q):
     u0 = H.cosine_init(N).values()
     out = np.empty_like(u0)
     dur = C.c_uint64(0)
@@ -32,7 +33,7 @@ for P in (4, 5, 10, 20):
         if N % P:
             continue
         geo = [C.c_int(0) for _ in range(5)]
-        ok = lib.heat_free_geometry(N, N // P, 8, *[C.byref(x) for x in geo]) == 0
+        ok = lib.heat_free_geometry(N, N // P, Q or 8, *[C.byref(x) for x in geo]) == 0
         geo = [x.value for x in geo]
         b = run(N, P, 0, False)
         f = run(N, P, 1, False)
