@@ -311,9 +311,16 @@ def config_dict(world, n=N_PER_GPU, strong=False, impl="b200", steps=10):
         d["kernel"] = "reference exec_run(Barriered), std::barrier per step, host threads"
         d["parallelism"] = "host threads"
         return d
-    d["steps_per_pass"] = steps_per_pass() if world == 1 else min(steps_per_pass(), slab_halo())
-    d["kernel"] = sync_kernel_name()
-    d["parallelism"] = "single GPU" if world == 1 else f"slab x{world} (NCCL halo exchange)"
+    if world == 1:
+        d["steps_per_pass"] = steps_per_pass()
+        d["kernel"] = sync_kernel_name()
+        d["parallelism"] = "single GPU"
+    else:
+        d["kernel"] = ("async_stream_kernel<48,64> with q=1 (the exact synchronous scheme), "
+                       "one persistent launch per rank for the whole run")
+        d["parallelism"] = (f"slab x{world}: halos by P2P stores into IPC-mapped neighbour "
+                            "receive rings over NVLink (NCCL/gloo only ship the IPC handles, "
+                            "seed barriers and the final gather)")
     return d
 
 
@@ -342,12 +349,16 @@ def run_b200(args, rank, world, local):
         def advance(k):
             plan.sync_advance(r, bc, k)
     else:
-        solver = MG.SlabSolver(n, r, bc, local, rank, world)
+        # N GPUs: K5 with q = 1 on each rank's slab -- the exact synchronous
+        # scheme -- with the slab halos moving by P2P stores over NVLink into
+        # the neighbours' receive rings; the timed region is ONE seeded run
+        # of all its steps (one launch per rank, no collective inside)
+        solver = MG.AsyncSlabSolver(n, n // ASYNC_PES, 1, bc, local, rank, world)
         solver.plan.fill_sine()  # each slab gets a sine profile (data-independent cost)
         plan = solver.plan
 
         def advance(k):
-            solver.advance(k)
+            solver.advance(r, k)
 
     def barrier():
         if world > 1:
@@ -367,14 +378,19 @@ def run_b200(args, rank, world, local):
         chk.capture(plan.download_range)
         torch.cuda.synchronize()
 
+    if world > 1:
+        solver.prepare()  # seed the run (IPC rings) before the timed region
     launches0 = H.kernel_launches()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
-        for _ in range(args.steps):
-            advance(STEPS_PER_BENCH_STEP)
+        if world == 1:
+            for _ in range(args.steps):
+                advance(STEPS_PER_BENCH_STEP)
+        else:
+            multi_stats = solver.run(r, STEPS_PER_BENCH_STEP * args.steps)
         e1.record(stream)
         barrier()
     plan.synchronize()
@@ -402,9 +418,12 @@ def run_b200(args, rank, world, local):
     # the bound is the FP64 pipe (4 DP instructions per update: 2 DMUL +
     # 2 DADD with the shared r*u products), reported as the headline, and the
     # 16 B/update effective bandwidth beside it.
-    spp = steps_per_pass() if world == 1 else min(steps_per_pass(), slab_halo())
-    passes_per_step = -(-STEPS_PER_BENCH_STEP // spp)
-    sync_launches = passes_per_step * args.steps
+    if world == 1:
+        spp = steps_per_pass()
+        passes_per_step = -(-STEPS_PER_BENCH_STEP // spp)
+        sync_launches = passes_per_step * args.steps
+    else:
+        sync_launches = 1  # one persistent K5 launch for the whole timed run
     per_launch_s = ms * 1e-3 / sync_launches
     updates = float(n) * STEPS_PER_BENCH_STEP * args.steps
     alg_bytes = BYTES_PER_UPDATE * updates / sync_launches  # per launch (average)
@@ -416,6 +435,7 @@ def run_b200(args, rank, world, local):
     fp64_achieved = alg_ops / per_launch_s / 1e12
     traffic = ncu_traffic_per_launch()
     roofline = {
+        "kernel": "sync_tb_kernel (K1)" if world == 1 else "async_stream_kernel (K5, q=1)",
         "bound": "fp64", "achieved": round(fp64_achieved, 3), "peak": round(fp64_peak, 3),
         "unit": "TFLOP/s", "frac": round(fp64_achieved / fp64_peak, 4),
         # ncu DRAM bytes of one 64-step pass over 2^30 points (scales with the points)
@@ -621,38 +641,52 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups, parity):
 
 
 def run_async_multi(args, H, MG, torch, stream, n, r, bc, sync_glups, rank, world, local):
-    """G-GPU legs over NVLink P2P (heat_plan_xlink_*): each rank runs K5 on its
-    2^30-point slab; PE boundaries between GPUs exchange edge values by P2P
-    stores into the neighbour's receive rings.  q=1 free mode is the exact
-    synchronous scheme with no collective in the loop; q=8 free-running."""
+    """The other G-GPU legs: K5 free-running (q = 8) over the same P2P rings,
+    timed as the headline (one seeded run of all steps), and -- for comparison
+    only -- K1 slabs with the 64-point halos moved by NCCL every pass."""
     import torch.distributed as dist
     per_pe = n // ASYNC_PES
     out = {"pes_per_gpu": ASYNC_PES, "points_per_pe": per_pe,
            "transport": "P2P stores into IPC-mapped neighbour receive rings (NVLink)"}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    for name, q in (("sync_p2p", 1), ("free", 8)):
-        solver = MG.AsyncSlabSolver(n, per_pe, q, bc, local, rank, world)
-        solver.plan.fill_sine()
-        for _ in range(max(1, args.warmup)):
-            solver.advance(r, STEPS_PER_BENCH_STEP)
+    total = STEPS_PER_BENCH_STEP * args.steps
+
+    def timed(fn):
         torch.cuda.synchronize()
         dist.barrier()
         e0.record(stream)
-        st = None
-        for _ in range(args.steps):
-            st = solver.advance(r, STEPS_PER_BENCH_STEP)
+        res = fn()
         e1.record(stream)
-        solver.plan.synchronize()
-        ms = e0.elapsed_time(e1)
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        v = float(n) * world * STEPS_PER_BENCH_STEP * args.steps / (ms * 1e-3) / 1e9
-        out[name] = {"value": round(v, 3), "unit": UNIT, "q": q,
-                     "max_delay": int(st.max_delay), "reads_per_run": int(st.reads),
-                     "vs_sync_nccl_halo": round(v / sync_glups, 4)}
-        solver.plan.close()
+        return res, float(n) * world * total / (ms * 1e-3) / 1e9
+
+    solver = MG.AsyncSlabSolver(n, per_pe, 8, bc, local, rank, world)
+    solver.plan.fill_sine()
+    solver.advance(r, STEPS_PER_BENCH_STEP)  # warm-up run
+    solver.prepare()
+    st, v = timed(lambda: solver.run(r, total))
+    out["free"] = {"value": round(v, 3), "unit": UNIT, "q": 8, "max_delay": int(st.max_delay),
+                   "reads_per_run": int(st.reads), "vs_sync": round(v / sync_glups, 4)}
+    solver.plan.close()
+
+    slab = MG.SlabSolver(n, r, bc, local, rank, world)
+    slab.plan.fill_sine()
+    slab.advance(STEPS_PER_BENCH_STEP)
+
+    def run_slab():
+        for _ in range(args.steps):
+            slab.advance(STEPS_PER_BENCH_STEP)
+    _, v = timed(run_slab)
+    out["sync_nccl_halo"] = {"value": round(v, 3), "unit": UNIT,
+                             "what": "K1 slabs, 64-point halos by NCCL send/recv every pass "
+                                     "(comparison only; the headline moves halos by P2P)",
+                             "vs_p2p_sync": round(v / sync_glups, 4)}
+    slab.plan.close()
     return out
 
 
@@ -699,10 +733,32 @@ def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance, parity):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
     v = float(n) * world * STEPS_PER_BENCH_STEP / t / 1e9
-    return {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-            "d2h_bytes_per_step": 8 * n, "steps": k,
-            "api": "heat_sync_run (C-ABI, pinned host buffers)" if world == 1 else
-                   "heat.Plan upload/advance/download per rank"}
+    out = {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+           "d2h_bytes_per_step": 8 * n, "steps": k,
+           "api": "heat_sync_run (C-ABI, pinned host buffers)" if world == 1 else
+                  "heat.Plan upload/advance/download per rank"}
+    if world == 1:
+        # The drop-in caller's case: the reference's API takes std::vector
+        # fields (integration/heat_core_b200.cpp passes their data pointers),
+        # i.e. PAGEABLE host memory -- the same call with ordinary numpy arrays.
+        import numpy as np
+        p_in = np.empty(n)
+        p_in[:] = a_in
+        p_out = np.empty(n)
+        pt = []
+        for i in range(3):
+            t0 = time.perf_counter()
+            H._lib.check(H._lib.lib().heat_sync_run(
+                H._lib.dptr(p_in), n, r, bc.kind, bc.c1, bc.c2, STEPS_PER_BENCH_STEP,
+                STEPS_PER_BENCH_STEP, H._lib.dptr(p_out), None, None, 0, None), "heat_sync_run")
+            if i > 0:
+                pt.append(time.perf_counter() - t0)
+        same = bool(np.array_equal(p_out.view(np.uint64), a_out.view(np.uint64)))
+        out["pageable"] = {"value": round(float(n) * STEPS_PER_BENCH_STEP / statistics.median(pt) / 1e9, 3),
+                           "unit": UNIT, "steps": len(pt), "same_result_as_pinned": same,
+                           "api": "heat_sync_run (C-ABI) with pageable numpy host buffers, "
+                                  "as heat::sync_run's std::vector fields arrive"}
+    return out
 
 
 def main():

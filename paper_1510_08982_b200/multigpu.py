@@ -140,37 +140,59 @@ class AsyncSlabSolver:
     """Asynchronous FTCS over G GPUs: each rank runs K5 on its slab; the PE
     boundaries between ranks exchange edge values by P2P stores over NVLink
     into the neighbour's receive rings (heat_plan_xlink_*).  NCCL/gloo only
-    ships the IPC handles and the per-run barrier after seeding; GPUs never
-    barrier per step.  q = 1 free mode is the exact synchronous scheme."""
+    ships the IPC handles and the per-run barriers around seeding; GPUs never
+    barrier per step.  q = 1 free mode is the exact synchronous scheme.
+
+    `link` is what holds the slab and its rings: the device plan (default), or
+    for the CPU tests a stand-in with the same five calls (xlink_setup ->
+    handle bytes, xlink_connect, xlink_seed, xlink_advance, synchronize) --
+    the host protocol here (handle exchange, drain + barrier before seeding,
+    barrier after) is the same for both."""
 
     def __init__(self, n_local: int, per_pe: int, q: int, bc, device: int, rank: int,
-                 world: int, group=None):
-        from .heat import Plan
-        torch.cuda.set_device(device)
+                 world: int, group=None, link=None):
         self.rank, self.world, self.group, self.bc = rank, world, group, bc
         self.periodic = not bc.is_dirichlet()
-        self.plan = Plan(n_local, device, rank, world)
-        stream = torch.cuda.current_stream(device)
-        if stream.cuda_stream == 0:
-            raise ValueError("AsyncSlabSolver needs a non-default current stream")
-        self.plan.set_stream(stream.cuda_stream)
+        if link is None:
+            from .heat import Plan
+            torch.cuda.set_device(device)
+            link = Plan(n_local, device, rank, world)
+            stream = torch.cuda.current_stream(device)
+            if stream.cuda_stream == 0:
+                raise ValueError("AsyncSlabSolver needs a non-default current stream")
+            link.set_stream(stream.cuda_stream)
+        self.plan = link
         handle = self.plan.xlink_setup(per_pe, q, bc)
         left, right = exchange_handles(handle, rank, world, self.periodic, group)
         self.plan.xlink_connect(left, right)
         dist.barrier(group=group)
 
-    def advance(self, r: float, steps: int, model=None):
-        """One fresh run of `steps` steps from the current field."""
-        # No neighbour may still be consuming the previous run when seeding
-        # rewrites its receive ring and resets its progress words: every rank
-        # drains its own stream, then all meet, then all seed.
+    def _drain(self):
         self.plan.synchronize()
-        torch.cuda.synchronize()
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+
+    def prepare(self):
+        """Seed a fresh run from the current field (the only collectives of a
+        run: two barriers).  No neighbour may still be consuming the previous
+        run when seeding rewrites its receive ring and resets its progress
+        words: every rank drains its own stream, then all meet, then all seed;
+        and no rank may start stepping before every neighbour has seeded."""
+        self._drain()
         dist.barrier(group=self.group)
         self.plan.xlink_seed()  # push my step-0 edges into the neighbours' rings
-        torch.cuda.synchronize()
+        self._drain()
         dist.barrier(group=self.group)
+
+    def run(self, r: float, steps: int, model=None):
+        """The seeded run: ONE persistent K5 launch per rank for all `steps`;
+        the ranks couple only through P2P stores into each other's rings."""
         return self.plan.xlink_advance(r, self.bc, steps, model)
+
+    def advance(self, r: float, steps: int, model=None):
+        """One fresh run of `steps` steps from the current field."""
+        self.prepare()
+        return self.run(r, steps, model)
 
     def gather(self) -> torch.Tensor:
         """The global field (device tensor on every rank)."""
