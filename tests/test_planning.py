@@ -170,25 +170,29 @@ def free_geometry(N, n, q=8):
 
 
 @pytest.mark.parametrize("N,n,expect", [
-    (100, 10, (2, 5, 4, 3, 1)), (1000, 100, (4, 25, 4, 3, 1)), (10000, 1000, (10, 25, 4, 10, 4)),
-    (100, 5, (1, 5, 4, 5, 1)), (1000, 50, (2, 25, 4, 5, 1)), (10000, 500, (20, 25, 4, 5, 1)),
-    (100, 25, (5, 5, 4, 1, 1)), (1024, 128, (4, 32, 4, 2, 1)), (4096, 32, (2, 16, 8, 16, 1)),
-    (256, 2, (1, 2, 8, 16, 1)), (1000, 250, (10, 25, 4, 1, 1)), (10000, 2500, (25, 25, 4, 4, 4)),
+    (100, 10, (4, 25, 1, 1, 0)), (1000, 100, (4, 25, 4, 3, 1)), (10000, 1000, (10, 25, 4, 10, 4)),
+    (100, 5, (4, 25, 1, 1, 0)), (1000, 50, (5, 10, 4, 5, 1)), (10000, 500, (20, 25, 4, 5, 1)),
+    (100, 25, (4, 25, 1, 1, 0)), (1024, 128, (4, 32, 4, 2, 1)), (4096, 32, (4, 8, 8, 16, 1)),
+    (256, 2, (2, 1, 8, 16, 1)), (100, 1, (4, 25, 1, 1, 0)), (1000, 250, (10, 25, 4, 1, 1)), (10000, 2500, (25, 25, 4, 4, 4)),
     (10000, 2000, (20, 25, 4, 5, 4)), (10000, 5000, (50, 25, 4, 2, 4))])
 def test_k10_free_geometry(N, n, expect):
     """K10 (exec_free.cu): Wp warps per PE of Lc lanes x V points, Wp*Lc*V = n
-    exactly with 2 <= Lc <= 32, chosen by the measured step-cost estimate; 4
-    warps per CTA (one per SM sub-partition) up to a 16-CTA cluster, then 8."""
+    exactly with 1 <= Lc <= 32 (Lc = 1: one thread per PE), chosen by the
+    measured step-cost estimate; 4 warps per CTA (one per SM sub-partition) up
+    to a 16-CTA cluster, then 8; Dirichlet fields of <= 160 points share one
+    warp (K10w, Wp reported 0)."""
     st, got = free_geometry(N, n)
     assert st == 0 and got == expect
     V, Lc, W, C, Wp = got
     P = N // n
-    assert V * Lc * Wp == n and 2 <= Lc <= 32 and W % Wp == 0
+    if Wp == 0:  # K10w: a Dirichlet field of <= 160 points in one warp, V = 4 or 5
+        assert V * Lc == N and V in (4, 5) and 2 <= Lc <= 32 and (W, C) == (1, 1)
+        return
+    assert V * Lc * Wp == n and 1 <= Lc <= 32 and W % Wp == 0
     assert W * C >= P * Wp and W * (C - 1) < P * Wp
 
 
 @pytest.mark.parametrize("N,n,q", [(1031 * 2, 1031, 8),   # prime PE width: no lanes split
-                                   (100, 1, 8),           # one point per PE
                                    (1000, 100, 17),       # q beyond the 32-slot ring
                                    (100, 100, 8),         # one PE: the sync path
                                    (129 * 4, 4, 8),       # 129 PEs > 16 x 8 warps
