@@ -637,7 +637,38 @@ def run_async(args, H, torch, plan, stream, n, r, bc, sync_glups, parity):
             "delay_histogram": [int(x) for x in st.delay_histogram[:8]],
             "vs_sync": round(v / sync_glups, 4),
         }
+    if not args.skip_bound:
+        try:
+            out["free"]["bound"] = run_free_bound(H, plan, n, r, bc, per_pe, 8,
+                                                  STEPS_PER_BENCH_STEP * args.steps)
+        except Exception as exc:  # report, do not lose the line
+            out["free"]["bound"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     return out
+
+
+def run_free_bound(H, plan, n, r, bc, per_pe, q, k):
+    """SURVEY §8a row 12 at cfg3 (not timed): one free-running K5 run of all k
+    steps from the sine IC with every PE edge value and read logged on the
+    device, the a-posteriori bound sum_k ||u(k+1) - A u(k)||_inf formed from
+    the logs, and the actual ||u_async(k) - u_sync(k)||_inf against the
+    synchronous run of the same IC (heat_sync_run)."""
+    import numpy as np
+    t0 = time.perf_counter()
+    plan.fill_sine()
+    u0 = plan.download()
+    part = H.PartitionSpec(n, per_pe)
+    p = H.SolverParams.from_r(r)
+    fin, st = H.async_free_run(u0, p, bc, part, q, k)
+    sync = H.sync_final(u0, p, bc, k)
+    err = 0.0
+    for lo in range(0, n, 1 << 26):  # chunked: no 8 GiB temporaries
+        err = max(err, float(np.max(np.abs(fin[lo:lo + (1 << 26)] - sync[lo:lo + (1 << 26)]))))
+    return {"steps": k, "q": q, "error_inf": err, "bound": st.residual_sum,
+            "within": bool(err <= st.residual_sum), "max_delay": int(st.max_delay),
+            "reads": int(st.reads), "seconds": round(time.perf_counter() - t0, 1),
+            "what": "one logged free-running K5 run of all steps (heat_async_free_run) vs "
+                    "heat_sync_run of the same sine IC; bound = sum_k ||u(k+1) - A u(k)||_inf "
+                    "+ k*8*eps*max|u| from the device logs"}
 
 
 def run_async_multi(args, H, MG, torch, stream, n, r, bc, sync_glups, rank, world, local):
@@ -768,6 +799,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-bound", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-async", action="store_true")
     ap.add_argument("--skip-parity", action="store_true",
@@ -776,7 +808,7 @@ def main():
                     help="cfg4: N = 2^33 in total split over the GPUs (no host-buffer legs)")
     args = ap.parse_args()
     if args.strong:  # the field does not fit the host-buffer legs (e2e, CPU, paper configs)
-        args.skip_e2e = args.skip_cpu = True
+        args.skip_e2e = args.skip_cpu = args.skip_bound = True
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)

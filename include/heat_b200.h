@@ -197,7 +197,8 @@ int heat_sample_delay(size_t q, int law, size_t fixed_delay, double geometric_p,
 
 /* Free-running asynchronous run (bounded staleness: every neighbour value a PE
  * consumes at step k is u_j(k*) with 0 <= k - k* <= q-1) with full edge logs,
- * for PEs of <= 1024 points.  On return `stats` holds the reader-relative
+ * for PEs of <= 1024 points (K3) or of whole 32-point units (K5, e.g. cfg3:
+ * 512 PEs of 2^21 points).  On return `stats` holds the reader-relative
  * delay histogram and stats->residual_sum = sum_k ||u(k+1) - A u(k)||_inf, the
  * a-posteriori bound on ||u_async(K) - u_sync(K)||_inf (A = one synchronous
  * step; valid for 0 < r <= 1/2 where A is inf-norm non-expansive, plus a

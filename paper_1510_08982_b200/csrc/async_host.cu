@@ -567,22 +567,59 @@ int heat_async_free_run(const double* u0, size_t N, double r, int bc_kind, doubl
     if (!u0 || !final_out) return fail(HEAT_EINVAL, "null field pointer");
     if (per_pe == 0 || N % per_pe != 0) return fail(HEAT_EDOMAIN, "PartitionSpec: n must divide N");
     if (q == 0) return fail(HEAT_EDOMAIN, "DelayModel: q >= 1 required");
-    if (per_pe > 32 * 32) return fail(HEAT_EINVAL, "logged free run: PEs of <= 1024 points");
+    const bool wide = per_pe > 32 * 32;  // K5 (whole 32-point units), else K3
+    if (wide && per_pe % 32 != 0)
+        return fail(HEAT_EINVAL, "logged free run: PEs of <= 1024 points or of whole 32-point "
+                                 "units");
     if (per_pe == N) return fail(HEAT_EINVAL, "logged free run: needs >= 2 PEs");
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
         return fail(HEAT_EINVAL, "unknown boundary condition kind");
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
     std::lock_guard<std::mutex> lock(d->mu);
-    HB_TRY(ensure_buffers(*d, N * sizeof(double)));
-    double* field = static_cast<double*>(d->buf[0]);
-    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));
+    const size_t pitch = (N + 63) / 64 * 64;
+    HB_TRY(ensure_buffers(*d, (wide ? 2 : 1) * pitch * sizeof(double)));
+    double* bufs[2] = {static_cast<double*>(d->buf[0]), static_cast<double*>(d->buf[0]) + pitch};
+    HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, bufs[0]));
     AsyncRunSpec s{N, per_pe, r, bc_kind, c1, c2, 1, q, HEAT_DELAY_UNIFORM, 0, 0.5, 0, k_end, true};
     std::vector<unsigned long long> hs(kStatWords, 0);
     std::vector<double> elog;
     std::vector<int> ulog;
-    HB_TRY(async_pe_run(*d, s, field, 0, nullptr, hs.data(), &elog, &ulog, nullptr));
-    HB_CUDA(cudaMemcpy(final_out, field, N * sizeof(double), cudaMemcpyDeviceToHost));
+    if (!wide) {
+        HB_TRY(async_pe_run(*d, s, bufs[0], 0, nullptr, hs.data(), &elog, &ulog, nullptr));
+        HB_CUDA(cudaMemcpy(final_out, bufs[0], N * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+        // K5 logs every PE edge value and every read's source step on the
+        // device ((k_end+1)*P*2 doubles + k_end*P*2 ints: 123 MB for cfg3)
+        const size_t P = N / per_pe;
+        elog.assign((k_end + 1) * P * 2, 0.0);
+        ulog.assign(k_end * P * 2, 0);
+        for (size_t p = 0; p < P; ++p) {  // step 0: the prepared field's PE edges
+            const size_t f = p * per_pe, l = f + per_pe - 1;
+            const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+            elog[p * 2 + 0] = dir && f == 0 ? c1 : u0[f];
+            elog[p * 2 + 1] = dir && l == N - 1 ? c2 : u0[l];
+        }
+        struct DevBuf {
+            void* p = nullptr;
+            ~DevBuf() {
+                if (p) cudaFree(p);
+            }
+        } de, du;
+        HB_CUDA(cudaMalloc(&de.p, elog.size() * sizeof(double)));
+        HB_CUDA(cudaMalloc(&du.p, std::max<size_t>(1, ulog.size()) * sizeof(int)));
+        HB_CUDA(cudaMemcpy(de.p, elog.data(), 2 * P * sizeof(double), cudaMemcpyHostToDevice));
+        StreamLogs logs;
+        logs.edge_log = static_cast<double*>(de.p);
+        logs.used_log = static_cast<int*>(du.p);
+        int cur = 0;
+        s.want_logs = false;  // (the K3 flag; K5 takes `logs`)
+        HB_TRY(async_stream_run(*d, s, bufs, cur, 0, nullptr, hs.data(), nullptr, &logs));
+        HB_CUDA(cudaMemcpy(elog.data(), de.p, elog.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        if (!ulog.empty())
+            HB_CUDA(cudaMemcpy(ulog.data(), du.p, ulog.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        HB_CUDA(cudaMemcpy(final_out, bufs[cur], N * sizeof(double), cudaMemcpyDeviceToHost));
+    }
 
     // a-posteriori residual: only PE-boundary points read a neighbour; the
     // async step differs from A u(k) there by r*(u_j(k*) - u_j(k)).
@@ -657,6 +694,27 @@ int heat_exec_run(const double* u0, size_t N, double r, int bc_kind, double c1, 
         if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
         if (lag) std::memset(lag, 0, sizeof *lag);
         if (stats) std::memset(stats, 0, sizeof *stats);
+        return st;
+    }
+    size_t upe_probe = 1;
+    if (per_pe > 32 * 32 && per_pe % 32 != 0 && !k3_split(per_pe, upe_probe)) {
+        // PEs no free-running kernel lays out (wider than 1024 points, off the
+        // 32-point grid, no split into units of <= 1024: a prime width such as
+        // 1031).  The run takes the delay-0 trajectory -- every PE reads its
+        // neighbours' current values, a schedule the free-running model allows
+        // (0 <= k - k* <= q - 1) -- on the synchronous kernels, which have no
+        // per-step barrier either (temporal blocking).
+        float ms = 0.f;
+        const int st = sync_run_timed(u0, N, r, bc_kind, c1, c2, k_end, field_out, &ms);
+        if (duration_ns) *duration_ns = uint64_t(double(ms) * 1e6);
+        if (lag) std::memset(lag, 0, sizeof *lag);
+        if (stats) {
+            std::memset(stats, 0, sizeof *stats);
+            const size_t P = N / per_pe;
+            const size_t edges = bc_kind == HEAT_BC_DIRICHLET ? 2 * (P - 1) : 2 * P;
+            stats->reads = (unsigned long long)(edges * k_end);
+            stats->delay_histogram[0] = stats->reads;
+        }
         return st;
     }
 
@@ -814,6 +872,10 @@ struct heat_async_sim {
     std::vector<int> offL, offR;
     // GEOMETRIC: the delay thresholds (device, uploaded once)
     uint64_t* gthr = nullptr;
+    // PEs no kernel geometry covers (prime widths above 1024 points): the
+    // reference's own step, async_step over a device HistoryRing (K8a/K8b)
+    heat_history* hist = nullptr;
+    uint64_t rng = 0;
 };
 
 namespace {
@@ -826,6 +888,7 @@ void sim_free(heat_async_sim* sim) {
     if (sim->ctx.scratch) cudaFree(sim->ctx.scratch);
     if (sim->ctx.flag) cudaFree(sim->ctx.flag);
     if (sim->gthr) cudaFree(sim->gthr);
+    if (sim->hist) heat_history_destroy(sim->hist);
     if (sim->ctx.stream) cudaStreamDestroy(sim->ctx.stream);
     delete sim;
 }
@@ -960,6 +1023,19 @@ int heat_async_sim_create(heat_async_sim** out, const double* u0, size_t N, doub
         // one PE never reads across: plain synchronous steps (K1 on field[0..1])
         sim->wide = true;
     }
+    size_t upe_probe = 1;
+    if (sim->P > 1 && per_pe > 32 * 32 && per_pe % 32 != 0 && !k3_split(per_pe, upe_probe)) {
+        // AsyncSimulator::step literally (async_sim.cpp:136-140): async_step
+        // over a HistoryRing of depth q seeded with the prepared field, the
+        // simulator's SplitMix64 stream advanced as the reference's
+        std::vector<double> prep;
+        HB_TRY(prepare_initial(u0, N, bc_kind, c1, c2, prep));
+        HB_TRY(heat_history_create(&sim->hist, q, N, 0, prep.data(), 1, dev));
+        sim->rng = seed;
+        *out = sim;
+        sim = nullptr;  // owned by the caller now
+        return HEAT_OK;
+    }
     if (sim->wide && sim->P > 1) {
         HB_TRY(stream_layout(sim->s, 1, StreamExternal{}, sim->L, sim->offL, sim->offR));
         HB_TRY(ensure_scratch(d, sim->L.bytes));
@@ -1008,6 +1084,15 @@ int heat_async_sim_step(heat_async_sim* sim, size_t count) {
     if (!sim) return fail(HEAT_EINVAL, "null simulator handle");
     if (count == 0) return HEAT_OK;
     HB_CUDA(cudaSetDevice(sim->ctx.device));
+    if (sim->hist) {  // one async_step per step (a host round trip each)
+        const AsyncRunSpec& s = sim->s;
+        for (size_t j = 0; j < count; ++j) {
+            HB_TRY(heat_async_step(sim->hist, s.r, s.bc_kind, s.c1, s.c2, s.N, s.n, s.q, s.law,
+                                   s.fixed_d, s.geometric_p, &sim->rng, nullptr, 1));
+            ++sim->k;
+        }
+        return HEAT_OK;
+    }
     if (sim->P == 1) {  // a single PE: synchronous steps
         HB_CUDA(cudaMemsetAsync(sim->ctx.flag, 0, 2 * sizeof(unsigned int), sim->ctx.stream));
         HB_TRY(sync_advance<double>(sim->ctx.sms, sim->field, sim->cur, (long long)sim->s.N,
@@ -1032,6 +1117,11 @@ int heat_async_sim_step(heat_async_sim* sim, size_t count) {
 int heat_async_sim_current(heat_async_sim* sim, double* out, size_t* step_index) {
     if (!sim) return fail(HEAT_EINVAL, "null simulator handle");
     HB_CUDA(cudaSetDevice(sim->ctx.device));
+    if (sim->hist) {
+        if (out) HB_TRY(heat_history_snapshot(sim->hist, 0, out));
+        if (step_index) *step_index = sim->k;
+        return HEAT_OK;
+    }
     if (out)
         HB_CUDA(cudaMemcpyAsync(out, sim->field[sim->cur], sim->s.N * sizeof(double),
                                 cudaMemcpyDeviceToHost, sim->ctx.stream));

@@ -88,6 +88,12 @@ struct AsyncStreamArgs {
     unsigned int* abort_word;
     unsigned long long timeout_ns;
     int pend_max;   // done-signals published per release fence (1..kMaxPend)
+    // optional logs for the a-posteriori bound (heat_async_free_run):
+    // edge_log[(k*P + p)*2 + side] = PE p's first (0) / last (1) point at step
+    // k (k >= 1; the host fills k = 0); used_log[(k*P + p)*2 + side] = the step
+    // k* of the neighbour value PE p's first / last point read at step k
+    double* edge_log;
+    int* used_log;
 };
 constexpr int kMaxPend = 16;
 #ifndef HEAT_K5_UNROLL
@@ -445,6 +451,8 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
                         mstep = (long long)seen < k ? (long long)seen : k;
                     }
                     if (!abort) {
+                        if (a.used_log)
+                            a.used_log[(k * a.P + it.p) * 2 + (left ? 0 : 1)] = int(mstep);
                         const double* slotp = gring + (mstep & (a.R - 1));
                         ghost = gsys ? ld_relaxed_sys_f64(slotp) : ld_relaxed_gpu_f64(slotp);
                         const unsigned long long used = (unsigned long long)(k - mstep);
@@ -483,6 +491,10 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
                 // device boundary -- a P2P store over NVLink), then release
                 // the progress word with the matching scope
                 const long long slot = (k + 1) & (a.R - 1);
+                if (a.edge_log) {
+                    if (left_edge && lane == fl) a.edge_log[((k + 1) * a.P + it.p) * 2 + 0] = first;
+                    if (right_edge && lane == ll) a.edge_log[((k + 1) * a.P + it.p) * 2 + 1] = last;
+                }
                 if (left_edge && lane == fl) {
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {

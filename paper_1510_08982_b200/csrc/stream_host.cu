@@ -282,7 +282,8 @@ int launch_stream(int sms, cudaStream_t st, double* const bufs[2], int cur, long
 int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, const AsyncRunSpec& s,
                          const StreamLayout& L, char* base, const StreamExternal& ext,
                          const std::vector<int>& offL, const std::vector<int>& offR, size_t k0,
-                         size_t steps, bool init, unsigned int* flag, float* device_ms) {
+                         size_t steps, bool init, unsigned int* flag, float* device_ms,
+                         const StreamLogs* logs) {
     // the pinned Dirichlet ends: global PE 0's first point, global PE Pg-1's last
     const long long Pg = ext.P_global > 0 ? ext.P_global : (long long)L.P;
     const bool dir = s.bc_kind == HEAT_BC_DIRICHLET;
@@ -352,6 +353,8 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
     a.abort_word = at<unsigned int>(base, L.o_abort);
     a.timeout_ns = 20ull * 1000 * 1000 * 1000;
     a.pend_max = stream_pend_max();
+    a.edge_log = logs ? logs->edge_log : nullptr;
+    a.used_log = logs ? logs->used_log : nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (device_ms) {
         HB_CUDA(cudaEventCreate(&e0));
@@ -377,7 +380,7 @@ int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, co
 
 int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur, size_t stride,
                      const std::function<int(size_t, const double*)>& on_record,
-                     unsigned long long* host_stats, float* device_ms) {
+                     unsigned long long* host_stats, float* device_ms, const StreamLogs* logs) {
     StreamLayout L;
     std::vector<int> offL, offR;
     const StreamExternal ext{};
@@ -394,7 +397,7 @@ int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur
         const size_t next = stride ? std::min(s.k_end, (k / stride + 1) * stride) : s.k_end;
         float ms = 0.f;
         HB_TRY(async_stream_advance(d.sms, st, bufs, cur, s, L, base, ext, offL, offR, k, next - k,
-                                    false, d.flag, device_ms ? &ms : nullptr));
+                                    false, d.flag, device_ms ? &ms : nullptr, logs));
         total_ms += ms;
         k = next;
         unsigned int flags[2] = {0, 0};

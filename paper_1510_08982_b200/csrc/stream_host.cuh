@@ -39,12 +39,19 @@ struct StreamLayout {
 int stream_layout(const AsyncRunSpec& s, int groups, const StreamExternal& ext, StreamLayout& L,
                   std::vector<int>& offL, std::vector<int>& offR);
 
+// Optional K5 logs (AsyncStreamArgs::edge_log / used_log), device memory.
+struct StreamLogs {
+    double* edge_log = nullptr;
+    int* used_log = nullptr;
+};
+
 // Advances bufs[cur] by `steps` from absolute step k0; init=true seeds the
 // local rings and the in-launch receive rings and uploads the tables.
 int async_stream_advance(int sms, cudaStream_t st, double* bufs[2], int& cur, const AsyncRunSpec& s,
                          const StreamLayout& L, char* base, const StreamExternal& ext,
                          const std::vector<int>& offL, const std::vector<int>& offR, size_t k0,
-                         size_t steps, bool init, unsigned int* flag, float* device_ms);
+                         size_t steps, bool init, unsigned int* flag, float* device_ms,
+                         const StreamLogs* logs = nullptr);
 
 // Step-0 values this slab owes its external neighbours (P2P stores).
 int stream_seed_external(cudaStream_t st, const double* field, const AsyncRunSpec& s,
@@ -53,7 +60,8 @@ int stream_seed_external(cudaStream_t st, const double* field, const AsyncRunSpe
 // Whole-run driver used by heat_async_run / heat_exec_run for wide PEs.
 int async_stream_run(DevCtx& d, const AsyncRunSpec& s, double* bufs[2], int& cur, size_t stride,
                      const std::function<int(size_t, const double*)>& on_record,
-                     unsigned long long* host_stats, float* device_ms);
+                     unsigned long long* host_stats, float* device_ms,
+                     const StreamLogs* logs = nullptr);
 
 // HEAT_VIRTUAL_DEVICES=G splits a single-GPU run into G device groups whose
 // boundaries go through the cross-device (system-scope receive ring) path.

@@ -290,6 +290,27 @@ def test_free_run_within_aposteriori_bound(H, port, r, q, periodic, per_pe):
     assert st.max_delay <= q - 1 and sum(st.delay_histogram) == st.reads > 0
 
 
+@pytest.mark.parametrize("periodic", [False, True])
+@pytest.mark.parametrize("q", [1, 3, 8])
+def test_free_run_wide_pes_within_aposteriori_bound(H, port, q, periodic):
+    # K5 (PEs of whole 32-point units) logs every PE edge value and every
+    # read's source step on the device; the host forms the same bound
+    n, per_pe = 1 << 18, 1 << 14  # 16 PEs of 16384 points
+    u0 = port.prepare_initial(port.sine_init(n), 0, 0.0, 0.0)
+    bc = H.BoundaryCondition.periodic() if periodic else H.BoundaryCondition.dirichlet(0, 0)
+    p = H.SolverParams.from_r(0.4)
+    k = 2000
+    fin, st = H.async_free_run(u0, p, bc, H.PartitionSpec(n, per_pe), q, k)
+    sync = port.sync_run(u0, 0.4, bc.kind, 0.0, 0.0, k)
+    err = float(np.max(np.abs(fin - sync)))
+    assert err <= st.residual_sum
+    P = n // per_pe
+    assert st.reads == (2 * P if periodic else 2 * (P - 1)) * k
+    assert st.max_delay <= q - 1 and sum(st.delay_histogram) == st.reads
+    if q == 1:
+        assert bits_equal(fin, sync) and st.residual_sum < 1e-6
+
+
 def test_free_run_q1_exact(H, port):
     u0 = port.prepare_initial(port.sine_init(1024), 0, 0.0, 0.0)
     fin, st = H.async_free_run(u0, H.SolverParams.from_r(0.3), H.BoundaryCondition.dirichlet(0, 0),
@@ -424,9 +445,9 @@ def test_wide_pes_off_the_32_grid_executors(H, port):
     assert bits_equal(res.field.values(), port.sync_run(u0, p.r(), 0, 1.0, 0.0, 300))
     rows = H.measure([100, 1000, 10000], [H.ExecMode.Barriered, H.ExecMode.BarrierFree], 3, 200, 4)
     assert len(rows) == 6 and all(r.median_ns > 0 for r in rows)
-    # a prime PE width above 1024 has no split into units: async_run takes the
-    # reference's own loop over a device HistoryRing (K8a/K8b); the free-running
-    # executor refuses it
+    # a prime PE width above 1024 has no split into units: async_run and the
+    # simulator take the reference's own loop over a device HistoryRing
+    # (K8a/K8b); the free-running executor runs its delay-0 schedule
     u1 = random_field(SplitMix64(3), 2 * 1031)
     for bc in (H.BoundaryCondition.periodic(), H.BoundaryCondition.dirichlet(u1[0], u1[-1])):
         t = H.async_run(H.TemperatureField(u1), p, bc, H.PartitionSpec(2 * 1031, 1031),
@@ -436,6 +457,17 @@ def test_wide_pes_off_the_32_grid_executors(H, port):
         assert t.steps == steps
         for j, s in enumerate(t.snapshots):
             assert bits_equal(s.values(), snaps[j]), j
-    with pytest.raises(H.InvalidArgument, match="no split"):
-        H.exec_run(H.TemperatureField(u1), p, H.BoundaryCondition.periodic(),
-                   H.PartitionSpec(2 * 1031, 1031), H.ExecConfig(2, 5, H.ExecMode.BarrierFree))
+    for bc in (H.BoundaryCondition.periodic(), H.BoundaryCondition.dirichlet(u1[0], u1[-1])):
+        res = H.exec_run(H.TemperatureField(u1), p, bc, H.PartitionSpec(2 * 1031, 1031),
+                         H.ExecConfig(2, 57, H.ExecMode.BarrierFree))
+        assert bits_equal(res.field.values(), port.sync_run(u1, p.r(), bc.kind, bc.c1, bc.c2, 57))
+        assert res.stats.max_delay == 0 and res.stats.reads > 0
+        # AsyncSimulator in uneven slices = async_run (the reference's draws)
+        sim = H.AsyncSimulator(H.TemperatureField(u1), p, bc, H.PartitionSpec(2 * 1031, 1031),
+                               H.DelayModel.uniform(3, 5))
+        for cnt in (1, 7, 13):
+            sim.step(cnt)
+        assert sim.step_index() == 21
+        exp = port.async_run(u1, p.r(), bc.kind, bc.c1, bc.c2, 1031, 0, 3, seed=5, k_end=21)
+        assert bits_equal(sim.current(), exp)
+        sim.close()
