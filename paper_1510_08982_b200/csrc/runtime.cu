@@ -7,6 +7,10 @@
 #include <memory>
 #include <utility>
 
+#include <cstring>
+#include <thread>
+#include <vector>
+
 #include "runtime.cuh"
 
 namespace hb {
@@ -108,6 +112,46 @@ int ensure_scratch(DevCtx& d, size_t bytes) {
     }
     d.scratch_bytes = bytes;
     return HEAT_OK;
+}
+
+int host_ring(DevCtx& d, unsigned char** slots) {
+    if (!d.ring) {
+        HB_CUDA(cudaHostAlloc(&d.ring, kRingSlots * kRingSlotBytes, cudaHostAllocDefault));
+        for (auto& e : d.ring_ev) HB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    for (int j = 0; j < kRingSlots; ++j)
+        slots[j] = static_cast<unsigned char*>(d.ring) + size_t(j) * kRingSlotBytes;
+    return HEAT_OK;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+    constexpr size_t kMinPart = 8ull << 20;
+    const int T = int(std::max<size_t>(1, std::min<size_t>(size_t(threads), bytes / kMinPart)));
+    if (T <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(size_t(T));
+    const size_t part = (bytes / size_t(T) + 63) / 64 * 64;
+    for (int t = 0; t < T; ++t) {
+        const size_t lo = size_t(t) * part;
+        if (lo >= bytes) break;
+        const size_t len = std::min(part, bytes - lo);
+        pool.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len);
+        });
+    }
+    for (auto& th : pool) th.join();
+}
+
+bool host_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear it: an unknown pointer is ordinary host memory
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
 }
 
 unsigned char* host_stage(DevCtx& d, size_t bytes) {

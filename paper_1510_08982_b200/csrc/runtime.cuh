@@ -115,7 +115,21 @@ struct DevCtx {
     size_t snaps_bytes = 0;
     void* host = nullptr;          // pinned staging of the small one-shot calls
     size_t host_bytes = 0;
+    // pinned ring for large PAGEABLE fields (the streamed sync_run): slots
+    // filled / drained by host threads while the copy engines move the rest
+    void* ring = nullptr;
+    cudaEvent_t ring_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+
+// A ring of kRingSlots pinned slots of kRingSlotBytes for staging a pageable
+// host field through the copy engines (allocated once per device).
+constexpr int kRingSlots = 4;
+constexpr size_t kRingSlotBytes = 128ull << 20;
+int host_ring(DevCtx& d, unsigned char** slots);
+// memcpy with up to `threads` host threads (large pageable <-> pinned copies)
+void parallel_memcpy(void* dst, const void* src, size_t bytes, int threads);
+// true when `p` is ordinary (unregistered, pageable) host memory
+bool host_pageable(const void* p);
 
 // Closes a plan's IPC mappings and frees its xlink state (xlink.cu).
 void xlink_release(heat_plan* p);

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <thread>
+#include <vector>
 
 #include <cudaTypedefs.h>
 
@@ -476,6 +478,25 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     cudaEvent_t ready = ev[C];
     auto E = [&](long long pi, int c) { return ev[size_t(C) + 1 + size_t(pi) * C + c]; };
 
+    // A PAGEABLE field (the drop-in caller's std::vector) would make every
+    // copy block the host inside the driver's own staging, which serialises
+    // the pipeline: it goes through a ring of pinned slots instead, filled
+    // and drained by host threads while the copy engines move the other slots.
+    const bool page_in = host_pageable(u0), page_out = host_pageable(final_out);
+    unsigned char* slots[kRingSlots] = {};
+    if (page_in || page_out) HB_TRY(host_ring(d, slots));
+    const int hthreads = int(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+    const long long slot_pts = (long long)(kRingSlotBytes / sizeof(double));
+    bool slot_busy[kRingSlots] = {};
+    int slot = 0;
+    auto take_slot = [&]() -> int {  // the next slot, once its last copy is done
+        const int j = slot;
+        slot = (slot + 1) % kRingSlots;
+        if (slot_busy[j]) HB_CUDA(cudaEventSynchronize(d.ring_ev[j]));
+        slot_busy[j] = false;
+        return HEAT_OK;
+    };
+
     // the flag reset precedes every upload and every kernel on either stream
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
     HB_CUDA(cudaEventRecord(ready, st));
@@ -484,8 +505,21 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     for (int c = 0; c < C; ++c) {
         const long long a0 = B[c], a1 = B[c + 1];
         cudaStream_t s_c = cs[c & 1];
-        HB_CUDA(cudaMemcpyAsync(bufs[0] + a0, u0 + a0, (a1 - a0) * sizeof(double),
-                                cudaMemcpyHostToDevice, d.h2d));
+        if (!page_in) {
+            HB_CUDA(cudaMemcpyAsync(bufs[0] + a0, u0 + a0, (a1 - a0) * sizeof(double),
+                                    cudaMemcpyHostToDevice, d.h2d));
+        } else {
+            for (long long o = a0; o < a1; o += slot_pts) {
+                const long long cnt = std::min(slot_pts, a1 - o);
+                const int j = slot;
+                HB_TRY(take_slot());
+                parallel_memcpy(slots[j], u0 + o, size_t(cnt) * sizeof(double), hthreads);
+                HB_CUDA(cudaMemcpyAsync(bufs[0] + o, slots[j], size_t(cnt) * sizeof(double),
+                                        cudaMemcpyHostToDevice, d.h2d));
+                HB_CUDA(cudaEventRecord(d.ring_ev[j], d.h2d));
+                slot_busy[j] = true;
+            }
+        }
         HB_CUDA(cudaEventRecord(up[c], d.h2d));
         HB_CUDA(cudaStreamWaitEvent(s_c, up[c], 0));  // chunks <= c are in
         prep_chunk_kernel<<<d.sms * 2, 256, 0, s_c>>>(bufs[0], a0, a1, N, c1, c2, d.flag);
@@ -503,12 +537,42 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // downloads last: a pageable destination makes each copy block the host,
     // which must not hold back the compute launches above
     const int fin = int(S & 1);
+    struct Pending {
+        int j;
+        double* dst;
+        size_t bytes;
+    };
+    std::vector<Pending> pend;  // slot downloads not yet copied out (FIFO)
+    size_t pend_head = 0;
+    auto drain_one = [&]() -> int {
+        const Pending pd = pend[pend_head++];
+        HB_CUDA(cudaEventSynchronize(d.ring_ev[pd.j]));
+        parallel_memcpy(pd.dst, slots[pd.j], pd.bytes, hthreads);
+        slot_busy[pd.j] = false;
+        return HEAT_OK;
+    };
     for (int c = 0; c < C; ++c) {
         const long long a0 = lo(c, S - 1), a1 = hi(c, S - 1);
         HB_CUDA(cudaStreamWaitEvent(d.d2h, E(S - 1, c), 0));
-        HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0, (a1 - a0) * sizeof(double),
-                                cudaMemcpyDeviceToHost, d.d2h));
+        if (!page_out) {
+            HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0, (a1 - a0) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, d.d2h));
+            continue;
+        }
+        for (long long o = a0; o < a1; o += slot_pts) {
+            const long long cnt = std::min(slot_pts, a1 - o);
+            // keep kRingSlots - 1 downloads in flight; copy out the oldest
+            while (pend.size() - pend_head >= size_t(kRingSlots - 1)) HB_TRY(drain_one());
+            const int j = slot;
+            HB_TRY(take_slot());
+            HB_CUDA(cudaMemcpyAsync(slots[j], bufs[fin] + o, size_t(cnt) * sizeof(double),
+                                    cudaMemcpyDeviceToHost, d.d2h));
+            HB_CUDA(cudaEventRecord(d.ring_ev[j], d.d2h));
+            slot_busy[j] = true;
+            pend.push_back({j, final_out + o, size_t(cnt) * sizeof(double)});
+        }
     }
+    while (pend_head < pend.size()) HB_TRY(drain_one());
     HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 1), 0));  // both streams done
     if (C > 1) HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 2), 0));
     unsigned int flags[4] = {0, 0, 0, 0};
