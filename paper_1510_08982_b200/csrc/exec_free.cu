@@ -51,7 +51,6 @@ struct FreeArgs {
     double* field;  // [N] prepared initial field in, final field out
     int n, P, Lc, W;
     int Wp;  // warps per PE (1, 2 or 4; divides W)
-    int dbg; // A/B only (HEAT_K10_DBG): 1 = no publish, 2 = no ghost probes (results wrong)
     double r, c, c1, c2;
     int dirichlet;
     long long k_end;
@@ -741,25 +740,19 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_pe_kernel(const F
             if (pinR) x[V - 1] = c2;
         };
         int k = 0;
-        const bool comm = (a.dbg & 3) != 3;  // A/B only: HEAT_K10_DBG=3 drops all exchange
-        const bool gh = (a.dbg & 2) == 0;    // 2: no ghost polls (publishes kept)
         for (int rounds = k_end / LH; rounds > 0; --rounds) {
-            if (comm && gh) {
-                side_ghost(needL, ringL, la, lb, k, k + LH - 1, mL, pgL, w * 2);
-                side_ghost(needR, ringR, ra, rb, k, k + LH - 1, mR, pgR, w * 2 + 1);
-            }
+            side_ghost(needL, ringL, la, lb, k, k + LH - 1, mL, pgL, w * 2);
+            side_ghost(needR, ringR, ra, rb, k, k + LH - 1, mR, pgR, w * 2 + 1);
 #pragma unroll
             for (int j = 0; j < LH; ++j) step();
             k += LH;
-            if (comm) {
-                // probes before the publish: a load issued after a DSMEM
-                // store waits for that store (~50 ns per round, measured)
-                la = ld_slot(slot_addr(ringL, k));
-                lb = ld_slot(slot_addr(ringL, k - LH));
-                ra = ld_slot(slot_addr(ringR, k));
-                rb = ld_slot(slot_addr(ringR, k - LH));
-                publish(k);
-            }
+            // probes before the publish: a load issued after a DSMEM store
+            // waits for that store (~10 ns per step, measured)
+            la = ld_slot(slot_addr(ringL, k));
+            lb = ld_slot(slot_addr(ringL, k - LH));
+            ra = ld_slot(slot_addr(ringR, k));
+            rb = ld_slot(slot_addr(ringR, k - LH));
+            publish(k);
         }
         if (k < k_end) {
             side_ghost(needL, ringL, la, lb, k, k_end - 1, mL, pgL, w * 2);
@@ -1054,8 +1047,6 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     a.Lc = Lc;
     a.W = W;
     a.Wp = Wp;
-    static const int dbg = std::getenv("HEAT_K10_DBG") ? std::atoi(std::getenv("HEAT_K10_DBG")) : 0;
-    a.dbg = dbg;
     a.r = r;
     a.c = 1.0 - 2.0 * r;  // core.hpp:108
     a.c1 = c1;
