@@ -243,8 +243,9 @@ __global__ void __launch_bounds__(SyncTB<double, V, H>::kThreads, SyncTB<double,
     // the host guarantees a PE's last tile holds >= H points, so no interior
     // tile's window reaches into the next PE
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the __shared__ array itself: a round trip
+    // through uintptr_t loses the address space (generic LD/ST, ptxas SASS)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char* wbase = smem + warp * 2 * T::kBufBytes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T::kWarpsPerCta * 2 * T::kBufBytes) + 2 * warp;

@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H, W>::kThreads, SyncTB<Real, 
     static_assert(NBUF == 1 || NBUF == 2, "one or two window buffers per warp");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 128B swizzle needs 1024-B aligned buffers
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the __shared__ array itself: a round trip
+    // through uintptr_t loses the address space (generic LD/ST, ptxas SASS)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const Real* __restrict__ src = static_cast<const Real*>(a.src);
     Real* __restrict__ dst = static_cast<Real*>(a.dst);
     const long long len = a.len;
