@@ -12,8 +12,9 @@
 //   heat::exec_run      async_exec.hpp:68-70    -> heat_exec_run
 //   heat::ensemble_run  analysis.hpp:36-52      -> heat_ensemble_run
 //
-// Everything else (AsyncSimulator stepping, CSV, the CLI) keeps running on the
-// reference's CPU code.  oracle/Makefile target `acceptance-b200` links
+//   heat::AsyncSimulator::step  async_sim.cpp:136-140  -> the device async_step
+//
+// Everything else (CSV, the CLI) keeps running on the reference's CPU code.  oracle/Makefile target `acceptance-b200` links
 // the reference's acceptance suite (proj/tests/acceptance.cpp) this way.
 #include <algorithm>
 #include <chrono>
@@ -150,16 +151,12 @@ Trajectory async_run(const TemperatureField& u0, const SolverParams& params,
     return t;
 }
 
-// async_step over the caller's (host) ring: the held snapshots go to a device
-// ring at the same step, K8a/K8b compute the step, and the caller's stream is
-// left where the reference would leave it (D draws, or through the failing
-// draw on a logic_error).  A one-PE partition draws nothing and is not touched.
-TemperatureField async_step(const HistoryRing& hist, const SolverParams& params,
-                            const BoundaryCondition& bc, const PartitionSpec& part,
-                            const DelayModel& model, SplitMix64& rng) {
-    sync_strict();
-    if (part.total() != hist.grid_size())  // async_sim.cpp:113-114
-        throw std::invalid_argument("async_step: partition inconsistent with grid");
+namespace {
+// The device step over a host ring into `out` (no TemperatureField: the
+// simulator's step does not validate, async_sim.cpp:136-140).
+void async_step_device(const HistoryRing& hist, const SolverParams& params,
+                       const BoundaryCondition& bc, const PartitionSpec& part,
+                       const DelayModel& model, SplitMix64& rng, std::vector<double>& out) {
     const std::size_t n = hist.grid_size(), k = hist.current_step();
     const std::size_t held = std::min(hist.depth(), k + 1);
     std::vector<double> rows(held * n);
@@ -170,7 +167,7 @@ TemperatureField async_step(const HistoryRing& hist, const SolverParams& params,
     const bool draws = part.total() / part.per_pe() > 1;
     const std::uint64_t s0 = draws ? take_position(rng) : 0;
     std::uint64_t s = s0;
-    std::vector<double> out(n);
+    out.resize(n);
     const int st = heat_async_step(h, params.r(), bc_kind(bc), bc.c1, bc.c2, part.total(),
                                    part.per_pe(), model.q, law_of(model), model.fixed_delay,
                                    model.geometric_p, &s, out.data(), 0);
@@ -180,6 +177,33 @@ TemperatureField async_step(const HistoryRing& hist, const SolverParams& params,
         for (std::uint64_t j = 1; j < m; ++j) rng.next();
     }
     throw_on(st);
+}
+}  // namespace
+
+// AsyncSimulator::step (async_sim.cpp:136-140) with the step on the device:
+// the simulator's own ring and SplitMix64 stream go through the same device
+// async_step as heat::async_step, then the push.  (The class's members are
+// laid out in the reference header; step() is the only out-of-line member
+// that computes, so it is the one substituted.)
+void AsyncSimulator::step() {
+    sync_strict();
+    async_step_device(ring_, params_, bc_, part_, model_, rng_, scratch_);
+    ring_.push(scratch_);
+    scratch_.resize(ring_.grid_size());
+}
+
+// async_step over the caller's (host) ring: the held snapshots go to a device
+// ring at the same step, K8a/K8b compute the step, and the caller's stream is
+// left where the reference would leave it (D draws, or through the failing
+// draw on a logic_error).  A one-PE partition draws nothing and is not touched.
+TemperatureField async_step(const HistoryRing& hist, const SolverParams& params,
+                            const BoundaryCondition& bc, const PartitionSpec& part,
+                            const DelayModel& model, SplitMix64& rng) {
+    sync_strict();
+    if (part.total() != hist.grid_size())  // async_sim.cpp:113-114
+        throw std::invalid_argument("async_step: partition inconsistent with grid");
+    std::vector<double> out;
+    async_step_device(hist, params, bc, part, model, rng, out);
     return TemperatureField(std::move(out));
 }
 

@@ -159,10 +159,12 @@ def test_sample_delay_stream(H):
 
 
 def test_reference_binding_async_step(gpu):
-    """heat::async_step through integration/heat_core_b200.cpp (the reference's
-    own types, GPU ring + K8a/K8b) prints exactly what the reference prints:
-    exception class, result hash, and the caller's stream position after the
-    call, for 200 seeded rings (oracle/binding_check.cpp)."""
+    """heat::async_step and heat::AsyncSimulator::step through
+    integration/heat_core_b200.cpp (the reference's own types, GPU ring +
+    K8a/K8b) print exactly what the reference prints: exception class, result
+    hash, and the caller's stream position after the call for 200 seeded rings;
+    field hashes and the step index of 60 seeded simulators stepped 1-40 times
+    (oracle/binding_check.cpp)."""
     import os
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -171,6 +173,6 @@ def test_reference_binding_async_step(gpu):
         pytest.skip("oracle/_ref/binding_check_* not built (needs /root/reference at build time)")
     ref, b200 = (subprocess.run([b], capture_output=True, text=True, timeout=300, check=True).stdout
                  for b in bins)
-    assert len(ref.splitlines()) == 200
-    assert "logic_error" in ref
+    assert len(ref.splitlines()) == 260
+    assert "logic_error" in ref and sum(l.startswith("sim ") for l in ref.splitlines()) == 60
     assert b200 == ref
