@@ -8,8 +8,10 @@ r = from_r(0.4), Dirichlet(0,0), sine initial profile, 10^4 FTCS time steps.
 One bench STEP = 1000 FTCS time steps over the whole field, so the default
 --steps 10 is exactly the cfg3 run.  For N > 1 GPUs (torchrun, one rank per
 GPU) each rank owns a 2^30-point slab of a G*2^30 domain (weak scaling; at
-G = 8 the total is cfg4's 2^33) and exchanges heat_slab_halo()-point ghosts
-(64) with its neighbours every pass of as many steps.
+G = 8 the total is cfg4's 2^33); the timed run is K5 with q = 1 (the exact
+synchronous scheme) whose slab-boundary tiles store their edge values
+straight into the neighbours' receive rings over NVLink (one seeded run, one
+launch per rank, no collective inside).
 
 Arms
   b200       the sm_100a kernels (libheat_b200.so) -- value is device-timed
@@ -391,6 +393,9 @@ def run_b200(args, rank, world, local):
                 advance(STEPS_PER_BENCH_STEP)
         else:
             multi_stats = solver.run(r, STEPS_PER_BENCH_STEP * args.steps)
+            if int(multi_stats.max_delay) != 0:  # q = 1 must read only current values
+                raise RuntimeError(f"P2P sync run consumed a stale value "
+                                   f"(max delay {multi_stats.max_delay})")
         e1.record(stream)
         barrier()
     plan.synchronize()
