@@ -148,8 +148,8 @@ int heat_set_device(int device);
 uint64_t heat_kernel_launches(void);
 /* The f64 synchronous pass kernel in use (HEAT_SYNC_VARIANT selects among
  * compiled variants): points per lane, window buffers per warp, exact points
- * per tile, steps per HBM pass (= halo points per side).  Host-only; no
- * device needed. */
+ * per tile (K1s: per chunk of tiles), steps per HBM pass (= halo points per
+ * side).  Host-only; no device needed. */
 int heat_sync_kernel_info(int* points_per_lane, int* buffers, int* exact_points_per_tile,
                           int* steps_per_pass);
 

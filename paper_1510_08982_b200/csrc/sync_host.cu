@@ -9,6 +9,7 @@
 #include <cudaTypedefs.h>
 
 #include "runtime.cuh"
+#include "sync_col.cuh"
 #include "sync_cta.cuh"
 #include "sync_tb.cuh"
 
@@ -59,6 +60,7 @@ int make_chunk_map(CUtensorMap* m, const void* base, long long nchunks, int box_
 // HEAT_SYNC_VARIANT selects one for A/B measurements, the default is the
 // fastest measured on B200 (profiles/).
 using SyncKernelFn = void (*)(CUtensorMap, CUtensorMap, SyncPassArgs);
+using SyncKernelFn3 = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, SyncPassArgs);
 struct SyncVariant {
     SyncKernelFn fn;
     int nbuf;
@@ -71,6 +73,11 @@ struct SyncVariant {
     int warps;                // warps per CTA
     int blocks_per_sm;        // filled by the occupancy query
     bool cta_tiles;           // one tile per CTA (K1c) instead of one per warp
+    SyncKernelFn3 fn3 = nullptr;  // K1s (strips with a carried column): `out` is a chunk's
+    int out1_units = 0;           // outputs; its later tiles store out1_units units
+    const void* kernel() const {
+        return fn3 ? reinterpret_cast<const void*>(fn3) : reinterpret_cast<const void*>(fn);
+    }
 };
 template <typename Real, int V, int NBUF, int UNR, bool TMA_ST = true, int H = 32, bool DYN = false,
           int W = 4>
@@ -86,6 +93,23 @@ SyncVariant variant_cta() {
     using C = SyncCTA<Real, V, H, G>;
     return {sync_cta_kernel<Real, V, H, G, PU>, 2, V, C::kOut, C::kWinUnits, C::kOutUnits,
             C::smem_bytes(), H, true, G, 0, true};
+}
+// K1s (sync_col.cuh): chunks of CH tiles per warp, boundary column carried
+template <typename Real, int V, int H, int CH, int PU>
+SyncVariant variant_col() {
+    using K = SyncCol<Real, V, H, CH>;
+    SyncVariant v{nullptr, 2, V, K::kChunkOut, SyncTB<Real, V, H>::kWinUnits, K::kOut0Units,
+                  K::smem_bytes(), H, true, 4, 0, false};
+    v.fn3 = sync_col_kernel<Real, V, H, CH, PU>;
+    v.out1_units = K::kOut1Units;
+    return v;
+}
+template <typename Real, int CH, int PU>
+SyncVariant variant_col48() {
+    if constexpr (sizeof(Real) == 8)
+        return variant_col<Real, 48, 64, CH, PU>();
+    else
+        return variant<Real, 64, 2, -4, true, 64, true>();  // = variant 15 for f32
 }
 template <typename Real, int PU>
 SyncVariant variant_cta48() {
@@ -109,9 +133,12 @@ SyncVariant variant48() {
 // that cap the steps per pass below the default halo get kHalo32Variant.  tools/ab_sync.sh.
 // 15: as 13 with the pipelined step loop unrolled x4 instead of x2: +0.45% (4017 vs 3998,
 // twice, same box); unrolled x1 (14) loses 1.7%.
-constexpr int kDefaultSyncVariant = 15;
+// 20: K1s (sync_col.cuh), chunks of 8 tiles with a carried boundary column:
+// 4076 vs 4036 GLUPS for 15 on the same box, three times (95.3% of the stepped
+// points exact against 91.7%; FP64 pipe 92.1% vs 93.4% active).
+constexpr int kDefaultSyncVariant = 20;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 20;
+constexpr int kSyncVariants = 23;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -147,6 +174,12 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant_cta48<Real, 4>(),
         // 19: as 18, step loop unrolled 2
         variant_cta48<Real, 2>(),
+        // 20-22: K1s, 48x64 tiles in chunks with a carried boundary column (the
+        //        chunk's later tiles need no left halo): chunks of 8 unrolled 4,
+        //        of 16 unrolled 4, of 8 unrolled 3 (unrolled 2: -1.0%, 1: -4.2%)
+        variant_col48<Real, 8, 4>(),
+        variant_col48<Real, 16, 4>(),
+        variant_col48<Real, 8, 3>(),
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
@@ -165,8 +198,7 @@ template <typename Real>
 int sync_variant(SyncVariant** out, int max_halo = 0) {
     SyncVariant& v = sync_variant_entry<Real>(max_halo);
     // per device (the current one): shared memory limit + occupancy
-    HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(v.fn), v.smem,
-                              v.warps * kWarp, &v.blocks_per_sm));
+    HB_TRY(kernel_smem_config(v.kernel(), v.smem, v.warps * kWarp, &v.blocks_per_sm));
     *out = &v;
     return HEAT_OK;
 }
@@ -193,7 +225,7 @@ struct SyncLauncher {
     SyncVariant* var = nullptr;
     int sms = 0;
     Real* bufs[2] = {nullptr, nullptr};
-    CUtensorMap load_map[2], store_map[2];
+    CUtensorMap load_map[2], store_map[2], store_map1[2];
     SyncPassArgs a{};
 
     int init(int sms_, Real* b[2], const SlabGeom& g, double r, double c1, double c2,
@@ -222,6 +254,9 @@ struct SyncLauncher {
         for (int i = 0; i < 2; ++i) {
             HB_TRY((make_chunk_map<Real, kV>(&load_map[i], bufs[i], a.nchunks, var->win_units)));
             HB_TRY((make_chunk_map<Real, kV>(&store_map[i], bufs[i], a.nchunks, var->out_units)));
+            if (var->fn3)
+                HB_TRY((make_chunk_map<Real, kV>(&store_map1[i], bufs[i], a.nchunks,
+                                                 var->out1_units)));
         }
         return HEAT_OK;
     }
@@ -235,13 +270,24 @@ struct SyncLauncher {
         if (out_lo % kV != 0) return fail(HEAT_ELOGIC, "sync pass: out_lo must be chunk aligned");
         if (out_hi <= out_lo) return HEAT_OK;
         if (nsteps > var->halo) return fail(HEAT_ELOGIC, "sync pass: more steps than the halo");
-        const long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
+        long long tiles = (out_hi - out_lo + var->out - 1) / var->out;
+        long long big = 0;
+        if (var->fn3) {
+            // K1s: chunks of CH tiles, then single tiles for the last ~4 per
+            // resident warp (a single tile emits the first-tile count, out0)
+            const long long out0 = (long long)var->out_units * 32;
+            const long long resident = (long long)sms * var->blocks_per_sm * var->warps;
+            const long long tail = std::min<long long>(out_hi - out_lo, 4 * resident * out0);
+            big = (out_hi - out_lo - tail) / var->out;
+            tiles = big + (out_hi - out_lo - big * var->out + out0 - 1) / out0;
+        }
         const long long want = var->cta_tiles ? tiles : (tiles + var->warps - 1) / var->warps;
         const int grid = int(std::min<long long>(want, (long long)sms * var->blocks_per_sm));
         SyncPassArgs p = a;
         p.out_lo = out_lo;
         p.out_hi = out_hi;
         p.tiles = tiles;
+        p.big_chunks = big;
         p.src = bufs[src];
         p.dst = bufs[src ^ 1];
         p.nsteps = nsteps;
@@ -250,7 +296,11 @@ struct SyncLauncher {
             p.counter = tile_counter_of(a.nonfinite) + counter_slot;
             HB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(unsigned long long), st));
         }
-        var->fn<<<grid, var->warps * kWarp, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
+        if (var->fn3)
+            var->fn3<<<grid, var->warps * kWarp, var->smem, st>>>(load_map[src], store_map[src ^ 1],
+                                                                 store_map1[src ^ 1], p);
+        else
+            var->fn<<<grid, var->warps * kWarp, var->smem, st>>>(load_map[src], store_map[src ^ 1], p);
         HB_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
@@ -448,8 +498,11 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
     // and the last download is short, while neighbouring chunks differ by
     // less than the compute/copy time ratio (~1.8), so neither the compute
     // nor the download stream starves.  Smaller fields: 16 equal chunks.
+    // (K1s: a wave of single tiles too -- each launch deals its range's last
+    // tiles one by one anyway -- so the chunk plan is the K1 one)
+    const long long tile_out = L.var->fn3 ? (long long)L.var->out_units * kV : L.var->out;
     const long long wave = (long long)d.sms * L.var->blocks_per_sm *
-                           (L.var->cta_tiles ? 1 : L.var->warps) * L.var->out;
+                           (L.var->cta_tiles ? 1 : L.var->warps) * tile_out;
     const std::vector<long long> B = stream_chunk_plan(N, wave);
     const int C = int(B.size()) - 1;
     for (int c = 0; c < C; ++c)

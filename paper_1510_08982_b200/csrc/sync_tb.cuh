@@ -291,6 +291,7 @@ struct SyncPassArgs {
     unsigned int* nonfinite;  // set to 1 when an exact output value is not finite
     int check_finite;         // test the outputs of this pass (the last of an advance)
     unsigned long long* counter;  // DYN kernels: tile counter, zero at launch
+    long long big_chunks;         // K1s: chunks of CH tiles before the single-tile tail
 };
 
 // NBUF = 2: the window of the next tile lands in the second buffer while this
