@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_kernel(const Free
 // products as the synchronous scheme (bit-identical when q = 1 forces k* = k,
 // which takes the plain kernel).  LH <= q/2: a neighbour one round behind
 // still satisfies the bound, so lockstep PEs never wait.
-template <int V, int LH, bool STATS>
+// RING = false: K10w (the whole field in one warp; no ring, no ghost, no publish)
+template <int V, int LH, bool STATS, bool RING = true>
 __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const FreeArgs a) {
     constexpr int E = V + 2 * LH;  // own points x[LH, LH+V)
     // lanes whose window holds the PE's outer neighbour position (-1 or
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
     const bool pin_first = active && dir && p == 0 && first_lane;
     const bool pin_last = active && dir && p == P - 1 && last_lane;
     const bool pinL = active && dir && p == 0, pinR = active && dir && p == P - 1;  // warp-uniform
-    const bool edge = (first_lane && needL) || (last_lane && needR);
+    const bool edge = RING && ((first_lane && needL) || (last_lane && needR));
     const int side = first_lane ? 0 : 1;
     const int nb = first_lane ? lpe : rpe;
     const uint32_t my_ring = smem_u32(rings + ((size_t)(active ? w : 0) * 2 + side) * kFreeR);
@@ -564,9 +565,11 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
         int k = 0;
         for (int rounds = k_end / LH; rounds > 0; --rounds) {  // count down: no k_end reload
             exchange();
-            ghost(k, k + LH - 1);
-            pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
-            pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            if constexpr (RING) {
+                ghost(k, k + LH - 1);
+                pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
+                pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            }
             round_steps(std::integral_constant<int, 0>{});
             round_steps(std::integral_constant<int, 1>{});
             if constexpr (LH > 2) {
@@ -574,14 +577,18 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
                 round_steps(std::integral_constant<int, 3>{});
             }
             k += LH;
-            sa = ld_slot(slot_addr(my_ring, k));  // answered while the halos move; issued
-            sb = ld_slot(slot_addr(my_ring, k - LH));  // before the publish (see K10t)
-            publish(k, A::mul(r, first_lane ? x[LH] : x[LH + V - 1]));
+            if constexpr (RING) {
+                sa = ld_slot(slot_addr(my_ring, k));  // answered while the halos move; issued
+                sb = ld_slot(slot_addr(my_ring, k - LH));  // before the publish (see K10t)
+                publish(k, A::mul(r, first_lane ? x[LH] : x[LH + V - 1]));
+            }
         }
         if (k < k_end) {  // the remaining steps, one at a time (plain halo refresh each)
-            ghost(k, k_end - 1);
-            pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
-            pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            if constexpr (RING) {
+                ghost(k, k_end - 1);
+                pgL = kG > 0 ? __shfl_sync(0xffffffffu, pg, 0) : pg;
+                pgR = kG > 0 ? __shfl_sync(0xffffffffu, pg, Lc - 1) : pg;
+            }
             for (; k < k_end; ++k) {
                 exchange();
                 round_steps(std::integral_constant<int, LH - 1>{});
@@ -1064,7 +1071,11 @@ int exec_free_run(DevCtx& d, const double* u0, size_t N, double r, int bc_kind, 
     const int LH = one_warp ? 4 : plain || Wp > 1 ? 0 : q >= 8 ? 4 : q >= 4 ? 2 : 0;
     const int LHt = q >= 8 ? 4 : q >= 4 ? 2 : 1;  // K10t rounds
     const void* fn =
-        Lc == 1 ? (stats_host ? free_pe_kernel_ptr<true>(V, LHt) : free_pe_kernel_ptr<false>(V, LHt))
+        one_warp ? (stats_host ? (V == 4 ? (const void*)exec_free_lh_kernel<4, 4, true, false>
+                                         : (const void*)exec_free_lh_kernel<5, 4, true, false>)
+                               : (V == 4 ? (const void*)exec_free_lh_kernel<4, 4, false, false>
+                                         : (const void*)exec_free_lh_kernel<5, 4, false, false>))
+        : Lc == 1 ? (stats_host ? free_pe_kernel_ptr<true>(V, LHt) : free_pe_kernel_ptr<false>(V, LHt))
         : LH    ? (stats_host ? free_lh_kernel_ptr<true>(V, LH) : free_lh_kernel_ptr<false>(V, LH))
                 : (stats_host ? free_kernel_ptr<true>(V, Wp > 1) : free_kernel_ptr<false>(V, Wp > 1));
     if (!fn) return fail(HEAT_ELOGIC, "K10: points per lane not compiled");
