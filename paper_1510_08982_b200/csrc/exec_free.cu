@@ -417,11 +417,13 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
     // inside the step loop (LDC + a short-scoreboard stall before the first
     // DMUL of every step, measured with ncu)
     __shared__ __align__(16) double s_coef[4];
+    __shared__ int s_qm1;
     if (threadIdx.x == 0) {
         s_coef[0] = a.r;
         s_coef[1] = a.c;
         s_coef[2] = a.c1;
         s_coef[3] = a.c2;
+        s_qm1 = a.q - 1;
     }
     cluster_sync_all();
 
@@ -472,7 +474,8 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
     unsigned long long waits = 0;
     int maxd = 0;
     bool dead = false;
-    const int qm1 = a.q - 1;
+    int qm1;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(qm1) : "r"(smem_u32(&s_qm1)) : "memory");
     const int k_end = int(a.k_end);
     FreeSlot sa = ld_slot(slot_addr(my_ring, 0)), sb = sa;  // probes: round starts k, k - LH
     // ghost for the round of steps k..last
@@ -485,7 +488,11 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
             m = k - LH;
             pg = slot_value(sb);
         }
-        if (edge && !dead && last - m > qm1) {
+        // warp-uniform test first: the common case (no lane needs to wait)
+        // costs one vote, no divergent branch and no reconvergence
+        const bool need = edge && !dead && last - m > qm1;
+        if (__any_sync(0xffffffffu, need)) {
+          if (need) {
             if (STATS) ++waits;
             const uint64_t t0 = globaltimer_ns();
             unsigned spins = 0;
@@ -503,8 +510,9 @@ __global__ void __launch_bounds__(kFreeMaxW * 32, 1) exec_free_lh_kernel(const F
                     break;
                 }
             }
+          }
+          __syncwarp();
         }
-        __syncwarp();
         if (STATS && edge) {
             for (int kk = k; kk <= last; ++kk) {
                 const int d = kk - m;
