@@ -61,7 +61,8 @@ def ncu_traffic_per_launch():
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get("sync_tb_kernel", {}).get("dram_bytes_per_launch")
+        key = "sync_col_kernel" if sync_kernel_info()["exact"] > 2000 else "sync_tb_kernel"
+        return d.get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
