@@ -64,7 +64,40 @@ struct AsyncSmallArgs {
     const int* offL;  // [P] draw rank of PE p's first-point left read, -1 none
     const int* offR;  // [P] ... last-point right read
     const uint64_t* gthr;  // geometric thresholds (q-1)
+    int ncta;  // CTAs in the cluster (CL kernels): each holds a full copy of the field
 };
+
+__device__ __forceinline__ uint32_t small_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void small_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// (x, y) into the same 16 bytes of every other CTA of the cluster
+__device__ __forceinline__ void put_peers2(const double2* p, double x, double y, int rank,
+                                           int ncta) {
+    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
+    for (int c = 0; c < ncta; ++c) {
+        if (c == rank) continue;
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
+        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(x), "d"(y)
+                     : "memory");
+    }
+}
+// v into the same shared-memory word of every other CTA of the cluster
+__device__ __forceinline__ void put_peers(const double* p, double v, int rank, int ncta) {
+    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
+    for (int c = 0; c < ncta; ++c) {
+        if (c == rank) continue;
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+    }
+}
 
 template <int LAW>
 __device__ __forceinline__ int small_delay(const AsyncSmallArgs& a, uint64_t z, int bound,
@@ -96,10 +129,15 @@ __device__ __forceinline__ double pick(const double (&h)[QH], int d) {
     return v;
 }
 
-template <int QH, int LAW>
+// CL: the warps are spread over a cluster of a.ncta CTAs (one warp per SM
+// sub-partition for cfg2); every CTA keeps a full copy of the field and the
+// history table, and the exact owners write their round results into all
+// copies (DSMEM stores) between two cluster barriers.
+template <int QH, int LAW, bool CL>
 __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArgs a) {
     extern __shared__ double smem[];
     __shared__ __align__(16) unsigned char sdel[kAsMaxN / kAsChunk][64 * kAsSub];  // per warp: [stream][step]
+    __shared__ int sstr[kAsMaxN / kAsChunk][64];  // per warp: draw rank of each delay stream
     double* su = smem;                                  // [N]
     double* tab = smem + ((a.N + 1) & ~1);              // [P][2][QH]
     int* soffL = reinterpret_cast<int*>(tab + a.P * 2 * QH);
@@ -108,6 +146,8 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(soffR + a.P) + 7) & ~uintptr_t(7));
     constexpr int V = kAsV, H = kAsHalo, C = kAsChunk;
     const int N = a.N, n = a.n, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rank = CL ? int(small_ctarank()) : 0;
+    const int gw = rank * int(blockDim.x >> 5) + w;  // window index in the field
 
     bool bad_in = false;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -124,7 +164,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     // TemperatureField ctor (core.hpp:45-51) on the raw upload, then
     // prepare_initial's snap of the ends (the host checked |u - c| <= 1e-9)
     if (__syncthreads_or(bad_in)) {
-        if (threadIdx.x == 0) atomicOr(a.flag + 2, 1u);
+        if (threadIdx.x == 0 && rank == 0) atomicOr(a.flag + 2, 1u);
         return;
     }
     if (a.dirichlet && threadIdx.x == 0) {
@@ -138,19 +178,22 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         const int p = i / (2 * QH), side = (i / QH) & 1;
         tab[i] = __dmul_rn(r, su[side ? p * n + n - 1 : p * n]);
     }
-    if (a.snaps)
+    if (a.snaps && rank == 0)
         for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[i] = su[i];
     __syncthreads();
 
-    const long long w0 = (long long)w * C - H;  // window start (unwrapped)
+    const long long w0 = (long long)gw * C - H;  // window start (unwrapped)
     const long long g0 = w0 + (long long)lane * V;
-    const bool active = (long long)w * C < N;  // warp-uniform
+    const bool active = (long long)gw * C < N;  // warp-uniform
     // N and the window starts are multiples of 8, so the Dirichlet ends are
     // always a lane's first (point 0) or last (point N-1) element: the
     // pipelined step re-pins them with two selects
     const bool pinF = a.dirichlet && g0 == 0;
     const bool pinL = a.dirichlet && g0 + V - 1 == N - 1;
     auto real = [&](long long g) { return !a.dirichlet || (g >= 0 && g < N); };
+    // N and g0 are multiples of 8: a lane's 8 points are all real or all
+    // padding, and they wrap together
+    const bool lreal = real(g0);
     auto wrapg = [&](long long g) -> int {
         long long x = g % N;
         return int(x < 0 ? x + N : x);
@@ -184,6 +227,12 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     const int cU = __popc(mU), nstreams = cU + __popc(mD);
     const unsigned below = (1u << lane) - 1u;
     const int sU = __popc(mU & below), sD = cU + __popc(mD & below);
+    if (active && isU) sstr[w][sU] = offU;
+    if (active && isD) sstr[w][sD] = offD;
+    __syncwarp();
+    const int wg0 = wrapg(g0);
+    // exact outputs: lanes 8..23 of the window (the 128-point chunk), inside the field
+    const bool lexact = active && lane >= H / V && lane < (H + C) / V && g0 < N;
     long long k = 0;
     long long next_rec = a.stride > 0 ? a.stride : a.k_end + 1;
     double u[V];
@@ -193,9 +242,11 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         s = min(s, next_rec - k);
         if (active) {
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-                const long long g = g0 + i;
-                u[i] = real(g) ? su[wrapg(g)] : 0.0;
+            for (int i = 0; i < V; i += 2) {
+                const double2 x = lreal ? *reinterpret_cast<const double2*>(&su[wg0 + i])
+                                        : make_double2(0.0, 0.0);
+                u[i] = x.x;
+                u[i + 1] = x.y;
             }
 #pragma unroll
             for (int j = 0; j < QH; ++j) {  // rows of PE edge points only
@@ -210,11 +261,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                 for (int base = 0; base < nstreams * kAsSub; base += 32) {
                     const int it = base + lane;
                     const int si = min(it / kAsSub, nstreams - 1), j = it % kAsSub;
-                    // both shuffles on every lane (convergent), then the pick
-                    const int oU = __shfl_sync(0xffffffffu, offU, __fns(mU, 0, min(si, cU - 1) + 1));
-                    const int oD = __shfl_sync(0xffffffffu, offD,
-                                               __fns(mD, 0, max(si - cU, 0) + 1));
-                    const int off = si < cU ? oU : oD;
+                    const int off = sstr[w][si];
                     const long long kk = kb + j;
                     const int bound = kk < (long long)(a.q - 1) ? int(kk) : a.q - 1;
                     const uint64_t z =
@@ -289,32 +336,49 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
             hF[0] = __dmul_rn(r, u[0]);
             hL[0] = __dmul_rn(r, u[V - 1]);
         }
-        __syncthreads();  // every window (and history row) has been read
+        // every window (and history row) of every copy has been read
+        if (CL)
+            small_cluster_sync();
+        else
+            __syncthreads();
         if (active) {
+            if (lexact) {
 #pragma unroll
-            for (int i = 0; i < V; ++i) {
-                const int idx = lane * V + i;
-                const long long g = g0 + i;
-                if (idx >= H && idx < H + C && g < N) su[g] = u[i];
+                for (int i = 0; i < V; i += 2) {
+                    double2* dst = reinterpret_cast<double2*>(&su[g0 + i]);
+                    *dst = make_double2(u[i], u[i + 1]);
+                    if (CL) put_peers2(dst, u[i], u[i + 1], rank, a.ncta);
+                }
             }
             // a PE edge point's products at steps k+s, k+s-1, ... (hF/hL were
             // maintained for every lane, so the exact owner has them whether
             // or not it also sends them)
             if (ex0)
 #pragma unroll
-                for (int j = 0; j < QH; ++j) tab[(peF * 2 + 0) * QH + j] = hF[j];
+                for (int j = 0; j < QH; ++j) {
+                    tab[(peF * 2 + 0) * QH + j] = hF[j];
+                    if (CL) put_peers(&tab[(peF * 2 + 0) * QH + j], hF[j], rank, a.ncta);
+                }
             if (ex7)
 #pragma unroll
-                for (int j = 0; j < QH; ++j) tab[(peL * 2 + 1) * QH + j] = hL[j];
+                for (int j = 0; j < QH; ++j) {
+                    tab[(peL * 2 + 1) * QH + j] = hL[j];
+                    if (CL) put_peers(&tab[(peL * 2 + 1) * QH + j], hL[j], rank, a.ncta);
+                }
         }
-        __syncthreads();
+        if (CL)
+            small_cluster_sync();
+        else
+            __syncthreads();
         k += s;
         if (a.snaps && (k == next_rec || k == a.k_end)) {
             const long long row = k % a.stride == 0 ? k / a.stride : k / a.stride + 1;
-            for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[row * N + i] = su[i];
+            if (rank == 0)  // every CTA advances next_rec: the round lengths must agree
+                for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[row * N + i] = su[i];
             if (k == next_rec) next_rec += a.stride;
         }
     }
+    if (rank != 0) return;  // the other copies are identical
     bool bad = false;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         bad |= !isfinite(su[i]);
@@ -418,26 +482,49 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     const int QH = history_slots(q);
     const int smem = int(small_smem_bytes(N, P, QH, q));
     const int warps = int((N + kAsChunk - 1) / kAsChunk);
-    auto launch = [&](auto kern) -> int {
+    // More than four windows: spread them over a cluster, one warp per SM
+    // sub-partition (K9 is latency-bound; two warps per sub-partition
+    // serialise their issue).  HEAT_K9_NO_CLUSTER=1: one CTA.
+    static const bool no_cluster = std::getenv("HEAT_K9_NO_CLUSTER") != nullptr;
+    const int ncta = no_cluster ? 1 : std::min(4, (warps + 3) / 4);
+    const int wpc = (warps + ncta - 1) / ncta;
+    a.ncta = ncta;
+    auto launch = [&](auto kern1, auto kernc) -> int {
         int per_sm = 0;
-        HB_TRY(kernel_smem_config(reinterpret_cast<const void*>(kern),
-                                  int(small_smem_bytes(kAsMaxN, kAsMaxN / kAsV, kAsMaxQ, kAsMaxQ)),
-                                  warps * 32, &per_sm));
-        kern<<<1, warps * 32, smem, st>>>(a);
-        HB_CUDA(cudaGetLastError());
+        const void* fn = ncta > 1 ? reinterpret_cast<const void*>(kernc)
+                                  : reinterpret_cast<const void*>(kern1);
+        HB_TRY(kernel_smem_config(fn, int(small_smem_bytes(kAsMaxN, kAsMaxN / kAsV, kAsMaxQ, kAsMaxQ)),
+                                  wpc * 32, &per_sm));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(ncta));
+        cfg.blockDim = dim3(unsigned(wpc * 32));
+        cfg.dynamicSmemBytes = size_t(smem);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(ncta);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = ncta > 1 ? 1 : 0;
+        void* params[] = {&a};
+        HB_CUDA(cudaLaunchKernelExC(&cfg, fn, params));
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
     };
-    auto by_law = [&](auto k0, auto k1, auto k2) -> int {
-        return law == HEAT_DELAY_UNIFORM ? launch(k0) : law == HEAT_DELAY_FIXED ? launch(k1)
-                                                                               : launch(k2);
-    };
+#define HB_K9(QHV)                                                                              \
+    (law == HEAT_DELAY_UNIFORM                                                                  \
+         ? launch(async_small_kernel<QHV, 0, false>, async_small_kernel<QHV, 0, true>)          \
+     : law == HEAT_DELAY_FIXED                                                                  \
+         ? launch(async_small_kernel<QHV, 1, false>, async_small_kernel<QHV, 1, true>)          \
+         : launch(async_small_kernel<QHV, 2, false>, async_small_kernel<QHV, 2, true>))
     if (QH == 2)
-        HB_TRY(by_law(async_small_kernel<2, 0>, async_small_kernel<2, 1>, async_small_kernel<2, 2>));
+        HB_TRY(HB_K9(2));
     else if (QH == 4)
-        HB_TRY(by_law(async_small_kernel<4, 0>, async_small_kernel<4, 1>, async_small_kernel<4, 2>));
+        HB_TRY(HB_K9(4));
     else
-        HB_TRY(by_law(async_small_kernel<8, 0>, async_small_kernel<8, 1>, async_small_kernel<8, 2>));
+        HB_TRY(HB_K9(8));
+#undef HB_K9
     size_t ns = 0;
     std::vector<size_t> ks;
     if (want) {
