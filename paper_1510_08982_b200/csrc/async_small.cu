@@ -49,7 +49,8 @@ constexpr int kAsMaxQ = 8;
 constexpr int kAsSub = 16;  // steps per delay word (16 nibbles)
 
 struct AsyncSmallArgs {
-    double* field;  // [N]: raw initial field in, final field out
+    const double* in;  // [N]: raw initial field (device, or mapped pinned host memory)
+    double* field;     // [N]: final field out (same)
     int N, n, P;
     double r, c, c1, c2;
     int dirichlet;
@@ -149,22 +150,49 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     const int rank = CL ? int(small_ctarank()) : 0;
     const int gw = rank * int(blockDim.x >> 5) + w;  // window index in the field
 
+    // The inputs may sit in mapped host memory (a microsecond per round
+    // trip): every thread issues all its loads before using any of them.
     bool bad_in = false;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const double v = a.field[i];
-        bad_in |= !isfinite(v);
-        su[i] = v;
+    {
+        const double2* in2 = reinterpret_cast<const double2*>(a.in);
+        const int n2 = N / 2;  // N is a multiple of 8
+        for (int base = 0; base < n2; base += 8 * int(blockDim.x)) {
+            const int t = threadIdx.x;
+            const int oL = t < a.P && base == 0 ? a.offL[t] : 0;
+            const int oR = t < a.P && base == 0 ? a.offR[t] : 0;
+            const uint64_t th = a.law == 2 && t < a.q - 1 && base == 0 ? a.gthr[t] : 0;
+            double2 x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = base + t + j * int(blockDim.x);
+                x[j] = i < n2 ? in2[i] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int i = base + t + j * int(blockDim.x);
+                if (i < n2) {
+                    bad_in |= !isfinite(x[j].x) || !isfinite(x[j].y);
+                    *reinterpret_cast<double2*>(&su[2 * i]) = x[j];
+                }
+            }
+            if (base == 0) {
+                if (t < a.P) {
+                    soffL[t] = oL;
+                    soffR[t] = oR;
+                }
+                if (a.law == 2 && t < a.q - 1) sthr[t] = th;
+            }
+        }
+        // P > blockDim.x (PEs of 8 points in a large field): the rest
+        for (int i = threadIdx.x + blockDim.x; i < a.P; i += blockDim.x) {
+            soffL[i] = a.offL[i];
+            soffR[i] = a.offR[i];
+        }
     }
-    for (int i = threadIdx.x; i < a.P; i += blockDim.x) {
-        soffL[i] = a.offL[i];
-        soffR[i] = a.offR[i];
-    }
-    if (a.law == 2)
-        for (int i = threadIdx.x; i < a.q - 1; i += blockDim.x) sthr[i] = a.gthr[i];
     // TemperatureField ctor (core.hpp:45-51) on the raw upload, then
     // prepare_initial's snap of the ends (the host checked |u - c| <= 1e-9)
     if (__syncthreads_or(bad_in)) {
-        if (threadIdx.x == 0 && rank == 0) atomicOr(a.flag + 2, 1u);
+        if (threadIdx.x == 0 && rank == 0) a.flag[2] = 1u;  // the only writer: a plain store
         return;
     }
     if (a.dirichlet && threadIdx.x == 0) {
@@ -234,12 +262,14 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     // exact outputs: lanes 8..23 of the window (the 128-point chunk), inside the field
     const bool lexact = active && lane >= H / V && lane < (H + C) / V && g0 < N;
     long long k = 0;
-    long long next_rec = a.stride > 0 ? a.stride : a.k_end + 1;
+    // trajectory rows (steps stride, 2 stride, ..., and k_end): written from
+    // the registers of the exact lanes at the end of a sub-round cut there,
+    // so records do not cut rounds
+    long long next_rec = a.stride > 0 ? min(a.stride, a.k_end) : a.k_end + 1;
     double u[V];
     double hF[QH], hL[QH];  // products of my first / last point, hX[j] at step k - j
     while (k < a.k_end) {
-        long long s = min((long long)H, a.k_end - k);
-        s = min(s, next_rec - k);
+        const long long s = min((long long)H, a.k_end - k);
         if (active) {
 #pragma unroll
             for (int i = 0; i < V; i += 2) {
@@ -253,9 +283,9 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                 hF[j] = edgeF ? tab[(peF * 2 + 0) * QH + j] : 0.0;
                 hL[j] = edgeL ? tab[(peL * 2 + 1) * QH + j] : 0.0;
             }
-            for (int t0 = 0; t0 < int(s); t0 += kAsSub) {
-                const int len = min(kAsSub, int(s) - t0);
+            for (int t0 = 0, len = 0; t0 < int(s); t0 += len) {
                 const long long kb = k + t0;
+                len = int(min((long long)min(kAsSub, int(s) - t0), next_rec - kb));
                 // -- the delays of this sub-round, one lane per (stream, step):
                 // stream i < cU is the i-th sending-up lane, then the sending-down ones
                 for (int base = 0; base < nstreams * kAsSub; base += 32) {
@@ -332,6 +362,18 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                         for (int t = 0; t < len; ++t) step(t, t + 1 < len);
                     }
                 }
+                if (kb + len == next_rec) {  // a trajectory row: my exact chunk
+                    const long long row = (next_rec + a.stride - 1) / a.stride;
+                    if (lexact) {
+#pragma unroll
+                        for (int i = 0; i < V; i += 2)
+                            *reinterpret_cast<double2*>(&a.snaps[row * N + g0 + i]) =
+                                make_double2(u[i], u[i + 1]);
+                    }
+                    next_rec = next_rec + a.stride > a.k_end && next_rec < a.k_end
+                                   ? a.k_end
+                                   : next_rec + a.stride;
+                }
             }
             hF[0] = __dmul_rn(r, u[0]);
             hL[0] = __dmul_rn(r, u[V - 1]);
@@ -371,12 +413,6 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         else
             __syncthreads();
         k += s;
-        if (a.snaps && (k == next_rec || k == a.k_end)) {
-            const long long row = k % a.stride == 0 ? k / a.stride : k / a.stride + 1;
-            if (rank == 0)  // every CTA advances next_rec: the round lengths must agree
-                for (int i = threadIdx.x; i < N; i += blockDim.x) a.snaps[row * N + i] = su[i];
-            if (k == next_rec) next_rec += a.stride;
-        }
     }
     if (rank != 0) return;  // the other copies are identical
     bool bad = false;
@@ -384,7 +420,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         bad |= !isfinite(su[i]);
         a.field[i] = su[i];
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(a.flag, 1u);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) a.flag[0] = 1u;
 }
 
 int history_slots(size_t q) { return q <= 2 ? 2 : q <= 4 ? 4 : 8; }
@@ -430,34 +466,57 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     double* field = static_cast<double*>(d->buf[0]);
     cudaStream_t st = d->stream;
     const bool ends_ok = !dir || (std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[N - 1] - c2) <= 1e-9);
-    HB_CUDA(cudaMemsetAsync(d->flag, 0, 4 * sizeof(unsigned int), st));
     if (!ends_ok) HB_TRY(upload_prepared(*d, u0, N, bc_kind, c1, c2, field));  // the right error
-    // pinned staging: [flags | input | final | trajectory rows]
+    // Zero-copy I/O through the pinned staging buffer (mapped into the
+    // device's address space under UVA): the kernel reads the field and the
+    // draw tables from it and writes the flags, the trajectory rows and the
+    // final field into it, so a call is one launch and one synchronize (no
+    // copy-engine round trips: -25 us per call, tools/probe_cfg2_parts.py).
+    // Layout: [flags 64 | input | final | tables | rows].
     const size_t nb = N * sizeof(double);
-    unsigned char* hs = host_stage(*d, 64 + 2 * nb + rows * nb);
-    const void* src = u0;
-    if (hs) {
-        std::memcpy(hs + 64, u0, nb);
-        src = hs + 64;
-    }
-    HB_CUDA(cudaMemcpyAsync(field, src, nb, cudaMemcpyHostToDevice, st));
-    // one upload of the draw tables (pageable host staging is fine: tiny)
-    std::vector<unsigned char> host(tab_bytes, 0);
-    std::memcpy(host.data(), offL.data(), P * sizeof(int));
-    std::memcpy(host.data() + P * sizeof(int), offR.data(), P * sizeof(int));
+    const size_t o_tab = 64 + 2 * nb;
+    const size_t o_rows = o_tab + (tab_bytes + 63) / 64 * 64;
+    unsigned char* hs = host_stage(*d, o_rows + rows * nb);
     const size_t o_thr = (2 * P * sizeof(int) + 7) / 8 * 8;
-    if (!gthr.empty()) std::memcpy(host.data() + o_thr, gthr.data(), gthr.size() * 8);
-    char* sbase = static_cast<char*>(d->scratch);
-    HB_CUDA(cudaMemcpyAsync(sbase, host.data(), tab_bytes, cudaMemcpyHostToDevice, st));
-    if (want && d->snaps_bytes < rows * N * sizeof(double)) {
-        if (d->snaps) cudaFree(d->snaps);
-        d->snaps = nullptr;
-        d->snaps_bytes = 0;
-        HB_CUDA(cudaMalloc(&d->snaps, rows * N * sizeof(double)));
-        d->snaps_bytes = rows * N * sizeof(double);
+    auto fill_tables = [&](unsigned char* t) {
+        std::memcpy(t, offL.data(), P * sizeof(int));
+        std::memcpy(t + P * sizeof(int), offR.data(), P * sizeof(int));
+        if (!gthr.empty()) std::memcpy(t + o_thr, gthr.data(), gthr.size() * 8);
+    };
+    const unsigned char* tabs = nullptr;
+    const double* in = field;
+    unsigned int* flag = d->flag;
+    double* out = field;
+    double* rows_dst = nullptr;
+    if (hs) {
+        std::memset(hs, 0, 64);
+        std::memcpy(hs + 64, u0, nb);
+        fill_tables(hs + o_tab);
+        in = reinterpret_cast<const double*>(hs + 64);
+        out = reinterpret_cast<double*>(hs + 64 + nb);
+        flag = reinterpret_cast<unsigned int*>(hs);
+        tabs = hs + o_tab;
+        rows_dst = want ? reinterpret_cast<double*>(hs + o_rows) : nullptr;
+    } else {  // staging too small for the rows: device buffers and copies
+        HB_CUDA(cudaMemsetAsync(d->flag, 0, 4 * sizeof(unsigned int), st));
+        HB_CUDA(cudaMemcpyAsync(field, u0, nb, cudaMemcpyHostToDevice, st));
+        std::vector<unsigned char> host(tab_bytes, 0);
+        fill_tables(host.data());
+        HB_CUDA(cudaMemcpyAsync(d->scratch, host.data(), tab_bytes, cudaMemcpyHostToDevice, st));
+        HB_CUDA(cudaStreamSynchronize(st));  // `host` goes out of scope
+        tabs = static_cast<const unsigned char*>(d->scratch);
+        if (want && d->snaps_bytes < rows * N * sizeof(double)) {
+            if (d->snaps) cudaFree(d->snaps);
+            d->snaps = nullptr;
+            d->snaps_bytes = 0;
+            HB_CUDA(cudaMalloc(&d->snaps, rows * N * sizeof(double)));
+            d->snaps_bytes = rows * N * sizeof(double);
+        }
+        rows_dst = want ? static_cast<double*>(d->snaps) : nullptr;
     }
     AsyncSmallArgs a{};
-    a.field = field;
+    a.in = in;
+    a.field = out;
     a.N = int(N);
     a.n = int(per_pe);
     a.P = int(P);
@@ -468,17 +527,17 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     a.dirichlet = dir;
     a.k_end = (long long)k_end;
     a.stride = want ? (long long)stride : 0;
-    a.snaps = want ? static_cast<double*>(d->snaps) : nullptr;
-    a.flag = d->flag;
+    a.snaps = rows_dst;
+    a.flag = flag;
     a.law = law;
     a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
     a.q = int(q);
     a.seed = seed;
     a.modq = make_modq(unsigned(q));
     a.D = D;
-    a.offL = reinterpret_cast<const int*>(sbase);
-    a.offR = reinterpret_cast<const int*>(sbase) + P;
-    a.gthr = reinterpret_cast<const uint64_t*>(sbase + o_thr);
+    a.offL = reinterpret_cast<const int*>(tabs);
+    a.offR = reinterpret_cast<const int*>(tabs) + P;
+    a.gthr = reinterpret_cast<const uint64_t*>(tabs + o_thr);
     const int QH = history_slots(q);
     const int smem = int(small_smem_bytes(N, P, QH, q));
     const int warps = int((N + kAsChunk - 1) / kAsChunk);
@@ -532,23 +591,21 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
         for (size_t kk = stride; kk <= k_end; kk += stride) ks.push_back(kk);
         if (k_end % stride) ks.push_back(k_end);
         ns = ks.size();
-        const size_t copy = std::min(ns, max_snapshots);
-        if (snapshots && copy)  // rows are contiguous on both sides: one copy
-            HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs + 64 + 2 * nb) : snapshots, d->snaps,
-                                    copy * nb, cudaMemcpyDeviceToHost, st));
     }
-    if (final_out)
-        HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs + 64 + nb) : final_out, field, nb,
-                                cudaMemcpyDeviceToHost, st));
+    const size_t copy = std::min(ns, max_snapshots);
     unsigned int flags[4] = {0, 0, 0, 0};
-    HB_CUDA(cudaMemcpyAsync(hs ? static_cast<void*>(hs) : flags, d->flag, sizeof flags,
-                            cudaMemcpyDeviceToHost, st));
-    HB_CUDA(cudaStreamSynchronize(st));
     if (hs) {
+        HB_CUDA(cudaStreamSynchronize(st));
         std::memcpy(flags, hs, sizeof flags);
         if (final_out) std::memcpy(final_out, hs + 64 + nb, nb);
-        if (want && snapshots)
-            std::memcpy(snapshots, hs + 64 + 2 * nb, std::min(ns, max_snapshots) * nb);
+        if (snapshots && copy) std::memcpy(snapshots, hs + o_rows, copy * nb);
+    } else {
+        if (snapshots && copy)  // rows are contiguous on both sides: one copy
+            HB_CUDA(cudaMemcpyAsync(snapshots, d->snaps, copy * nb, cudaMemcpyDeviceToHost, st));
+        if (final_out)
+            HB_CUDA(cudaMemcpyAsync(final_out, field, nb, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+        HB_CUDA(cudaStreamSynchronize(st));
     }
     if (flags[2]) return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
     if (flags[0]) {

@@ -8,3 +8,4 @@ timeout 120 python tools/probe_cfg2_parts.py
 HEAT_K9_NO_CLUSTER=1 timeout 120 python tools/probe_cfg2_parts.py | sed 's/^/one-cta /'
 timeout 120 python tools/probe_cfg2.py
 HEAT_K9_NO_CLUSTER=1 timeout 120 python tools/probe_cfg2.py | sed 's/^/one-cta /'
+(cd tools/micro && ./call_floor && HEAT_K9_NO_CLUSTER=1 ./call_floor | grep heat_async | sed 's/^/one-cta /')
