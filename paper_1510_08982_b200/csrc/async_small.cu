@@ -77,27 +77,32 @@ __device__ __forceinline__ void small_cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
                      : "memory");
 }
-// (x, y) into the same 16 bytes of every other CTA of the cluster
-__device__ __forceinline__ void put_peers2(const double2* p, double x, double y, int rank,
-                                           int ncta) {
+// (x, y) into the same 16 bytes of every other CTA of the cluster, each
+// store completing its bytes on that CTA's mbarrier `bar` (st.async: no
+// fence, no cluster barrier; the receiver waits on its own mbarrier)
+__device__ __forceinline__ void put_peers2(const void* p, double x, double y, uint32_t bar,
+                                           int rank, int ncta) {
     const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
     for (int c = 0; c < ncta; ++c) {
         if (c == rank) continue;
-        uint32_t ra;
+        uint32_t ra, rb;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
-        asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(x), "d"(y)
-                     : "memory");
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+            "d"(x), "d"(y), "r"(rb)
+            : "memory");
     }
 }
-// v into the same shared-memory word of every other CTA of the cluster
-__device__ __forceinline__ void put_peers(const double* p, double v, int rank, int ncta) {
-    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
-    for (int c = 0; c < ncta; ++c) {
-        if (c == rank) continue;
-        uint32_t ra;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
-        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
-    }
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
 }
 
 template <int LAW>
@@ -132,16 +137,24 @@ __device__ __forceinline__ double pick(const double (&h)[QH], int d) {
 
 // CL: the warps are spread over a cluster of a.ncta CTAs (one warp per SM
 // sub-partition for cfg2); every CTA keeps a full copy of the field and the
-// history table, and the exact owners write their round results into all
-// copies (DSMEM stores) between two cluster barriers.
+// history table.  The field and the table are double-buffered: round j reads
+// buffer j&1 and its exact owners write buffer (j+1)&1 of every copy -- their
+// own with plain stores, the others' with st.async, whose bytes complete on
+// the receiver's mbarrier (j+1)&1.  A round ends with one __syncthreads and
+// the wait for that mbarrier phase (the expected bytes are everything the
+// other CTAs own); no cluster barrier, no memory fence.  A peer can only
+// write a buffer after it has received this CTA's writes of the round that
+// read it, so one phase per buffer and round is enough.
 template <int QH, int LAW, bool CL>
 __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArgs a) {
     extern __shared__ double smem[];
     __shared__ __align__(16) unsigned char sdel[kAsMaxN / kAsChunk][64 * kAsSub];  // per warp: [stream][step]
     __shared__ int sstr[kAsMaxN / kAsChunk][64];  // per warp: draw rank of each delay stream
-    double* su = smem;                                  // [N]
-    double* tab = smem + ((a.N + 1) & ~1);              // [P][2][QH]
-    int* soffL = reinterpret_cast<int*>(tab + a.P * 2 * QH);
+    __shared__ __align__(8) unsigned long long sbar[2];  // CL: round mbarriers, by buffer
+    const int Np = (a.N + 1) & ~1, TB = a.P * 2 * QH;
+    double* su = smem;              // [2][Np]: the field, double-buffered
+    double* tab = smem + 2 * Np;    // [2][P][2][QH]: edge products, double-buffered
+    int* soffL = reinterpret_cast<int*>(tab + 2 * TB);
     int* soffR = soffL + a.P;
     uint64_t* sthr =  // [q-1] geometric thresholds, 8-B aligned after the offsets
         reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(soffR + a.P) + 7) & ~uintptr_t(7));
@@ -261,6 +274,21 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     const int wg0 = wrapg(g0);
     // exact outputs: lanes 8..23 of the window (the 128-point chunk), inside the field
     const bool lexact = active && lane >= H / V && lane < (H + C) / V && g0 < N;
+    const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&sbar[0]));
+    uint32_t incoming = 0;  // CL: bytes the other CTAs write into this one per round
+    if (CL) {
+        const int own = __syncthreads_count(lexact) * V * 8 +
+                        (__syncthreads_count(ex0) + __syncthreads_count(ex7)) * QH * 8;
+        incoming = uint32_t(N * 8 + 2 * a.P * QH * 8 - own);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        small_cluster_sync();  // every CTA's barriers exist before the first st.async
+    }
+    int par = 0;              // buffer read by this round
+    uint32_t phases = 0;      // CL: bit b = parity of the next wait on mbarrier b
     long long k = 0;
     // trajectory rows (steps stride, 2 stride, ..., and k_end): written from
     // the registers of the exact lanes at the end of a sub-round cut there,
@@ -270,18 +298,27 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     double hF[QH], hL[QH];  // products of my first / last point, hX[j] at step k - j
     while (k < a.k_end) {
         const long long s = min((long long)H, a.k_end - k);
+        const double* cu = su + par * Np;
+        const double* ct = tab + par * TB;
+        double* nu = su + (par ^ 1) * Np;
+        double* nt = tab + (par ^ 1) * TB;
+        const uint32_t nbar = bar0 + 8u * uint32_t(par ^ 1);
+        if (CL && threadIdx.x == 0)  // this round's phase: my arrival + the peers' bytes
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(nbar),
+                         "r"(incoming)
+                         : "memory");
         if (active) {
 #pragma unroll
             for (int i = 0; i < V; i += 2) {
-                const double2 x = lreal ? *reinterpret_cast<const double2*>(&su[wg0 + i])
+                const double2 x = lreal ? *reinterpret_cast<const double2*>(&cu[wg0 + i])
                                         : make_double2(0.0, 0.0);
                 u[i] = x.x;
                 u[i + 1] = x.y;
             }
 #pragma unroll
             for (int j = 0; j < QH; ++j) {  // rows of PE edge points only
-                hF[j] = edgeF ? tab[(peF * 2 + 0) * QH + j] : 0.0;
-                hL[j] = edgeL ? tab[(peL * 2 + 1) * QH + j] : 0.0;
+                hF[j] = edgeF ? ct[(peF * 2 + 0) * QH + j] : 0.0;
+                hL[j] = edgeL ? ct[(peL * 2 + 1) * QH + j] : 0.0;
             }
             for (int t0 = 0, len = 0; t0 < int(s); t0 += len) {
                 const long long kb = k + t0;
@@ -378,18 +415,13 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
             hF[0] = __dmul_rn(r, u[0]);
             hL[0] = __dmul_rn(r, u[V - 1]);
         }
-        // every window (and history row) of every copy has been read
-        if (CL)
-            small_cluster_sync();
-        else
-            __syncthreads();
         if (active) {
             if (lexact) {
 #pragma unroll
                 for (int i = 0; i < V; i += 2) {
-                    double2* dst = reinterpret_cast<double2*>(&su[g0 + i]);
+                    double2* dst = reinterpret_cast<double2*>(&nu[g0 + i]);
                     *dst = make_double2(u[i], u[i + 1]);
-                    if (CL) put_peers2(dst, u[i], u[i + 1], rank, a.ncta);
+                    if (CL) put_peers2(dst, u[i], u[i + 1], nbar, rank, a.ncta);
                 }
             }
             // a PE edge point's products at steps k+s, k+s-1, ... (hF/hL were
@@ -397,24 +429,30 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
             // or not it also sends them)
             if (ex0)
 #pragma unroll
-                for (int j = 0; j < QH; ++j) {
-                    tab[(peF * 2 + 0) * QH + j] = hF[j];
-                    if (CL) put_peers(&tab[(peF * 2 + 0) * QH + j], hF[j], rank, a.ncta);
+                for (int j = 0; j < QH; j += 2) {
+                    double2* dst = reinterpret_cast<double2*>(&nt[(peF * 2 + 0) * QH + j]);
+                    *dst = make_double2(hF[j], hF[j + 1]);
+                    if (CL) put_peers2(dst, hF[j], hF[j + 1], nbar, rank, a.ncta);
                 }
             if (ex7)
 #pragma unroll
-                for (int j = 0; j < QH; ++j) {
-                    tab[(peL * 2 + 1) * QH + j] = hL[j];
-                    if (CL) put_peers(&tab[(peL * 2 + 1) * QH + j], hL[j], rank, a.ncta);
+                for (int j = 0; j < QH; j += 2) {
+                    double2* dst = reinterpret_cast<double2*>(&nt[(peL * 2 + 1) * QH + j]);
+                    *dst = make_double2(hL[j], hL[j + 1]);
+                    if (CL) put_peers2(dst, hL[j], hL[j + 1], nbar, rank, a.ncta);
                 }
         }
-        if (CL)
-            small_cluster_sync();
-        else
-            __syncthreads();
+        __syncthreads();  // my own copy of buffer par^1 is complete
+        if (CL) {         // ... and the other CTAs' parts of it have landed
+            const int b = par ^ 1;
+            mbar_wait_parity(nbar, (phases >> b) & 1u);
+            phases ^= 1u << b;
+        }
+        par ^= 1;
         k += s;
     }
     if (rank != 0) return;  // the other copies are identical
+    su += par * Np;         // the last round's output
     bool bad = false;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         bad |= !isfinite(su[i]);
@@ -426,7 +464,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
 int history_slots(size_t q) { return q <= 2 ? 2 : q <= 4 ? 4 : 8; }
 
 size_t small_smem_bytes(size_t N, size_t P, int QH, size_t q) {
-    return ((N + 1) & ~size_t(1)) * 8 + P * 2 * QH * 8 + 2 * P * 4 + 8 + q * 8;
+    return 2 * ((N + 1) & ~size_t(1)) * 8 + 2 * P * 2 * QH * 8 + 2 * P * 4 + 8 + q * 8;
 }
 
 }  // namespace
