@@ -37,6 +37,7 @@
 
 #include "runtime.cuh"
 #include "sync_tb.cuh"
+#include "small_cluster.cuh"
 
 namespace hb {
 namespace {
@@ -67,43 +68,6 @@ struct AsyncSmallArgs {
     const uint64_t* gthr;  // geometric thresholds (q-1)
     int ncta;  // CTAs in the cluster (CL kernels): each holds a full copy of the field
 };
-
-__device__ __forceinline__ uint32_t small_ctarank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void small_cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                     : "memory");
-}
-// (x, y) into the same 16 bytes of every other CTA of the cluster, each
-// store completing its bytes on that CTA's mbarrier `bar` (st.async: no
-// fence, no cluster barrier; the receiver waits on its own mbarrier)
-__device__ __forceinline__ void put_peers2(const void* p, double x, double y, uint32_t bar,
-                                           int rank, int ncta) {
-    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
-    for (int c = 0; c < ncta; ++c) {
-        if (c == rank) continue;
-        uint32_t ra, rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
-        asm volatile(
-            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
-            "d"(x), "d"(y), "r"(rb)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(bar), "r"(parity)
-            : "memory");
-}
 
 template <int LAW>
 __device__ __forceinline__ int small_delay(const AsyncSmallArgs& a, uint64_t z, int bound,

@@ -233,7 +233,7 @@ size_t sync_small_max_points();
 int sync_run_small(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                    size_t k_end, size_t stride, double* final_out, double* snapshots,
                    size_t* steps_out, size_t max_snapshots, size_t* n_snapshots,
-                   float* kernel_ms = nullptr);
+                   float* kernel_ms = nullptr, bool one_cta = false);
 // K10 (exec_free.cu): exec_run(BarrierFree) of PEs that fit one warp each, all
 // in one thread-block cluster; stats in the kStat layout (optional).
 bool free_eligible(size_t N, size_t per_pe, size_t q, size_t k_end);

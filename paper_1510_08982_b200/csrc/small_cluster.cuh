@@ -1,0 +1,68 @@
+// small_cluster.cuh -- the cluster plumbing shared by the small-field kernels
+// K7c (sync_small.cu) and K9 (async_small.cu): each CTA of the cluster keeps
+// a full copy of the field in shared memory, double-buffered; the exact
+// owners write each round's results into every copy, their own with plain
+// stores and the other CTAs' with st.async, whose bytes complete on the
+// receiver's mbarrier for that buffer.  A round ends with one __syncthreads
+// and one wait for the mbarrier phase -- no cluster barrier, no memory fence.
+#pragma once
+#include <cstdint>
+
+namespace hb {
+namespace {
+
+__device__ __forceinline__ uint32_t small_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void small_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+// (x, y) into the same 16 bytes of every other CTA of the cluster, each
+// store completing its bytes on that CTA's mbarrier `bar` (st.async: no
+// fence, no cluster barrier; the receiver waits on its own mbarrier)
+__device__ __forceinline__ void put_peers2(const void* p, double x, double y, uint32_t bar,
+                                           int rank, int ncta) {
+    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
+    for (int c = 0; c < ncta; ++c) {
+        if (c == rank) continue;
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
+        asm volatile(
+            "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
+            "d"(x), "d"(y), "r"(rb)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+}
+
+}  // namespace
+}  // namespace hb
+
+namespace hb {
+namespace {
+// the two round mbarriers (one arrival each: the local expect_tx), visible to
+// the cluster before any st.async targets them
+__device__ __forceinline__ void small_bars_init(uint32_t bar0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void small_bar_expect(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+}  // namespace
+}  // namespace hb

@@ -736,7 +736,7 @@ template <typename Real>
 int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                   size_t k_end, size_t stride, double* final_out, double* snapshots,
                   size_t* steps_out, size_t max_snapshots, size_t* n_snapshots,
-                  float* kernel_ms = nullptr) {
+                  float* kernel_ms = nullptr, bool one_cta = false) {
     if (n < 3) return fail(HEAT_EDOMAIN, "TemperatureField requires N >= 3");
     if (!u0) return fail(HEAT_EINVAL, "null field pointer");
     if (bc_kind != HEAT_BC_DIRICHLET && bc_kind != HEAT_BC_PERIODIC)
@@ -746,7 +746,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     if (sizeof(Real) == 8 && n <= sync_small_max_points() && !std::getenv("HEAT_NO_SMALL_SYNC"))
         return sync_run_small(reinterpret_cast<const double*>(u0), n, r, bc_kind, c1, c2, k_end,
                               stride, final_out, snapshots, steps_out, max_snapshots,
-                              n_snapshots, kernel_ms);
+                              n_snapshots, kernel_ms, one_cta);
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));
@@ -850,8 +850,10 @@ namespace hb {
 int sync_run_timed(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
                    size_t k_end, double* final_out, float* kernel_ms) {
     *kernel_ms = 0.f;
+    // exec_run(Barriered): K7, the executor whose PE warps all meet at one CTA
+    // barrier per round (K7c, sync_run's kernel, has no barrier across CTAs)
     return sync_run_impl<double>(u0, n, r, bc_kind, c1, c2, k_end, k_end, final_out, nullptr,
-                                 nullptr, 0, nullptr, kernel_ms);
+                                 nullptr, 0, nullptr, kernel_ms, true);
 }
 }  // namespace hb
 
