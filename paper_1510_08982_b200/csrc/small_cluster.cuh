@@ -26,8 +26,8 @@ __device__ __forceinline__ void small_cluster_sync() {
 __device__ __forceinline__ void put_peers2(const void* p, double x, double y, uint32_t bar,
                                            int rank, int ncta) {
     const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
-    for (int c = 0; c < ncta; ++c) {
-        if (c == rank) continue;
+    for (int j = 1; j < ncta; ++j) {  // the other CTAs, no skip branch
+        const int c = rank + j < ncta ? rank + j : rank + j - ncta;
         uint32_t ra, rb;
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
@@ -35,6 +35,24 @@ __device__ __forceinline__ void put_peers2(const void* p, double x, double y, ui
             "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(ra),
             "d"(x), "d"(y), "r"(rb)
             : "memory");
+    }
+}
+// 8 doubles (4 x 16 B) into every other CTA: one mapa pair per peer
+__device__ __forceinline__ void put_peers8(const double* p, const double (&v)[8], uint32_t bar,
+                                           int rank, int ncta) {
+    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
+    for (int j = 1; j < ncta; ++j) {
+        const int c = rank + j < ncta ? rank + j : rank + j - ncta;
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
+#pragma unroll
+        for (int i = 0; i < 8; i += 2)
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                    ra + 8u * i),
+                "d"(v[i]), "d"(v[i + 1]), "r"(rb)
+                : "memory");
     }
 }
 __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {

@@ -296,11 +296,9 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
             }
             if (lexact) {
 #pragma unroll
-                for (int i = 0; i < V; i += 2) {
-                    double2* dst = reinterpret_cast<double2*>(&nu[g0 + i]);
-                    *dst = make_double2(u[i], u[i + 1]);
-                    if (CL) put_peers2(dst, u[i], u[i + 1], nbar, rank, a.ncta);
-                }
+                for (int i = 0; i < V; i += 2)
+                    *reinterpret_cast<double2*>(&nu[g0 + i]) = make_double2(u[i], u[i + 1]);
+                if (CL) put_peers8(&nu[g0], u, nbar, rank, a.ncta);
             }
         }
         __syncthreads();
