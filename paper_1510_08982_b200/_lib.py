@@ -113,10 +113,10 @@ SIGNATURES = {
     "heat_prepare_initial": (_i, [_pd, _sz, _i, _d, _d, _pd]),
     "heat_trajectory_length": (_sz, [_sz, _sz, _sz]),
     "heat_sync_step": (_i, [_pd, _sz, _d, _i, _d, _d, _pd]),
-    "heat_sync_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd, _pd, _psz, _sz, _psz]),
-    "heat_sync_run_f32": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _pd, _pd, _psz, _sz, _psz]),
-    "heat_async_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _u64, _sz, _sz,
-                            _pd, _pd, _psz, _sz, _psz]),
+    "heat_sync_run": (_i, [_vp, _sz, _d, _i, _d, _d, _sz, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "heat_sync_run_f32": (_i, [_vp, _sz, _d, _i, _d, _d, _sz, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "heat_async_run": (_i, [_vp, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _u64, _sz, _sz,
+                            _vp, _vp, _vp, _sz, _vp]),
     "heat_sample_delay": (_i, [_sz, _i, _sz, _d, _u64, _u64, _sz, _psz]),
     "heat_async_free_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _sz, _pd, _P(AsyncStatsC)]),
     "heat_ensemble_run": (_i, [_pd, _sz, _d, _i, _d, _d, _sz, _sz, _i, _sz, _d, _sz, _sz, _sz, _u64,

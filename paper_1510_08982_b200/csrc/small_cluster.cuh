@@ -37,8 +37,9 @@ __device__ __forceinline__ void put_peers2(const void* p, double x, double y, ui
             : "memory");
     }
 }
-// 8 doubles (4 x 16 B) into every other CTA: one mapa pair per peer
-__device__ __forceinline__ void put_peers8(const double* p, const double (&v)[8], uint32_t bar,
+// V doubles (V/2 x 16 B) into every other CTA: one mapa pair per peer
+template <int V>
+__device__ __forceinline__ void put_peers8(const double* p, const double (&v)[V], uint32_t bar,
                                            int rank, int ncta) {
     const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
     for (int j = 1; j < ncta; ++j) {
@@ -47,7 +48,7 @@ __device__ __forceinline__ void put_peers8(const double* p, const double (&v)[8]
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
 #pragma unroll
-        for (int i = 0; i < 8; i += 2)
+        for (int i = 0; i < V; i += 2)
             asm volatile(
                 "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
                     ra + 8u * i),

@@ -151,10 +151,9 @@ struct SmallClArgs {
 
 constexpr int kClMaxN = 8192;
 
-template <bool PIN>
-__device__ __forceinline__ void cl_steps(double (&u)[8], double r, double c, double c1, double c2,
+template <int V, bool PIN>
+__device__ __forceinline__ void cl_steps(double (&u)[V], double r, double c, double c1, double c2,
                                          bool pinF, bool pinL, int nsteps) {
-    constexpr int V = 8;
     double pF = __dmul_rn(r, u[0]);
     double pLs = __dmul_rn(r, u[V - 1]);
     double pL = __shfl_up_sync(0xffffffffu, pLs, 1);
@@ -194,11 +193,15 @@ __device__ __forceinline__ void cl_steps(double (&u)[8], double r, double c, dou
     }
 }
 
-template <bool CL>
+// V points per lane, 8 halo lanes per side: windows of 32V points (16V
+// exact), rounds of 8V steps.  Each warp has its own sub-partition, so the
+// step time is the per-warp time: fewer points per lane (more warps, more
+// CTAs) is faster per step until the per-round cost dominates.
+template <int V, bool CL>
 __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs a) {
     extern __shared__ double smem[];
     __shared__ __align__(8) unsigned long long sbar[2];
-    constexpr int V = 8, H = 64, C = 32 * V - 2 * H;
+    constexpr int H = 8 * V, C = 32 * V - 2 * H;
     const int N = a.n, Np = (N + 1) & ~1;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CL ? int(small_ctarank()) : 0;
@@ -279,9 +282,9 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
                 const long long kb = k + t0;
                 len = int(min(s - t0, next_rec - kb));
                 if (pinned)
-                    cl_steps<true>(u, r, c, c1, c2, pinF, pinL, len);
+                    cl_steps<V, true>(u, r, c, c1, c2, pinF, pinL, len);
                 else
-                    cl_steps<false>(u, r, c, c1, c2, pinF, pinL, len);
+                    cl_steps<V, false>(u, r, c, c1, c2, pinF, pinL, len);
                 if (kb + len == next_rec) {  // a trajectory row: my exact chunk
                     if (lexact) {
                         double* row = a.snaps + ((next_rec + a.stride - 1) / a.stride) * N + g0;
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
 #pragma unroll
                 for (int i = 0; i < V; i += 2)
                     *reinterpret_cast<double2*>(&nu[g0 + i]) = make_double2(u[i], u[i + 1]);
-                if (CL) put_peers8(&nu[g0], u, nbar, rank, a.ncta);
+                if (CL) put_peers8<V>(&nu[g0], u, nbar, rank, a.ncta);
             }
         }
         __syncthreads();
@@ -377,7 +380,14 @@ static int sync_run_small_cl(const double* u0, size_t n, double r, int bc_kind, 
     a.dirichlet = bc_kind == HEAT_BC_DIRICHLET;
     a.k_end = (long long)k_end;
     a.stride = want ? (long long)stride : 0;
-    const int warps = int((n + 127) / 128);
+    // points per lane: HEAT_K7C_V in {4, 8} forces one (N must be a multiple)
+    static const int forced_v = [] {
+        const char* e = std::getenv("HEAT_K7C_V");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int V = forced_v == 4 || forced_v == 8 ? forced_v : 8;
+    if (n % size_t(V)) return fail(HEAT_ELOGIC, "K7c: N is not a multiple of the lane width");
+    const int warps = int((n + 16 * V - 1) / (16 * V));
     // more than four windows: a cluster, one warp per SM sub-partition
     static const bool no_cluster = std::getenv("HEAT_K7_NO_CLUSTER") != nullptr;
     const int ncta = no_cluster ? 1 : std::min(8, (warps + 3) / 4);
@@ -385,8 +395,11 @@ static int sync_run_small_cl(const double* u0, size_t n, double r, int bc_kind, 
     if (wpc > 16) return fail(HEAT_ELOGIC, "K7c: too many warps per CTA");
     a.ncta = ncta;
     const int smem = int(2 * ((n + 1) & ~size_t(1)) * sizeof(double));
-    const void* fn = ncta > 1 ? reinterpret_cast<const void*>(sync_small_cl_kernel<true>)
-                              : reinterpret_cast<const void*>(sync_small_cl_kernel<false>);
+    const void* fn =
+        V == 4 ? (ncta > 1 ? reinterpret_cast<const void*>(sync_small_cl_kernel<4, true>)
+                           : reinterpret_cast<const void*>(sync_small_cl_kernel<4, false>))
+               : (ncta > 1 ? reinterpret_cast<const void*>(sync_small_cl_kernel<8, true>)
+                           : reinterpret_cast<const void*>(sync_small_cl_kernel<8, false>));
     int per_sm = 0;
     HB_TRY(kernel_smem_config(fn, int(2 * kClMaxN * sizeof(double)), wpc * 32, &per_sm));
     cudaLaunchConfig_t cfg{};

@@ -253,21 +253,25 @@ def _field(u0) -> np.ndarray:
     return np.ascontiguousarray(TemperatureField(u0).values())
 
 
+_NULL_PD = C.cast(None, _lib._pd)
+
+
 def _trajectory(fn, what, u0, params, bc, k_end, stride, extra=()) -> Trajectory:
     v = _field(u0)
     n = v.size
-    L = _lib.lib()
-    count = L.heat_trajectory_length(n, k_end, stride)
+    if stride == 0:
+        stride = default_stride(n)  # as the library does (sync_solver.hpp:52-54)
+    # rows 0, stride, ..., and k_end when it is not a multiple (heat_trajectory_length)
+    count = 1 + k_end // stride + (1 if k_end % stride else 0)
     snaps = np.empty((count, n), np.float64)
     steps = np.empty(count, np.uintp)
     ns = C.c_size_t(0)
-    _lib.check(fn(_lib.dptr(v), n, params.r(), bc.kind, bc.c1, bc.c2, *extra, k_end, stride,
-                  C.cast(None, _lib._pd), _lib.dptr(snaps), _lib.szptr(steps), count,
-                  C.byref(ns)), what)
+    _lib.check(fn(v.ctypes.data, n, params.r(), bc.kind, bc.c1, bc.c2, *extra, k_end, stride,
+                  _NULL_PD, snaps.ctypes.data, steps.ctypes.data, count, C.byref(ns)), what)
     m = ns.value
     snaps.setflags(write=False)  # rows are shared by the snapshots, never copied
-    return Trajectory([TemperatureField._adopt(snaps[j]) for j in range(m)],
-                      [int(s) for s in steps[:m]], params, bc)
+    adopt = TemperatureField._adopt
+    return Trajectory([adopt(row) for row in snaps[:m]], steps[:m].tolist(), params, bc)
 
 
 def sync_step(u: TemperatureField, params: SolverParams, bc: BoundaryCondition) -> TemperatureField:

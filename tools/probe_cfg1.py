@@ -34,3 +34,6 @@ fin = np.empty(n)
 print(f"sync_run cfg1 C   k=1000 final:     {best(lambda: H.sync_final(u0, p, bc, 1000)):.1f} us")
 t = best(lambda: H.sync_final(u0, p, bc, 20000), 5)
 print(f"sync_run cfg1 k=20000: {t:.1f} us, {t / 20000 * 1e3:.1f} ns/step")
+bp = H.BoundaryCondition.periodic()
+t = best(lambda: H.sync_final(u0, p, bp, 20000), 5)
+print(f"sync_run cfg1-periodic k=20000: {t:.1f} us, {t / 20000 * 1e3:.1f} ns/step")
