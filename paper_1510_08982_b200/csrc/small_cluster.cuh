@@ -37,6 +37,26 @@ __device__ __forceinline__ void put_peers2(const void* p, double x, double y, ui
             : "memory");
     }
 }
+// V doubles (V/2 x 16 B) into the CTAs of `mask` (bit c: CTA c)
+template <int V>
+__device__ __forceinline__ void put_mask(const double* p, const double (&v)[V], uint32_t bar,
+                                         uint32_t mask) {
+    const uint32_t addr = uint32_t(__cvta_generic_to_shared(p));
+    while (mask) {
+        const int c = __ffs(mask) - 1;
+        mask &= mask - 1;
+        uint32_t ra, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(addr), "r"(c));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(bar), "r"(c));
+#pragma unroll
+        for (int i = 0; i < V; i += 2)
+            asm volatile(
+                "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(
+                    ra + 8u * i),
+                "d"(v[i]), "d"(v[i + 1]), "r"(rb)
+                : "memory");
+    }
+}
 // V doubles (V/2 x 16 B) into every other CTA: one mapa pair per peer
 template <int V>
 __device__ __forceinline__ void put_peers8(const double* p, const double (&v)[V], uint32_t bar,
@@ -83,5 +103,31 @@ __device__ __forceinline__ void small_bar_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
+}  // namespace
+}  // namespace hb
+
+namespace hb {
+namespace {
+// Halo-only exchange geometry.  CTA c of a cluster owns the exact points
+// [lo_c, hi_c), lo_c = c * wpc * C, hi_c = min(lo_c + wpc * C, N), C being
+// a window's exact width; its windows read H points beyond each end (mod N
+// when periodic, clipped to the field for Dirichlet).  A lane group of V
+// points starting at g (V | H, V | C, V | N) is sent to CTA c iff it lies in
+// c's halo and c does not own it; the receiver counts the same groups.
+struct HaloGeo {
+    int N, C, H, wpc, ncta, periodic;
+    __device__ __forceinline__ int owner(int x) const { return (x / C) / wpc; }
+    __device__ __forceinline__ bool needs(int c, int g) const {
+        const int lo = c * wpc * C;
+        if (lo >= N || owner(g) == c) return false;
+        const int hi = min(lo + wpc * C, N);
+        if (periodic) {
+            const int dl = ((lo - g) % N + N) % N;  // g in [lo - H, lo) mod N
+            const int dr = ((g - hi) % N + N) % N;  // g in [hi, hi + H) mod N
+            return (dl >= 1 && dl <= H) || dr < H;
+        }
+        return (g >= lo - H && g < lo) || (g >= hi && g < hi + H);
+    }
+};
 }  // namespace
 }  // namespace hb

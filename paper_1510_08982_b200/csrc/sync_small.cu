@@ -253,9 +253,19 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
     const bool pinned = __any_sync(0xffffffffu, pinF || pinL);  // warp-uniform
     const bool lexact = active && lane >= H / V && lane < (H + C) / V && g0 < N;
     const uint32_t bar0 = uint32_t(__cvta_generic_to_shared(&sbar[0]));
-    uint32_t incoming = 0;
+    uint32_t incoming = 0;  // CL: bytes of halo groups the other CTAs send per round
+    uint32_t send = 0;      // CL: CTAs that need my exact group (bit c)
     if (CL) {
-        incoming = uint32_t(N * 8 - __syncthreads_count(lexact) * V * 8);
+        const HaloGeo geo{N, C, H, int(blockDim.x >> 5), a.ncta, !a.dirichlet};
+        int cnt = 0;
+        for (int base = 0; base < N; base += V * int(blockDim.x)) {
+            const int g = base + V * int(threadIdx.x);
+            cnt += __syncthreads_count(g < N && geo.needs(rank, g));
+        }
+        incoming = uint32_t(cnt * V * 8);
+        if (lexact)
+            for (int cc = 0; cc < a.ncta; ++cc)
+                if (geo.needs(cc, int(g0))) send |= 1u << cc;
         if (threadIdx.x == 0) small_bars_init(bar0);
         small_cluster_sync();  // every CTA's barriers exist before the first st.async
     }
@@ -301,7 +311,7 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
 #pragma unroll
                 for (int i = 0; i < V; i += 2)
                     *reinterpret_cast<double2*>(&nu[g0 + i]) = make_double2(u[i], u[i + 1]);
-                if (CL) put_peers8<V>(&nu[g0], u, nbar, rank, a.ncta);
+                if (CL) put_mask<V>(&nu[g0], u, nbar, send);
             }
         }
         __syncthreads();
@@ -313,10 +323,11 @@ __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs
         par ^= 1;
         k += s;
     }
-    if (rank != 0) return;
+    // each CTA writes the points it owns (its copy of the rest is stale)
     su += par * Np;
+    const int lo = rank * int(blockDim.x >> 5) * C, hi = min(lo + int(blockDim.x >> 5) * C, N);
     bool bad = false;
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    for (int i = lo + int(threadIdx.x); i < hi; i += blockDim.x) {
         bad |= !isfinite(su[i]);
         a.field[i] = su[i];
     }
