@@ -1,3 +1,4 @@
+export PYTHONPATH=.
 set -x
 nproc; lscpu | head -20 > gpurun_out/lscpu.txt
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gputests.log 2>&1; echo "tests rc=$?"
