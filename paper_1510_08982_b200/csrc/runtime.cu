@@ -25,6 +25,7 @@ std::vector<std::unique_ptr<DevCtx>> g_ctx;
 }  // namespace
 
 void set_error(const std::string& msg) { t_error = msg; }
+std::string last_error_msg() { return t_error; }
 
 int dev_ctx(int device, DevCtx** out) {
     if (device < 0) {

@@ -40,6 +40,7 @@ struct heat_plan {
 namespace hb {
 
 void set_error(const std::string& msg);
+std::string last_error_msg();  // this thread's last fail() message
 inline int fail(int code, const std::string& msg) {
     set_error(msg);
     return code;
@@ -118,12 +119,12 @@ struct DevCtx {
     // pinned ring for large PAGEABLE fields (the streamed sync_run): slots
     // filled / drained by host threads while the copy engines move the rest
     void* ring = nullptr;
-    cudaEvent_t ring_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ring_ev[8] = {};
 };
 
 // A ring of kRingSlots pinned slots of kRingSlotBytes for staging a pageable
 // host field through the copy engines (allocated once per device).
-constexpr int kRingSlots = 4;
+constexpr int kRingSlots = 8;  // 4 for uploads, 4 for downloads
 constexpr size_t kRingSlotBytes = 128ull << 20;
 int host_ring(DevCtx& d, unsigned char** slots);
 // memcpy with up to `threads` host threads (large pageable <-> pinned copies)

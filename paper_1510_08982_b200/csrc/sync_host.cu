@@ -1,8 +1,12 @@
 // sync_host.cu -- launch logic for K1 (sync_tb.cuh) and the synchronous
 // C-ABI entry points: heat_sync_step / heat_sync_run / heat_sync_run_f32.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <atomic>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -416,7 +420,19 @@ __global__ void prep_chunk_kernel(double* __restrict__ u, long long lo, long lon
 
 constexpr size_t kStreamMinPoints = size_t(1) << 24;  // below: copies are cheap, one shot
 constexpr int kStreamChunks = 16;
-constexpr size_t kStreamMaxPasses = 128;              // above: copies are a small share
+// above: copies are a small share (and the S x C pass events add up).  At
+// cfg3 (157 passes) streaming hides both copies: 2.64 s against 2.94 s for
+// the one-shot path with pinned buffers, 2.65 s against 3.79 s with pageable
+// ones (tools/pageable_trace.py, HEAT_STREAM_TRACE=1)
+constexpr size_t kStreamMaxPasses = 1024;
+// HEAT_STREAM_MAX_PASSES overrides kStreamMaxPasses (A/B only)
+static size_t stream_max_passes() {
+    static const size_t v = [] {
+        const char* e = std::getenv("HEAT_STREAM_MAX_PASSES");
+        return e ? size_t(std::atoll(e)) : kStreamMaxPasses;
+    }();
+    return v;
+}
 
 }  // namespace
 
@@ -533,28 +549,118 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
 
     // A PAGEABLE field (the drop-in caller's std::vector) would make every
     // copy block the host inside the driver's own staging, which serialises
-    // the pipeline: it goes through a ring of pinned slots instead, filled
-    // and drained by host threads while the copy engines move the other slots.
+    // the pipeline: it goes through rings of pinned slots instead (4 for the
+    // uploads, 4 for the downloads), filled and drained by host threads while
+    // the copy engines move the other slots.  Downloads run on their own host
+    // thread, so a chunk's result leaves as soon as its last pass is done,
+    // while later chunks are still being uploaded.
     const bool page_in = host_pageable(u0), page_out = host_pageable(final_out);
+    // HEAT_STREAM_TRACE=1: host-side phase times on stderr (A/B only)
+    static const bool trace = std::getenv("HEAT_STREAM_TRACE") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto t_start = clk::now();
+    auto secs = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double>(b - a).count();
+    };
     unsigned char* slots[kRingSlots] = {};
     if (page_in || page_out) HB_TRY(host_ring(d, slots));
-    const int hthreads = int(std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+    const int ncpu = int(std::max(1u, std::thread::hardware_concurrency()));
+    const int hthreads = std::min(8, std::max(1, page_in && page_out ? ncpu / 2 : ncpu));
     const long long slot_pts = (long long)(kRingSlotBytes / sizeof(double));
-    bool slot_busy[kRingSlots] = {};
-    int slot = 0;
-    auto take_slot = [&]() -> int {  // the next slot, once its last copy is done
-        const int j = slot;
-        slot = (slot + 1) % kRingSlots;
-        if (slot_busy[j]) HB_CUDA(cudaEventSynchronize(d.ring_ev[j]));
-        slot_busy[j] = false;
+    constexpr int kHalf = kRingSlots / 2;
+    struct Ring {  // one direction's slots: j in [base, base + kHalf)
+        int base, next = 0;
+        bool busy[kHalf] = {};
+    };
+    auto take_slot = [&](Ring& R, int* j) -> int {  // the next slot, once its last copy is done
+        const int i = R.next;
+        R.next = (R.next + 1) % kHalf;
+        if (R.busy[i]) HB_CUDA(cudaEventSynchronize(d.ring_ev[R.base + i]));
+        R.busy[i] = false;
+        *j = R.base + i;
         return HEAT_OK;
     };
+    Ring rin{0}, rout{kHalf};
+    double t_copy_in = 0, t_copy_out = 0, t_drain_wait = 0, t_down_end = 0;
 
     // the flag reset precedes every upload and every kernel on either stream
     HB_CUDA(cudaMemsetAsync(d.flag, 0, 4 * sizeof(unsigned int), st));
     HB_CUDA(cudaEventRecord(ready, st));
     HB_CUDA(cudaStreamWaitEvent(d.h2d, ready, 0));
     HB_CUDA(cudaStreamWaitEvent(cs[1], ready, 0));
+
+    const int fin = int(S & 1);
+    // downloads: chunk c's final range once E(S-1, c) is recorded (enq > c)
+    std::atomic<int> enq{0};
+    std::atomic<bool> abort_dl{false};
+    auto download_all = [&]() -> int {
+        struct Pending {
+            int j;
+            double* dst;
+            size_t bytes;
+        };
+        std::vector<Pending> pend;  // slot downloads not yet copied out (FIFO)
+        size_t head = 0;
+        auto drain_one = [&]() -> int {
+            const Pending pd = pend[head++];
+            const auto w0 = clk::now();
+            HB_CUDA(cudaEventSynchronize(d.ring_ev[pd.j]));
+            const auto c0 = clk::now();
+            t_drain_wait += secs(w0, c0);
+            parallel_memcpy(pd.dst, slots[pd.j], pd.bytes, hthreads);
+            t_copy_out += secs(c0, clk::now());
+            rout.busy[pd.j - rout.base] = false;
+            return HEAT_OK;
+        };
+        for (int c = 0; c < C; ++c) {
+            while (enq.load(std::memory_order_acquire) <= c) {
+                if (abort_dl.load()) return HEAT_OK;
+                std::this_thread::yield();
+            }
+            const long long a0 = lo(c, S - 1), a1 = hi(c, S - 1);
+            HB_CUDA(cudaStreamWaitEvent(d.d2h, E(S - 1, c), 0));
+            if (!page_out) {
+                HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0,
+                                        (a1 - a0) * sizeof(double), cudaMemcpyDeviceToHost, d.d2h));
+                continue;
+            }
+            for (long long o = a0; o < a1; o += slot_pts) {
+                const long long cnt = std::min(slot_pts, a1 - o);
+                // keep kHalf - 1 downloads in flight; copy out the oldest
+                while (pend.size() - head >= size_t(kHalf - 1)) HB_TRY(drain_one());
+                int j = 0;
+                HB_TRY(take_slot(rout, &j));
+                HB_CUDA(cudaMemcpyAsync(slots[j], bufs[fin] + o, size_t(cnt) * sizeof(double),
+                                        cudaMemcpyDeviceToHost, d.d2h));
+                HB_CUDA(cudaEventRecord(d.ring_ev[j], d.d2h));
+                rout.busy[j - rout.base] = true;
+                pend.push_back({j, final_out + o, size_t(cnt) * sizeof(double)});
+            }
+        }
+        while (head < pend.size()) HB_TRY(drain_one());
+        t_down_end = secs(t_start, clk::now());
+        return HEAT_OK;
+    };
+    int dl_status = HEAT_OK;
+    std::string dl_msg;
+    std::thread downloader;
+    if (page_out)
+        downloader = std::thread([&] {
+            cudaSetDevice(d.device);
+            dl_status = download_all();
+            if (dl_status != HEAT_OK) dl_msg = last_error_msg();
+        });
+    struct Joiner {
+        std::thread& t;
+        std::atomic<bool>& ab;
+        ~Joiner() {
+            if (t.joinable()) {
+                ab.store(true);
+                t.join();
+            }
+        }
+    } joiner{downloader, abort_dl};
+
     for (int c = 0; c < C; ++c) {
         const long long a0 = B[c], a1 = B[c + 1];
         cudaStream_t s_c = cs[c & 1];
@@ -564,13 +670,15 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
         } else {
             for (long long o = a0; o < a1; o += slot_pts) {
                 const long long cnt = std::min(slot_pts, a1 - o);
-                const int j = slot;
-                HB_TRY(take_slot());
+                int j = 0;
+                HB_TRY(take_slot(rin, &j));
+                const auto c0 = clk::now();
                 parallel_memcpy(slots[j], u0 + o, size_t(cnt) * sizeof(double), hthreads);
+                t_copy_in += secs(c0, clk::now());
                 HB_CUDA(cudaMemcpyAsync(bufs[0] + o, slots[j], size_t(cnt) * sizeof(double),
                                         cudaMemcpyHostToDevice, d.h2d));
                 HB_CUDA(cudaEventRecord(d.ring_ev[j], d.h2d));
-                slot_busy[j] = true;
+                rin.busy[j - rin.base] = true;
             }
         }
         HB_CUDA(cudaEventRecord(up[c], d.h2d));
@@ -586,46 +694,21 @@ int sync_run_streamed(DevCtx& d, const double* u0, size_t n, double r, double c1
             HB_CUDA(cudaEventRecord(E(pi, c), s_c));
             left -= size_t(s);
         }
+        enq.store(c + 1, std::memory_order_release);
     }
-    // downloads last: a pageable destination makes each copy block the host,
-    // which must not hold back the compute launches above
-    const int fin = int(S & 1);
-    struct Pending {
-        int j;
-        double* dst;
-        size_t bytes;
-    };
-    std::vector<Pending> pend;  // slot downloads not yet copied out (FIFO)
-    size_t pend_head = 0;
-    auto drain_one = [&]() -> int {
-        const Pending pd = pend[pend_head++];
-        HB_CUDA(cudaEventSynchronize(d.ring_ev[pd.j]));
-        parallel_memcpy(pd.dst, slots[pd.j], pd.bytes, hthreads);
-        slot_busy[pd.j] = false;
-        return HEAT_OK;
-    };
-    for (int c = 0; c < C; ++c) {
-        const long long a0 = lo(c, S - 1), a1 = hi(c, S - 1);
-        HB_CUDA(cudaStreamWaitEvent(d.d2h, E(S - 1, c), 0));
-        if (!page_out) {
-            HB_CUDA(cudaMemcpyAsync(final_out + a0, bufs[fin] + a0, (a1 - a0) * sizeof(double),
-                                    cudaMemcpyDeviceToHost, d.d2h));
-            continue;
-        }
-        for (long long o = a0; o < a1; o += slot_pts) {
-            const long long cnt = std::min(slot_pts, a1 - o);
-            // keep kRingSlots - 1 downloads in flight; copy out the oldest
-            while (pend.size() - pend_head >= size_t(kRingSlots - 1)) HB_TRY(drain_one());
-            const int j = slot;
-            HB_TRY(take_slot());
-            HB_CUDA(cudaMemcpyAsync(slots[j], bufs[fin] + o, size_t(cnt) * sizeof(double),
-                                    cudaMemcpyDeviceToHost, d.d2h));
-            HB_CUDA(cudaEventRecord(d.ring_ev[j], d.d2h));
-            slot_busy[j] = true;
-            pend.push_back({j, final_out + o, size_t(cnt) * sizeof(double)});
-        }
+    const auto t_enq = clk::now();
+    if (page_out) {
+        downloader.join();
+        if (dl_status != HEAT_OK) return fail(dl_status, dl_msg);
+    } else {
+        HB_TRY(download_all());  // pinned destination: the copies are only enqueued
     }
-    while (pend_head < pend.size()) HB_TRY(drain_one());
+    if (trace)
+        std::fprintf(stderr,
+                     "[stream] chunks %d passes %lld: uploads+enqueue %.3f s (copy-in %.3f), "
+                     "downloads done at %.3f s (drain waits %.3f, copy-out %.3f), end %.3f s\n",
+                     C, S, secs(t_start, t_enq), t_copy_in, t_down_end, t_drain_wait, t_copy_out,
+                     secs(t_start, clk::now()));
     HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 1), 0));  // both streams done
     if (C > 1) HB_CUDA(cudaStreamWaitEvent(st, E(S - 1, C - 2), 0));
     unsigned int flags[4] = {0, 0, 0, 0};
@@ -759,7 +842,7 @@ int sync_run_impl(const double* u0, size_t n, double r, int bc_kind, double c1, 
     if (!f32 && final_out && !snapshots && !steps_out && bc_kind == HEAT_BC_DIRICHLET &&
         n >= kStreamMinPoints && k_end > 0 &&
         (k_end + sync_variant_entry<double>().halo - 1) / sync_variant_entry<double>().halo <=
-            kStreamMaxPasses &&
+            stream_max_passes() &&
         std::abs(u0[0] - c1) <= 1e-9 && std::abs(u0[n - 1] - c2) <= 1e-9 && !kernel_ms &&
         !std::getenv("HEAT_NO_STREAMED_SYNC"))
         return sync_run_streamed(*d, reinterpret_cast<const double*>(u0), n, r, c1, c2, k_end,

@@ -37,7 +37,7 @@ def _oneshot(H, u, r, bc, k):
         del os.environ["HEAT_NO_STREAMED_SYNC"]
 
 
-@pytest.mark.parametrize("k", [1, 31, 32, 33, 100, 1000])
+@pytest.mark.parametrize("k", [1, 31, 32, 33, 100, 1000, 10000])
 def test_streamed_matches_one_shot(H, k):
     bc = H.BoundaryCondition.dirichlet(0.75, -0.25)
     u = _field(k, 0.75, -0.25)
@@ -85,6 +85,31 @@ def test_streamed_errors(H):
     u = _field(6, 0.0, 0.0)
     assert bits_equal(H.sync_final(u, H.SolverParams.from_r(0.4), bc, 64),
                       _oneshot(H, u, 0.4, bc, 64))
+
+
+def test_streamed_many_passes_pageable_and_pinned(H, port):
+    # cfg3's pass count (10^4 steps: 157 passes of 64) on a 2^25-point field,
+    # once from ordinary numpy buffers (the pinned staging ring) and once
+    # from pinned ones: the same bits, and the oracle's light cone around
+    # the field ends and a few interior points
+    import torch
+    n = (1 << 25) + 77
+    k = 10000
+    rng = np.random.default_rng(21)
+    u = rng.uniform(-1.0, 1.0, n)
+    u[0], u[-1] = 0.0, 0.0
+    bc = H.BoundaryCondition.dirichlet(0.0, 0.0)
+    p = H.SolverParams.from_r(0.4)
+    got = H.sync_final(u, p, bc, k)
+    pin_in = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pin_out = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    pin_in[:] = u
+    from paper_1510_08982_b200 import _lib
+    _lib.check(_lib.lib().heat_sync_run(_lib.dptr(pin_in), n, 0.4, 0, 0.0, 0.0, k, k,
+                                        _lib.dptr(pin_out), None, None, 0, None), "sync_run")
+    assert bits_equal(got, pin_out)
+    for i in (0, 1, 5, n // 3, n // 2 + 1, n - 6, n - 2, n - 1):
+        assert port.sync_lightcone(u, 0.4, 0, 0.0, 0.0, k, i) == got[i], i
 
 
 def test_streamed_graded_chunks_large(H):
