@@ -15,8 +15,10 @@ launch per rank, no collective inside).
 
 Arms
   b200       the sm_100a kernels (libheat_b200.so) -- value is device-timed
-             with inputs resident in HBM; e2e is timed through the C-ABI
-             (heat_sync_run with pinned host buffers, copies included).
+             with inputs resident in HBM; e2e is timed through the C-ABI:
+             one heat_sync_run call per e2e step running the whole K x 1000
+             steps (cfg3: 10^4) from pinned host buffers, copies included
+             (also with pageable buffers, and with 1000-step calls).
   reference  the reference's own CPU executor (exec_run Barriered, all host
              threads) from oracle/_ref (compiled from /root/reference), or the
              C port when that library is absent; rank 0 only.
@@ -735,50 +737,64 @@ def run_async_multi(args, H, MG, torch, stream, n, r, bc, sync_glups, rank, worl
 
 
 def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance, parity):
-    """Same metric through the public API with HOST buffers: per step the
-    pinned host field goes H2D, 1000 FTCS steps run, the result comes back D2H."""
-    k = max(1, min(args.steps, 3))
+    """Same metric through the public API with HOST buffers.  One e2e step is
+    one call that runs the timed region's whole workload (cfg3: 10^4 FTCS
+    steps, as a caller's sync_run(u0, params, bc, 10000) does): the host field
+    goes H2D, the steps run, the result comes back D2H, all inside the timed
+    call.  `per_call_1000` repeats it with 1000-step calls (the copies are
+    then a larger share)."""
+    kc = STEPS_PER_BENCH_STEP * args.steps  # FTCS steps per e2e call
+    k = 2 if kc >= 5000 else 3
     host_in = torch.empty(n, dtype=torch.float64, pin_memory=True)
     host_out = torch.empty(n, dtype=torch.float64, pin_memory=True)
     plan.download(host_in.numpy())  # a valid (prepared) field to start from
     a_in, a_out = host_in.numpy(), host_out.numpy()
-    times = []
-    for i in range(k + 1):
-        if world == 1:
-            t0 = time.perf_counter()
-            H._lib.check(H._lib.lib().heat_sync_run(
-                H._lib.dptr(a_in), n, r, bc.kind, bc.c1, bc.c2, STEPS_PER_BENCH_STEP,
-                STEPS_PER_BENCH_STEP, H._lib.dptr(a_out), None, None, 0, None), "heat_sync_run")
-            t1 = time.perf_counter()
-        else:
-            import torch.distributed as dist
-            dist.barrier()
-            t0 = time.perf_counter()
-            plan.upload(a_in)
-            advance(STEPS_PER_BENCH_STEP)
-            plan.download(a_out)
-            dist.barrier()
-            t1 = time.perf_counter()
-        if i > 0:
-            times.append(t1 - t0)
+
+    def c_call(src, dst, steps):
+        H._lib.check(H._lib.lib().heat_sync_run(
+            H._lib.dptr(src), n, r, bc.kind, bc.c1, bc.c2, steps, steps, H._lib.dptr(dst), None,
+            None, 0, None), "heat_sync_run")
+
+    def timed_calls(src, dst, steps, reps):
+        ts = []
+        for i in range(reps + 1):
+            if world == 1:
+                t0 = time.perf_counter()
+                c_call(src, dst, steps)
+                t1 = time.perf_counter()
+            else:
+                import torch.distributed as dist
+                dist.barrier()
+                t0 = time.perf_counter()
+                plan.upload(src)
+                advance(steps)
+                plan.download(dst)
+                dist.barrier()
+                t1 = time.perf_counter()
+            if i > 0:
+                ts.append(t1 - t0)
+        return ts
+
+    times = timed_calls(a_in, a_out, kc, k)
     if world == 1 and not args.skip_parity:  # the last call's output against its input
         from oracle import oracle as O
         from oracle.lightcone import WindowCheck
         port = O.port()
-        chk = WindowCheck(n, STEPS_PER_BENCH_STEP, sync_centres(n))
+        chk = WindowCheck(n, kc, sync_centres(n))
         chk.capture(lambda lo, c: a_in[lo:lo + c])
         parity["e2e"] = chk.verify(
             lambda lo, c: a_out[lo:lo + c],
-            lambda w, lo: port.sync_window(w, lo, n, r, 0.0, 0.0, STEPS_PER_BENCH_STEP))
+            lambda w, lo: port.sync_window(w, lo, n, r, 0.0, 0.0, kc))
     t = statistics.median(times)
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
-    v = float(n) * world * STEPS_PER_BENCH_STEP / t / 1e9
+    v = float(n) * world * kc / t / 1e9
     out = {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-           "d2h_bytes_per_step": 8 * n, "steps": k,
+           "d2h_bytes_per_step": 8 * n, "steps": k, "ftcs_steps_per_step": kc,
+           "seconds_per_step": round(t, 4),
            "api": "heat_sync_run (C-ABI, pinned host buffers)" if world == 1 else
                   "heat.Plan upload/advance/download per rank"}
     if world == 1:
@@ -789,19 +805,20 @@ def run_e2e(args, H, torch, n, r, bc, rank, world, plan, advance, parity):
         p_in = np.empty(n)
         p_in[:] = a_in
         p_out = np.empty(n)
-        pt = []
-        for i in range(3):
-            t0 = time.perf_counter()
-            H._lib.check(H._lib.lib().heat_sync_run(
-                H._lib.dptr(p_in), n, r, bc.kind, bc.c1, bc.c2, STEPS_PER_BENCH_STEP,
-                STEPS_PER_BENCH_STEP, H._lib.dptr(p_out), None, None, 0, None), "heat_sync_run")
-            if i > 0:
-                pt.append(time.perf_counter() - t0)
+        pt = timed_calls(p_in, p_out, kc, 2)
         same = bool(np.array_equal(p_out.view(np.uint64), a_out.view(np.uint64)))
-        out["pageable"] = {"value": round(float(n) * STEPS_PER_BENCH_STEP / statistics.median(pt) / 1e9, 3),
+        out["pageable"] = {"value": round(float(n) * kc / statistics.median(pt) / 1e9, 3),
                            "unit": UNIT, "steps": len(pt), "same_result_as_pinned": same,
                            "api": "heat_sync_run (C-ABI) with pageable numpy host buffers, "
                                   "as heat::sync_run's std::vector fields arrive"}
+        if kc != STEPS_PER_BENCH_STEP:
+            t1k = statistics.median(timed_calls(a_in, a_out, STEPS_PER_BENCH_STEP, 3))
+            p1k = statistics.median(timed_calls(p_in, p_out, STEPS_PER_BENCH_STEP, 2))
+            out["per_call_1000"] = {
+                "pinned": round(float(n) * STEPS_PER_BENCH_STEP / t1k / 1e9, 3),
+                "pageable": round(float(n) * STEPS_PER_BENCH_STEP / p1k / 1e9, 3), "unit": UNIT,
+                "what": "1000-step calls: 8 GiB in and out per 1000 steps (pageable: bound by the "
+                        "host's memory bandwidth, DESIGN §5)"}
     return out
 
 
