@@ -46,8 +46,9 @@ struct SyncCol {
 // left neighbour product from colr (null: a chunk's first tile, which has a
 // left halo instead), and lane kPL stores its element kPE's product of every
 // time level into colw.
+// Steps s0 .. s1-1 of the tile (the column index is the step).
 template <typename Real, int V, int PU, int PE>
-__device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int nsteps,
+__device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int s0, int s1,
                                                const Real* colr, Real* colw, bool wlane,
                                                int lane) {
     using A = Arith<Real>;
@@ -59,9 +60,9 @@ __device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int
     // the column value of the next step is loaded beside its shuffle and
     // selected only where the step uses it (selecting at once would wait for
     // the shuffle: -2.8%, ncu short_sb)
-    Real pLc = rd ? colr[0] : Real(0);
+    Real pLc = rd ? colr[s0] : Real(0);
 #pragma unroll PU
-    for (int s = 0; s < nsteps; ++s) {
+    for (int s = s0; s < s1; ++s) {
         const Real p1 = A::mul(r, u[1]);
         const Real pVm2 = A::mul(r, u[V - 2]);
         const Real nF = stencil_p(p1, A::mul(c, u[0]), rd ? pLc : pL);
@@ -70,7 +71,7 @@ __device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int
         const Real pLs2 = A::mul(r, nL);
         pL = __shfl_up_sync(0xffffffffu, pLs2, 1);  // for step s+1
         pR = __shfl_down_sync(0xffffffffu, pF2, 1);
-        if (rd && s + 1 < nsteps) pLc = colr[s + 1];
+        if (rd && s + 1 < s1) pLc = colr[s + 1];
         Real pm1 = pF, p0 = p1;
 #pragma unroll
         for (int i = 1; i <= V - 2; ++i) {
@@ -93,7 +94,11 @@ __device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int
     }
 }
 
-template <typename Real, int V, int H, int CH, int PU>
+// MID: issue the next tile's TMA load half way through this tile's steps
+// instead of right after its window is read.  The load goes into the other
+// buffer, whose last TMA store (the previous tile's output) must have read
+// it first: right after the window read that store was only just committed.
+template <typename Real, int V, int H, int CH, int PU, bool MID = false>
 __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, 2)
     sync_col_kernel(const __grid_constant__ CUtensorMap tm_src,
                     const __grid_constant__ CUtensorMap tm_dst0,
@@ -194,13 +199,23 @@ __global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, 2)
         }
         const long long nch = more ? ch : (long long)__shfl_sync(0xffffffffu, nraw, 0);
         const int nti = more ? ti + 1 : 0;
-        if (nch < a.tiles && interior(win_start(nch, nti))) issue(b ^ 1, win_start(nch, nti));
+        const bool next_tma = nch < a.tiles && interior(win_start(nch, nti));
+        const bool plain_steps = !(inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0)));
+        if (next_tma && (!MID || plain_steps)) issue(b ^ 1, win_start(nch, nti));
 
         const Real* colr = ti == 0 ? nullptr : cols + ((ti - 1) & 1) * H;
         Real* colw = cols + (ti & 1) * H;
         const bool wlane = lane == K::kPL;
-        if (inter || (!in_window(a.pin_lo, w0) && !in_window(a.pin_hi, w0))) {
-            warp_steps_col<Real, V, PU, K::kPE>(u, r, c, a.nsteps, colr, colw, wlane, lane);
+        if (!plain_steps) {
+            if (MID) {
+                const int half = a.nsteps / 2;
+                warp_steps_col<Real, V, PU, K::kPE>(u, r, c, 0, half, colr, colw, wlane, lane);
+                if (next_tma) issue(b ^ 1, win_start(nch, nti));
+                warp_steps_col<Real, V, PU, K::kPE>(u, r, c, half, a.nsteps, colr, colw, wlane,
+                                                    lane);
+            } else {
+                warp_steps_col<Real, V, PU, K::kPE>(u, r, c, 0, a.nsteps, colr, colw, wlane, lane);
+            }
         } else {
             for (int s = 0; s < a.nsteps; ++s) {
                 const Real pFirst = Arith<Real>::mul(r, u[0]);

@@ -99,19 +99,19 @@ SyncVariant variant_cta() {
             C::smem_bytes(), H, true, G, 0, true};
 }
 // K1s (sync_col.cuh): chunks of CH tiles per warp, boundary column carried
-template <typename Real, int V, int H, int CH, int PU>
+template <typename Real, int V, int H, int CH, int PU, bool MID = false>
 SyncVariant variant_col() {
     using K = SyncCol<Real, V, H, CH>;
     SyncVariant v{nullptr, 2, V, K::kChunkOut, SyncTB<Real, V, H>::kWinUnits, K::kOut0Units,
                   K::smem_bytes(), H, true, 4, 0, false};
-    v.fn3 = sync_col_kernel<Real, V, H, CH, PU>;
+    v.fn3 = sync_col_kernel<Real, V, H, CH, PU, MID>;
     v.out1_units = K::kOut1Units;
     return v;
 }
-template <typename Real, int CH, int PU>
+template <typename Real, int CH, int PU, bool MID = false>
 SyncVariant variant_col48() {
     if constexpr (sizeof(Real) == 8)
-        return variant_col<Real, 48, 64, CH, PU>();
+        return variant_col<Real, 48, 64, CH, PU, MID>();
     else
         return variant<Real, 64, 2, -4, true, 64, true>();  // = variant 15 for f32
 }
@@ -139,10 +139,11 @@ SyncVariant variant48() {
 // twice, same box); unrolled x1 (14) loses 1.7%.
 // 20: K1s (sync_col.cuh), chunks of 8 tiles with a carried boundary column:
 // 4076 vs 4036 GLUPS for 15 on the same box, three times (95.3% of the stepped
-// points exact against 91.7%; FP64 pipe 92.1% vs 93.4% active).
+// points exact against 91.7%; FP64 pipe 92.1% vs 93.4% active).  23: the same
+// with the next tile's load issued half way through the steps (MID).
 constexpr int kDefaultSyncVariant = 20;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 23;
+constexpr int kSyncVariants = 24;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -184,6 +185,7 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant_col48<Real, 8, 4>(),
         variant_col48<Real, 16, 4>(),
         variant_col48<Real, 8, 3>(),
+        variant_col48<Real, 8, 4, true>(),
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
