@@ -95,3 +95,25 @@ def test_variants_agree(env):
     out = subprocess.run([sys.executable, "-c", code], env=env_, cwd=ROOT, capture_output=True,
                          text=True, timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_k7c_and_k9_device_staging_fallback(H, port):
+    # a trajectory larger than the pinned staging buffer (64 MB: 9001 rows of
+    # 8 KB) takes the device-buffer path with copies instead of zero-copy
+    n, k = 1024, 9000
+    gen = SplitMix64(4242)
+    u0 = random_field(gen, n)
+    bc = H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    p = H.SolverParams.from_r(0.35)
+    t = H.sync_run(H.TemperatureField(u0), p, bc, k, 1)
+    steps, snaps = port.sync_run(u0, p.r(), bc.kind, bc.c1, bc.c2, k, 1, record=True)
+    assert t.steps == steps
+    for j in (0, 1, 63, 64, 65, 4500, k):
+        assert bits_equal(t.snapshots[j].values(), snaps[j]), j
+    m = H.DelayModel.uniform(3, 9)
+    ta = H.async_run(H.TemperatureField(u0), p, bc, H.PartitionSpec(n, 128), m, k, 1)
+    st, sn = port.async_run(u0, p.r(), bc.kind, bc.c1, bc.c2, 128, 0, 3, seed=9, k_end=k,
+                            stride=1, record=True)
+    assert ta.steps == st
+    for j in (0, 1, 63, 64, 65, 4500, k):
+        assert bits_equal(ta.snapshots[j].values(), sn[j]), j
