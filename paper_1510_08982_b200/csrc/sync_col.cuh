@@ -38,7 +38,9 @@ struct SyncCol {
         return T::kWarpsPerCta * (2 * T::kBufBytes + kColBytes + 2 * 8) + 1024;
     }
     static_assert(kE1 - 1 == kLastPos, "both tile kinds end at the same window position");
-    static_assert(kPE >= 1 && kPE + 2 < V, "the column point is an interior element of its lane");
+    // (the pipelined step takes element PE's product as pn of interior point
+    // PE-1: PE = V-2 is pVm2 and PE = V-1 is the lane's last product pLs)
+    static_assert(kPE >= 2 && kPE <= V - 1, "the column point is a pn of the step");
     static_assert(kE0 % T::kUnit == 0 && kE1 % T::kUnit == 0, "outputs of whole units");
 };
 
@@ -99,7 +101,7 @@ __device__ __forceinline__ void warp_steps_col(Real (&u)[V], Real r, Real c, int
 // buffer, whose last TMA store (the previous tile's output) must have read
 // it first: right after the window read that store was only just committed.
 template <typename Real, int V, int H, int CH, int PU, bool MID = false>
-__global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, 2)
+__global__ void __launch_bounds__(SyncTB<Real, V, H>::kThreads, V <= 32 ? 3 : 2)
     sync_col_kernel(const __grid_constant__ CUtensorMap tm_src,
                     const __grid_constant__ CUtensorMap tm_dst0,
                     const __grid_constant__ CUtensorMap tm_dst1, const SyncPassArgs a) {

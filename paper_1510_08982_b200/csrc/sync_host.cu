@@ -115,6 +115,16 @@ SyncVariant variant_col48() {
     else
         return variant<Real, 64, 2, -4, true, 64, true>();  // = variant 15 for f32
 }
+// 24: K1s with 32-point lanes (3 CTAs of 4 warps per SM instead of 2)
+template <typename Real, int CH, int PU>
+SyncVariant variant_col32() {
+    if constexpr (sizeof(Real) == 8) {
+        SyncVariant v = variant_col<Real, 32, 64, CH, PU>();
+        return v;
+    } else {
+        return variant<Real, 64, 2, -4, true, 64, true>();  // = variant 15 for f32
+    }
+}
 template <typename Real, int PU>
 SyncVariant variant_cta48() {
     if constexpr (sizeof(Real) == 8)
@@ -140,10 +150,11 @@ SyncVariant variant48() {
 // 20: K1s (sync_col.cuh), chunks of 8 tiles with a carried boundary column:
 // 4076 vs 4036 GLUPS for 15 on the same box, three times (95.3% of the stepped
 // points exact against 91.7%; FP64 pipe 92.1% vs 93.4% active).  23: the same
-// with the next tile's load issued half way through the steps (MID).
+// with the next tile's load issued half way through the steps (MID): 4077.8 vs
+// 4076.0.  24: 32-point lanes, 3 CTAs per SM: 3956 vs 4073.
 constexpr int kDefaultSyncVariant = 20;
 constexpr int kHalo32Variant = 6;
-constexpr int kSyncVariants = 24;
+constexpr int kSyncVariants = 25;
 
 // The selected variant's table entry (no CUDA calls); `max_halo` (> 0) caps
 // the halo, i.e. the steps per pass the caller will ask for.
@@ -186,6 +197,7 @@ SyncVariant& sync_variant_entry(int max_halo = 0) {
         variant_col48<Real, 16, 4>(),
         variant_col48<Real, 8, 3>(),
         variant_col48<Real, 8, 4, true>(),
+        variant_col32<Real, 8, 4>(),
     };
     static const int idx = [] {
         const char* e = std::getenv("HEAT_SYNC_VARIANT");
