@@ -244,11 +244,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         const int own = __syncthreads_count(lexact) * V * 8 +
                         (__syncthreads_count(ex0) + __syncthreads_count(ex7)) * QH * 8;
         incoming = uint32_t(N * 8 + 2 * a.P * QH * 8 - own);
-        if (threadIdx.x == 0) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
+        if (threadIdx.x == 0) small_bars_init(bar0);
         small_cluster_sync();  // every CTA's barriers exist before the first st.async
     }
     int par = 0;              // buffer read by this round
@@ -268,9 +264,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         double* nt = tab + (par ^ 1) * TB;
         const uint32_t nbar = bar0 + 8u * uint32_t(par ^ 1);
         if (CL && threadIdx.x == 0)  // this round's phase: my arrival + the peers' bytes
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(nbar),
-                         "r"(incoming)
-                         : "memory");
+            small_bar_expect(nbar, incoming);
         if (active) {
 #pragma unroll
             for (int i = 0; i < V; i += 2) {

@@ -4,7 +4,10 @@
 // owners write each round's results into every copy, their own with plain
 // stores and the other CTAs' with st.async, whose bytes complete on the
 // receiver's mbarrier for that buffer.  A round ends with one __syncthreads
-// and one wait for the mbarrier phase -- no cluster barrier, no memory fence.
+// and one wait for the mbarrier phase -- no cluster barrier, no memory fence
+// (a fenced barrier.cluster compiles to MEMBAR.ALL.GPU + CCTL.IVALL).  K7c
+// sends only the lane groups another CTA's halo needs (HaloGeo, put_mask);
+// K9 sends its whole exact chunk and history rows (put_peers8 / put_peers2).
 #pragma once
 #include <cstdint>
 
@@ -87,11 +90,6 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
             : "memory");
 }
 
-}  // namespace
-}  // namespace hb
-
-namespace hb {
-namespace {
 // the two round mbarriers (one arrival each: the local expect_tx), visible to
 // the cluster before any st.async targets them
 __device__ __forceinline__ void small_bars_init(uint32_t bar0) {
@@ -103,12 +101,7 @@ __device__ __forceinline__ void small_bar_expect(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
-}  // namespace
-}  // namespace hb
-
-namespace hb {
-namespace {
-// Halo-only exchange geometry.  CTA c of a cluster owns the exact points
+// Halo-only exchange geometry (K7c).  CTA c of a cluster owns the exact points
 // [lo_c, hi_c), lo_c = c * wpc * C, hi_c = min(lo_c + wpc * C, N), C being
 // a window's exact width; its windows read H points beyond each end (mod N
 // when periodic, clipped to the field for Dirichlet).  A lane group of V
