@@ -39,7 +39,7 @@ def _check(H, port, n, periodic, k_end, stride, seed):
         assert bits_equal(s.values(), snaps[j]), (n, periodic, k_end, stride, j)
 
 
-@pytest.mark.parametrize("n", [8, 64, 128, 136, 1000, 1024, 1032, 2048, 4096, 4104, 8192])
+@pytest.mark.parametrize("n", [8, 64, 128, 136, 520, 1000, 1024, 1032, 1544, 2048, 4096, 4104, 8192])
 @pytest.mark.parametrize("periodic", [False, True])
 def test_k7c_trajectories(H, port, n, periodic):
     for i, (k, stride) in enumerate([(0, 1), (1, 1), (64, 7), (130, 64), (333, 100), (200, 1)]):
