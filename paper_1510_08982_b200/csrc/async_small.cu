@@ -5,7 +5,8 @@
 // Replaces async_run (async_sim.cpp:118-160) -- Eq. (4): a PE's first/last
 // point reads its cross-PE neighbour at step k - d, d drawn from the run's
 // SplitMix64 stream in the reference's order (async_sim.cpp:86-101) -- for
-// N <= 2048 with PEs of a multiple of 8 points and q <= 8.
+// N <= 8192 with PEs of a multiple of 8 points and q <= 8 (up to 2048 points
+// in one CTA, beyond that over a thread-block cluster).
 //
 // Why temporal blocking still works with delays: a point at step k+1 depends
 // on its two neighbours at steps k - d (d <= q-1 <= k), i.e. still on points
@@ -45,7 +46,9 @@ namespace {
 constexpr int kAsV = 8;                       // points per lane
 constexpr int kAsHalo = 64;                   // steps per round = halo points per side
 constexpr int kAsChunk = 32 * kAsV - 2 * kAsHalo;  // 128 exact points per warp
-constexpr int kAsMaxN = 2048;                 // 16 warps (128 registers per thread)
+constexpr int kAsMaxN = 8192;                 // 64 windows: 8 CTAs x 8 warps
+constexpr int kAsMaxWarpsCta = 16;            // 512 threads (128 registers per thread)
+constexpr size_t kAsSmemCap = 200 * 1024;     // dynamic shared memory of one CTA's copies
 constexpr int kAsMaxQ = 8;
 constexpr int kAsSub = 16;  // steps per delay word (16 nibbles)
 
@@ -112,8 +115,8 @@ __device__ __forceinline__ double pick(const double (&h)[QH], int d) {
 template <int QH, int LAW, bool CL>
 __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArgs a) {
     extern __shared__ double smem[];
-    __shared__ __align__(16) unsigned char sdel[kAsMaxN / kAsChunk][64 * kAsSub];  // per warp: [stream][step]
-    __shared__ int sstr[kAsMaxN / kAsChunk][64];  // per warp: draw rank of each delay stream
+    __shared__ __align__(16) unsigned char sdel[kAsMaxWarpsCta][64 * kAsSub];  // per warp: [stream][step]
+    __shared__ int sstr[kAsMaxWarpsCta][64];  // per warp: draw rank of each delay stream
     __shared__ __align__(8) unsigned long long sbar[2];  // CL: round mbarriers, by buffer
     const int Np = (a.N + 1) & ~1, TB = a.P * 2 * QH;
     double* su = smem;              // [2][Np]: the field, double-buffered
@@ -425,9 +428,17 @@ size_t small_smem_bytes(size_t N, size_t P, int QH, size_t q) {
 
 }  // namespace
 
+// Fields of <= 2048 points fit one CTA (16 windows); up to 8192 points the
+// windows spread over a cluster of <= 8 CTAs, each holding the field and the
+// history table twice (<= kAsSmemCap).
 bool async_small_eligible(size_t N, size_t per_pe, size_t q) {
     if (std::getenv("HEAT_NO_SMALL_ASYNC")) return false;
-    return N <= (size_t)kAsMaxN && per_pe % kAsV == 0 && per_pe < N && q <= (size_t)kAsMaxQ;
+    if (!(N <= (size_t)kAsMaxN && per_pe % kAsV == 0 && per_pe < N && q <= (size_t)kAsMaxQ))
+        return false;
+    static const bool no_cluster = std::getenv("HEAT_K9_NO_CLUSTER") != nullptr;
+    const size_t warps = (N + kAsChunk - 1) / kAsChunk;
+    if (no_cluster && warps > (size_t)kAsMaxWarpsCta) return false;
+    return small_smem_bytes(N, N / per_pe, history_slots(q), q) <= kAsSmemCap;
 }
 
 // Whole deterministic async_run of a small field on one CTA (K9).  The caller
@@ -539,15 +550,15 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     // sub-partition (K9 is latency-bound; two warps per sub-partition
     // serialise their issue).  HEAT_K9_NO_CLUSTER=1: one CTA.
     static const bool no_cluster = std::getenv("HEAT_K9_NO_CLUSTER") != nullptr;
-    const int ncta = no_cluster ? 1 : std::min(4, (warps + 3) / 4);
+    const int ncta = no_cluster ? 1 : std::min(8, (warps + 3) / 4);
     const int wpc = (warps + ncta - 1) / ncta;
     a.ncta = ncta;
     auto launch = [&](auto kern1, auto kernc) -> int {
         int per_sm = 0;
         const void* fn = ncta > 1 ? reinterpret_cast<const void*>(kernc)
                                   : reinterpret_cast<const void*>(kern1);
-        HB_TRY(kernel_smem_config(fn, int(small_smem_bytes(kAsMaxN, kAsMaxN / kAsV, kAsMaxQ, kAsMaxQ)),
-                                  wpc * 32, &per_sm));
+        if (wpc > kAsMaxWarpsCta) return fail(HEAT_ELOGIC, "K9: too many windows per CTA");
+        HB_TRY(kernel_smem_config(fn, int(kAsSmemCap), wpc * 32, &per_sm));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(ncta));
         cfg.blockDim = dim3(unsigned(wpc * 32));

@@ -388,6 +388,29 @@ def test_small_async_kernel_bit_exact(H, port, seed):
             assert bits_equal(s.values(), snaps[j]), (n, per_pe, q, law, periodic, k_end, stride, j)
 
 
+@pytest.mark.parametrize("n,per_pe,q,law,bc", [
+    (2056, 8, 3, 0, 0), (2056, 8, 3, 0, 1), (4096, 64, 8, 2, 1), (4104, 216, 5, 1, 0),
+    (6144, 8, 3, 0, 1), (8192, 512, 2, 0, 0), (8192, 8, 1, 0, 1), (8184, 24, 7, 2, 0)])
+def test_small_async_cluster_sizes_bit_exact(H, port, n, per_pe, q, law, bc):
+    # K9 beyond one CTA (N = 2049..8192: windows over clusters of up to 8 CTAs,
+    # each with the whole field and history table; shapes whose tables do not
+    # fit take K3) against the oracle, rows cut by an odd stride
+    gen = SplitMix64(n * 13 + per_pe + q)
+    u0 = random_field(gen, n)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    fd = q - 1 if law == 1 else 0
+    gp = 0.4
+    model = H.DelayModel(q, H.Distribution(law), fd, gp, 99 + n)
+    p = H.SolverParams.from_r(0.4)
+    k_end, stride = 211, 37
+    t = H.async_run(H.TemperatureField(u0), p, b, H.PartitionSpec(n, per_pe), model, k_end, stride)
+    steps, snaps = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, law, q, fd, gp, 99 + n,
+                                  k_end, stride, record=True)
+    assert t.steps == steps
+    for j, s_ in enumerate(t.snapshots):
+        assert bits_equal(s_.values(), snaps[j]), (n, per_pe, q, law, bc, j)
+
+
 @pytest.mark.parametrize("n,per_pe,q,bc", [(2048, 8, 4, 0), (2048, 1024, 2, 1), (2048, 64, 8, 1),
                                            (16, 8, 3, 1), (24, 8, 2, 0)])
 def test_small_async_kernel_equals_k3(H, port, monkeypatch, n, per_pe, q, bc):
