@@ -1,7 +1,7 @@
 """Thread safety of the C-ABI (include/heat_b200.h: "every entry point may be
 called from any host thread"): the reference's ensemble_run runs its members
 on many std::threads at once (analysis.cpp:68-85), and a drop-in caller may do
-the same with sync_run / async_run / exec_run.  Eight host threads call the
+the same with sync_run / async_run / exec_run.  Ten host threads call the
 library concurrently (ctypes releases the GIL for the duration of each call)
 on different fields, sizes and partitions, repeatedly, and every result must be
 bit-identical with the oracle -- no shared scratch, tile counter or flag word
@@ -25,8 +25,8 @@ def H(gpu):
 
 def _case(i):
     gen = SplitMix64(1000 + i)
-    kind = i % 4
-    N = [1024, 5000, 1 << 17, 3 << 12][kind]
+    kind = i % 5
+    N = [1024, 5000, 1 << 17, 3 << 12, 1024][kind]
     u0 = random_field(gen, N)
     r = 0.1 + 0.39 * gen.next_double()
     return kind, N, u0, r
@@ -40,10 +40,10 @@ def _work(H, port, i, reps, errors):
     try:
         for rep in range(reps):
             k = 50 + 37 * rep + i
-            if kind in (0, 2):  # sync_run (K7 / K1)
+            if kind in (0, 2):  # sync_run (K7c cluster + zero-copy staging / K1)
                 got = H.sync_final(u0, p, bc, k)
                 exp = port.sync_run(u0, r, O.DIRICHLET, c1, c2, k)
-            elif kind == 1:  # deterministic async_run (K3 / K9)
+            elif kind in (1, 4):  # deterministic async_run (K3 / K9 cluster + zero-copy)
                 n = N // 8
                 got = H.async_final(u0, p, bc, H.PartitionSpec(N, n), H.DelayModel.uniform(3, 7 + i), k)
                 exp = port.async_run(u0, r, O.DIRICHLET, c1, c2, n, O.UNIFORM, 3, seed=7 + i, k_end=k)
@@ -62,7 +62,7 @@ def _work(H, port, i, reps, errors):
 
 def test_eight_threads_bit_exact(H, port):
     errors = []
-    threads = [threading.Thread(target=_work, args=(H, port, i, 4, errors)) for i in range(8)]
+    threads = [threading.Thread(target=_work, args=(H, port, i, 4, errors)) for i in range(10)]
     for t in threads:
         t.start()
     for t in threads:
