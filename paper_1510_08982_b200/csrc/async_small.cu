@@ -1,6 +1,7 @@
 // async_small.cu -- K9: deterministic asynchronous runs of small fields (the
-// paper's regime: cfg2 is N = 1024, 8 PEs, q = 2) in ONE CTA, temporal-blocked
-// like K7 (sync_small.cu).
+// paper's regime: cfg2 is N = 1024, 8 PEs, q = 2) on one SM or a thread-block
+// cluster of up to 8 (small_cluster.cuh), temporal-blocked like K7
+// (sync_small.cu); I/O zero-copy through the mapped pinned staging buffer.
 //
 // Replaces async_run (async_sim.cpp:118-160) -- Eq. (4): a PE's first/last
 // point reads its cross-PE neighbour at step k - d, d drawn from the run's

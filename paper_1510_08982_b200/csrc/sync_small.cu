@@ -1,6 +1,8 @@
-// sync_small.cu -- K7: synchronous runs of small fields (N <= 16384, the
-// paper's regime: cfg1 is N = 1024) in ONE CTA, the field resident in shared
-// memory for the whole run.
+// sync_small.cu -- K7 and K7c: synchronous runs of small fields (N <= 16384,
+// the paper's regime: cfg1 is N = 1024), the field resident in shared memory
+// for the whole run.  K7 (below) is one CTA; K7c (further down) spreads the
+// same windows over a thread-block cluster for N = 8m <= 8192 and is what
+// sync_run uses there; exec_run(Barriered) keeps K7.
 //
 // Replaces detail::sync_step_into iterated by run_impl (sync_solver.hpp:26-39,
 // sync_solver.cpp:52-91) for small N, where K1's one launch per pass would be
