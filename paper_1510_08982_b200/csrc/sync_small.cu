@@ -199,11 +199,14 @@ __device__ __forceinline__ void cl_steps(double (&u)[V], double r, double c, dou
 // exact), rounds of 8V steps.  Each warp has its own sub-partition, so the
 // step time is the per-warp time: fewer points per lane (more warps, more
 // CTAs) is faster per step until the per-round cost dominates.
-template <int V, bool CL>
+// HL halo lanes per side (H = HL*V points = steps per round): more halo
+// lanes mean longer rounds (fewer exchanges per step) but fewer exact points
+// per window, i.e. more windows, CTAs and SMs for the same field.
+template <int V, bool CL, int HL = 8>
 __global__ void __launch_bounds__(512, 1) sync_small_cl_kernel(const SmallClArgs a) {
     extern __shared__ double smem[];
     __shared__ __align__(8) unsigned long long sbar[2];
-    constexpr int H = 8 * V, C = 32 * V - 2 * H;
+    constexpr int H = HL * V, C = 32 * V - 2 * H;
     const int N = a.n, Np = (N + 1) & ~1;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CL ? int(small_ctarank()) : 0;
@@ -399,8 +402,21 @@ static int sync_run_small_cl(const double* u0, size_t n, double r, int bc_kind, 
         return e ? std::atoi(e) : 0;
     }();
     const int V = forced_v == 4 || forced_v == 8 ? forced_v : 8;
+    // halo lanes per side: HEAT_K7C_HL in {8, 10, 12} (V = 8 only)
+    static const int forced_hl = [] {
+        const char* e = std::getenv("HEAT_K7C_HL");
+        return e ? std::atoi(e) : 0;
+    }();
+    // default: 10 halo lanes (80-step rounds) while that keeps one window per
+    // SM sub-partition (<= 32 windows: N <= 3072; cfg1 50.3 ns/step against
+    // 53.3 with 8, 50.9 with 12), else 8
+    const int HL = V != 8                                      ? 8
+                   : forced_hl == 8 || forced_hl == 10 || forced_hl == 12 ? forced_hl
+                   : (n + 95) / 96 <= 32                        ? 10
+                                                                : 8;
     if (n % size_t(V)) return fail(HEAT_ELOGIC, "K7c: N is not a multiple of the lane width");
-    const int warps = int((n + 16 * V - 1) / (16 * V));
+    const int Cw = (32 - 2 * HL) * V;  // exact points per window
+    const int warps = int((n + Cw - 1) / Cw);
     // more than four windows: a cluster, one warp per SM sub-partition
     static const bool no_cluster = std::getenv("HEAT_K7_NO_CLUSTER") != nullptr;
     const int ncta = no_cluster ? 1 : std::min(8, (warps + 3) / 4);
@@ -408,11 +424,14 @@ static int sync_run_small_cl(const double* u0, size_t n, double r, int bc_kind, 
     if (wpc > 16) return fail(HEAT_ELOGIC, "K7c: too many warps per CTA");
     a.ncta = ncta;
     const int smem = int(2 * ((n + 1) & ~size_t(1)) * sizeof(double));
+    auto pick = [&](auto k1, auto kc) {
+        return ncta > 1 ? reinterpret_cast<const void*>(kc) : reinterpret_cast<const void*>(k1);
+    };
     const void* fn =
-        V == 4 ? (ncta > 1 ? reinterpret_cast<const void*>(sync_small_cl_kernel<4, true>)
-                           : reinterpret_cast<const void*>(sync_small_cl_kernel<4, false>))
-               : (ncta > 1 ? reinterpret_cast<const void*>(sync_small_cl_kernel<8, true>)
-                           : reinterpret_cast<const void*>(sync_small_cl_kernel<8, false>));
+        V == 4     ? pick(sync_small_cl_kernel<4, false>, sync_small_cl_kernel<4, true>)
+        : HL == 10 ? pick(sync_small_cl_kernel<8, false, 10>, sync_small_cl_kernel<8, true, 10>)
+        : HL == 12 ? pick(sync_small_cl_kernel<8, false, 12>, sync_small_cl_kernel<8, true, 12>)
+                   : pick(sync_small_cl_kernel<8, false>, sync_small_cl_kernel<8, true>);
     int per_sm = 0;
     HB_TRY(kernel_smem_config(fn, int(2 * kClMaxN * sizeof(double)), wpc * 32, &per_sm));
     cudaLaunchConfig_t cfg{};
