@@ -113,11 +113,21 @@ __device__ __forceinline__ double pick(const double (&h)[QH], int d) {
 // other CTAs own); no cluster barrier, no memory fence.  A peer can only
 // write a buffer after it has received this CTA's writes of the round that
 // read it, so one phase per buffer and round is enough.
-template <int QH, int LAW, bool CL>
+// WS: every stepping warp has a producer warp (the second half of the CTA)
+// that draws the delays of its next 16-step sub-round into the other half of
+// a double-buffered table while it steps the current one; the pair meets at
+// a named barrier once per sub-round, the stepping warps at another once per
+// round.  The draws leave the stepping warp's critical path.
+__device__ __forceinline__ void k9_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int QH, int LAW, bool CL, bool WS = false>
 __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArgs a) {
     extern __shared__ double smem[];
     __shared__ __align__(16) unsigned char sdel[kAsMaxWarpsCta][64 * kAsSub];  // per warp: [stream][step]
     __shared__ int sstr[kAsMaxWarpsCta][64];  // per warp: draw rank of each delay stream
+    __shared__ int snstr[kAsMaxWarpsCta];     // WS: per stepping warp, its stream count
     __shared__ __align__(8) unsigned long long sbar[2];  // CL: round mbarriers, by buffer
     const int Np = (a.N + 1) & ~1, TB = a.P * 2 * QH;
     double* su = smem;              // [2][Np]: the field, double-buffered
@@ -129,7 +139,9 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     constexpr int V = kAsV, H = kAsHalo, C = kAsChunk;
     const int N = a.N, n = a.n, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CL ? int(small_ctarank()) : 0;
-    const int gw = rank * int(blockDim.x >> 5) + w;  // window index in the field
+    const int nw = int(blockDim.x >> 5) / (WS ? 2 : 1);  // stepping warps per CTA
+    const bool producer = WS && w >= nw;
+    const int gw = rank * nw + (producer ? w - nw : w);  // window index in the field
 
     // The inputs may sit in mapped host memory (a microsecond per round
     // trip): every thread issues all its loads before using any of them.
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
 
     const long long w0 = (long long)gw * C - H;  // window start (unwrapped)
     const long long g0 = w0 + (long long)lane * V;
-    const bool active = (long long)gw * C < N;  // warp-uniform
+    const bool active = !producer && (long long)gw * C < N;  // warp-uniform
     // N and the window starts are multiples of 8, so the Dirichlet ends are
     // always a lane's first (point 0) or last (point N-1) element: the
     // pipelined step re-pins them with two selects
@@ -238,6 +250,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     const int sU = __popc(mU & below), sD = cU + __popc(mD & below);
     if (active && isU) sstr[w][sU] = offU;
     if (active && isD) sstr[w][sD] = offD;
+    if (WS && !producer && lane == 0) snstr[w] = nstreams;
     __syncwarp();
     const int wg0 = wrapg(g0);
     // exact outputs: lanes 8..23 of the window (the 128-point chunk), inside the field
@@ -251,6 +264,7 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         if (threadIdx.x == 0) small_bars_init(bar0);
         small_cluster_sync();  // every CTA's barriers exist before the first st.async
     }
+    if (WS) __syncthreads();  // the producers read their stepping warp's streams
     int par = 0;              // buffer read by this round
     uint32_t phases = 0;      // CL: bit b = parity of the next wait on mbarrier b
     long long k = 0;
@@ -260,7 +274,40 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
     long long next_rec = a.stride > 0 ? min(a.stride, a.k_end) : a.k_end + 1;
     double u[V];
     double hF[QH], hL[QH];  // products of my first / last point, hX[j] at step k - j
-    while (k < a.k_end) {
+    int sub = 0;            // WS: sub-rounds so far (the table half in use)
+    if (WS && producer) {   // the same rounds and sub-rounds as the stepping warp
+        const int wc = w - nw, ns = snstr[wc];
+        const bool cact = (long long)gw * C < N;
+        while (k < a.k_end) {
+            const long long s = min((long long)H, a.k_end - k);
+            for (int t0 = 0, len = 0; cact && t0 < int(s); t0 += len) {
+                const long long kb = k + t0;
+                len = int(min((long long)min(kAsSub, int(s) - t0), next_rec - kb));
+                unsigned char* dst = sdel[wc + (sub & 1) * nw];
+                for (int base = 0; base < ns * kAsSub; base += 32) {
+                    const int it = base + lane;
+                    const int si = min(it / kAsSub, ns - 1), j = it % kAsSub;
+                    const int off = sstr[wc][si];
+                    const long long kk = kb + j;
+                    const int bound = kk < (long long)(a.q - 1) ? int(kk) : a.q - 1;
+                    const uint64_t z =
+                        a.seed + (uint64_t(kk) * uint64_t(a.D) + uint64_t(off) + 1) * gamma;
+                    if (it < ns * kAsSub)
+                        dst[it] = (unsigned char)small_delay<LAW>(a, z, bound, sthr);
+                }
+                __syncwarp();
+                k9_bar(2 + wc, 64);  // sub-round `sub` is in; the other half is free
+                ++sub;
+                if (kb + len == next_rec)
+                    next_rec = next_rec + a.stride > a.k_end && next_rec < a.k_end
+                                   ? a.k_end
+                                   : next_rec + a.stride;
+            }
+            par ^= 1;
+            k += s;
+        }
+    }
+    while (!producer && k < a.k_end) {
         const long long s = min((long long)H, a.k_end - k);
         const double* cu = su + par * Np;
         const double* ct = tab + par * TB;
@@ -287,7 +334,13 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                 len = int(min((long long)min(kAsSub, int(s) - t0), next_rec - kb));
                 // -- the delays of this sub-round, one lane per (stream, step):
                 // stream i < cU is the i-th sending-up lane, then the sending-down ones
-                for (int base = 0; base < nstreams * kAsSub; base += 32) {
+                const unsigned char* dsrc = sdel[w];
+                if (WS) {  // drawn by this warp's producer
+                    k9_bar(2 + w, 64);
+                    dsrc = sdel[w + (sub & 1) * nw];
+                    ++sub;
+                }
+                for (int base = 0; !WS && base < nstreams * kAsSub; base += 32) {
                     const int it = base + lane;
                     const int si = min(it / kAsSub, nstreams - 1), j = it % kAsSub;
                     const int off = sstr[w][si];
@@ -300,8 +353,8 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                 }
                 __syncwarp();
                 uint64_t wU = 0, wD = 0;
-                if (isU) wU = pack_nibbles(&sdel[w][sU * kAsSub]);
-                if (isD) wD = pack_nibbles(&sdel[w][sD * kAsSub]);
+                if (isU) wU = pack_nibbles(&dsrc[sU * kAsSub]);
+                if (isD) wD = pack_nibbles(&dsrc[sD * kAsSub]);
                 __syncwarp();
                 {
                     // software-pipelined as warp_steps_pipelined: the end points
@@ -402,8 +455,11 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
                     if (CL) put_peers2(dst, hL[j], hL[j + 1], nbar, rank, a.ncta);
                 }
         }
-        __syncthreads();  // my own copy of buffer par^1 is complete
-        if (CL) {         // ... and the other CTAs' parts of it have landed
+        if (WS)  // my own copy of buffer par^1 is complete
+            k9_bar(1, nw * 32);
+        else
+            __syncthreads();
+        if (CL) {  // ... and the other CTAs' parts of it have landed
             const int b = par ^ 1;
             mbar_wait_parity(nbar, (phases >> b) & 1u);
             phases ^= 1u << b;
@@ -411,8 +467,9 @@ __global__ void __launch_bounds__(512, 1) async_small_kernel(const AsyncSmallArg
         par ^= 1;
         k += s;
     }
-    if (rank != 0) return;  // the other copies are identical
-    su += par * Np;         // the last round's output
+    if (WS) __syncthreads();  // the producers finish early: the last round must be in
+    if (rank != 0) return;    // the other copies are identical
+    su += par * Np;           // the last round's output
     bool bad = false;
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
         bad |= !isfinite(su[i]);
@@ -554,15 +611,23 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     const int ncta = no_cluster ? 1 : std::min(8, (warps + 3) / 4);
     const int wpc = (warps + ncta - 1) / ncta;
     a.ncta = ncta;
-    auto launch = [&](auto kern1, auto kernc) -> int {
+    // producer warps for the draws (WS) while each stepping warp still has an
+    // SM sub-partition to itself (<= 4 per CTA: cfg2 98.4 -> 86.4 ns/step;
+    // with 8 per CTA it lost 3%); HEAT_K9_NO_WS=1: the stepping warps draw
+    static const bool no_ws = std::getenv("HEAT_K9_NO_WS") != nullptr;
+    const bool ws = !no_ws && wpc <= 4;
+    const int threads = (ws ? 2 : 1) * wpc * 32;
+    auto launch = [&](auto kern1, auto kernc, auto kern1w, auto kerncw) -> int {
         int per_sm = 0;
-        const void* fn = ncta > 1 ? reinterpret_cast<const void*>(kernc)
-                                  : reinterpret_cast<const void*>(kern1);
+        const void* fn = ws ? (ncta > 1 ? reinterpret_cast<const void*>(kerncw)
+                                        : reinterpret_cast<const void*>(kern1w))
+                            : (ncta > 1 ? reinterpret_cast<const void*>(kernc)
+                                        : reinterpret_cast<const void*>(kern1));
         if (wpc > kAsMaxWarpsCta) return fail(HEAT_ELOGIC, "K9: too many windows per CTA");
-        HB_TRY(kernel_smem_config(fn, int(kAsSmemCap), wpc * 32, &per_sm));
+        HB_TRY(kernel_smem_config(fn, int(kAsSmemCap), threads, &per_sm));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(unsigned(ncta));
-        cfg.blockDim = dim3(unsigned(wpc * 32));
+        cfg.blockDim = dim3(unsigned(threads));
         cfg.dynamicSmemBytes = size_t(smem);
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -577,12 +642,13 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return HEAT_OK;
     };
-#define HB_K9(QHV)                                                                              \
-    (law == HEAT_DELAY_UNIFORM                                                                  \
-         ? launch(async_small_kernel<QHV, 0, false>, async_small_kernel<QHV, 0, true>)          \
-     : law == HEAT_DELAY_FIXED                                                                  \
-         ? launch(async_small_kernel<QHV, 1, false>, async_small_kernel<QHV, 1, true>)          \
-         : launch(async_small_kernel<QHV, 2, false>, async_small_kernel<QHV, 2, true>))
+#define HB_K9_LAW(QHV, L)                                                                     \
+    launch(async_small_kernel<QHV, L, false>, async_small_kernel<QHV, L, true>,                 \
+           async_small_kernel<QHV, L, false, true>, async_small_kernel<QHV, L, true, true>)
+#define HB_K9(QHV)                                                                            \
+    (law == HEAT_DELAY_UNIFORM ? HB_K9_LAW(QHV, 0)                                            \
+     : law == HEAT_DELAY_FIXED ? HB_K9_LAW(QHV, 1)                                            \
+                               : HB_K9_LAW(QHV, 2))
     if (QH == 2)
         HB_TRY(HB_K9(2));
     else if (QH == 4)
@@ -590,6 +656,7 @@ int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1
     else
         HB_TRY(HB_K9(8));
 #undef HB_K9
+#undef HB_K9_LAW
     size_t ns = 0;
     std::vector<size_t> ks;
     if (want) {
