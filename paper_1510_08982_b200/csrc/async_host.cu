@@ -512,6 +512,10 @@ int async_run_core(const double* u0, size_t N, double r, int bc_kind, double c1,
         return async_run_small(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
                                geometric_p, seed, k_end, stride, final_out, snapshots, steps_out,
                                max_snapshots, n_snapshots);
+    if (async_member_eligible(N, per_pe, q))  // K6, one member: PEs K9 does not lay out
+        return async_run_member(u0, N, r, bc_kind, c1, c2, per_pe, q, law, fixed_delay,
+                                geometric_p, seed, k_end, stride, final_out, snapshots, steps_out,
+                                max_snapshots, n_snapshots);
 
     DevCtx* d = nullptr;
     HB_TRY(dev_ctx(-1, &d));

@@ -45,6 +45,7 @@ struct EnsembleArgs {
     double* norms;      // [runs][n_rec]
     double* terminals;  // [runs][n] (may be null)
     unsigned int* flag; // [0] non-finite
+    double* rows;       // one-member async_run: [n_rec][n] trajectory rows (may be null)
 };
 
 // l2_norm (core.cpp:50-56): sequential sum of squares, then sqrt -- one
@@ -76,6 +77,8 @@ __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
     for (int i = t; i < n; i += T) hist[i] = a.u0[i];  // slot 0 = step 0
     __syncthreads();
     if (t == 0 && a.norms) a.norms[(size_t)blockIdx.x * a.n_rec] = seq_l2(hist, n);
+    if (a.rows)
+        for (int i = t; i < n; i += T) a.rows[i] = hist[i];
 
     int ci[PT], li[PT], ri[PT], offL[PT], offR[PT], dL[PT], dR[PT];
     bool live[PT], pin[PT];
@@ -167,6 +170,8 @@ __global__ void __launch_bounds__(1024) ensemble_kernel(const EnsembleArgs a) {
         if (k + 1 == next_rec || (k + 1 == a.k_end && next_rec != k + 1)) {
             if (t == 0 && a.norms)
                 a.norms[(size_t)blockIdx.x * a.n_rec + rec] = seq_l2(hist + slot * n, n);
+            if (a.rows)
+                for (int i = t; i < n; i += T) a.rows[(size_t)rec * n + i] = hist[slot * n + i];
             ++rec;
             if (k + 1 == next_rec) next_rec += a.stride;
         }
@@ -311,6 +316,109 @@ int ensemble_via_simulators(const double* u0, size_t n, double r, int bc_kind, d
 }
 
 }  // namespace
+}  // namespace hb
+
+
+namespace hb {
+// async_run (async_sim.cpp:142-160) of a small field whose PEs K9 does not lay
+// out (e.g. the paper's one point per PE): one K6 member with seed `seed`
+// (member j of an ensemble draws from base_seed + j: the same stream), the
+// trajectory rows written by the kernel.  K3 steps these at ~600 ns/step,
+// K6 at ~230 (N = 100, q = 5; tools/probe_paper_member.py).  K6's step is
+// one CTA barrier per step over all N points, K3's a warp per PE: K6 wins up
+// to ~640 points (N = 600, PEs of 75: 585 vs 701 ns/step) and for PEs of
+// fewer than 8 points at any N <= 1024 (N = 1024, PEs of 4: 919 vs 2159);
+// K3 wins for N = 1000 with PEs of 10-125 (700-810 vs 920)
+// (tools/probe_member_vs_k3.py).
+bool async_member_eligible(size_t n, size_t per_pe, size_t q) {
+    if (std::getenv("HEAT_NO_MEMBER_ASYNC")) return false;
+    return n >= 3 && n <= 1024 && (n <= 640 || per_pe < 8) &&
+           (q + 1) * n * sizeof(double) + q * 8 <= 200 * 1024;
+}
+
+int async_run_member(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                     size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                     uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                     double* snapshots, size_t* steps_out, size_t max_snapshots,
+                     size_t* n_snapshots) {
+    std::vector<size_t> steps{0};
+    for (size_t k = stride; k < k_end; k += stride) steps.push_back(k);
+    if (k_end > 0 && steps.back() != k_end) steps.push_back(k_end);
+    const size_t S = steps.size();
+    const bool want = snapshots != nullptr || steps_out != nullptr;
+    std::vector<uint64_t> gthr;
+    if (law == HEAT_DELAY_GEOMETRIC) HB_TRY(geometric_thresholds(geometric_p, q, gthr));
+    const int PT = n <= 1024 ? 1 : n <= 2048 ? 2 : 4;
+    const int T = int(((n + PT - 1) / PT + 31) / 32 * 32);
+    const size_t smem = (q + 1) * n * sizeof(double) + gthr.size() * sizeof(uint64_t);
+
+    DevCtx* d = nullptr;
+    HB_TRY(dev_ctx(-1, &d));
+    std::lock_guard<std::mutex> lock(d->mu);
+    const bool dir = bc_kind == HEAT_BC_DIRICHLET;
+    std::vector<int> offL, offR;
+    const long long D = point_offsets(int(n), int(per_pe), dir, offL, offR);
+    auto a256 = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t o_u0 = 0, o_offL = o_u0 + a256(n * 8), o_offR = o_offL + a256(n * 4),
+                 o_gthr = o_offR + a256(n * 4), o_term = o_gthr + a256(gthr.size() * 8 + 8),
+                 o_rows = o_term + a256(n * 8), total = o_rows + a256(want ? S * n * 8 : 8);
+    HB_TRY(ensure_scratch(*d, total));
+    char* base = static_cast<char*>(d->scratch);
+    cudaStream_t st = d->stream;
+    HB_TRY(upload_prepared(*d, u0, n, bc_kind, c1, c2, reinterpret_cast<double*>(base + o_u0)));
+    HB_CUDA(cudaMemcpyAsync(base + o_offL, offL.data(), n * 4, cudaMemcpyHostToDevice, st));
+    HB_CUDA(cudaMemcpyAsync(base + o_offR, offR.data(), n * 4, cudaMemcpyHostToDevice, st));
+    if (!gthr.empty())
+        HB_CUDA(cudaMemcpyAsync(base + o_gthr, gthr.data(), gthr.size() * 8, cudaMemcpyHostToDevice,
+                                st));
+    HB_CUDA(cudaMemsetAsync(d->flag, 0, 2 * sizeof(unsigned int), st));
+    EnsembleArgs a{};
+    a.u0 = reinterpret_cast<const double*>(base + o_u0);
+    a.n = int(n);
+    a.r = r;
+    a.c = 1.0 - 2.0 * r;  // core.hpp:108
+    a.c1 = c1;
+    a.c2 = c2;
+    a.dirichlet = dir;
+    a.q = int(q);
+    a.law = law;
+    a.fixed_d = int(std::min<size_t>(fixed_delay, 1u << 30));
+    a.gthr = reinterpret_cast<const uint64_t*>(base + o_gthr);
+    a.base_seed = seed;
+    a.modq = make_modq(unsigned(q));
+    a.D = D;
+    a.offL = reinterpret_cast<const int*>(base + o_offL);
+    a.offR = reinterpret_cast<const int*>(base + o_offR);
+    a.k_end = (long long)k_end;
+    a.stride = (long long)stride;
+    a.n_rec = int(S);
+    a.norms = nullptr;
+    a.terminals = reinterpret_cast<double*>(base + o_term);
+    a.rows = want ? reinterpret_cast<double*>(base + o_rows) : nullptr;
+    a.flag = d->flag;
+    const EnsembleKernel kern = pick_kernel(PT, law);
+    if (smem > 48 * 1024)
+        HB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<1, T, smem, st>>>(a);
+    HB_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const size_t copy = std::min(S, max_snapshots);
+    if (want && snapshots && copy)
+        HB_CUDA(cudaMemcpyAsync(snapshots, a.rows, copy * n * 8, cudaMemcpyDeviceToHost, st));
+    if (final_out)
+        HB_CUDA(cudaMemcpyAsync(final_out, a.terminals, n * 8, cudaMemcpyDeviceToHost, st));
+    unsigned int flags[2] = {0, 0};
+    HB_CUDA(cudaMemcpyAsync(flags, d->flag, sizeof flags, cudaMemcpyDeviceToHost, st));
+    HB_CUDA(cudaStreamSynchronize(st));
+    if (flags[0]) {
+        if (g_strict.load()) return fail(HEAT_EDIVERGE, "non-finite value produced by async step");
+        return fail(HEAT_EDOMAIN, "TemperatureField values must be finite");
+    }
+    if (steps_out)
+        for (size_t j = 0; j < S && j < max_snapshots; ++j) steps_out[j] = steps[j];
+    if (n_snapshots) *n_snapshots = want ? S : 0;
+    return HEAT_OK;
+}
 }  // namespace hb
 
 using namespace hb;

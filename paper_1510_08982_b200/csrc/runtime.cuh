@@ -225,6 +225,13 @@ int draw_offsets(size_t N, size_t n, int dirichlet, std::vector<int>& offL, std:
 // points in one CTA; arguments and errors as heat_sync_run (validated by the caller).
 // K9 (async_small.cu): deterministic async_run of small fields on one CTA
 bool async_small_eligible(size_t N, size_t per_pe, size_t q);
+// K6 with one member (ensemble.cu): async_run of fields K9 does not lay out
+bool async_member_eligible(size_t n, size_t per_pe, size_t q);
+int async_run_member(const double* u0, size_t n, double r, int bc_kind, double c1, double c2,
+                     size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
+                     uint64_t seed, size_t k_end, size_t stride, double* final_out,
+                     double* snapshots, size_t* steps_out, size_t max_snapshots,
+                     size_t* n_snapshots);
 int async_run_small(const double* u0, size_t N, double r, int bc_kind, double c1, double c2,
                     size_t per_pe, size_t q, int law, size_t fixed_delay, double geometric_p,
                     uint64_t seed, size_t k_end, size_t stride, double* final_out,

@@ -414,7 +414,8 @@ def test_small_async_cluster_sizes_bit_exact(H, port, n, per_pe, q, law, bc):
 @pytest.mark.parametrize("n,per_pe,q,bc", [(2048, 8, 4, 0), (2048, 1024, 2, 1), (2048, 64, 8, 1),
                                            (16, 8, 3, 1), (24, 8, 2, 0)])
 def test_small_async_kernel_equals_k3(H, port, monkeypatch, n, per_pe, q, bc):
-    # K9 and K3 (HEAT_NO_SMALL_ASYNC) both give the oracle's bits
+    # K9, the one-member K6 (HEAT_NO_SMALL_ASYNC, small fields) and K3 (both
+    # off) all give the oracle's bits
     gen = SplitMix64(n * 7 + q)
     u0 = random_field(gen, n)
     b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
@@ -423,9 +424,37 @@ def test_small_async_kernel_equals_k3(H, port, monkeypatch, n, per_pe, q, bc):
     model = H.DelayModel.uniform(q, 5)
     k9 = H.async_final(u0, p, b, part, model, 777)
     monkeypatch.setenv("HEAT_NO_SMALL_ASYNC", "1")
+    k6 = H.async_final(u0, p, b, part, model, 777)
+    monkeypatch.setenv("HEAT_NO_MEMBER_ASYNC", "1")
     k3 = H.async_final(u0, p, b, part, model, 777)
     exp = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, 0, q, seed=5, k_end=777)
-    assert bits_equal(k9, exp) and bits_equal(k3, exp)
+    assert bits_equal(k9, exp) and bits_equal(k6, exp) and bits_equal(k3, exp)
+
+
+@pytest.mark.parametrize("n,per_pe,q,law,bc", [
+    (100, 1, 5, 0, 0), (100, 1, 5, 0, 1), (97, 1, 3, 2, 0), (600, 75, 6, 1, 1), (1024, 4, 2, 0, 0),
+    (5, 1, 2, 0, 1), (640, 5, 16, 2, 1)])
+def test_member_async_trajectories_bit_exact(H, port, monkeypatch, n, per_pe, q, law, bc):
+    # async_run of shapes K9 does not lay out on the one-member K6
+    # (ensemble.cu async_run_member): the paper's one point per PE, odd N,
+    # the three laws, rows cut at an odd stride; and K3 on the same shape
+    gen = SplitMix64(n * 31 + per_pe + q)
+    u0 = random_field(gen, n)
+    b = H.BoundaryCondition.periodic() if bc else H.BoundaryCondition.dirichlet(u0[0], u0[-1])
+    fd = q - 1 if law == 1 else 0
+    model = H.DelayModel(q, H.Distribution(law), fd, 0.35, 11 + n)
+    p = H.SolverParams.from_r(0.4)
+    k_end, stride = 1500, 77
+    steps, snaps = port.async_run(u0, p.r(), b.kind, b.c1, b.c2, per_pe, law, q, fd, 0.35, 11 + n,
+                                  k_end, stride, record=True)
+    for env in (None, "HEAT_NO_MEMBER_ASYNC"):
+        if env:
+            monkeypatch.setenv(env, "1")
+        t = H.async_run(H.TemperatureField(u0), p, b, H.PartitionSpec(n, per_pe), model, k_end,
+                        stride)
+        assert t.steps == steps, env
+        for j, s_ in enumerate(t.snapshots):
+            assert bits_equal(s_.values(), snaps[j]), (env, n, per_pe, q, law, bc, j)
 
 
 @pytest.mark.parametrize("n_total,per_pe,q,bc,law", [
